@@ -1,0 +1,249 @@
+/* SPDX-License-Identifier: Apache-2.0
+ *
+ * vc.h — C-ABI of the B200-native FT-reconstruction (FTR) frame path.
+ *
+ * Drop-in boundary for the reference's proj/core reconstruction interface
+ * (/root/reference/proj/core/include/volcap/...):
+ *
+ *   recon::reconstruct_frame        reconstruct.hpp:38-39  -> vc_reconstruct_frame
+ *   appearance::vertex_visibility   texture.hpp:32-35      -> (fused into vc_reconstruct_frame,
+ *   appearance::assign_texture      texture.hpp:39-42          and vc_stage_texture)
+ *   recon::build_cloud              cloud.hpp:32-33        -> vc_stage_preprocess
+ *   recon::confidence_weights       cloud.hpp:37-38        -> vc_stage_preprocess (fused)
+ *   recon::fit_grid                 reconstruct.hpp:42     -> vc_fit_grid / vc_stage_preprocess
+ *   recon::splat                    volume_recon.hpp:33-34 -> vc_stage_splat
+ *   recon::integrate_fft            volume_recon.hpp:46    -> vc_stage_integrate
+ *   recon::iso_level                volume_recon.hpp:49    -> vc_stage_iso_level
+ *   recon::marching_cubes           marching_cubes.hpp:16  -> vc_stage_marching_cubes
+ *
+ * Plain pointers and sizes only; no C++ or torch types cross this boundary.
+ * Every entry point returns a vc_status; no exception crosses the ABI.  The
+ * reference's exceptions map as: std::invalid_argument -> VC_ERR_INVALID_ARGUMENT,
+ * std::runtime_error("empty foreground in all views") -> VC_ERR_EMPTY_SCENE.
+ *
+ * Threading: one vc_ctx = one CUDA device + one stream.  Distinct contexts
+ * are independent and may be used from different threads; calls on one
+ * context must be serialised by the caller (the reference's reconstruct_frame
+ * is a pure function; here state lives in the context).
+ *
+ * Ownership: inputs are borrowed for the duration of a call.  Outputs are
+ * context-owned (vertex/triangle counts are data-dependent) and stay valid
+ * until the next call on the same context or vc_ctx_destroy.
+ *
+ * All world units are millimetres (types.hpp:17).  Arrays are row-major;
+ * volumes are x-fastest (volume.hpp:31-34): index = x + nx*(y + ny*z).
+ */
+#ifndef VC_VC_H_
+#define VC_VC_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define VC_ABI_VERSION 1
+
+typedef enum vc_status {
+  VC_OK = 0,
+  VC_ERR_INVALID_ARGUMENT = 1, /* std::invalid_argument in the reference */
+  VC_ERR_EMPTY_SCENE = 2,      /* "empty foreground in all views" (reconstruct.cpp:65-66) */
+  VC_ERR_CAPACITY = 3,         /* marching-cubes output exceeded capacity (retried internally) */
+  VC_ERR_CUDA = 4,
+  VC_ERR_NCCL = 5,
+  VC_ERR_OOM = 6,
+  VC_ERR_NO_DEVICE = 7
+} vc_status;
+
+/* types.hpp:26-39 — pinhole, pixel-centre convention. */
+typedef struct vc_intrinsics {
+  double fx, fy, cx, cy;
+  int32_t width, height;
+} vc_intrinsics;
+
+/* types.hpp:42-57 — camera-to-world rigid transform, R row-major. */
+typedef struct vc_pose {
+  double R[9];
+  double t[3];
+} vc_pose;
+
+/* types.hpp:68-76 — depth camera + RGB camera (pose relative to depth). */
+typedef struct vc_sensor {
+  vc_intrinsics depth_intr;
+  vc_pose pose;
+  vc_intrinsics rgb_intr;
+  vc_pose rgb_relative;
+} vc_sensor;
+
+typedef enum vc_mem_kind { VC_MEM_HOST = 0, VC_MEM_DEVICE = 1 } vc_mem_kind;
+
+/* image.hpp:50-64 — one RgbdFrame.  depth: uint16 mm (0 = invalid),
+ * mask: uint8 (nonzero = foreground), rgb: packed RGB8 of rgb_intr size.
+ * Pitches are in bytes; 0 means tightly packed. */
+typedef struct vc_view {
+  const uint16_t* depth;
+  const uint8_t* mask;
+  const uint8_t* rgb;
+  int32_t depth_pitch, mask_pitch, rgb_pitch;
+  int32_t mem_kind; /* vc_mem_kind */
+} vc_view;
+
+typedef enum vc_splat_mode { VC_SPLAT_WEIGHTED = 0, VC_SPLAT_SIMPLE = 1 } vc_splat_mode;
+
+/* reconstruct.hpp:12-18 (ReconConfig) + the texture eps (texture.hpp:35).
+ * Grid dims: r > 0 selects the reference lattice 2^r x 2^(r+1) x 2^r
+ * (reconstruct.cpp:18-20); r == 0 uses nx,ny,nz (powers of two, 4..1024). */
+typedef struct vc_recon_config {
+  int32_t r;
+  int32_t nx, ny, nz;
+  int32_t mode; /* vc_splat_mode */
+  double discontinuity_mm;
+  int32_t padding_voxels;
+  int32_t silhouette_radius_px;
+  double eps_vis_mm;
+} vc_recon_config;
+
+/* volume_recon.hpp:24-28 */
+typedef struct vc_grid_spec {
+  int32_t nx, ny, nz;
+  double origin[3];
+  double edge_mm;
+} vc_grid_spec;
+
+/* reconstruct.hpp:20-24 (StageTimings) + the CLI's "other" texture column
+ * (volcap.cpp:475-481), measured with CUDA events on the context stream.
+ * preprocess = build_cloud + confidence_weights (fused kernels; weights_ms
+ * is reported as 0).  The split fields break volumetric_ms down. */
+typedef struct vc_stage_timings {
+  double raw_ms, weights_ms, volumetric_ms, texture_ms, total_ms;
+  double splat_ms, fft_ms, iso_ms, mc_ms;
+  double h2d_ms, d2h_ms;
+} vc_stage_timings;
+
+/* TexturedMesh (texture.hpp:16-28) + FrameReconstruction's volume/iso level
+ * (reconstruct.hpp:26-30) + the blended per-vertex colour.
+ * Per-sensor arrays are [sensor][vertex]. */
+typedef struct vc_textured_mesh {
+  int32_t vertex_count, triangle_count, sensor_count, point_count;
+  const float* positions;   /* 3V, world mm */
+  const float* normals;     /* 3V, unit, outward */
+  const int32_t* triangles; /* 3T */
+  const uint8_t* visible;   /* K*V */
+  const float* uv;          /* 2*K*V, normalised [0,1]^2 (texture.hpp:45-47) */
+  const float* weight;      /* K*V */
+  const uint8_t* untextured;/* V */
+  const uint8_t* rgb;       /* 3V blended colour */
+  const double* positions_f64; /* 3V, the exact vertex positions */
+  double iso_level;
+  vc_grid_spec grid;
+  int32_t mem_kind;         /* where the pointers above live */
+} vc_textured_mesh;
+
+typedef struct vc_ctx vc_ctx;
+
+/* ---------------------------------------------------------------- context */
+int vc_abi_version(void);
+const char* vc_status_string(vc_status s);
+vc_status vc_ctx_create(int device, vc_ctx** out);
+vc_status vc_ctx_destroy(vc_ctx* ctx);
+const char* vc_last_error(const vc_ctx* ctx);
+/* Output placement for vc_reconstruct_frame: VC_MEM_HOST (default; D2H into
+ * context-owned pinned buffers) or VC_MEM_DEVICE (pointers into HBM). */
+vc_status vc_ctx_set_output(vc_ctx* ctx, int32_t mem_kind);
+/* Collect per-stage CUDA-event timings (adds event records; default off). */
+vc_status vc_ctx_set_profiling(vc_ctx* ctx, int32_t enable);
+/* Replay the whole frame as one CUDA graph (default on). */
+vc_status vc_ctx_set_graphs(vc_ctx* ctx, int32_t enable);
+/* The CUDA stream (cudaStream_t) of the context, for interop. */
+void* vc_ctx_stream(vc_ctx* ctx);
+/* Number of kernels one vc_reconstruct_frame launches (excluding retries). */
+int32_t vc_ctx_kernels_per_frame(const vc_ctx* ctx);
+/* Per-kernel CUDA-event times (ms) of the last frame run with profiling on,
+ * in launch order: preprocess(4 kernels), clear, splat, fft_x, fft_y, fft_z,
+ * ifft_y, ifft_x, iso(2), mc(4), texture(2).  Returns the count written. */
+int32_t vc_ctx_kernel_times(const vc_ctx* ctx, double* ms, int32_t max_n);
+/* Pinned host memory helpers (for zero-staging H2D of views). */
+vc_status vc_host_alloc(vc_ctx* ctx, size_t bytes, void** out);
+vc_status vc_host_free(vc_ctx* ctx, void* p);
+vc_status vc_device_alloc(vc_ctx* ctx, size_t bytes, void** out);
+vc_status vc_device_free(vc_ctx* ctx, void* p);
+vc_status vc_memcpy(vc_ctx* ctx, void* dst, const void* src, size_t bytes, int32_t dst_kind, int32_t src_kind);
+vc_status vc_synchronize(vc_ctx* ctx);
+
+/* ------------------------------------------------------------ the hot path */
+/* reconstruct.cpp:37-78 + texture.cpp:11-72 + per-vertex blend:
+ * k views (one per reconstruction sensor, sensors[0..k)) in, textured mesh out. */
+vc_status vc_reconstruct_frame(vc_ctx* ctx, const vc_sensor* sensors, const vc_view* views, int32_t k,
+                               const vc_recon_config* config, vc_textured_mesh* out,
+                               vc_stage_timings* timings);
+
+/* A (fp32, x-fastest, nx*ny*nz) of the last frame, for the mocap consumers
+ * (volcap.cpp:427-429).  dst_kind: VC_MEM_HOST or VC_MEM_DEVICE. */
+vc_status vc_export_volume(vc_ctx* ctx, float* dst, int32_t dst_kind);
+/* Oriented points of the last frame (clouds concatenated in sensor order):
+ * pos/nrm 3P doubles, weight P doubles, pix 3P int32 (px, py, sensor);
+ * weight_maps k*h*w floats (cloud.hpp:21-26).  Any pointer may be NULL. */
+vc_status vc_export_points(vc_ctx* ctx, double* pos, double* nrm, double* weight, int32_t* pix,
+                           float* weight_maps);
+
+/* ------------------------------------------------ per-stage entry points
+ * Host arrays in, host arrays out; each runs the same kernels as the frame
+ * path on the context's stream.  For parity tests against the reference's
+ * stage functions. */
+
+/* build_cloud + confidence_weights for k views; returns the point count in
+ * *n_points and keeps the points resident (vc_export_points reads them). */
+vc_status vc_stage_preprocess(vc_ctx* ctx, const vc_sensor* sensors, const vc_view* views, int32_t k,
+                              const vc_recon_config* config, int64_t* n_points, vc_grid_spec* grid);
+/* reconstruct.cpp:16-35 with dims given (r-mode callers pass 2^r,2^(r+1),2^r). */
+vc_status vc_fit_grid(const double lo[3], const double hi[3], const int32_t dims[3], int32_t padding_voxels,
+                      vc_grid_spec* out);
+/* splat.cpp:33-89 (+ the negation of reconstruct.cpp:71 when negate != 0):
+ * field 3N floats (x,y,z interleaved per voxel), density N floats in the
+ * reference's units (d = sum g(dist;sigma2) W; simple mode: sample count). */
+vc_status vc_stage_splat(vc_ctx* ctx, const double* pos, const double* nrm, const double* weight, int64_t n,
+                         const vc_grid_spec* grid, int32_t mode, int32_t negate, float* field, float* density);
+/* integrate.cpp:19-74: field 3N floats (interleaved) -> A N floats. */
+vc_status vc_stage_integrate(vc_ctx* ctx, const float* field, int32_t nx, int32_t ny, int32_t nz, float* A);
+/* splat.cpp:91-101: mean trilinear A (fp32 volume) at the points. */
+vc_status vc_stage_iso_level(vc_ctx* ctx, const float* A, const vc_grid_spec* grid, const double* pos, int64_t n,
+                             double* level);
+/* marching_cubes.cpp:131-210 on an fp32 volume at a double level.  Vertices
+ * are numbered by global edge id ((z*ny+y)*nx+x)*3+axis (ascending);
+ * triangles are in the reference's cell-scan order.  Outputs are
+ * context-owned host arrays valid until the next call. */
+vc_status vc_stage_marching_cubes(vc_ctx* ctx, const float* A, const vc_grid_spec* grid, double level,
+                                  int32_t* n_vertices, int32_t* n_triangles, const double** positions,
+                                  const float** normals, const int32_t** triangles, const uint64_t** edge_ids);
+/* texture.cpp:11-72 + blend for given vertices (3V doubles) and views;
+ * weight_maps: k*h*w floats (the clouds' confidence maps). */
+vc_status vc_stage_texture(vc_ctx* ctx, const vc_sensor* sensors, const vc_view* views, const float* weight_maps,
+                           int32_t k, const double* vertices, int32_t n_vertices, double eps_vis_mm,
+                           uint8_t* visible, float* uv, float* weight, uint8_t* untextured, uint8_t* rgb);
+
+/* ------------------------------------------------------- synthetic capture
+ * The reference's synthetic fixture (synth/capsule.cpp, scene.cpp,
+ * render.cpp), rendered on the GPU.  Body layout: 15 joints (xyz), 14 radii,
+ * 14 RGB8 bone colours (capsule.hpp:25-34). */
+typedef struct vc_body {
+  double joints[45];
+  double radii[14];
+  uint8_t colors[42];
+} vc_body;
+
+vc_status vc_synth_circle_rig(int32_t recon, int32_t held_out, double radius_mm, double target_height_mm,
+                              int32_t width, int32_t height, double focal_px, vc_sensor* out);
+vc_status vc_synth_xpose_body(vc_body* out);
+vc_status vc_synth_kick_body(int32_t frames, int32_t frame, vc_body* out);
+/* render.cpp:23-80: depth (w*h uint16), mask (w*h uint8), rgb (rgb_w*rgb_h*3);
+ * dst_kind selects host or device destinations.  Depth noise (sigma > 0)
+ * follows render.cpp:50-61 (std::mt19937_64 + normal_distribution, host). */
+vc_status vc_synth_render(vc_ctx* ctx, const vc_sensor* sensor, const vc_body* body, double depth_sigma_mm_at_2m,
+                          uint64_t seed, double gain, int32_t camera, int32_t frame, uint16_t* depth, uint8_t* mask,
+                          uint8_t* rgb, int32_t dst_kind);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* VC_VC_H_ */

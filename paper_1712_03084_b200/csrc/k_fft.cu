@@ -1,0 +1,564 @@
+// SPDX-License-Identifier: Apache-2.0
+//
+// K4-K8 — spectral Poisson integration (integrate.cpp:19-74) as five
+// HBM-streaming radix kernels on sm_100a (fp32 complex, shared-memory
+// exchange, warp shuffles; tensor cores unused: ~3 flop/byte).
+//
+//   F-x  acc(float4 U',d') -> V = -s*U'/d' (splat.cpp:83-87 + negation,
+//        reconstruct.cpp:71) -> R2C along x for the 3 components (two real
+//        sequences per complex FFT) -> S0 = wx*X, S1 = Y, S2 = Z   [kx half]
+//   F-y  C2C along y of S0,S1,S2 -> S0 = D = FFT(wx X) + wy FFT(Y), S1 = Z
+//        (the divergence is formed before z: 2 components instead of 3)
+//   Z    C2C along z of D and Z, filter -j(D + wz Z)/|w|^2 with DC = 0
+//        (integrate.cpp:46-60), inverse C2C along z -> S0           [in place]
+//   I-y  inverse C2C along y of S0                                  [in place]
+//   I-x  C2R along x (numpy irfftn / FFTW c2r semantics: Re() of bins 0 and
+//        nx/2), scale 1/N (integrate.cpp:70-72) -> A (fp32)
+//
+// Spectra are [comp][z][y][kx] with kx pitch H = roundup4(nx/2+1) complex
+// (sector-aligned 128 B column chunks).  Every line FFT is a "four-step"
+// n = R1*R2 transform: a team of R2 threads each holding R1 elements; step 1
+// = R1/R2 register DFTs of length R2 per thread + twiddle W_n^(j1 k2), one
+// shared-memory exchange, step 2 = one register DFT of length R1.
+#include <cmath>
+#include <vector>
+
+#include "vc_shared.hpp"
+
+namespace vc {
+namespace {
+
+__constant__ float2 c_w32[32];  // W_32^k = exp(-2 pi i k / 32)
+
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ float2 cmul(float2 a, float2 b) {
+  return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+__device__ __forceinline__ float2 cmulc(float2 a, float2 b) {  // a * conj(b)
+  return make_float2(a.x * b.x + a.y * b.y, a.y * b.x - a.x * b.y);
+}
+
+__host__ __device__ constexpr int ilog2(int n) { return n <= 1 ? 0 : 1 + ilog2(n >> 1); }
+__host__ __device__ constexpr int bitrev(int i, int bits) {
+  int r = 0;
+  for (int b = 0; b < bits; ++b)
+    if (i & (1 << b)) r |= 1 << (bits - 1 - b);
+  return r;
+}
+
+template <int N>
+struct Shape {
+  static constexpr int LOG = ilog2(N);
+  static constexpr int R2 = 1 << (LOG / 2);   // threads per team
+  static constexpr int R1 = N / R2;           // elements per thread (R1 = R2 or 2*R2)
+  static constexpr int Q = R1 / R2;
+  static_assert(R1 * R2 == N && (Q == 1 || Q == 2), "power of two");
+};
+
+// In-register DFT of length M (<= 32), natural order in and out.
+template <int M, bool INV>
+__device__ __forceinline__ void dft_reg(float2* v) {
+  constexpr int LOG = ilog2(M);
+#pragma unroll
+  for (int i = 0; i < M; ++i) {
+    const int r = bitrev(i, LOG);
+    if (i < r) {
+      const float2 t = v[i];
+      v[i] = v[r];
+      v[r] = t;
+    }
+  }
+#pragma unroll
+  for (int half = 1; half < M; half <<= 1) {
+#pragma unroll
+    for (int i = 0; i < M; i += 2 * half) {
+#pragma unroll
+      for (int j = 0; j < half; ++j) {
+        const float2 a = v[i + j], b = v[i + j + half];
+        const int widx = j * (16 / half);  // W_{2 half}^j = W_32^(j*32/(2 half))
+        float2 t;
+        if (widx == 0) {
+          t = b;
+        } else if (widx == 8) {
+          t = INV ? make_float2(-b.y, b.x) : make_float2(b.y, -b.x);
+        } else {
+          const float2 w = c_w32[widx];
+          t = INV ? cmulc(b, w) : cmul(b, w);
+        }
+        v[i + j] = cadd(a, t);
+        v[i + j + half] = csub(a, t);
+      }
+    }
+  }
+}
+
+// Four-step line FFT.  In:  v[q*R2 + j2] = x[t + R2*q + R1*j2]
+//                      Out: v[k1]        = X[t + R2*k1]
+// EX::st(j1, k2, val), EX::ld(j1, k2), EX::sync() address the exchange.
+template <int N, bool INV, class EX>
+__device__ __forceinline__ void fft_line(float2* v, int t, const float2* __restrict__ tw, EX& ex) {
+  using S = Shape<N>;
+#pragma unroll
+  for (int q = 0; q < S::Q; ++q) {
+    dft_reg<S::R2, INV>(v + q * S::R2);
+    const int j1 = t + S::R2 * q;
+#pragma unroll
+    for (int k2 = 1; k2 < S::R2; ++k2) {
+      const float2 w = __ldg(tw + j1 * k2);
+      v[q * S::R2 + k2] = INV ? cmulc(v[q * S::R2 + k2], w) : cmul(v[q * S::R2 + k2], w);
+    }
+#pragma unroll
+    for (int k2 = 0; k2 < S::R2; ++k2) ex.st(j1, k2, v[q * S::R2 + k2]);
+  }
+  ex.sync();
+#pragma unroll
+  for (int j1 = 0; j1 < S::R1; ++j1) v[j1] = ex.ld(j1, t);
+  ex.sync();
+  dft_reg<S::R1, INV>(v);
+}
+
+// Forward-output layout (v[k1] = X[t + R2 k1]) -> inverse-input layout
+// (v[q*R2 + j2] = X[t + R2 q + R1 j2]), i.e. k1 = q + Q*j2.
+template <int N>
+__device__ __forceinline__ void relayout_for_inverse(float2* v) {
+  using S = Shape<N>;
+  if constexpr (S::Q == 2) {
+    float2 tmp[S::R1];
+#pragma unroll
+    for (int i = 0; i < S::R1; ++i) tmp[i] = v[i];
+#pragma unroll
+    for (int q = 0; q < 2; ++q)
+#pragma unroll
+      for (int j2 = 0; j2 < S::R2; ++j2) v[q * S::R2 + j2] = tmp[q + 2 * j2];
+  }
+}
+
+// Exchange for teams of consecutive lanes (x passes): per-team padded tile.
+template <int N>
+struct ExTeam {
+  float2* buf;  // R1 x (R2 + 1)
+  __device__ void st(int j1, int k2, float2 v) { buf[j1 * (Shape<N>::R2 + 1) + k2] = v; }
+  __device__ float2 ld(int j1, int k2) { return buf[j1 * (Shape<N>::R2 + 1) + k2]; }
+  __device__ void sync() { __syncthreads(); }
+};
+// Exchange for column tiles (y/z passes): column index innermost.
+template <int N, int CW>
+struct ExCols {
+  float2* buf;  // (R1*R2) x CW
+  int c;
+  __device__ void st(int j1, int k2, float2 v) { buf[(j1 * Shape<N>::R2 + k2) * CW + c] = v; }
+  __device__ float2 ld(int j1, int k2) { return buf[(j1 * Shape<N>::R2 + k2) * CW + c]; }
+  __device__ void sync() { __syncthreads(); }
+};
+
+__device__ __forceinline__ float signed_freq(int i, int n) {  // integrate.cpp:37-40
+  const int m = i <= n / 2 ? i : i - n;
+  return (float)(2.0 * 3.14159265358979323846 * (double)m / (double)n);
+}
+
+// x passes: TEAMS teams of T lanes; keep the exchange tiles under ~48 KB.
+template <int N>
+struct XCfg {
+  static constexpr int T = Shape<N>::R2;
+  static constexpr int TILE = Shape<N>::R1 * (T + 1);  // float2 per team
+  static constexpr int T0 = 256 / T;
+  static constexpr int TEAMS = (T0 * TILE * 8 <= 48 * 1024) ? T0 : (T0 / 2 * TILE * 8 <= 48 * 1024 ? T0 / 2 : T0 / 4);
+  static constexpr int THREADS = T * TEAMS;
+  static constexpr int SMEM = TEAMS * TILE * 8;
+};
+// y/z passes: CW columns per tile (16 x 8 B = 128 B; 8 for long lines).
+template <int N>
+struct CCfg {
+  static constexpr int CW = N >= 512 ? 8 : 16;
+  static constexpr int THREADS = CW * Shape<N>::R2;
+  static constexpr int SMEM = N * CW * 8;
+};
+
+// ------------------------------------------------------------------ F-x
+template <int NX>
+__global__ void __launch_bounds__(XCfg<NX>::THREADS, 2) fx_kernel(const float4* __restrict__ acc, float2* __restrict__ S0,
+                                                       float2* __restrict__ S1, float2* __restrict__ S2, int rows,
+                                                       int H, size_t cstride, int mode,
+                                                       const float2* __restrict__ tw) {
+  using S = Shape<NX>;
+  constexpr int T = S::R2, R1 = S::R1, TEAMS = XCfg<NX>::TEAMS;
+  extern __shared__ float2 dyn_smem[];
+  const int team = threadIdx.x / T, t = threadIdx.x % T;
+  const int lane = threadIdx.x & 31, team_lane0 = lane - t;
+  ExTeam<NX> ex{dyn_smem + team * XCfg<NX>::TILE};
+  const int pair = blockIdx.x * TEAMS + team;
+  const int l0 = 2 * pair, l1 = l0 + 1;
+  const bool live = l1 < rows;
+
+  auto load_line = [&](int l, float2* xy, float* zc) {
+#pragma unroll
+    for (int q = 0; q < S::Q; ++q)
+#pragma unroll
+      for (int j2 = 0; j2 < T; ++j2) {
+        const int j = t + T * q + R1 * j2;
+        float4 a = live ? __ldcs(acc + (size_t)l * NX + j) : make_float4(0.f, 0.f, 0.f, 0.f);
+        float s = 0.f;
+        if (mode == 0) {
+          if (a.w >= 1e-6f) s = -1.2247448713915890f / a.w;  // -sqrt(1.5)/d'
+        } else {
+          if (a.w > 0.f) s = -1.f / a.w;
+        }
+        xy[q * T + j2] = make_float2(a.x * s, a.y * s);
+        zc[q * T + j2] = a.z * s;
+      }
+  };
+  // Split C = FFT(a + i b) into A = FFT(a), B = FFT(b) for this thread's bins
+  // k = t + T*k1 (partner bin n-k lives in lane T-t, element R1-1-k1).
+  auto split_store = [&](float2* v, float2* outA, size_t offA, float2* outB, size_t offB, bool scale_wx) {
+    const int src = team_lane0 + ((T - t) & (T - 1));
+#pragma unroll
+    for (int k1 = 0; k1 <= R1 / 2; ++k1) {
+      const float2 pv = make_float2(__shfl_sync(0xffffffffu, v[R1 - 1 - k1].x, src),
+                                    __shfl_sync(0xffffffffu, v[R1 - 1 - k1].y, src));
+      const float2 own = v[(R1 - k1) & (R1 - 1)];
+      const float2 e = t == 0 ? own : pv;  // C[n-k]
+      const float2 d = v[k1];
+      const int k = t + T * k1;
+      if (k1 < R1 / 2 || t == 0) {
+        float2 A = make_float2(0.5f * (d.x + e.x), 0.5f * (d.y - e.y));  // (d + conj e)/2
+        const float2 B = make_float2(0.5f * (d.y + e.y), -0.5f * (d.x - e.x));  // (d - conj e)/(2i)
+        if (scale_wx) {
+          const float wx = (float)(2.0 * 3.14159265358979323846 * (double)k / (double)NX);
+          A.x *= wx, A.y *= wx;
+        }
+        if (live) {
+          __stcs(outA + offA + k, A);
+          __stcs(outB + offB + k, B);
+        }
+      }
+    }
+  };
+
+  float2 v[R1];
+  float z0[R1];
+  load_line(l0, v, z0);
+  fft_line<NX, false>(v, t, tw, ex);
+  split_store(v, S0, (size_t)l0 * H, S1, (size_t)l0 * H, true);
+  float z1[R1];
+  load_line(l1, v, z1);
+  fft_line<NX, false>(v, t, tw, ex);
+  split_store(v, S0, (size_t)l1 * H, S1, (size_t)l1 * H, true);
+#pragma unroll
+  for (int i = 0; i < R1; ++i) v[i] = make_float2(z0[i], z1[i]);
+  fft_line<NX, false>(v, t, tw, ex);
+  split_store(v, S2, (size_t)l0 * H, S2, (size_t)l1 * H, false);
+  (void)cstride;
+}
+
+// ------------------------------------------------------------------ F-y
+template <int NY>
+__global__ void __launch_bounds__(CCfg<NY>::THREADS, 2) fy_kernel(float2* __restrict__ S0, float2* __restrict__ S1,
+                                                                 const float2* __restrict__ S2, int nxh, int H,
+                                                                 const float2* __restrict__ tw) {
+  using S = Shape<NY>;
+  constexpr int T = S::R2, R1 = S::R1, kCW = CCfg<NY>::CW;
+  extern __shared__ float2 sh[];
+  const int c = threadIdx.x % kCW, t = threadIdx.x / kCW;
+  const int kx = blockIdx.x * kCW + c;
+  const bool live = kx < nxh;
+  const size_t plane = (size_t)blockIdx.y * NY * H;
+  ExCols<NY, kCW> ex{sh, c};
+  auto load = [&](const float2* src, float2* v) {
+#pragma unroll
+    for (int q = 0; q < S::Q; ++q)
+#pragma unroll
+      for (int j2 = 0; j2 < T; ++j2) {
+        const int j = t + T * q + R1 * j2;
+        v[q * T + j2] = live ? __ldcs(src + plane + (size_t)j * H + kx) : make_float2(0.f, 0.f);
+      }
+  };
+  float2 d[R1], v[R1];
+  load(S0, d);
+  fft_line<NY, false>(d, t, tw, ex);
+  load(S1, v);
+  fft_line<NY, false>(v, t, tw, ex);
+#pragma unroll
+  for (int k1 = 0; k1 < R1; ++k1) {
+    const float wy = signed_freq(t + T * k1, NY);
+    d[k1] = make_float2(d[k1].x + wy * v[k1].x, d[k1].y + wy * v[k1].y);
+  }
+  load(S2, v);
+  fft_line<NY, false>(v, t, tw, ex);
+  if (live) {
+#pragma unroll
+    for (int k1 = 0; k1 < R1; ++k1) {
+      const size_t o = plane + (size_t)(t + T * k1) * H + kx;
+      __stcs(S0 + o, d[k1]);
+      __stcs(S1 + o, v[k1]);
+    }
+  }
+}
+
+// ------------------------------------------------------------------ Z (fused)
+template <int NZ>
+__global__ void __launch_bounds__(CCfg<NZ>::THREADS, 2) z_kernel(float2* __restrict__ S0,
+                                                                const float2* __restrict__ S1, int nx, int ny,
+                                                                int H, const float2* __restrict__ tw) {
+  using S = Shape<NZ>;
+  constexpr int T = S::R2, R1 = S::R1, kCW = CCfg<NZ>::CW;
+  extern __shared__ float2 sh[];
+  const int c = threadIdx.x % kCW, t = threadIdx.x / kCW;
+  const int kx = blockIdx.x * kCW + c;
+  const int ky = blockIdx.y;
+  const bool live = kx <= nx / 2;
+  const size_t zstride = (size_t)ny * H;
+  const size_t base = (size_t)ky * H + kx;
+  ExCols<NZ, kCW> ex{sh, c};
+  auto load = [&](const float2* src, float2* v) {
+#pragma unroll
+    for (int q = 0; q < S::Q; ++q)
+#pragma unroll
+      for (int j2 = 0; j2 < T; ++j2) {
+        const int j = t + T * q + R1 * j2;
+        v[q * T + j2] = live ? __ldcs(src + base + (size_t)j * zstride) : make_float2(0.f, 0.f);
+      }
+  };
+  float2 d[R1], z[R1];
+  load(S0, d);
+  fft_line<NZ, false>(d, t, tw, ex);
+  load(S1, z);
+  fft_line<NZ, false>(z, t, tw, ex);
+  const float wx = signed_freq(kx, nx), wy = signed_freq(ky, ny);
+  const float wxy = wx * wx + wy * wy;
+#pragma unroll
+  for (int k1 = 0; k1 < R1; ++k1) {
+    const int kz = t + T * k1;
+    const float wz = signed_freq(kz, NZ);
+    const float w2 = wxy + wz * wz;
+    const float2 s = make_float2(d[k1].x + wz * z[k1].x, d[k1].y + wz * z[k1].y);
+    const float inv = (kx == 0 && ky == 0 && kz == 0) ? 0.f : 1.f / w2;
+    d[k1] = make_float2(s.y * inv, -s.x * inv);  // (-i/|w|^2) * s
+  }
+  relayout_for_inverse<NZ>(d);
+  fft_line<NZ, true>(d, t, tw, ex);
+  if (live) {
+#pragma unroll
+    for (int k1 = 0; k1 < R1; ++k1) __stcs(S0 + base + (size_t)(t + T * k1) * zstride, d[k1]);
+  }
+}
+
+// ------------------------------------------------------------------ I-y
+template <int NY>
+__global__ void __launch_bounds__(CCfg<NY>::THREADS, 2) iy_kernel(float2* __restrict__ S0, int nxh, int H,
+                                                                 const float2* __restrict__ tw) {
+  using S = Shape<NY>;
+  constexpr int T = S::R2, R1 = S::R1, kCW = CCfg<NY>::CW;
+  extern __shared__ float2 sh[];
+  const int c = threadIdx.x % kCW, t = threadIdx.x / kCW;
+  const int kx = blockIdx.x * kCW + c;
+  const bool live = kx < nxh;
+  const size_t plane = (size_t)blockIdx.y * NY * H;
+  ExCols<NY, kCW> ex{sh, c};
+  float2 v[R1];
+#pragma unroll
+  for (int q = 0; q < S::Q; ++q)
+#pragma unroll
+    for (int j2 = 0; j2 < T; ++j2) {
+      const int j = t + T * q + R1 * j2;
+      v[q * T + j2] = live ? __ldcs(S0 + plane + (size_t)j * H + kx) : make_float2(0.f, 0.f);
+    }
+  fft_line<NY, true>(v, t, tw, ex);
+  if (live) {
+#pragma unroll
+    for (int k1 = 0; k1 < R1; ++k1) __stcs(S0 + plane + (size_t)(t + T * k1) * H + kx, v[k1]);
+  }
+}
+
+// ------------------------------------------------------------------ I-x
+template <int NX>
+__global__ void __launch_bounds__(XCfg<NX>::THREADS, 2) ix_kernel(const float2* __restrict__ S0, float* __restrict__ A,
+                                                       int rows, int H, float scale,
+                                                       const float2* __restrict__ tw) {
+  using S = Shape<NX>;
+  constexpr int T = S::R2, R1 = S::R1, TEAMS = XCfg<NX>::TEAMS, NH = NX / 2;
+  extern __shared__ float2 dyn_smem[];
+  const int team = threadIdx.x / T, t = threadIdx.x % T;
+  float2* const tile = dyn_smem + team * XCfg<NX>::TILE;
+  ExTeam<NX> ex{tile};
+  const int pair = blockIdx.x * TEAMS + team;
+  const int l0 = 2 * pair, l1 = l0 + 1;
+  const bool live = l1 < rows;
+  float2* h0 = tile;
+  float2* h1 = tile + (NH + 1);
+  for (int k = t; k <= NH; k += T) {
+    h0[k] = live ? __ldcs(S0 + (size_t)l0 * H + k) : make_float2(0.f, 0.f);
+    h1[k] = live ? __ldcs(S0 + (size_t)l1 * H + k) : make_float2(0.f, 0.f);
+  }
+  __syncthreads();
+  // Hermitian extension with Re() of bins 0 and n/2 (numpy irfft / FFTW c2r)
+  auto full = [&](const float2* h, int j) {
+    if (j == 0) return make_float2(h[0].x, 0.f);
+    if (j == NH) return make_float2(h[NH].x, 0.f);
+    if (j < NH) return h[j];
+    const float2 c = h[NX - j];
+    return make_float2(c.x, -c.y);
+  };
+  float2 v[R1];
+#pragma unroll
+  for (int q = 0; q < S::Q; ++q)
+#pragma unroll
+    for (int j2 = 0; j2 < T; ++j2) {
+      const int j = t + T * q + R1 * j2;
+      const float2 f0 = full(h0, j), f1 = full(h1, j);
+      v[q * T + j2] = make_float2(f0.x - f1.y, f0.y + f1.x);  // F0 + i F1
+    }
+  __syncthreads();
+  fft_line<NX, true>(v, t, tw, ex);
+  if (live) {
+#pragma unroll
+    for (int k1 = 0; k1 < R1; ++k1) {
+      const int k = t + T * k1;
+      __stcs(A + (size_t)l0 * NX + k, v[k1].x * scale);
+      __stcs(A + (size_t)l1 * NX + k, v[k1].y * scale);
+    }
+  }
+}
+
+// ------------------------------------------------------------------ dispatch
+template <template <int> class F, typename... Args>
+void dispatch_n(int n, Args&&... args) {
+  switch (n) {
+    case 4: F<4>::run(args...); break;
+    case 8: F<8>::run(args...); break;
+    case 16: F<16>::run(args...); break;
+    case 32: F<32>::run(args...); break;
+    case 64: F<64>::run(args...); break;
+    case 128: F<128>::run(args...); break;
+    case 256: F<256>::run(args...); break;
+    case 512: F<512>::run(args...); break;
+    case 1024: F<1024>::run(args...); break;
+    default: break;  // validated on the host
+  }
+}
+
+struct FftArgs {
+  const float4* acc;
+  float2 *S0, *S1, *S2;
+  float* A;
+  int nx, ny, nz, H, mode;
+  const float2 *twx, *twy, *twz;
+  cudaStream_t st;
+};
+
+inline int hpitch(int nx) { return ((nx / 2 + 1) + 3) & ~3; }
+
+// Opt-in dynamic shared memory above 48 KB.  Called from prepare_integrate
+// (whenever the grid dims change), never inside a graph capture.
+template <class K>
+void allow_smem(K* kernel, int bytes) {
+  if (bytes > 48 * 1024) cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+}
+template <int N>
+struct Prep {
+  static void run(int axis) {
+    if (axis == 0) {
+      allow_smem(fx_kernel<N>, XCfg<N>::SMEM);
+      allow_smem(ix_kernel<N>, XCfg<N>::SMEM);
+    } else if (axis == 1) {
+      allow_smem(fy_kernel<N>, CCfg<N>::SMEM);
+      allow_smem(iy_kernel<N>, CCfg<N>::SMEM);
+    } else {
+      allow_smem(z_kernel<N>, CCfg<N>::SMEM);
+    }
+  }
+};
+
+template <int N>
+struct RunFx {
+  static void run(const FftArgs& a) {
+    using C = XCfg<N>;
+    const int rows = a.ny * a.nz;
+    const int grid = (rows / 2 + C::TEAMS - 1) / C::TEAMS;
+    fx_kernel<N><<<grid, C::THREADS, C::SMEM, a.st>>>(a.acc, a.S0, a.S1, a.S2, rows, a.H, 0, a.mode, a.twx);
+  }
+};
+template <int N>
+struct RunFy {
+  static void run(const FftArgs& a) {
+    using C = CCfg<N>;
+    dim3 grid((a.nx / 2 + 1 + C::CW - 1) / C::CW, a.nz);
+    fy_kernel<N><<<grid, C::THREADS, C::SMEM, a.st>>>(a.S0, a.S1, a.S2, a.nx / 2 + 1, a.H, a.twy);
+  }
+};
+template <int N>
+struct RunZ {
+  static void run(const FftArgs& a) {
+    using C = CCfg<N>;
+    dim3 grid((a.nx / 2 + 1 + C::CW - 1) / C::CW, a.ny);
+    z_kernel<N><<<grid, C::THREADS, C::SMEM, a.st>>>(a.S0, a.S1, a.nx, a.ny, a.H, a.twz);
+  }
+};
+template <int N>
+struct RunIy {
+  static void run(const FftArgs& a) {
+    using C = CCfg<N>;
+    dim3 grid((a.nx / 2 + 1 + C::CW - 1) / C::CW, a.nz);
+    iy_kernel<N><<<grid, C::THREADS, C::SMEM, a.st>>>(a.S0, a.nx / 2 + 1, a.H, a.twy);
+  }
+};
+template <int N>
+struct RunIx {
+  static void run(const FftArgs& a) {
+    using C = XCfg<N>;
+    const int rows = a.ny * a.nz;
+    const int grid = (rows / 2 + C::TEAMS - 1) / C::TEAMS;
+    const float scale = (float)(1.0 / ((double)a.nx * a.ny * a.nz));
+    ix_kernel<N><<<grid, C::THREADS, C::SMEM, a.st>>>(a.S0, a.A, rows, a.H, scale, a.twx);
+  }
+};
+
+}  // namespace
+
+void prepare_integrate(int nx, int ny, int nz) {
+  dispatch_n<Prep>(nx, 0);
+  dispatch_n<Prep>(ny, 1);
+  dispatch_n<Prep>(nz, 2);
+}
+
+size_t spectrum_elems(int nx, int ny, int nz) { return (size_t)hpitch(nx) * ny * nz; }
+size_t twiddle_elems(int nx, int ny, int nz) { return (size_t)nx + ny + nz; }
+
+void upload_twiddles(float2* dev, int nx, int ny, int nz, cudaStream_t st) {
+  static bool w32_done = false;
+  if (!w32_done) {
+    float2 w[32];
+    for (int k = 0; k < 32; ++k)
+      w[k] = make_float2((float)std::cos(-2.0 * M_PI * k / 32.0), (float)std::sin(-2.0 * M_PI * k / 32.0));
+    cudaMemcpyToSymbol(c_w32, w, sizeof(w));
+    w32_done = true;
+  }
+  std::vector<float2> h;
+  for (int n : {nx, ny, nz})
+    for (int m = 0; m < n; ++m)
+      h.push_back(make_float2((float)std::cos(-2.0 * M_PI * m / n), (float)std::sin(-2.0 * M_PI * m / n)));
+  cudaMemcpyAsync(dev, h.data(), h.size() * sizeof(float2), cudaMemcpyHostToDevice, st);
+  cudaStreamSynchronize(st);
+}
+
+void launch_integrate(const float4* acc, float2* spec, float* A, int nx, int ny, int nz, int mode,
+                      const float2* tw, cudaStream_t st, cudaEvent_t* ev) {
+  FftArgs a;
+  const size_t cs = spectrum_elems(nx, ny, nz);
+  a.acc = acc, a.S0 = spec, a.S1 = spec + cs, a.S2 = spec + 2 * cs, a.A = A;
+  a.nx = nx, a.ny = ny, a.nz = nz, a.H = hpitch(nx), a.mode = mode;
+  a.twx = tw, a.twy = tw + nx, a.twz = tw + nx + ny, a.st = st;
+  if (ev) record_event(ev[0], st);
+  dispatch_n<RunFx>(nx, a);
+  if (ev) record_event(ev[1], st);
+  dispatch_n<RunFy>(ny, a);
+  if (ev) record_event(ev[2], st);
+  dispatch_n<RunZ>(nz, a);
+  if (ev) record_event(ev[3], st);
+  dispatch_n<RunIy>(ny, a);
+  if (ev) record_event(ev[4], st);
+  dispatch_n<RunIx>(nx, a);
+  if (ev) record_event(ev[5], st);
+}
+
+}  // namespace vc

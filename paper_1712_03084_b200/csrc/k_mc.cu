@@ -1,0 +1,340 @@
+// SPDX-License-Identifier: Apache-2.0
+//
+// K9 — iso level (splat.cpp:91-101 with sample_trilinear, volume.hpp:59-81)
+// K10 — marching cubes (marching_cubes.cpp:131-210) as classify / scan /
+// emit, with no host round trip (counts live in DevCtl; capacity overflow
+// sets a flag the host checks once per frame).
+//
+//   mc_count  one thread per voxel: owned cut edges (+x,+y,+z from the voxel,
+//             sign test vals >= level in fp64, marching_cubes.cpp:168-171)
+//             and the cell's triangle count from the generated table;
+//             per-CTA totals (vertices, triangles, active cells)
+//   mc_scan   single-CTA exclusive scan of the CTA totals
+//   mc_emit   recompute; vertex ids = rank of the cut edge in global edge id
+//             order ((z*ny+y)*nx+x)*3+axis (marching_cubes.cpp:139-142);
+//             positions (fp64, :153-155, volume.hpp:45) and gradient normals
+//             (:180-207); compact list of active cells in scan order
+//   mc_tris   one thread per active cell: triangles in the reference's cell
+//             scan order (z, y, x), table order within the cell
+#include <cfloat>
+
+#include "vc_device.cuh"
+
+namespace vc {
+namespace {
+
+__constant__ int8_t c_mc_count[256];
+__constant__ int8_t c_mc_tris[256][5][3];
+__constant__ int8_t c_edge_c0[12];  // low corner of each cube edge
+__constant__ int8_t c_edge_axis[12];
+
+constexpr int kMcThreads = 256;
+
+__device__ __forceinline__ float vol_at(const float* A, int nx, int ny, int x, int y, int z) {
+  return __ldg(A + ((size_t)z * ny + y) * nx + x);
+}
+
+// volume.hpp:59-81 on the fp32 volume, evaluated in fp64
+__device__ double trilinear(const float* A, const DevGrid& g, double vx, double vy, double vz) {
+  auto clampf = [](double x, double lo, double hi) { return x < lo ? lo : (x > hi ? hi : x); };
+  const double fx = clampf(vx, 0.0, g.nx - 1.0), fy = clampf(vy, 0.0, g.ny - 1.0), fz = clampf(vz, 0.0, g.nz - 1.0);
+  const int x0 = min((int)fx, g.nx - 2 >= 0 ? g.nx - 2 : 0);
+  const int y0 = min((int)fy, g.ny - 2 >= 0 ? g.ny - 2 : 0);
+  const int z0 = min((int)fz, g.nz - 2 >= 0 ? g.nz - 2 : 0);
+  const int x1 = min(x0 + 1, g.nx - 1), y1 = min(y0 + 1, g.ny - 1), z1 = min(z0 + 1, g.nz - 1);
+  const double tx = dsub(fx, (double)x0), ty = dsub(fy, (double)y0), tz = dsub(fz, (double)z0);
+  const double v000 = vol_at(A, g.nx, g.ny, x0, y0, z0), v100 = vol_at(A, g.nx, g.ny, x1, y0, z0);
+  const double v010 = vol_at(A, g.nx, g.ny, x0, y1, z0), v110 = vol_at(A, g.nx, g.ny, x1, y1, z0);
+  const double v001 = vol_at(A, g.nx, g.ny, x0, y0, z1), v101 = vol_at(A, g.nx, g.ny, x1, y0, z1);
+  const double v011 = vol_at(A, g.nx, g.ny, x0, y1, z1), v111 = vol_at(A, g.nx, g.ny, x1, y1, z1);
+  const double ux = dsub(1.0, tx), uy = dsub(1.0, ty), uz = dsub(1.0, tz);
+  const double c00 = dadd(dmul(v000, ux), dmul(v100, tx));
+  const double c10 = dadd(dmul(v010, ux), dmul(v110, tx));
+  const double c01 = dadd(dmul(v001, ux), dmul(v101, tx));
+  const double c11 = dadd(dmul(v011, ux), dmul(v111, tx));
+  const double c0 = dadd(dmul(c00, uy), dmul(c10, ty));
+  const double c1 = dadd(dmul(c01, uy), dmul(c11, ty));
+  return dadd(dmul(c0, uz), dmul(c1, tz));
+}
+
+constexpr int kIsoBlocks = 296;
+
+__global__ void __launch_bounds__(256) iso_partial_kernel(const double* __restrict__ pos, const float* __restrict__ A,
+                                                          const DevCtl* __restrict__ ctl, double* partial) {
+  __shared__ double sh[256];
+  double sum = 0.0;
+  if (ctl->status == 0) {
+    const DevGrid g = ctl->grid;
+    const int P = ctl->P;
+    for (int p = blockIdx.x * 256 + threadIdx.x; p < P; p += gridDim.x * 256) {
+      const double vx = ddiv(dsub(pos[3 * p + 0], g.origin[0]), g.edge);
+      const double vy = ddiv(dsub(pos[3 * p + 1], g.origin[1]), g.edge);
+      const double vz = ddiv(dsub(pos[3 * p + 2], g.origin[2]), g.edge);
+      sum = dadd(sum, trilinear(A, g, vx, vy, vz));
+    }
+  }
+  sh[threadIdx.x] = sum;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if (threadIdx.x < o) sh[threadIdx.x] = dadd(sh[threadIdx.x], sh[threadIdx.x + o]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) partial[blockIdx.x] = sh[0];
+}
+
+__global__ void iso_final_kernel(const double* partial, int n, DevCtl* ctl) {
+  __shared__ double sh[512];
+  sh[threadIdx.x] = threadIdx.x < n ? partial[threadIdx.x] : 0.0;
+  __syncthreads();
+  for (int o = 256; o > 0; o >>= 1) {
+    if (threadIdx.x < o) sh[threadIdx.x] = dadd(sh[threadIdx.x], sh[threadIdx.x + o]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0 && ctl->status == 0) ctl->level = ddiv(sh[0], (double)ctl->P);
+}
+
+struct VoxelInfo {
+  int mask;  // cut edges owned by this voxel (bit axis)
+  int cfg;   // cell case, -1 if no cell
+};
+
+__device__ __forceinline__ VoxelInfo classify(const float* A, int nx, int ny, int nz, size_t v, double L) {
+  const int x = (int)(v % nx), y = (int)((v / nx) % ny), z = (int)(v / ((size_t)nx * ny));
+  const size_t plane = (size_t)nx * ny;
+  const bool a0 = (double)__ldg(A + v) >= L;
+  VoxelInfo r{0, -1};
+  if (x + 1 < nx && (((double)__ldg(A + v + 1) >= L) != a0)) r.mask |= 1;
+  if (y + 1 < ny && (((double)__ldg(A + v + nx) >= L) != a0)) r.mask |= 2;
+  if (z + 1 < nz && (((double)__ldg(A + v + plane) >= L) != a0)) r.mask |= 4;
+  if (x + 1 < nx && y + 1 < ny && z + 1 < nz) {
+    int cfg = a0 ? 1 : 0;
+    cfg |= ((double)__ldg(A + v + 1) >= L) << 1;
+    cfg |= ((double)__ldg(A + v + nx) >= L) << 2;
+    cfg |= ((double)__ldg(A + v + nx + 1) >= L) << 3;
+    cfg |= ((double)__ldg(A + v + plane) >= L) << 4;
+    cfg |= ((double)__ldg(A + v + plane + 1) >= L) << 5;
+    cfg |= ((double)__ldg(A + v + plane + nx) >= L) << 6;
+    cfg |= ((double)__ldg(A + v + plane + nx + 1) >= L) << 7;
+    r.cfg = cfg;
+  }
+  return r;
+}
+
+__device__ __forceinline__ int3 block_exclusive_scan3(int3 v, int3* total) {
+  __shared__ int3 warp_tot[kMcThreads / 32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  int3 inc = v;
+  for (int o = 1; o < 32; o <<= 1) {
+    const int a = __shfl_up_sync(0xffffffffu, inc.x, o), b = __shfl_up_sync(0xffffffffu, inc.y, o),
+              c = __shfl_up_sync(0xffffffffu, inc.z, o);
+    if (lane >= o) inc.x += a, inc.y += b, inc.z += c;
+  }
+  if (lane == 31) warp_tot[wid] = inc;
+  __syncthreads();
+  int3 pre = make_int3(0, 0, 0), tot = make_int3(0, 0, 0);
+  for (int i = 0; i < kMcThreads / 32; ++i) {
+    if (i < wid) pre.x += warp_tot[i].x, pre.y += warp_tot[i].y, pre.z += warp_tot[i].z;
+    tot.x += warp_tot[i].x, tot.y += warp_tot[i].y, tot.z += warp_tot[i].z;
+  }
+  __syncthreads();
+  *total = tot;
+  return make_int3(pre.x + inc.x - v.x, pre.y + inc.y - v.y, pre.z + inc.z - v.z);
+}
+
+__global__ void __launch_bounds__(kMcThreads) mc_count_kernel(const float* __restrict__ A, const DevCtl* ctl, int nx,
+                                                              int ny, int nz, int3* blk) {
+  const size_t N = (size_t)nx * ny * nz;
+  const size_t v = (size_t)blockIdx.x * kMcThreads + threadIdx.x;
+  int3 c = make_int3(0, 0, 0);
+  if (v < N && ctl->status == 0) {
+    const VoxelInfo vi = classify(A, nx, ny, nz, v, ctl->level);
+    const int nt = vi.cfg >= 0 ? c_mc_count[vi.cfg] : 0;
+    c = make_int3(__popc(vi.mask), nt, nt > 0 ? 1 : 0);
+  }
+  int3 tot;
+  block_exclusive_scan3(c, &tot);
+  if (threadIdx.x == 0) blk[blockIdx.x] = tot;
+}
+
+__global__ void __launch_bounds__(1024) mc_scan_kernel(int3* blk, int n, DevCtl* ctl, int v_cap, int t_cap,
+                                                       int c_cap) {
+  __shared__ int3 warp_sums[32];
+  __shared__ int3 carry;
+  if (threadIdx.x == 0) carry = make_int3(0, 0, 0);
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int base = 0; base < n; base += 1024) {
+    const int i = base + threadIdx.x;
+    const int3 v = i < n ? blk[i] : make_int3(0, 0, 0);
+    int3 inc = v;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int a = __shfl_up_sync(0xffffffffu, inc.x, o), b = __shfl_up_sync(0xffffffffu, inc.y, o),
+                c = __shfl_up_sync(0xffffffffu, inc.z, o);
+      if (lane >= o) inc.x += a, inc.y += b, inc.z += c;
+    }
+    if (lane == 31) warp_sums[wid] = inc;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      int3 ws = warp_sums[threadIdx.x];
+      for (int o = 1; o < 32; o <<= 1) {
+        const int a = __shfl_up_sync(0xffffffffu, ws.x, o), b = __shfl_up_sync(0xffffffffu, ws.y, o),
+                  c = __shfl_up_sync(0xffffffffu, ws.z, o);
+        if (threadIdx.x >= o) ws.x += a, ws.y += b, ws.z += c;
+      }
+      warp_sums[threadIdx.x] = ws;
+    }
+    __syncthreads();
+    const int3 wp = wid ? warp_sums[wid - 1] : make_int3(0, 0, 0);
+    const int3 cr = carry;
+    if (i < n) blk[i] = make_int3(cr.x + wp.x + inc.x - v.x, cr.y + wp.y + inc.y - v.y, cr.z + wp.z + inc.z - v.z);
+    __syncthreads();
+    if (threadIdx.x == 1023) carry = make_int3(cr.x + wp.x + inc.x, cr.y + wp.y + inc.y, cr.z + wp.z + inc.z);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    const int3 t = carry;
+    ctl->V = t.x, ctl->T = t.y, ctl->C = t.z;
+    ctl->overflow = (t.x > v_cap || t.y > t_cap || t.z > c_cap) ? 1 : 0;
+  }
+}
+
+// marching_cubes.cpp:178-207: outward normal = -normalize(trilinear blend of
+// central-difference gradients at the 8 surrounding nodes, clamped borders)
+__device__ void vertex_normal(const float* A, int nx, int ny, int nz, double px, double py, double pz, float* out) {
+  auto val = [&](int x, int y, int z) {
+    x = x < 0 ? 0 : (x > nx - 1 ? nx - 1 : x);
+    y = y < 0 ? 0 : (y > ny - 1 ? ny - 1 : y);
+    z = z < 0 ? 0 : (z > nz - 1 ? nz - 1 : z);
+    return (double)vol_at(A, nx, ny, x, y, z);
+  };
+  const int x0 = max(0, min((int)px, nx - 2)), y0 = max(0, min((int)py, ny - 2)), z0 = max(0, min((int)pz, nz - 2));
+  const double tx = dsub(px, (double)x0), ty = dsub(py, (double)y0), tz = dsub(pz, (double)z0);
+  double gx = 0, gy = 0, gz = 0;
+#pragma unroll
+  for (int dz = 0; dz <= 1; ++dz)
+#pragma unroll
+    for (int dy = 0; dy <= 1; ++dy)
+#pragma unroll
+      for (int dx = 0; dx <= 1; ++dx) {
+        const double w = dmul(dmul(dx ? tx : dsub(1.0, tx), dy ? ty : dsub(1.0, ty)), dz ? tz : dsub(1.0, tz));
+        if (w > 0) {
+          const int x = x0 + dx, y = y0 + dy, z = z0 + dz;
+          const double g0 = dmul(dsub(val(x + 1, y, z), val(x - 1, y, z)), 0.5);
+          const double g1 = dmul(dsub(val(x, y + 1, z), val(x, y - 1, z)), 0.5);
+          const double g2 = dmul(dsub(val(x, y, z + 1), val(x, y, z - 1)), 0.5);
+          gx = dadd(gx, dmul(w, g0)), gy = dadd(gy, dmul(w, g1)), gz = dadd(gz, dmul(w, g2));
+        }
+      }
+  const double len = norm3(mk3(gx, gy, gz));
+  if (len > 1e-12) {
+    out[0] = (float)ddiv(-gx, len), out[1] = (float)ddiv(-gy, len), out[2] = (float)ddiv(-gz, len);
+  } else {
+    out[0] = 0.f, out[1] = 0.f, out[2] = 1.f;
+  }
+}
+
+__global__ void __launch_bounds__(kMcThreads) mc_emit_kernel(const float* __restrict__ A, const DevCtl* ctl, int nx,
+                                                             int ny, int nz, const int3* __restrict__ blk,
+                                                             MeshBufs mb) {
+  const size_t N = (size_t)nx * ny * nz;
+  const size_t v = (size_t)blockIdx.x * kMcThreads + threadIdx.x;
+  const bool ok = ctl->status == 0;
+  const double L = ctl->level;
+  VoxelInfo vi{0, -1};
+  int nt = 0;
+  if (v < N && ok) {
+    vi = classify(A, nx, ny, nz, v, L);
+    nt = vi.cfg >= 0 ? c_mc_count[vi.cfg] : 0;
+  }
+  int3 tot;
+  const int3 ex = block_exclusive_scan3(make_int3(__popc(vi.mask), nt, nt > 0 ? 1 : 0), &tot);
+  const int3 b = blk[blockIdx.x];
+  const int vb = b.x + ex.x, tb = b.y + ex.y, cb = b.z + ex.z;
+  if (vi.mask) {
+    if (vb + __popc(vi.mask) <= mb.v_cap) {
+      mb.vbase[v] = ((uint32_t)vb << 3) | (uint32_t)vi.mask;
+      const DevGrid g = ctl->grid;
+      const int x = (int)(v % nx), y = (int)((v / nx) % ny), z = (int)(v / ((size_t)nx * ny));
+      const double v0 = (double)__ldg(A + v);
+      const size_t step[3] = {1, (size_t)nx, (size_t)nx * ny};
+      int id = vb;
+      for (int a = 0; a < 3; ++a) {
+        if (!(vi.mask & (1 << a))) continue;
+        const double v1 = (double)__ldg(A + v + step[a]);
+        double t = ddiv(dsub(L, v0), dsub(v1, v0));
+        t = t < 1e-6 ? 1e-6 : (t > 1.0 - 1e-6 ? 1.0 - 1e-6 : t);
+        double p[3] = {(double)x, (double)y, (double)z};
+        p[a] = dadd(p[a], t);
+        for (int c = 0; c < 3; ++c) mb.pos[3 * (size_t)id + c] = dadd(g.origin[c], dmul(g.edge, p[c]));
+        vertex_normal(A, nx, ny, nz, p[0], p[1], p[2], mb.nrm + 3 * (size_t)id);
+        mb.edge_id[id] = (uint64_t)v * 3 + a;
+        ++id;
+      }
+    }
+  }
+  if (nt > 0 && cb < mb.c_cap) {
+    mb.cells[cb] = (int32_t)v;
+    mb.cell_tri[cb] = tb;
+  }
+}
+
+__global__ void __launch_bounds__(256) mc_tris_kernel(const float* __restrict__ A, const DevCtl* ctl, int nx, int ny,
+                                                      int nz, MeshBufs mb) {
+  if (ctl->status != 0 || ctl->overflow) return;
+  const int C = ctl->C;
+  const double L = ctl->level;
+  const size_t plane = (size_t)nx * ny;
+  for (int i = blockIdx.x * 256 + threadIdx.x; i < C; i += gridDim.x * 256) {
+    const size_t v = (size_t)mb.cells[i];
+    const int tb = mb.cell_tri[i];
+    const VoxelInfo vi = classify(A, nx, ny, nz, v, L);
+    const int n = c_mc_count[vi.cfg];
+    for (int tri = 0; tri < n; ++tri) {
+      int ids[3];
+      for (int m = 0; m < 3; ++m) {
+        const int e = c_mc_tris[vi.cfg][tri][m];
+        const int c0 = c_edge_c0[e], axis = c_edge_axis[e];
+        const size_t owner = v + (c0 & 1) + ((c0 >> 1) & 1) * (size_t)nx + ((c0 >> 2) & 1) * plane;
+        const uint32_t pk = mb.vbase[owner];
+        ids[m] = (int)(pk >> 3) + __popc(pk & 7u & ((1u << axis) - 1u));
+      }
+      int32_t* o = mb.tri + 3 * (size_t)(tb + tri);
+      o[0] = ids[0], o[1] = ids[1], o[2] = ids[2];
+    }
+  }
+}
+
+}  // namespace
+
+void upload_case_table_data(const int8_t* counts, const int8_t* tris, cudaStream_t st) {
+  cudaMemcpyToSymbolAsync(c_mc_count, counts, 256, 0, cudaMemcpyHostToDevice, st);
+  cudaMemcpyToSymbolAsync(c_mc_tris, tris, 256 * 15, 0, cudaMemcpyHostToDevice, st);
+  const int8_t c0[12] = {0, 2, 4, 6, 0, 1, 4, 5, 0, 1, 2, 3};  // marching_cubes.cpp:15-19
+  const int8_t ax[12] = {0, 0, 0, 0, 1, 1, 1, 1, 2, 2, 2, 2};
+  cudaMemcpyToSymbolAsync(c_edge_c0, c0, 12, 0, cudaMemcpyHostToDevice, st);
+  cudaMemcpyToSymbolAsync(c_edge_axis, ax, 12, 0, cudaMemcpyHostToDevice, st);
+  cudaStreamSynchronize(st);
+}
+
+int iso_blocks() { return kIsoBlocks; }
+
+void launch_iso_level(const DevPoints& pts, const float* A, DevCtl* ctl, double* partial, int, cudaStream_t st) {
+  iso_partial_kernel<<<kIsoBlocks, 256, 0, st>>>(pts.pos, A, ctl, partial);
+  iso_final_kernel<<<1, 512, 0, st>>>(partial, kIsoBlocks, ctl);
+}
+
+int mc_blocks(int nx, int ny, int nz) {
+  const size_t N = (size_t)nx * ny * nz;
+  return (int)((N + kMcThreads - 1) / kMcThreads);
+}
+
+void launch_marching_cubes(const float* A, DevCtl* ctl, MeshBufs mb, int nx, int ny, int nz, cudaStream_t st) {
+  const int nb = mc_blocks(nx, ny, nz);
+  int3* blk = reinterpret_cast<int3*>(mb.blk);
+  mc_count_kernel<<<nb, kMcThreads, 0, st>>>(A, ctl, nx, ny, nz, blk);
+  mc_scan_kernel<<<1, 1024, 0, st>>>(blk, nb, ctl, mb.v_cap, mb.t_cap, mb.c_cap);
+  mc_emit_kernel<<<nb, kMcThreads, 0, st>>>(A, ctl, nx, ny, nz, blk, mb);
+  mc_tris_kernel<<<148 * 4, 256, 0, st>>>(A, ctl, nx, ny, nz, mb);
+}
+
+}  // namespace vc

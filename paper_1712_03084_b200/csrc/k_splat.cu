@@ -1,0 +1,123 @@
+// SPDX-License-Identifier: Apache-2.0
+//
+// K3 — oriented-point splatting on sm_100a (splat.cpp:11-89).
+//
+// The reference makes two passes (density d, then sum g1*(W/d)*N) over
+// z-slabs.  Since d(q) is final during its second pass, that equals
+//   V(q) = (sum_p g1*W*N) / d(q) = sqrt(1.5) * U'(q) / d'(q)
+// with U' = sum exp(-s/0.75)*W*N and d' = sum exp(-s/1.125)*W, s the squared
+// point-voxel distance in voxel units (sigma1^2 = 0.75 e^2, sigma2^2 =
+// 1.125 e^2), and the density threshold d >= 1e-6 g(0;sigma2) <=> d' >= 1e-6.
+// So ONE scatter pass accumulates float4 (U'x, U'y, U'z, d') per voxel with a
+// vector L2 reduction (red.global.add.v4.f32); the division, threshold and
+// the negation of reconstruct.cpp:71 are fused into the FFT's first pass.
+//
+// Binning is bit-exact: to_voxel (volume.hpp:44) and floor/lround are fp64
+// with the reference's operation order.
+#include "vc_device.cuh"
+
+namespace vc {
+namespace {
+
+constexpr int kSplatThreads = 256;
+
+__global__ void __launch_bounds__(256) clear_kernel(float4* acc, size_t n) {
+  const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+    acc[i] = z;
+}
+
+__device__ __forceinline__ void red_add_v4(float4* addr, float4 v) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(addr), "f"(v.x), "f"(v.y), "f"(v.z),
+               "f"(v.w)
+               : "memory");
+}
+
+// splat.cpp:58-87 weighted mode: 64 threads per point, one per support voxel
+// floor(c)-1 .. floor(c)+2 per axis (support_around, splat.cpp:19-29).
+__global__ void __launch_bounds__(kSplatThreads) splat_weighted_kernel(const double* __restrict__ pos,
+                                                                       const double* __restrict__ nrm,
+                                                                       const double* __restrict__ wgt,
+                                                                       const DevCtl* __restrict__ ctl,
+                                                                       float4* __restrict__ acc) {
+  const int P = ctl->P;
+  if (ctl->status != 0) return;
+  const DevGrid g = ctl->grid;
+  const int sub = threadIdx.x & 63;
+  const int ox = sub & 3, oy = (sub >> 2) & 3, oz = sub >> 4;
+  // exp(-s/0.75) = exp2(s * k1), exp(-s/1.125) = exp2(s * k2)
+  const float k1 = -1.4426950408889634f / 0.75f, k2 = -1.4426950408889634f / 1.125f;
+  for (int p = blockIdx.x * (kSplatThreads / 64) + (threadIdx.x >> 6); p < P; p += gridDim.x * (kSplatThreads / 64)) {
+    const double cx = ddiv(dsub(__ldg(pos + 3 * p + 0), g.origin[0]), g.edge);
+    const double cy = ddiv(dsub(__ldg(pos + 3 * p + 1), g.origin[1]), g.edge);
+    const double cz = ddiv(dsub(__ldg(pos + 3 * p + 2), g.origin[2]), g.edge);
+    const int x = (int)floor(cx) - 1 + ox, y = (int)floor(cy) - 1 + oy, z = (int)floor(cz) - 1 + oz;
+    if (x < 0 || y < 0 || z < 0 || x >= g.nx || y >= g.ny || z >= g.nz) continue;
+    const float dx = (float)(cx - (double)x), dy = (float)(cy - (double)y), dz = (float)(cz - (double)z);
+    const float s = dx * dx + dy * dy + dz * dz;
+    const float w = (float)__ldg(wgt + p);
+    const float g1w = exp2f(s * k1) * w, g2w = exp2f(s * k2) * w;
+    const float4 v = make_float4(g1w * (float)__ldg(nrm + 3 * p + 0), g1w * (float)__ldg(nrm + 3 * p + 1),
+                                 g1w * (float)__ldg(nrm + 3 * p + 2), g2w);
+    red_add_v4(acc + ((size_t)z * g.ny + y) * g.nx + x, v);
+  }
+}
+
+// splat.cpp:40-56 simple mode: lround nearest voxel, (sum N, count)
+__global__ void __launch_bounds__(256) splat_simple_kernel(const double* __restrict__ pos,
+                                                           const double* __restrict__ nrm,
+                                                           const DevCtl* __restrict__ ctl, float4* __restrict__ acc) {
+  const int P = ctl->P;
+  if (ctl->status != 0) return;
+  const DevGrid g = ctl->grid;
+  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < P; p += gridDim.x * blockDim.x) {
+    const double cx = ddiv(dsub(pos[3 * p + 0], g.origin[0]), g.edge);
+    const double cy = ddiv(dsub(pos[3 * p + 1], g.origin[1]), g.edge);
+    const double cz = ddiv(dsub(pos[3 * p + 2], g.origin[2]), g.edge);
+    const long long x = lround_d(cx), y = lround_d(cy), z = lround_d(cz);
+    if (!(x >= 0 && x < g.nx && y >= 0 && y < g.ny && z >= 0 && z < g.nz)) continue;
+    red_add_v4(acc + ((size_t)z * g.ny + y) * g.nx + x,
+               make_float4((float)nrm[3 * p + 0], (float)nrm[3 * p + 1], (float)nrm[3 * p + 2], 1.f));
+  }
+}
+
+// Stage API only: the reference's GradientField view of the accumulator.
+__global__ void splat_finalize_kernel(const float4* acc, size_t n, int mode, int negate, double sigma2,
+                                      float* field, float* density) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    const float4 a = acc[i];
+    float s = 0.f, d;
+    if (mode == 0) {
+      if (a.w >= 1e-6f) s = 1.2247448713915890f / a.w;
+      d = (float)((double)a.w / sigma2);
+    } else {
+      if (a.w > 0.f) s = 1.f / a.w;
+      d = a.w;
+    }
+    if (negate) s = -s;
+    field[3 * i + 0] = a.x * s;
+    field[3 * i + 1] = a.y * s;
+    field[3 * i + 2] = a.z * s;
+    density[i] = d;
+  }
+}
+
+}  // namespace
+
+void launch_clear(float4* acc, size_t n, cudaStream_t st) {
+  clear_kernel<<<148 * 8, 256, 0, st>>>(acc, n);
+}
+
+void launch_splat(const DevPoints& pts, const DevCtl* ctl, float4* acc, int mode, cudaStream_t st) {
+  if (mode == 0)
+    splat_weighted_kernel<<<148 * 8, kSplatThreads, 0, st>>>(pts.pos, pts.nrm, pts.weight, ctl, acc);
+  else
+    splat_simple_kernel<<<148 * 4, 256, 0, st>>>(pts.pos, pts.nrm, ctl, acc);
+}
+
+void launch_splat_finalize(const float4* acc, size_t n, int mode, int negate, double sigma2, float* field,
+                           float* density, cudaStream_t st) {
+  splat_finalize_kernel<<<148 * 4, 256, 0, st>>>(acc, n, mode, negate, sigma2, field, density);
+}
+
+}  // namespace vc

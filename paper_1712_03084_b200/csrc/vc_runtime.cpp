@@ -1,0 +1,947 @@
+// SPDX-License-Identifier: Apache-2.0
+//
+// Host runtime of the B200 FTR path behind the C-ABI in include/vc/vc.h:
+// context (device, stream, pooled HBM buffers, pinned staging), the frame
+// orchestration of recon::reconstruct_frame (reconstruct.cpp:37-78) +
+// vertex_visibility / assign_texture (texture.cpp:11-72) as one CUDA graph
+// with no host synchronisation until the single control-block read-back,
+// marching-cubes capacity retry, CUDA-event stage timings and the
+// per-stage entry points used by the parity tests.
+//
+// Built with -ffp-contract=off: the host-side pose algebra (Pose::inverse,
+// Pose::compose, types.hpp:46-49) must round like the reference.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <random>
+#include <string>
+#include <vector>
+
+#include "vc/vc.h"
+#include "vc_shared.hpp"
+
+namespace vc {
+void circle_rig(int recon, int held_out, double radius, double target_h, int w, int h, double f, vc_sensor* out);
+void xpose_body(vc_body* b);
+void kick_body(int frames, int f, vc_body* b);
+}  // namespace vc
+
+using namespace vc;
+
+namespace {
+
+struct Buf {
+  void* p = nullptr;
+  size_t bytes = 0;
+};
+
+struct HostBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+};
+
+constexpr int kEvents = 24;
+constexpr int kKernelGroups = 13;  // events 12..24 bracket the kernel groups
+
+}  // namespace
+
+struct vc_ctx {
+  int device = 0;
+  cudaStream_t st = nullptr;
+  std::string err;
+  int out_kind = VC_MEM_HOST;
+  bool profiling = false;
+  bool graphs = true;
+
+  // grid-dependent
+  int nx = 0, ny = 0, nz = 0;
+  Buf acc, spec, A, tw, vbase, blk;
+  // view staging + clouds
+  Buf views, pts_pos, pts_nrm, pts_w, pts_pix, wmaps, pre_scratch, iso_partial;
+  int pts_cap = 0;
+  SensorSet ss{};
+  // control block
+  DevCtl* ctl = nullptr;
+  DevCtl* ctl_h = nullptr;
+  // mesh + texture
+  Buf m_pos, m_nrm, m_tri, m_eid, m_cells, m_celltri, m_posf, t_vis, t_uv, t_w, t_untex, t_rgb;
+  int v_cap = 0, t_cap = 0, c_cap = 0;
+  // host outputs (pinned)
+  HostBuf h_posf, h_nrm, h_tri, h_vis, h_uv, h_w, h_untex, h_rgb, h_pos, h_eid;
+  // stage-API host scratch
+  std::vector<uint8_t> scratch;
+  // graph
+  cudaGraphExec_t gexec = nullptr;
+  std::vector<uint8_t> gkey;
+  cudaEvent_t ev[kEvents] = {};
+  bool table_ready = false;
+  int last_k = 0;
+  int kernels_per_frame = 0;
+};
+
+namespace {
+
+vc_status fail(vc_ctx* c, vc_status s, const std::string& msg) {
+  if (c) c->err = msg;
+  return s;
+}
+
+#define VC_CUDA(call)                                                                             \
+  do {                                                                                            \
+    const cudaError_t e_ = (call);                                                                \
+    if (e_ != cudaSuccess) {                                                                      \
+      return fail(ctx, e_ == cudaErrorMemoryAllocation ? VC_ERR_OOM : VC_ERR_CUDA,                \
+                  std::string(#call) + ": " + cudaGetErrorString(e_));                            \
+    }                                                                                             \
+  } while (0)
+
+#define VC_TRY(expr)                  \
+  do {                                \
+    const vc_status s_ = (expr);      \
+    if (s_ != VC_OK) return s_;       \
+  } while (0)
+
+vc_status ensure(vc_ctx* ctx, Buf& b, size_t bytes) {
+  if (b.bytes >= bytes && b.p) return VC_OK;
+  if (b.p) cudaFree(b.p);
+  b.p = nullptr;
+  b.bytes = 0;
+  const size_t want = std::max<size_t>(bytes, 256);
+  VC_CUDA(cudaMalloc(&b.p, want));
+  b.bytes = want;
+  if (ctx->gexec) {  // pointers baked into the graph changed
+    cudaGraphExecDestroy(ctx->gexec);
+    ctx->gexec = nullptr;
+  }
+  return VC_OK;
+}
+
+vc_status ensure_host(vc_ctx* ctx, HostBuf& b, size_t bytes) {
+  if (b.bytes >= bytes && b.p) return VC_OK;
+  if (b.p) cudaFreeHost(b.p);
+  b.p = nullptr;
+  b.bytes = 0;
+  const size_t want = std::max<size_t>(bytes * 5 / 4, 4096);
+  VC_CUDA(cudaHostAlloc(&b.p, want, cudaHostAllocDefault));
+  b.bytes = want;
+  return VC_OK;
+}
+
+template <class T>
+T* P(const Buf& b) {
+  return static_cast<T*>(b.p);
+}
+
+bool pow2_ok(int n) { return n >= 4 && n <= 1024 && (n & (n - 1)) == 0; }
+
+// types.hpp:48 Pose::inverse = {R^T, -(R^T t)}; types.hpp:49 compose.
+void fill_sensor(const vc_sensor& in, DevSensor& o) {
+  o.fx = in.depth_intr.fx, o.fy = in.depth_intr.fy, o.cx = in.depth_intr.cx, o.cy = in.depth_intr.cy;
+  o.w = in.depth_intr.width, o.h = in.depth_intr.height;
+  for (int i = 0; i < 9; ++i) o.R[i] = in.pose.R[i];
+  for (int i = 0; i < 3; ++i) o.t[i] = in.pose.t[i];
+  for (int r = 0; r < 3; ++r)
+    for (int c = 0; c < 3; ++c) o.Ri[r * 3 + c] = in.pose.R[c * 3 + r];
+  for (int r = 0; r < 3; ++r)
+    o.ti[r] = -((o.Ri[r * 3 + 0] * in.pose.t[0] + o.Ri[r * 3 + 1] * in.pose.t[1]) + o.Ri[r * 3 + 2] * in.pose.t[2]);
+  o.rfx = in.rgb_intr.fx, o.rfy = in.rgb_intr.fy, o.rcx = in.rgb_intr.cx, o.rcy = in.rgb_intr.cy;
+  o.rw = in.rgb_intr.width, o.rh = in.rgb_intr.height;
+  const double* A = in.pose.R;
+  const double* B = in.rgb_relative.R;
+  for (int r = 0; r < 3; ++r)
+    for (int c = 0; c < 3; ++c) o.Rc[r * 3 + c] = (A[r * 3 + 0] * B[c] + A[r * 3 + 1] * B[3 + c]) + A[r * 3 + 2] * B[6 + c];
+  for (int r = 0; r < 3; ++r)
+    o.tc[r] = ((A[r * 3 + 0] * in.rgb_relative.t[0] + A[r * 3 + 1] * in.rgb_relative.t[1]) +
+               A[r * 3 + 2] * in.rgb_relative.t[2]) +
+              in.pose.t[r];
+}
+
+vc_status check_sensors(vc_ctx* ctx, const vc_sensor* s, int k) {
+  if (!s || k < 1 || k > kMaxViews) return fail(ctx, VC_ERR_INVALID_ARGUMENT, "need 1..16 sensors");
+  for (int i = 0; i < k; ++i) {
+    const auto& d = s[i].depth_intr;
+    const auto& r = s[i].rgb_intr;
+    if (d.width <= 0 || d.height <= 0 || r.width <= 0 || r.height <= 0 || d.fx <= 0 || d.fy <= 0 || r.fx <= 0 ||
+        r.fy <= 0)
+      return fail(ctx, VC_ERR_INVALID_ARGUMENT, "Intrinsics: focal lengths / image sizes must be positive");
+    if (d.width > 8192) return fail(ctx, VC_ERR_INVALID_ARGUMENT, "depth width > 8192");
+  }
+  return VC_OK;
+}
+
+// Stage the k views into context-owned device buffers (graph-stable addresses).
+vc_status stage_views(vc_ctx* ctx, const vc_sensor* sensors, const vc_view* views, int k, bool need_rgb) {
+  size_t bytes = 0;
+  std::vector<size_t> off(3 * k);
+  for (int i = 0; i < k; ++i) {
+    const size_t n = (size_t)sensors[i].depth_intr.width * sensors[i].depth_intr.height;
+    const size_t nr = (size_t)sensors[i].rgb_intr.width * sensors[i].rgb_intr.height * 3;
+    off[3 * i] = bytes;
+    bytes += (n * 2 + 255) & ~size_t(255);
+    off[3 * i + 1] = bytes;
+    bytes += (n + 255) & ~size_t(255);
+    off[3 * i + 2] = bytes;
+    bytes += (nr + 255) & ~size_t(255);
+  }
+  VC_TRY(ensure(ctx, ctx->views, bytes));
+  uint8_t* base = P<uint8_t>(ctx->views);
+  for (int i = 0; i < k; ++i) {
+    const int w = sensors[i].depth_intr.width, h = sensors[i].depth_intr.height;
+    const int rw = sensors[i].rgb_intr.width, rh = sensors[i].rgb_intr.height;
+    const vc_view& v = views[i];
+    if (!v.depth || !v.mask) return fail(ctx, VC_ERR_INVALID_ARGUMENT, "view depth/mask missing");
+    const cudaMemcpyKind kind = v.mem_kind == VC_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    VC_CUDA(cudaMemcpy2DAsync(base + off[3 * i], (size_t)w * 2, v.depth, v.depth_pitch ? v.depth_pitch : (size_t)w * 2,
+                              (size_t)w * 2, h, kind, ctx->st));
+    VC_CUDA(cudaMemcpy2DAsync(base + off[3 * i + 1], (size_t)w, v.mask, v.mask_pitch ? v.mask_pitch : (size_t)w,
+                              (size_t)w, h, kind, ctx->st));
+    if (v.rgb && need_rgb)
+      VC_CUDA(cudaMemcpy2DAsync(base + off[3 * i + 2], (size_t)rw * 3, v.rgb, v.rgb_pitch ? v.rgb_pitch : (size_t)rw * 3,
+                                (size_t)rw * 3, rh, kind, ctx->st));
+    ViewPtrs& vp = ctx->ss.v[i];
+    vp.depth = reinterpret_cast<const uint16_t*>(base + off[3 * i]);
+    vp.mask = base + off[3 * i + 1];
+    vp.rgb = (v.rgb && need_rgb) ? base + off[3 * i + 2] : nullptr;
+    vp.dpitch = w, vp.mpitch = w, vp.rpitch = rw * 3;
+  }
+  return VC_OK;
+}
+
+vc_status setup_sensorset(vc_ctx* ctx, const vc_sensor* sensors, int k) {
+  SensorSet& ss = ctx->ss;
+  ss.k = k;
+  ss.pix_offset[0] = 0;
+  ss.row_offset[0] = 0;
+  for (int i = 0; i < k; ++i) {
+    fill_sensor(sensors[i], ss.s[i]);
+    ss.pix_offset[i + 1] = ss.pix_offset[i] + (int64_t)sensors[i].depth_intr.width * sensors[i].depth_intr.height;
+    ss.row_offset[i + 1] = ss.row_offset[i] + sensors[i].depth_intr.height;
+  }
+  const int64_t npix = ss.pix_offset[k];
+  VC_TRY(ensure(ctx, ctx->pts_pos, npix * 3 * sizeof(double)));
+  VC_TRY(ensure(ctx, ctx->pts_nrm, npix * 3 * sizeof(double)));
+  VC_TRY(ensure(ctx, ctx->pts_w, npix * sizeof(double)));
+  VC_TRY(ensure(ctx, ctx->pts_pix, npix * 3 * sizeof(int32_t)));
+  VC_TRY(ensure(ctx, ctx->wmaps, npix * sizeof(float)));
+  VC_TRY(ensure(ctx, ctx->pre_scratch, preprocess_scratch_bytes(ss)));
+  ctx->pts_cap = (int)npix;
+  ctx->last_k = k;
+  return VC_OK;
+}
+
+DevPoints points(vc_ctx* ctx) {
+  return DevPoints{P<double>(ctx->pts_pos), P<double>(ctx->pts_nrm), P<double>(ctx->pts_w), P<int32_t>(ctx->pts_pix),
+                   ctx->pts_cap};
+}
+
+vc_status ensure_tables(vc_ctx* ctx) {
+  if (ctx->table_ready) return VC_OK;
+  int8_t counts[256], tris[256][5][3];
+  build_mc_table(counts, tris);
+  upload_case_table_data(counts, &tris[0][0][0], ctx->st);
+  VC_CUDA(cudaGetLastError());
+  ctx->table_ready = true;
+  return VC_OK;
+}
+
+vc_status ensure_mesh_caps(vc_ctx* ctx, int v_cap, int k) {
+  const int t_cap = 2 * v_cap + 1024, c_cap = v_cap;
+  VC_TRY(ensure(ctx, ctx->m_pos, (size_t)v_cap * 3 * sizeof(double)));
+  VC_TRY(ensure(ctx, ctx->m_nrm, (size_t)v_cap * 3 * sizeof(float)));
+  VC_TRY(ensure(ctx, ctx->m_posf, (size_t)v_cap * 3 * sizeof(float)));
+  VC_TRY(ensure(ctx, ctx->m_eid, (size_t)v_cap * sizeof(uint64_t)));
+  VC_TRY(ensure(ctx, ctx->m_tri, (size_t)t_cap * 3 * sizeof(int32_t)));
+  VC_TRY(ensure(ctx, ctx->m_cells, (size_t)c_cap * sizeof(int32_t)));
+  VC_TRY(ensure(ctx, ctx->m_celltri, (size_t)c_cap * sizeof(int32_t)));
+  VC_TRY(ensure(ctx, ctx->t_vis, (size_t)v_cap * k));
+  VC_TRY(ensure(ctx, ctx->t_uv, (size_t)v_cap * k * sizeof(float2)));
+  VC_TRY(ensure(ctx, ctx->t_w, (size_t)v_cap * k * sizeof(float)));
+  VC_TRY(ensure(ctx, ctx->t_untex, (size_t)v_cap));
+  VC_TRY(ensure(ctx, ctx->t_rgb, (size_t)v_cap * 3));
+  ctx->v_cap = v_cap, ctx->t_cap = t_cap, ctx->c_cap = c_cap;
+  return VC_OK;
+}
+
+vc_status ensure_grid(vc_ctx* ctx, int nx, int ny, int nz) {
+  const size_t N = (size_t)nx * ny * nz;
+  VC_TRY(ensure(ctx, ctx->acc, N * sizeof(float4)));
+  VC_TRY(ensure(ctx, ctx->spec, 3 * spectrum_elems(nx, ny, nz) * sizeof(float2)));
+  VC_TRY(ensure(ctx, ctx->A, N * sizeof(float)));
+  VC_TRY(ensure(ctx, ctx->vbase, N * sizeof(uint32_t)));
+  VC_TRY(ensure(ctx, ctx->blk, (size_t)mc_blocks(nx, ny, nz) * 3 * sizeof(int32_t)));
+  VC_TRY(ensure(ctx, ctx->tw, twiddle_elems(nx, ny, nz) * sizeof(float2)));
+  VC_TRY(ensure(ctx, ctx->iso_partial, 1024 * sizeof(double)));
+  if (ctx->nx != nx || ctx->ny != ny || ctx->nz != nz) {
+    upload_twiddles(P<float2>(ctx->tw), nx, ny, nz, ctx->st);
+    prepare_integrate(nx, ny, nz);
+    VC_CUDA(cudaGetLastError());
+    ctx->nx = nx, ctx->ny = ny, ctx->nz = nz;
+  }
+  if (ctx->v_cap == 0) {
+    const int v_cap = (int)std::min<size_t>(std::max<size_t>(N / 16, 1 << 16), (size_t)1 << 26);
+    VC_TRY(ensure_mesh_caps(ctx, v_cap, kMaxViews));
+  }
+  return VC_OK;
+}
+
+MeshBufs mesh_bufs(vc_ctx* ctx) {
+  MeshBufs mb;
+  mb.pos = P<double>(ctx->m_pos);
+  mb.nrm = P<float>(ctx->m_nrm);
+  mb.tri = P<int32_t>(ctx->m_tri);
+  mb.edge_id = P<uint64_t>(ctx->m_eid);
+  mb.vbase = P<uint32_t>(ctx->vbase);
+  mb.cells = P<int32_t>(ctx->m_cells);
+  mb.cell_tri = P<int32_t>(ctx->m_celltri);
+  mb.v_cap = ctx->v_cap, mb.t_cap = ctx->t_cap, mb.c_cap = ctx->c_cap;
+  mb.blk = P<int32_t>(ctx->blk);
+  mb.nblk = mc_blocks(ctx->nx, ctx->ny, ctx->nz);
+  return mb;
+}
+
+struct FrameCfg {
+  int nx, ny, nz, mode, pad, sil_r;
+  double disc, eps_vis;
+};
+
+void record(vc_ctx* ctx, int i) {
+  if (ctx->profiling) record_event(ctx->ev[i], ctx->st);
+}
+
+// The frame's kernel sequence (captured once into a CUDA graph).  With
+// profiling on, events 0..6 bracket the reference's stage split and events
+// 12..23 bracket every kernel group (vc_ctx_kernel_times).
+int enqueue_frame(vc_ctx* ctx, const FrameCfg& f) {
+  cudaStream_t st = ctx->st;
+  int n = 0;
+  record(ctx, 0);
+  launch_preprocess(ctx->ss, points(ctx), P<float>(ctx->wmaps), P<int32_t>(ctx->pre_scratch), ctx->ctl, f.nx, f.ny,
+                    f.nz, f.pad, f.disc, f.sil_r, st);
+  n += 4;
+  record(ctx, 1);
+  const size_t N = (size_t)f.nx * f.ny * f.nz;
+  record(ctx, 12);
+  launch_clear(P<float4>(ctx->acc), N, st);
+  record(ctx, 13);
+  launch_splat(points(ctx), ctx->ctl, P<float4>(ctx->acc), f.mode, st);
+  n += 2;
+  record(ctx, 2);
+  launch_integrate(P<float4>(ctx->acc), P<float2>(ctx->spec), P<float>(ctx->A), f.nx, f.ny, f.nz, f.mode,
+                   P<float2>(ctx->tw), st, ctx->profiling ? &ctx->ev[14] : nullptr);
+  n += 5;
+  record(ctx, 3);
+  launch_iso_level(points(ctx), P<float>(ctx->A), ctx->ctl, P<double>(ctx->iso_partial), 1024, st);
+  n += 2;
+  record(ctx, 4);
+  launch_marching_cubes(P<float>(ctx->A), ctx->ctl, mesh_bufs(ctx), f.nx, f.ny, f.nz, st);
+  n += 4;
+  record(ctx, 5);
+  launch_texture(ctx->ss, P<float>(ctx->wmaps), P<double>(ctx->m_pos), ctx->ctl, f.eps_vis, P<uint8_t>(ctx->t_vis),
+                 P<float2>(ctx->t_uv), P<float>(ctx->t_w), P<uint8_t>(ctx->t_untex), P<uint8_t>(ctx->t_rgb),
+                 ctx->v_cap, st);
+  launch_mesh_to_f32(P<double>(ctx->m_pos), P<float>(ctx->m_posf), ctx->ctl, ctx->v_cap, st);
+  n += 2;
+  record(ctx, 6);
+  return n;
+}
+
+vc_status run_frame(vc_ctx* ctx, const FrameCfg& f) {
+  if (!ctx->graphs || ctx->profiling) {  // profiled frames: direct launches + events
+    ctx->kernels_per_frame = enqueue_frame(ctx, f);
+    VC_CUDA(cudaGetLastError());
+    return VC_OK;
+  }
+  // graph key: everything baked into the kernels' parameters
+  std::vector<uint8_t> key(sizeof(SensorSet) + sizeof(FrameCfg) + 16);
+  std::memcpy(key.data(), &ctx->ss, sizeof(SensorSet));
+  std::memcpy(key.data() + sizeof(SensorSet), &f, sizeof(FrameCfg));
+  key[sizeof(SensorSet) + sizeof(FrameCfg)] = ctx->profiling ? 1 : 0;
+  if (!ctx->gexec || key != ctx->gkey) {
+    if (ctx->gexec) cudaGraphExecDestroy(ctx->gexec);
+    ctx->gexec = nullptr;
+    cudaGraph_t g;
+    VC_CUDA(cudaStreamBeginCapture(ctx->st, cudaStreamCaptureModeThreadLocal));
+    ctx->kernels_per_frame = enqueue_frame(ctx, f);
+    const cudaError_t le = cudaGetLastError();
+    const cudaError_t ce = cudaStreamEndCapture(ctx->st, &g);
+    VC_CUDA(le);
+    VC_CUDA(ce);
+    VC_CUDA(cudaGraphInstantiate(&ctx->gexec, g, 0));
+    cudaGraphDestroy(g);
+    ctx->gkey = key;
+  }
+  VC_CUDA(cudaGraphLaunch(ctx->gexec, ctx->st));
+  return VC_OK;
+}
+
+vc_status resolve_dims(vc_ctx* ctx, const vc_recon_config* c, int* nx, int* ny, int* nz) {
+  if (c->r > 0) {
+    if (c->r > 9) return fail(ctx, VC_ERR_INVALID_ARGUMENT, "r must be <= 9");
+    *nx = 1 << c->r, *ny = 1 << (c->r + 1), *nz = 1 << c->r;
+  } else {
+    *nx = c->nx, *ny = c->ny, *nz = c->nz;
+  }
+  if (!pow2_ok(*nx) || !pow2_ok(*ny) || !pow2_ok(*nz))
+    return fail(ctx, VC_ERR_INVALID_ARGUMENT, "grid dims must be powers of two in [4, 1024]");
+  const int d[3] = {*nx, *ny, *nz};
+  for (int a = 0; a < 3; ++a)
+    if (d[a] - 1 - 2 * c->padding_voxels < 1)
+      return fail(ctx, VC_ERR_INVALID_ARGUMENT, "fit_grid: padding leaves no usable voxels");  // reconstruct.cpp:25-26
+  if (c->mode != VC_SPLAT_WEIGHTED && c->mode != VC_SPLAT_SIMPLE)
+    return fail(ctx, VC_ERR_INVALID_ARGUMENT, "unknown splat mode");
+  if (c->silhouette_radius_px < 0) return fail(ctx, VC_ERR_INVALID_ARGUMENT, "silhouette radius < 0");
+  return VC_OK;
+}
+
+float ev_ms(vc_ctx* ctx, int a, int b) {
+  float ms = 0.f;
+  if (cudaEventElapsedTime(&ms, ctx->ev[a], ctx->ev[b]) != cudaSuccess) {
+    cudaGetLastError();  // not recorded in this frame: report NaN, leave no stale error
+    return -1.f;
+  }
+  return ms;
+}
+
+vc_status read_ctl(vc_ctx* ctx) {
+  VC_CUDA(cudaMemcpyAsync(ctx->ctl_h, ctx->ctl, sizeof(DevCtl), cudaMemcpyDeviceToHost, ctx->st));
+  VC_CUDA(cudaStreamSynchronize(ctx->st));
+  return VC_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int vc_abi_version(void) { return VC_ABI_VERSION; }
+
+const char* vc_status_string(vc_status s) {
+  switch (s) {
+    case VC_OK: return "ok";
+    case VC_ERR_INVALID_ARGUMENT: return "invalid argument";
+    case VC_ERR_EMPTY_SCENE: return "empty foreground in all views";
+    case VC_ERR_CAPACITY: return "capacity exceeded";
+    case VC_ERR_CUDA: return "CUDA error";
+    case VC_ERR_NCCL: return "NCCL error";
+    case VC_ERR_OOM: return "out of device memory";
+    case VC_ERR_NO_DEVICE: return "no CUDA device";
+  }
+  return "unknown";
+}
+
+vc_status vc_ctx_create(int device, vc_ctx** out) {
+  if (!out) return VC_ERR_INVALID_ARGUMENT;
+  *out = nullptr;
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) return VC_ERR_NO_DEVICE;
+  if (device < 0 || device >= n) return VC_ERR_INVALID_ARGUMENT;
+  auto* ctx = new vc_ctx;
+  ctx->device = device;
+  auto cleanup = [&](vc_status s) {
+    delete ctx;
+    return s;
+  };
+  if (cudaSetDevice(device) != cudaSuccess) return cleanup(VC_ERR_CUDA);
+  if (cudaStreamCreateWithFlags(&ctx->st, cudaStreamNonBlocking) != cudaSuccess) return cleanup(VC_ERR_CUDA);
+  if (cudaMalloc(&ctx->ctl, sizeof(DevCtl)) != cudaSuccess) return cleanup(VC_ERR_OOM);
+  if (cudaHostAlloc(&ctx->ctl_h, sizeof(DevCtl), cudaHostAllocDefault) != cudaSuccess) return cleanup(VC_ERR_OOM);
+  for (auto& e : ctx->ev)
+    if (cudaEventCreate(&e) != cudaSuccess) return cleanup(VC_ERR_CUDA);
+  *out = ctx;
+  return VC_OK;
+}
+
+vc_status vc_ctx_destroy(vc_ctx* ctx) {
+  if (!ctx) return VC_OK;
+  cudaSetDevice(ctx->device);
+  if (ctx->st) cudaStreamSynchronize(ctx->st);
+  if (ctx->gexec) cudaGraphExecDestroy(ctx->gexec);
+  for (Buf* b : {&ctx->acc, &ctx->spec, &ctx->A, &ctx->tw, &ctx->vbase, &ctx->blk, &ctx->views, &ctx->pts_pos,
+                 &ctx->pts_nrm, &ctx->pts_w, &ctx->pts_pix, &ctx->wmaps, &ctx->pre_scratch, &ctx->iso_partial,
+                 &ctx->m_pos, &ctx->m_nrm, &ctx->m_tri, &ctx->m_eid, &ctx->m_cells, &ctx->m_celltri, &ctx->m_posf,
+                 &ctx->t_vis, &ctx->t_uv, &ctx->t_w, &ctx->t_untex, &ctx->t_rgb})
+    if (b->p) cudaFree(b->p);
+  for (HostBuf* b : {&ctx->h_posf, &ctx->h_nrm, &ctx->h_tri, &ctx->h_vis, &ctx->h_uv, &ctx->h_w, &ctx->h_untex,
+                     &ctx->h_rgb, &ctx->h_pos, &ctx->h_eid})
+    if (b->p) cudaFreeHost(b->p);
+  if (ctx->ctl) cudaFree(ctx->ctl);
+  if (ctx->ctl_h) cudaFreeHost(ctx->ctl_h);
+  for (auto& e : ctx->ev)
+    if (e) cudaEventDestroy(e);
+  if (ctx->st) cudaStreamDestroy(ctx->st);
+  delete ctx;
+  return VC_OK;
+}
+
+const char* vc_last_error(const vc_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+vc_status vc_ctx_set_output(vc_ctx* ctx, int32_t kind) {
+  if (!ctx || (kind != VC_MEM_HOST && kind != VC_MEM_DEVICE)) return VC_ERR_INVALID_ARGUMENT;
+  ctx->out_kind = kind;
+  return VC_OK;
+}
+vc_status vc_ctx_set_profiling(vc_ctx* ctx, int32_t enable) {
+  if (!ctx) return VC_ERR_INVALID_ARGUMENT;
+  ctx->profiling = enable != 0;
+  return VC_OK;
+}
+vc_status vc_ctx_set_graphs(vc_ctx* ctx, int32_t enable) {
+  if (!ctx) return VC_ERR_INVALID_ARGUMENT;
+  ctx->graphs = enable != 0;
+  return VC_OK;
+}
+void* vc_ctx_stream(vc_ctx* ctx) { return ctx ? (void*)ctx->st : nullptr; }
+int32_t vc_ctx_kernels_per_frame(const vc_ctx* ctx) { return ctx ? ctx->kernels_per_frame : 0; }
+
+int32_t vc_ctx_kernel_times(const vc_ctx* ctx, double* ms, int32_t max_n) {
+  if (!ctx || !ms) return 0;
+  vc_ctx* c = const_cast<vc_ctx*>(ctx);
+  // preprocess, clear, splat, fx, fy, z, iy, ix, iso, mc, texture
+  const int pairs[11][2] = {{0, 1}, {12, 13}, {13, 2}, {14, 15}, {15, 16}, {16, 17}, {17, 18}, {18, 19},
+                            {3, 4}, {4, 5}, {5, 6}};
+  int n = 0;
+  for (; n < 11 && n < max_n; ++n) ms[n] = ev_ms(c, pairs[n][0], pairs[n][1]);
+  return n;
+}
+
+vc_status vc_host_alloc(vc_ctx* ctx, size_t bytes, void** out) {
+  if (!ctx || !out) return VC_ERR_INVALID_ARGUMENT;
+  cudaSetDevice(ctx->device);
+  VC_CUDA(cudaHostAlloc(out, bytes, cudaHostAllocDefault));
+  return VC_OK;
+}
+vc_status vc_host_free(vc_ctx* ctx, void* p) {
+  if (!ctx) return VC_ERR_INVALID_ARGUMENT;
+  VC_CUDA(cudaFreeHost(p));
+  return VC_OK;
+}
+vc_status vc_device_alloc(vc_ctx* ctx, size_t bytes, void** out) {
+  if (!ctx || !out) return VC_ERR_INVALID_ARGUMENT;
+  cudaSetDevice(ctx->device);
+  VC_CUDA(cudaMalloc(out, bytes));
+  return VC_OK;
+}
+vc_status vc_device_free(vc_ctx* ctx, void* p) {
+  if (!ctx) return VC_ERR_INVALID_ARGUMENT;
+  VC_CUDA(cudaFree(p));
+  return VC_OK;
+}
+vc_status vc_memcpy(vc_ctx* ctx, void* dst, const void* src, size_t bytes, int32_t dk, int32_t sk) {
+  if (!ctx) return VC_ERR_INVALID_ARGUMENT;
+  const cudaMemcpyKind kind = dk == VC_MEM_DEVICE ? (sk == VC_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice)
+                                                  : (sk == VC_MEM_DEVICE ? cudaMemcpyDeviceToHost : cudaMemcpyHostToHost);
+  VC_CUDA(cudaMemcpyAsync(dst, src, bytes, kind, ctx->st));
+  VC_CUDA(cudaStreamSynchronize(ctx->st));
+  return VC_OK;
+}
+vc_status vc_synchronize(vc_ctx* ctx) {
+  if (!ctx) return VC_ERR_INVALID_ARGUMENT;
+  VC_CUDA(cudaStreamSynchronize(ctx->st));
+  return VC_OK;
+}
+
+// ------------------------------------------------------------- hot path
+vc_status vc_reconstruct_frame(vc_ctx* ctx, const vc_sensor* sensors, const vc_view* views, int32_t k,
+                               const vc_recon_config* config, vc_textured_mesh* out, vc_stage_timings* timings) {
+  if (!ctx || !views || !config || !out) return fail(ctx, VC_ERR_INVALID_ARGUMENT, "null argument");
+  cudaSetDevice(ctx->device);
+  VC_CUDA(cudaGetLastError());
+  VC_TRY(check_sensors(ctx, sensors, k));
+  int nx, ny, nz;
+  VC_TRY(resolve_dims(ctx, config, &nx, &ny, &nz));
+  VC_TRY(ensure_tables(ctx));
+  VC_TRY(ensure_grid(ctx, nx, ny, nz));
+  VC_TRY(setup_sensorset(ctx, sensors, k));
+  const bool prof = ctx->profiling || timings;
+  const bool prof_saved = ctx->profiling;
+  ctx->profiling = prof;
+
+  if (prof) record_event(ctx->ev[8], ctx->st);
+  VC_TRY(stage_views(ctx, sensors, views, k, true));
+  if (prof) record_event(ctx->ev[9], ctx->st);
+  const FrameCfg f{nx, ny, nz, config->mode, config->padding_voxels, config->silhouette_radius_px,
+                   config->discontinuity_mm, config->eps_vis_mm};
+  vc_status s = run_frame(ctx, f);
+  ctx->profiling = prof_saved;
+  if (s != VC_OK) return s;
+  VC_TRY(read_ctl(ctx));
+  const DevCtl& c = *ctx->ctl_h;
+  if (c.status == 2) return fail(ctx, VC_ERR_EMPTY_SCENE, "reconstruct_frame: empty foreground in all views");
+  if (c.status != 0) return fail(ctx, VC_ERR_CUDA, "preprocess failed");
+  if (c.overflow) {  // grow and redo MC + texture (rare; invalidates the graph)
+    const int want = std::max(c.V, std::max(c.C, c.T / 2)) * 2;
+    VC_TRY(ensure_mesh_caps(ctx, want, kMaxViews));
+    launch_marching_cubes(P<float>(ctx->A), ctx->ctl, mesh_bufs(ctx), nx, ny, nz, ctx->st);
+    launch_texture(ctx->ss, P<float>(ctx->wmaps), P<double>(ctx->m_pos), ctx->ctl, config->eps_vis_mm,
+                   P<uint8_t>(ctx->t_vis), P<float2>(ctx->t_uv), P<float>(ctx->t_w), P<uint8_t>(ctx->t_untex),
+                   P<uint8_t>(ctx->t_rgb), ctx->v_cap, ctx->st);
+    launch_mesh_to_f32(P<double>(ctx->m_pos), P<float>(ctx->m_posf), ctx->ctl, ctx->v_cap, ctx->st);
+    VC_CUDA(cudaGetLastError());
+    VC_TRY(read_ctl(ctx));
+    if (ctx->ctl_h->overflow) return fail(ctx, VC_ERR_CAPACITY, "marching cubes capacity");
+  }
+  const int V = ctx->ctl_h->V, T = ctx->ctl_h->T;
+  std::memset(out, 0, sizeof(*out));
+  out->vertex_count = V, out->triangle_count = T, out->sensor_count = k, out->point_count = ctx->ctl_h->P;
+  out->iso_level = ctx->ctl_h->level;
+  out->grid.nx = nx, out->grid.ny = ny, out->grid.nz = nz;
+  for (int a = 0; a < 3; ++a) out->grid.origin[a] = ctx->ctl_h->grid.origin[a];
+  out->grid.edge_mm = ctx->ctl_h->grid.edge;
+  out->mem_kind = ctx->out_kind;
+  if (prof) record_event(ctx->ev[10], ctx->st);
+  if (ctx->out_kind == VC_MEM_DEVICE) {
+    out->positions = P<float>(ctx->m_posf), out->normals = P<float>(ctx->m_nrm), out->triangles = P<int32_t>(ctx->m_tri);
+    out->visible = P<uint8_t>(ctx->t_vis), out->uv = P<float>(ctx->t_uv), out->weight = P<float>(ctx->t_w);
+    out->untextured = P<uint8_t>(ctx->t_untex), out->rgb = P<uint8_t>(ctx->t_rgb);
+    out->positions_f64 = P<double>(ctx->m_pos);
+  } else {
+    VC_TRY(ensure_host(ctx, ctx->h_posf, (size_t)V * 12));
+    VC_TRY(ensure_host(ctx, ctx->h_nrm, (size_t)V * 12));
+    VC_TRY(ensure_host(ctx, ctx->h_tri, (size_t)T * 12));
+    VC_TRY(ensure_host(ctx, ctx->h_vis, (size_t)V * k));
+    VC_TRY(ensure_host(ctx, ctx->h_uv, (size_t)V * k * 8));
+    VC_TRY(ensure_host(ctx, ctx->h_w, (size_t)V * k * 4));
+    VC_TRY(ensure_host(ctx, ctx->h_untex, (size_t)V));
+    VC_TRY(ensure_host(ctx, ctx->h_rgb, (size_t)V * 3));
+    VC_TRY(ensure_host(ctx, ctx->h_pos, (size_t)V * 24));
+    auto d2h = [&](HostBuf& h, const Buf& d, size_t bytes) {
+      return bytes ? cudaMemcpyAsync(h.p, d.p, bytes, cudaMemcpyDeviceToHost, ctx->st) : cudaSuccess;
+    };
+    VC_CUDA(d2h(ctx->h_posf, ctx->m_posf, (size_t)V * 12));
+    VC_CUDA(d2h(ctx->h_nrm, ctx->m_nrm, (size_t)V * 12));
+    VC_CUDA(d2h(ctx->h_tri, ctx->m_tri, (size_t)T * 12));
+    VC_CUDA(d2h(ctx->h_vis, ctx->t_vis, (size_t)V * k));
+    VC_CUDA(d2h(ctx->h_uv, ctx->t_uv, (size_t)V * k * 8));
+    VC_CUDA(d2h(ctx->h_w, ctx->t_w, (size_t)V * k * 4));
+    VC_CUDA(d2h(ctx->h_untex, ctx->t_untex, (size_t)V));
+    VC_CUDA(d2h(ctx->h_rgb, ctx->t_rgb, (size_t)V * 3));
+    VC_CUDA(d2h(ctx->h_pos, ctx->m_pos, (size_t)V * 24));
+    out->positions = (const float*)ctx->h_posf.p, out->normals = (const float*)ctx->h_nrm.p;
+    out->triangles = (const int32_t*)ctx->h_tri.p, out->visible = (const uint8_t*)ctx->h_vis.p;
+    out->uv = (const float*)ctx->h_uv.p, out->weight = (const float*)ctx->h_w.p;
+    out->untextured = (const uint8_t*)ctx->h_untex.p, out->rgb = (const uint8_t*)ctx->h_rgb.p;
+    out->positions_f64 = (const double*)ctx->h_pos.p;
+  }
+  if (prof) record_event(ctx->ev[11], ctx->st);
+  VC_CUDA(cudaStreamSynchronize(ctx->st));
+  if (timings) {
+    std::memset(timings, 0, sizeof(*timings));
+    timings->h2d_ms = ev_ms(ctx, 8, 9);
+    timings->raw_ms = ev_ms(ctx, 0, 1);
+    timings->weights_ms = 0.0;  // fused into the preprocess kernels
+    timings->splat_ms = ev_ms(ctx, 1, 2);
+    timings->fft_ms = ev_ms(ctx, 2, 3);
+    timings->iso_ms = ev_ms(ctx, 3, 4);
+    timings->mc_ms = ev_ms(ctx, 4, 5);
+    timings->volumetric_ms = ev_ms(ctx, 1, 5);
+    timings->texture_ms = ev_ms(ctx, 5, 6);
+    timings->d2h_ms = ev_ms(ctx, 10, 11);
+    timings->total_ms = ev_ms(ctx, 8, 11);
+  }
+  return VC_OK;
+}
+
+vc_status vc_export_volume(vc_ctx* ctx, float* dst, int32_t kind) {
+  if (!ctx || !dst || !ctx->A.p) return fail(ctx, VC_ERR_INVALID_ARGUMENT, "no volume");
+  const size_t bytes = (size_t)ctx->nx * ctx->ny * ctx->nz * sizeof(float);
+  VC_CUDA(cudaMemcpyAsync(dst, ctx->A.p, bytes, kind == VC_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+                          ctx->st));
+  VC_CUDA(cudaStreamSynchronize(ctx->st));
+  return VC_OK;
+}
+
+vc_status vc_export_points(vc_ctx* ctx, double* pos, double* nrm, double* weight, int32_t* pix, float* wmaps) {
+  if (!ctx || !ctx->pts_pos.p) return fail(ctx, VC_ERR_INVALID_ARGUMENT, "no points");
+  VC_TRY(read_ctl(ctx));
+  const size_t n = (size_t)ctx->ctl_h->P;
+  if (pos) VC_CUDA(cudaMemcpyAsync(pos, ctx->pts_pos.p, n * 24, cudaMemcpyDeviceToHost, ctx->st));
+  if (nrm) VC_CUDA(cudaMemcpyAsync(nrm, ctx->pts_nrm.p, n * 24, cudaMemcpyDeviceToHost, ctx->st));
+  if (weight) VC_CUDA(cudaMemcpyAsync(weight, ctx->pts_w.p, n * 8, cudaMemcpyDeviceToHost, ctx->st));
+  if (pix) VC_CUDA(cudaMemcpyAsync(pix, ctx->pts_pix.p, n * 12, cudaMemcpyDeviceToHost, ctx->st));
+  if (wmaps)
+    VC_CUDA(cudaMemcpyAsync(wmaps, ctx->wmaps.p, (size_t)ctx->ss.pix_offset[ctx->ss.k] * 4, cudaMemcpyDeviceToHost,
+                            ctx->st));
+  VC_CUDA(cudaStreamSynchronize(ctx->st));
+  return VC_OK;
+}
+
+// ------------------------------------------------------------- stage entry points
+vc_status vc_stage_preprocess(vc_ctx* ctx, const vc_sensor* sensors, const vc_view* views, int32_t k,
+                              const vc_recon_config* config, int64_t* n_points, vc_grid_spec* grid) {
+  if (!ctx || !views || !config) return fail(ctx, VC_ERR_INVALID_ARGUMENT, "null argument");
+  cudaSetDevice(ctx->device);
+  VC_TRY(check_sensors(ctx, sensors, k));
+  int nx, ny, nz;
+  VC_TRY(resolve_dims(ctx, config, &nx, &ny, &nz));
+  VC_TRY(setup_sensorset(ctx, sensors, k));
+  VC_TRY(stage_views(ctx, sensors, views, k, false));
+  launch_preprocess(ctx->ss, points(ctx), P<float>(ctx->wmaps), P<int32_t>(ctx->pre_scratch), ctx->ctl, nx, ny, nz,
+                    config->padding_voxels, config->discontinuity_mm, config->silhouette_radius_px, ctx->st);
+  VC_CUDA(cudaGetLastError());
+  VC_TRY(read_ctl(ctx));
+  if (n_points) *n_points = ctx->ctl_h->P;
+  if (grid) {
+    grid->nx = nx, grid->ny = ny, grid->nz = nz;
+    for (int a = 0; a < 3; ++a) grid->origin[a] = ctx->ctl_h->grid.origin[a];
+    grid->edge_mm = ctx->ctl_h->grid.edge;
+  }
+  if (ctx->ctl_h->status == 2) return fail(ctx, VC_ERR_EMPTY_SCENE, "empty foreground in all views");
+  return VC_OK;
+}
+
+vc_status vc_fit_grid(const double lo[3], const double hi[3], const int32_t dims[3], int32_t pad, vc_grid_spec* g) {
+  if (!lo || !hi || !dims || !g) return VC_ERR_INVALID_ARGUMENT;
+  double edge = 1e-9;
+  for (int a = 0; a < 3; ++a) {
+    const int usable = dims[a] - 1 - 2 * pad;
+    if (usable < 1) return VC_ERR_INVALID_ARGUMENT;
+    const double e = (hi[a] - lo[a]) / usable;
+    edge = edge < e ? e : edge;
+  }
+  g->nx = dims[0], g->ny = dims[1], g->nz = dims[2];
+  g->edge_mm = edge;
+  for (int a = 0; a < 3; ++a) g->origin[a] = 0.5 * (lo[a] + hi[a]) - edge * (dims[a] - 1) / 2.0;
+  return VC_OK;
+}
+
+namespace {
+vc_status upload_points(vc_ctx* ctx, const double* pos, const double* nrm, const double* w, int64_t n,
+                        const vc_grid_spec* grid, int status_ok) {
+  VC_TRY(ensure(ctx, ctx->pts_pos, std::max<int64_t>(n, 1) * 24));
+  VC_TRY(ensure(ctx, ctx->pts_nrm, std::max<int64_t>(n, 1) * 24));
+  VC_TRY(ensure(ctx, ctx->pts_w, std::max<int64_t>(n, 1) * 8));
+  VC_TRY(ensure(ctx, ctx->pts_pix, std::max<int64_t>(n, 1) * 12));
+  ctx->pts_cap = (int)std::max<int64_t>(n, 1);
+  if (n) {
+    VC_CUDA(cudaMemcpyAsync(ctx->pts_pos.p, pos, n * 24, cudaMemcpyHostToDevice, ctx->st));
+    if (nrm) VC_CUDA(cudaMemcpyAsync(ctx->pts_nrm.p, nrm, n * 24, cudaMemcpyHostToDevice, ctx->st));
+    if (w) VC_CUDA(cudaMemcpyAsync(ctx->pts_w.p, w, n * 8, cudaMemcpyHostToDevice, ctx->st));
+  }
+  DevCtl& c = *ctx->ctl_h;
+  std::memset(&c, 0, sizeof(c));
+  c.P = (int32_t)n;
+  c.status = status_ok ? 0 : 2;
+  c.grid.nx = grid->nx, c.grid.ny = grid->ny, c.grid.nz = grid->nz;
+  for (int a = 0; a < 3; ++a) c.grid.origin[a] = grid->origin[a];
+  c.grid.edge = grid->edge_mm;
+  VC_CUDA(cudaMemcpyAsync(ctx->ctl, &c, sizeof(DevCtl), cudaMemcpyHostToDevice, ctx->st));
+  VC_CUDA(cudaStreamSynchronize(ctx->st));
+  return VC_OK;
+}
+}  // namespace
+
+vc_status vc_stage_splat(vc_ctx* ctx, const double* pos, const double* nrm, const double* weight, int64_t n,
+                         const vc_grid_spec* grid, int32_t mode, int32_t negate, float* field, float* density) {
+  if (!ctx || !grid || !field || !density || (n > 0 && (!pos || !nrm))) return fail(ctx, VC_ERR_INVALID_ARGUMENT, "null");
+  if (mode != 0 && mode != 1) return fail(ctx, VC_ERR_INVALID_ARGUMENT, "mode");
+  cudaSetDevice(ctx->device);
+  const size_t N = (size_t)grid->nx * grid->ny * grid->nz;
+  VC_TRY(ensure(ctx, ctx->acc, N * sizeof(float4)));
+  std::vector<double> ones;
+  if (!weight) ones.assign(std::max<int64_t>(n, 1), 1.0), weight = ones.data();
+  VC_TRY(upload_points(ctx, pos, nrm, weight, n, grid, 1));
+  Buf fbuf, dbuf;
+  VC_TRY(ensure(ctx, fbuf, N * 12));
+  VC_TRY(ensure(ctx, dbuf, N * 4));
+  launch_clear(P<float4>(ctx->acc), N, ctx->st);
+  launch_splat(points(ctx), ctx->ctl, P<float4>(ctx->acc), mode, ctx->st);
+  const double sigma2 = std::sqrt(1.5) * (std::sqrt(3.0) / 2.0 * grid->edge_mm);  // splat.cpp:35-36
+  launch_splat_finalize(P<float4>(ctx->acc), N, mode, negate, sigma2, P<float>(fbuf), P<float>(dbuf), ctx->st);
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) e = cudaMemcpyAsync(field, fbuf.p, N * 12, cudaMemcpyDeviceToHost, ctx->st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(density, dbuf.p, N * 4, cudaMemcpyDeviceToHost, ctx->st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->st);
+  cudaFree(fbuf.p);
+  cudaFree(dbuf.p);
+  if (e != cudaSuccess) return fail(ctx, VC_ERR_CUDA, cudaGetErrorString(e));
+  return VC_OK;
+}
+
+vc_status vc_stage_integrate(vc_ctx* ctx, const float* field, int32_t nx, int32_t ny, int32_t nz, float* A) {
+  if (!ctx || !field || !A) return fail(ctx, VC_ERR_INVALID_ARGUMENT, "null");
+  if (!pow2_ok(nx) || !pow2_ok(ny) || !pow2_ok(nz))
+    return fail(ctx, VC_ERR_INVALID_ARGUMENT, "grid dims must be powers of two in [4, 1024]");
+  cudaSetDevice(ctx->device);
+  VC_TRY(ensure_grid(ctx, nx, ny, nz));
+  const size_t N = (size_t)nx * ny * nz;
+  // acc = (-V, 1) under the simple-mode normalisation V = -U/d gives V exactly
+  std::vector<float4> h(N);
+  for (size_t i = 0; i < N; ++i) h[i] = make_float4(-field[3 * i], -field[3 * i + 1], -field[3 * i + 2], 1.f);
+  VC_CUDA(cudaMemcpyAsync(ctx->acc.p, h.data(), N * sizeof(float4), cudaMemcpyHostToDevice, ctx->st));
+  launch_integrate(P<float4>(ctx->acc), P<float2>(ctx->spec), P<float>(ctx->A), nx, ny, nz, 1, P<float2>(ctx->tw),
+                   ctx->st, nullptr);
+  VC_CUDA(cudaGetLastError());
+  VC_CUDA(cudaMemcpyAsync(A, ctx->A.p, N * 4, cudaMemcpyDeviceToHost, ctx->st));
+  VC_CUDA(cudaStreamSynchronize(ctx->st));
+  return VC_OK;
+}
+
+vc_status vc_stage_iso_level(vc_ctx* ctx, const float* A, const vc_grid_spec* grid, const double* pos, int64_t n,
+                             double* level) {
+  if (!ctx || !A || !grid || !level) return fail(ctx, VC_ERR_INVALID_ARGUMENT, "null");
+  if (n <= 0) return fail(ctx, VC_ERR_INVALID_ARGUMENT, "iso_level: no input samples");  // splat.cpp:99
+  cudaSetDevice(ctx->device);
+  const size_t N = (size_t)grid->nx * grid->ny * grid->nz;
+  Buf a;
+  VC_TRY(ensure(ctx, a, N * 4));
+  VC_TRY(ensure(ctx, ctx->iso_partial, 1024 * sizeof(double)));
+  VC_CUDA(cudaMemcpyAsync(a.p, A, N * 4, cudaMemcpyHostToDevice, ctx->st));
+  VC_TRY(upload_points(ctx, pos, nullptr, nullptr, n, grid, 1));
+  launch_iso_level(points(ctx), P<float>(a), ctx->ctl, P<double>(ctx->iso_partial), 1024, ctx->st);
+  cudaError_t e = cudaGetLastError();
+  cudaFree(a.p);
+  if (e != cudaSuccess) return fail(ctx, VC_ERR_CUDA, cudaGetErrorString(e));
+  VC_TRY(read_ctl(ctx));
+  *level = ctx->ctl_h->level;
+  return VC_OK;
+}
+
+vc_status vc_stage_marching_cubes(vc_ctx* ctx, const float* A, const vc_grid_spec* grid, double level,
+                                  int32_t* n_vertices, int32_t* n_triangles, const double** positions,
+                                  const float** normals, const int32_t** triangles, const uint64_t** edge_ids) {
+  if (!ctx || !A || !grid || !n_vertices || !n_triangles) return fail(ctx, VC_ERR_INVALID_ARGUMENT, "null");
+  const int nx = grid->nx, ny = grid->ny, nz = grid->nz;
+  if (nx < 2 || ny < 2 || nz < 2) {  // marching_cubes.cpp:135
+    *n_vertices = *n_triangles = 0;
+    return VC_OK;
+  }
+  cudaSetDevice(ctx->device);
+  VC_TRY(ensure_tables(ctx));
+  const size_t N = (size_t)nx * ny * nz;
+  VC_TRY(ensure(ctx, ctx->A, N * 4));
+  VC_TRY(ensure(ctx, ctx->vbase, N * 4));
+  VC_TRY(ensure(ctx, ctx->blk, (size_t)mc_blocks(nx, ny, nz) * 12));
+  ctx->nx = ctx->ny = ctx->nz = 0;  // grid buffers no longer match a frame config
+  if (ctx->v_cap == 0) VC_TRY(ensure_mesh_caps(ctx, (int)std::max<size_t>(N / 16, 1 << 16), kMaxViews));
+  VC_CUDA(cudaMemcpyAsync(ctx->A.p, A, N * 4, cudaMemcpyHostToDevice, ctx->st));
+  VC_TRY(upload_points(ctx, nullptr, nullptr, nullptr, 0, grid, 1));
+  ctx->ctl_h->level = level;
+  VC_CUDA(cudaMemcpyAsync(ctx->ctl, ctx->ctl_h, sizeof(DevCtl), cudaMemcpyHostToDevice, ctx->st));
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    MeshBufs mb = mesh_bufs(ctx);
+    mb.nblk = mc_blocks(nx, ny, nz);
+    launch_marching_cubes(P<float>(ctx->A), ctx->ctl, mb, nx, ny, nz, ctx->st);
+    VC_CUDA(cudaGetLastError());
+    VC_TRY(read_ctl(ctx));
+    if (!ctx->ctl_h->overflow) break;
+    const DevCtl c = *ctx->ctl_h;
+    VC_TRY(ensure_mesh_caps(ctx, std::max(c.V, std::max(c.C, c.T / 2)) * 2, kMaxViews));
+    if (attempt == 1) return fail(ctx, VC_ERR_CAPACITY, "marching cubes capacity");
+  }
+  const int V = ctx->ctl_h->V, T = ctx->ctl_h->T;
+  *n_vertices = V, *n_triangles = T;
+  const size_t bytes = (size_t)V * 24 + (size_t)V * 12 + (size_t)T * 12 + (size_t)V * 8 + 64;
+  ctx->scratch.resize(bytes);
+  uint8_t* p = ctx->scratch.data();
+  double* hp = reinterpret_cast<double*>(p);
+  float* hn = reinterpret_cast<float*>(p + (size_t)V * 24);
+  uint64_t* he = reinterpret_cast<uint64_t*>(p + (size_t)V * 36);
+  int32_t* ht = reinterpret_cast<int32_t*>(p + (size_t)V * 44);
+  if (V) {
+    VC_CUDA(cudaMemcpyAsync(hp, ctx->m_pos.p, (size_t)V * 24, cudaMemcpyDeviceToHost, ctx->st));
+    VC_CUDA(cudaMemcpyAsync(hn, ctx->m_nrm.p, (size_t)V * 12, cudaMemcpyDeviceToHost, ctx->st));
+    VC_CUDA(cudaMemcpyAsync(he, ctx->m_eid.p, (size_t)V * 8, cudaMemcpyDeviceToHost, ctx->st));
+  }
+  if (T) VC_CUDA(cudaMemcpyAsync(ht, ctx->m_tri.p, (size_t)T * 12, cudaMemcpyDeviceToHost, ctx->st));
+  VC_CUDA(cudaStreamSynchronize(ctx->st));
+  if (positions) *positions = hp;
+  if (normals) *normals = hn;
+  if (triangles) *triangles = ht;
+  if (edge_ids) *edge_ids = he;
+  return VC_OK;
+}
+
+vc_status vc_stage_texture(vc_ctx* ctx, const vc_sensor* sensors, const vc_view* views, const float* weight_maps,
+                           int32_t k, const double* vertices, int32_t V, double eps_vis_mm, uint8_t* visible, float* uv,
+                           float* weight, uint8_t* untextured, uint8_t* rgb) {
+  if (!ctx || !views || !weight_maps || (V > 0 && !vertices)) return fail(ctx, VC_ERR_INVALID_ARGUMENT, "null");
+  cudaSetDevice(ctx->device);
+  VC_TRY(check_sensors(ctx, sensors, k));
+  VC_TRY(setup_sensorset(ctx, sensors, k));
+  VC_TRY(stage_views(ctx, sensors, views, k, true));
+  VC_TRY(ensure_tables(ctx));
+  if (ctx->v_cap < V) VC_TRY(ensure_mesh_caps(ctx, V, kMaxViews));
+  if (ctx->v_cap == 0) VC_TRY(ensure_mesh_caps(ctx, 1 << 16, kMaxViews));
+  const size_t npix = (size_t)ctx->ss.pix_offset[k];
+  VC_CUDA(cudaMemcpyAsync(ctx->wmaps.p, weight_maps, npix * 4, cudaMemcpyHostToDevice, ctx->st));
+  if (V) VC_CUDA(cudaMemcpyAsync(ctx->m_pos.p, vertices, (size_t)V * 24, cudaMemcpyHostToDevice, ctx->st));
+  DevCtl& c = *ctx->ctl_h;
+  std::memset(&c, 0, sizeof(c));
+  c.V = V;
+  VC_CUDA(cudaMemcpyAsync(ctx->ctl, &c, sizeof(DevCtl), cudaMemcpyHostToDevice, ctx->st));
+  launch_texture(ctx->ss, P<float>(ctx->wmaps), P<double>(ctx->m_pos), ctx->ctl, eps_vis_mm, P<uint8_t>(ctx->t_vis),
+                 P<float2>(ctx->t_uv), P<float>(ctx->t_w), P<uint8_t>(ctx->t_untex), P<uint8_t>(ctx->t_rgb), ctx->v_cap,
+                 ctx->st);
+  VC_CUDA(cudaGetLastError());
+  if (V) {
+    if (visible) VC_CUDA(cudaMemcpyAsync(visible, ctx->t_vis.p, (size_t)V * k, cudaMemcpyDeviceToHost, ctx->st));
+    if (uv) VC_CUDA(cudaMemcpyAsync(uv, ctx->t_uv.p, (size_t)V * k * 8, cudaMemcpyDeviceToHost, ctx->st));
+    if (weight) VC_CUDA(cudaMemcpyAsync(weight, ctx->t_w.p, (size_t)V * k * 4, cudaMemcpyDeviceToHost, ctx->st));
+    if (untextured) VC_CUDA(cudaMemcpyAsync(untextured, ctx->t_untex.p, (size_t)V, cudaMemcpyDeviceToHost, ctx->st));
+    if (rgb) VC_CUDA(cudaMemcpyAsync(rgb, ctx->t_rgb.p, (size_t)V * 3, cudaMemcpyDeviceToHost, ctx->st));
+  }
+  VC_CUDA(cudaStreamSynchronize(ctx->st));
+  return VC_OK;
+}
+
+// ------------------------------------------------------------- synthetic capture
+vc_status vc_synth_circle_rig(int32_t recon, int32_t held_out, double radius, double target_h, int32_t w, int32_t h,
+                              double f, vc_sensor* out) {
+  if (!out || recon < 1 || held_out < 0 || w <= 0 || h <= 0 || f <= 0) return VC_ERR_INVALID_ARGUMENT;
+  circle_rig(recon, held_out, radius, target_h, w, h, f, out);
+  return VC_OK;
+}
+vc_status vc_synth_xpose_body(vc_body* out) {
+  if (!out) return VC_ERR_INVALID_ARGUMENT;
+  xpose_body(out);
+  return VC_OK;
+}
+vc_status vc_synth_kick_body(int32_t frames, int32_t frame, vc_body* out) {
+  if (!out || frames < 1 || frame < 0 || frame >= frames) return VC_ERR_INVALID_ARGUMENT;
+  kick_body(frames, frame, out);
+  return VC_OK;
+}
+
+vc_status vc_synth_render(vc_ctx* ctx, const vc_sensor* sensor, const vc_body* body, double sigma, uint64_t seed,
+                          double gain, int32_t camera, int32_t frame, uint16_t* depth, uint8_t* mask, uint8_t* rgb,
+                          int32_t dst_kind) {
+  if (!ctx || !sensor || !body) return fail(ctx, VC_ERR_INVALID_ARGUMENT, "null");
+  VC_TRY(check_sensors(ctx, sensor, 1));
+  cudaSetDevice(ctx->device);
+  DevSensor s;
+  fill_sensor(*sensor, s);
+  const size_t n = (size_t)s.w * s.h, nr = (size_t)s.rw * s.rh * 3;
+  uint8_t* tmp = nullptr;
+  VC_CUDA(cudaMalloc(&tmp, n * 3 + nr + 64));
+  uint16_t* dd = reinterpret_cast<uint16_t*>(tmp);
+  uint8_t* dm = tmp + n * 2;
+  uint8_t* dr = tmp + n * 3;
+  launch_render(s, body->joints, body->radii, body->colors, gain, dd, dm, dr, ctx->st);
+  cudaError_t e = cudaGetLastError();
+  const cudaMemcpyKind kind = dst_kind == VC_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+  if (sigma > 0 && e == cudaSuccess) {  // render.cpp:50-61 on the host (libstdc++ RNG)
+    std::vector<uint16_t> h(n);
+    e = cudaMemcpyAsync(h.data(), dd, n * 2, cudaMemcpyDeviceToHost, ctx->st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->st);
+    std::mt19937_64 rng(seed * 46337 + camera * 131 + frame);
+    std::normal_distribution<double> gauss(0.0, 1.0);
+    for (size_t i = 0; i < n; ++i) {
+      uint16_t& d = h[i];
+      if (d == 0) continue;
+      const double sg = sigma * d / 2000.0;
+      d = static_cast<uint16_t>(std::clamp(std::lround(d + sg * gauss(rng)), 1L, 65535L));
+    }
+    if (e == cudaSuccess) e = cudaMemcpyAsync(dd, h.data(), n * 2, cudaMemcpyHostToDevice, ctx->st);
+  }
+  if (e == cudaSuccess && depth) e = cudaMemcpyAsync(depth, dd, n * 2, kind, ctx->st);
+  if (e == cudaSuccess && mask) e = cudaMemcpyAsync(mask, dm, n, kind, ctx->st);
+  if (e == cudaSuccess && rgb) e = cudaMemcpyAsync(rgb, dr, nr, kind, ctx->st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->st);
+  cudaFree(tmp);
+  if (e != cudaSuccess) return fail(ctx, VC_ERR_CUDA, cudaGetErrorString(e));
+  return VC_OK;
+}
+
+}  // extern "C"

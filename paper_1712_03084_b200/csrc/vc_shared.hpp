@@ -1,0 +1,124 @@
+// SPDX-License-Identifier: Apache-2.0
+// Host/device shared plain types and kernel-launcher declarations.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+
+namespace vc {
+
+constexpr int kMaxViews = 16;
+
+// volume_recon.hpp:24-28 — same layout as vc_grid_spec.
+struct DevGrid {
+  int32_t nx, ny, nz;
+  double origin[3];
+  double edge;
+};
+
+// One sensor, pre-digested on the host with the reference's own formulas
+// (types.hpp:46-49): inverse pose {R^T, -(R^T t)} and the RGB camera pose
+// pose.compose(rgb_relative).
+struct DevSensor {
+  double fx, fy, cx, cy;
+  int32_t w, h;
+  double R[9], t[3];    // depth camera -> world
+  double Ri[9], ti[3];  // world -> depth camera (Pose::inverse)
+  double rfx, rfy, rcx, rcy;
+  int32_t rw, rh;
+  double Rc[9], tc[3];  // RGB camera -> world
+};
+
+struct ViewPtrs {
+  const uint16_t* depth;
+  const uint8_t* mask;
+  const uint8_t* rgb;
+  int32_t dpitch, mpitch, rpitch;  // in elements (uint16 / uint8 / bytes)
+};
+
+struct SensorSet {
+  int32_t k;
+  DevSensor s[kMaxViews];
+  ViewPtrs v[kMaxViews];
+  int64_t pix_offset[kMaxViews + 1];  // prefix of w*h, for per-pixel arrays
+  int32_t row_offset[kMaxViews + 1];  // prefix of h, for per-row block counts
+};
+
+// Device control block: data-dependent scalars produced on the GPU and read
+// back once per frame.
+struct DevCtl {
+  int32_t P;          // oriented points
+  int32_t status;     // 0 ok, 2 empty scene
+  int32_t V, T, C;    // vertices, triangles, active cells
+  int32_t overflow;   // MC capacity exceeded
+  int32_t pad[2];
+  double bbox[6];
+  DevGrid grid;
+  double level;
+};
+
+// Point cloud (SoA, reference order: views in sensor order, pixels row-major).
+struct DevPoints {
+  double* pos;     // 3P
+  double* nrm;     // 3P
+  double* weight;  // P
+  int32_t* pix;    // 3P: px, py, sensor
+  int32_t cap;
+};
+
+struct MeshBufs {
+  double* pos;       // 3V
+  float* nrm;        // 3V
+  int32_t* tri;      // 3T
+  uint64_t* edge_id; // V
+  uint32_t* vbase;   // N (sparse): first vertex id * 8 | cut mask
+  int32_t* cells;    // C: active cell linear index
+  int32_t* cell_tri; // C: first triangle id
+  int32_t v_cap, t_cap, c_cap;
+  int32_t* blk;      // per-block (nv, nt, nc) x nblocks, then scanned offsets
+  int32_t nblk;
+};
+
+// Stage-timing events.  Profiled frames are launched directly (never from a
+// captured graph), so a plain record suffices.
+inline void record_event(cudaEvent_t e, cudaStream_t s) { cudaEventRecord(e, s); }
+
+// ----------------------------------------------------------------- launchers
+// k_preprocess.cu — build_cloud + confidence_weights + bbox + fit_grid
+size_t preprocess_scratch_bytes(const SensorSet& ss);
+void launch_preprocess(const SensorSet& ss, DevPoints pts, float* weight_maps, int32_t* scratch, DevCtl* ctl,
+                       int dims_x, int dims_y, int dims_z, int padding, double disc_mm, int sil_r, cudaStream_t st);
+// k_splat.cu
+void launch_clear(float4* acc, size_t n, cudaStream_t st);
+void launch_splat(const DevPoints& pts, const DevCtl* ctl, float4* acc, int mode, cudaStream_t st);
+void launch_splat_finalize(const float4* acc, size_t n, int mode, int negate, double sigma2, float* field,
+                           float* density, cudaStream_t st);
+// k_fft.cu — integrate_fft chain: acc (float4 U,d) -> A
+size_t spectrum_elems(int nx, int ny, int nz);  // complex elements per component
+void launch_integrate(const float4* acc, float2* spec, float* A, int nx, int ny, int nz, int mode,
+                      const float2* twiddles, cudaStream_t st, cudaEvent_t* ev /*nullable, 6 events*/);
+void upload_twiddles(float2* dev, int nx, int ny, int nz, cudaStream_t st);
+void prepare_integrate(int nx, int ny, int nz);
+size_t twiddle_elems(int nx, int ny, int nz);
+// k_mc.cu
+int iso_blocks();
+void launch_iso_level(const DevPoints& pts, const float* A, DevCtl* ctl, double* partial, int nblk_max,
+                      cudaStream_t st);
+int mc_blocks(int nx, int ny, int nz);
+void launch_marching_cubes(const float* A, DevCtl* ctl, MeshBufs mb, int nx, int ny, int nz, cudaStream_t st);
+void upload_case_table_data(const int8_t* counts, const int8_t* tris, cudaStream_t st);
+// k_texture.cu
+void launch_texture(const SensorSet& ss, const float* weight_maps, const double* vpos, const DevCtl* ctl,
+                    double eps_vis, uint8_t* vis, float2* uv, float* w, uint8_t* untex, uint8_t* rgb, int v_cap,
+                    cudaStream_t st);
+void launch_mesh_to_f32(const double* pos, float* posf, const DevCtl* ctl, int v_cap, cudaStream_t st);
+// k_synth.cu
+void launch_render(const DevSensor& s, const double* joints, const double* radii, const uint8_t* colors,
+                   double gain, uint16_t* depth, uint8_t* mask, uint8_t* rgb, cudaStream_t st);
+
+// vc_tables.cpp (host)
+void build_mc_table(int8_t counts[256], int8_t tris[256][5][3]);
+
+}  // namespace vc
