@@ -374,7 +374,7 @@ __global__ void __launch_bounds__(CCfg<NY>::THREADS, 2) iy_kernel(float2* __rest
 template <int NX>
 __global__ void __launch_bounds__(XCfg<NX>::THREADS, 2) ix_kernel(const float2* __restrict__ S0, float* __restrict__ A,
                                                        int rows, int H, float scale,
-                                                       const float2* __restrict__ tw) {
+                                                       const float2* __restrict__ tw, float2* __restrict__ rowmm) {
   using S = Shape<NX>;
   constexpr int T = S::R2, R1 = S::R1, TEAMS = XCfg<NX>::TEAMS, NH = NX / 2;
   extern __shared__ float2 dyn_smem[];
@@ -410,13 +410,26 @@ __global__ void __launch_bounds__(XCfg<NX>::THREADS, 2) ix_kernel(const float2* 
     }
   __syncthreads();
   fft_line<NX, true>(v, t, tw, ex);
-  if (live) {
+  float lo0 = 3.4e38f, hi0 = -3.4e38f, lo1 = 3.4e38f, hi1 = -3.4e38f;
 #pragma unroll
-    for (int k1 = 0; k1 < R1; ++k1) {
-      const int k = t + T * k1;
-      __stcs(A + (size_t)l0 * NX + k, v[k1].x * scale);
-      __stcs(A + (size_t)l1 * NX + k, v[k1].y * scale);
+  for (int k1 = 0; k1 < R1; ++k1) {
+    const int k = t + T * k1;
+    const float a0 = v[k1].x * scale, a1 = v[k1].y * scale;
+    lo0 = fminf(lo0, a0), hi0 = fmaxf(hi0, a0), lo1 = fminf(lo1, a1), hi1 = fmaxf(hi1, a1);
+    if (live) {
+      __stcs(A + (size_t)l0 * NX + k, a0);
+      __stcs(A + (size_t)l1 * NX + k, a1);
     }
+  }
+  // per-row min/max for marching-cubes row culling (team = T adjacent lanes)
+#pragma unroll
+  for (int o = T / 2; o > 0; o >>= 1) {
+    lo0 = fminf(lo0, __shfl_xor_sync(0xffffffffu, lo0, o)), hi0 = fmaxf(hi0, __shfl_xor_sync(0xffffffffu, hi0, o));
+    lo1 = fminf(lo1, __shfl_xor_sync(0xffffffffu, lo1, o)), hi1 = fmaxf(hi1, __shfl_xor_sync(0xffffffffu, hi1, o));
+  }
+  if (rowmm && live && t == 0) {
+    rowmm[l0] = make_float2(lo0, hi0);
+    rowmm[l1] = make_float2(lo1, hi1);
   }
 }
 
@@ -444,6 +457,7 @@ struct FftArgs {
   int nx, ny, nz, H, mode;
   const float2 *twx, *twy, *twz;
   cudaStream_t st;
+  float2* rowmm;
 };
 
 inline int hpitch(int nx) { return ((nx / 2 + 1) + 3) & ~3; }
@@ -509,7 +523,7 @@ struct RunIx {
     const int rows = a.ny * a.nz;
     const int grid = (rows / 2 + C::TEAMS - 1) / C::TEAMS;
     const float scale = (float)(1.0 / ((double)a.nx * a.ny * a.nz));
-    ix_kernel<N><<<grid, C::THREADS, C::SMEM, a.st>>>(a.S0, a.A, rows, a.H, scale, a.twx);
+    ix_kernel<N><<<grid, C::THREADS, C::SMEM, a.st>>>(a.S0, a.A, rows, a.H, scale, a.twx, a.rowmm);
   }
 };
 
@@ -542,8 +556,9 @@ void upload_twiddles(float2* dev, int nx, int ny, int nz, cudaStream_t st) {
 }
 
 void launch_integrate(const float4* acc, float2* spec, float* A, int nx, int ny, int nz, int mode,
-                      const float2* tw, cudaStream_t st, cudaEvent_t* ev) {
+                      const float2* tw, cudaStream_t st, cudaEvent_t* ev, float2* rowmm) {
   FftArgs a;
+  a.rowmm = rowmm;
   const size_t cs = spectrum_elems(nx, ny, nz);
   a.acc = acc, a.S0 = spec, a.S1 = spec + cs, a.S2 = spec + 2 * cs, a.A = A;
   a.nx = nx, a.ny = ny, a.nz = nz, a.H = hpitch(nx), a.mode = mode;

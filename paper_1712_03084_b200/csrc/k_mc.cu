@@ -1,21 +1,22 @@
 // SPDX-License-Identifier: Apache-2.0
 //
 // K9 — iso level (splat.cpp:91-101 with sample_trilinear, volume.hpp:59-81)
-// K10 — marching cubes (marching_cubes.cpp:131-210) as classify / scan /
-// emit, with no host round trip (counts live in DevCtl; capacity overflow
-// sets a flag the host checks once per frame).
+// K10 — marching cubes (marching_cubes.cpp:131-210) as row culling /
+// classify / scan / emit, with no host round trip (counts live in DevCtl;
+// capacity overflow sets a flag the host checks once per frame).
 //
-//   mc_count  one thread per voxel: owned cut edges (+x,+y,+z from the voxel,
-//             sign test vals >= level in fp64, marching_cubes.cpp:168-171)
-//             and the cell's triangle count from the generated table;
-//             per-CTA totals (vertices, triangles, active cells)
-//   mc_scan   single-CTA exclusive scan of the CTA totals
-//   mc_emit   recompute; vertex ids = rank of the cut edge in global edge id
-//             order ((z*ny+y)*nx+x)*3+axis (marching_cubes.cpp:139-142);
-//             positions (fp64, :153-155, volume.hpp:45) and gradient normals
-//             (:180-207); compact list of active cells in scan order
-//   mc_tris   one thread per active cell: triangles in the reference's cell
-//             scan order (z, y, x), table order within the cell
+//   mc_rows     per voxel row (y,z): can it hold a cut edge or cell?  (row
+//               min/max from the last FFT pass vs the level) -> ordered list
+//   mc_count    one CTA per active row, one thread per voxel: owned cut edges
+//               (+x,+y,+z, sign test vals >= level in fp64, :168-171) and the
+//               cell's triangle count from the generated table
+//   mc_scan     single-CTA exclusive scan of the per-row totals
+//   mc_emit     recompute; vertex ids = rank of the cut edge in global edge id
+//               order ((z*ny+y)*nx+x)*3+axis (:139-142); fp64 positions
+//               (:153-155, volume.hpp:45); compact list of active cells
+//   mc_normals  one thread per vertex: gradient normals (:180-207)
+//   mc_tris     one thread per active cell: triangles in the reference's cell
+//               scan order (z, y, x), table order within the cell
 #include <cfloat>
 
 #include "vc_device.cuh"
@@ -122,7 +123,7 @@ __device__ __forceinline__ VoxelInfo classify(const float* A, int nx, int ny, in
 
 __device__ __forceinline__ int3 block_exclusive_scan3(int3 v, int3* total) {
   __shared__ int3 warp_tot[kMcThreads / 32];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
   int3 inc = v;
   for (int o = 1; o < 32; o <<= 1) {
     const int a = __shfl_up_sync(0xffffffffu, inc.x, o), b = __shfl_up_sync(0xffffffffu, inc.y, o),
@@ -132,7 +133,7 @@ __device__ __forceinline__ int3 block_exclusive_scan3(int3 v, int3* total) {
   if (lane == 31) warp_tot[wid] = inc;
   __syncthreads();
   int3 pre = make_int3(0, 0, 0), tot = make_int3(0, 0, 0);
-  for (int i = 0; i < kMcThreads / 32; ++i) {
+  for (int i = 0; i < nw; ++i) {
     if (i < wid) pre.x += warp_tot[i].x, pre.y += warp_tot[i].y, pre.z += warp_tot[i].z;
     tot.x += warp_tot[i].x, tot.y += warp_tot[i].y, tot.z += warp_tot[i].z;
   }
@@ -141,25 +142,103 @@ __device__ __forceinline__ int3 block_exclusive_scan3(int3 v, int3* total) {
   return make_int3(pre.x + inc.x - v.x, pre.y + inc.y - v.y, pre.z + inc.z - v.z);
 }
 
-__global__ void __launch_bounds__(kMcThreads) mc_count_kernel(const float* __restrict__ A, const DevCtl* ctl, int nx,
-                                                              int ny, int nz, int3* blk) {
-  const size_t N = (size_t)nx * ny * nz;
-  const size_t v = (size_t)blockIdx.x * kMcThreads + threadIdx.x;
-  int3 c = make_int3(0, 0, 0);
-  if (v < N && ctl->status == 0) {
-    const VoxelInfo vi = classify(A, nx, ny, nz, v, ctl->level);
-    const int nt = vi.cfg >= 0 ? c_mc_count[vi.cfg] : 0;
-    c = make_int3(__popc(vi.mask), nt, nt > 0 ? 1 : 0);
+// ---------------------------------------------------------------- row culling
+// Work unit = voxel row (y, z): its x-edges, the y-edges to row y+1, the
+// z-edges to row z+1 and the cells (x, y, z).  A unit can hold a cut edge or
+// a non-trivial cell only if its 2-4 rows have values on both sides of the
+// level (max >= L and min < L), so per-row min/max (written by the final FFT
+// pass) skip the empty ~90% of the volume without reading it.
+__global__ void row_minmax_kernel(const float* __restrict__ A, int nx, int rows, float2* rowmm) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (warp >= rows) return;
+  float lo = 3.4e38f, hi = -3.4e38f;
+  for (int x = lane; x < nx; x += 32) {
+    const float v = __ldg(A + (size_t)warp * nx + x);
+    lo = fminf(lo, v), hi = fmaxf(hi, v);
   }
-  int3 tot;
-  block_exclusive_scan3(c, &tot);
-  if (threadIdx.x == 0) blk[blockIdx.x] = tot;
+  for (int o = 16; o > 0; o >>= 1) lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, o)), hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+  if (lane == 0) rowmm[warp] = make_float2(lo, hi);
 }
 
-__global__ void __launch_bounds__(1024) mc_scan_kernel(int3* blk, int n, DevCtl* ctl, int v_cap, int t_cap,
-                                                       int c_cap) {
+constexpr int kRowThreads = 256;
+
+__global__ void __launch_bounds__(kRowThreads) mc_rows_kernel(const float2* __restrict__ rowmm, const DevCtl* ctl,
+                                                              int ny, int nz, int32_t* blocklist, int32_t* blkcnt) {
+  const int u = blockIdx.x * kRowThreads + threadIdx.x;
+  bool active = false;
+  if (u < ny * nz && ctl->status == 0) {
+    const double L = ctl->level;
+    const int y = u % ny, z = u / ny;
+    float2 m = rowmm[u];
+    float lo = m.x, hi = m.y;
+    if (y + 1 < ny) m = rowmm[u + 1], lo = fminf(lo, m.x), hi = fmaxf(hi, m.y);
+    if (z + 1 < nz) m = rowmm[u + ny], lo = fminf(lo, m.x), hi = fmaxf(hi, m.y);
+    if (y + 1 < ny && z + 1 < nz) m = rowmm[u + ny + 1], lo = fminf(lo, m.x), hi = fmaxf(hi, m.y);
+    active = (double)hi >= L && (double)lo < L;
+  }
+  __shared__ int wc[kRowThreads / 32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const unsigned b = __ballot_sync(0xffffffffu, active);
+  if (lane == 0) wc[wid] = __popc(b);
+  __syncthreads();
+  int pre = 0, tot = 0;
+  for (int i = 0; i < kRowThreads / 32; ++i) pre += i < wid ? wc[i] : 0, tot += wc[i];
+  if (active) blocklist[blockIdx.x * kRowThreads + pre + __popc(b & ((1u << lane) - 1u))] = u;
+  if (threadIdx.x == 0) blkcnt[blockIdx.x] = tot;
+}
+
+// single CTA: gather the active units into one ordered list
+__global__ void __launch_bounds__(1024) mc_units_kernel(const int32_t* blocklist, const int32_t* blkcnt, int nblk,
+                                                        int32_t* units, DevCtl* ctl) {
+  __shared__ int off[4097];  // nblk <= 4096 (ny*nz <= 1M)
+  if (threadIdx.x == 0) {
+    int s = 0;
+    for (int b = 0; b < nblk; ++b) off[b] = s, s += blkcnt[b];
+    off[nblk] = s;
+    ctl->units = s;  // active unit count
+  }
+  __syncthreads();
+  for (int b = threadIdx.x >> 5; b < nblk; b += 32)
+    for (int j = threadIdx.x & 31; j < blkcnt[b]; j += 32) units[off[b] + j] = blocklist[b * kRowThreads + j];
+}
+
+__device__ __forceinline__ int3 block_reduce3(int3 v) {
+  __shared__ int3 wsum[32];
+  for (int o = 16; o > 0; o >>= 1)
+    v.x += __shfl_xor_sync(0xffffffffu, v.x, o), v.y += __shfl_xor_sync(0xffffffffu, v.y, o),
+        v.z += __shfl_xor_sync(0xffffffffu, v.z, o);
+  if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = v;
+  __syncthreads();
+  int3 t = make_int3(0, 0, 0);
+  for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t.x += wsum[i].x, t.y += wsum[i].y, t.z += wsum[i].z;
+  __syncthreads();
+  return t;
+}
+
+// per active unit: (owned cut edges, triangles, non-trivial cells)
+__global__ void __launch_bounds__(256) mc_count_kernel(const float* __restrict__ A, const DevCtl* ctl, int nx, int ny,
+                                                       int nz, const int32_t* __restrict__ units, int3* unitcnt) {
+  if (ctl->status != 0) return;
+  const int U = ctl->units;
+  const double L = ctl->level;
+  for (int i = blockIdx.x; i < U; i += gridDim.x) {
+    const size_t row0 = (size_t)units[i] * nx;
+    int3 c = make_int3(0, 0, 0);
+    for (int x = threadIdx.x; x < nx; x += blockDim.x) {
+      const VoxelInfo vi = classify(A, nx, ny, nz, row0 + x, L);
+      const int nt = vi.cfg >= 0 ? c_mc_count[vi.cfg] : 0;
+      c.x += __popc(vi.mask), c.y += nt, c.z += nt > 0 ? 1 : 0;
+    }
+    const int3 t = block_reduce3(c);
+    if (threadIdx.x == 0) unitcnt[i] = t;
+  }
+}
+
+__global__ void __launch_bounds__(1024) mc_scan_kernel(int3* blk, const DevCtl* ctl_in, DevCtl* ctl, int v_cap,
+                                                       int t_cap, int c_cap) {
   __shared__ int3 warp_sums[32];
   __shared__ int3 carry;
+  const int n = ctl_in->status == 0 ? ctl_in->units : 0;
   if (threadIdx.x == 0) carry = make_int3(0, 0, 0);
   __syncthreads();
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -198,6 +277,55 @@ __global__ void __launch_bounds__(1024) mc_scan_kernel(int3* blk, int n, DevCtl*
   }
 }
 
+// per active unit, in order: vertex ids = rank of the cut edge in global edge
+// id order; fp64 positions (marching_cubes.cpp:153-155, volume.hpp:45)
+__global__ void __launch_bounds__(256) mc_emit_kernel(const float* __restrict__ A, const DevCtl* ctl, int nx, int ny,
+                                                      int nz, const int32_t* __restrict__ units,
+                                                      const int3* __restrict__ unitoff, MeshBufs mb) {
+  if (ctl->status != 0 || ctl->overflow) return;
+  const int U = ctl->units;
+  const double L = ctl->level;
+  const DevGrid g = ctl->grid;
+  const size_t step[3] = {1, (size_t)nx, (size_t)nx * ny};
+  for (int i = blockIdx.x; i < U; i += gridDim.x) {
+    const int u = units[i];
+    const size_t row0 = (size_t)u * nx;
+    const int y = u % ny, z = u / ny;
+    int3 carry = unitoff[i];
+    for (int x0 = 0; x0 < nx; x0 += blockDim.x) {
+      const int x = x0 + threadIdx.x;
+      VoxelInfo vi{0, -1};
+      if (x < nx) vi = classify(A, nx, ny, nz, row0 + x, L);
+      const int nt = vi.cfg >= 0 ? c_mc_count[vi.cfg] : 0;
+      int3 tot;
+      const int3 ex = block_exclusive_scan3(make_int3(__popc(vi.mask), nt, nt > 0 ? 1 : 0), &tot);
+      const int vb = carry.x + ex.x, tb = carry.y + ex.y, cb = carry.z + ex.z;
+      const size_t v = row0 + x;
+      if (vi.mask) {
+        mb.vbase[v] = ((uint32_t)vb << 3) | (uint32_t)vi.mask;
+        const double v0 = (double)__ldg(A + v);
+        int id = vb;
+        for (int a = 0; a < 3; ++a) {
+          if (!(vi.mask & (1 << a))) continue;
+          const double v1 = (double)__ldg(A + v + step[a]);
+          double t = ddiv(dsub(L, v0), dsub(v1, v0));
+          t = t < 1e-6 ? 1e-6 : (t > 1.0 - 1e-6 ? 1.0 - 1e-6 : t);
+          double p[3] = {(double)x, (double)y, (double)z};
+          p[a] = dadd(p[a], t);
+          for (int c = 0; c < 3; ++c) mb.pos[3 * (size_t)id + c] = dadd(g.origin[c], dmul(g.edge, p[c]));
+          mb.edge_id[id] = (uint64_t)v * 3 + a;
+          ++id;
+        }
+      }
+      if (nt > 0) {
+        mb.cells[cb] = (int32_t)v;
+        mb.cell_tri[cb] = tb;
+      }
+      carry = make_int3(carry.x + tot.x, carry.y + tot.y, carry.z + tot.z);
+    }
+  }
+}
+
 // marching_cubes.cpp:178-207: outward normal = -normalize(trilinear blend of
 // central-difference gradients at the 8 surrounding nodes, clamped borders)
 __device__ void vertex_normal(const float* A, int nx, int ny, int nz, double px, double py, double pz, float* out) {
@@ -233,48 +361,24 @@ __device__ void vertex_normal(const float* A, int nx, int ny, int nz, double px,
   }
 }
 
-__global__ void __launch_bounds__(kMcThreads) mc_emit_kernel(const float* __restrict__ A, const DevCtl* ctl, int nx,
-                                                             int ny, int nz, const int3* __restrict__ blk,
-                                                             MeshBufs mb) {
-  const size_t N = (size_t)nx * ny * nz;
-  const size_t v = (size_t)blockIdx.x * kMcThreads + threadIdx.x;
-  const bool ok = ctl->status == 0;
+// one thread per vertex: marching_cubes.cpp:178-207 normals (fp64)
+__global__ void __launch_bounds__(256) mc_normals_kernel(const float* __restrict__ A, const DevCtl* ctl, int nx,
+                                                         int ny, int nz, MeshBufs mb) {
+  if (ctl->status != 0 || ctl->overflow) return;
+  const int V = ctl->V;
   const double L = ctl->level;
-  VoxelInfo vi{0, -1};
-  int nt = 0;
-  if (v < N && ok) {
-    vi = classify(A, nx, ny, nz, v, L);
-    nt = vi.cfg >= 0 ? c_mc_count[vi.cfg] : 0;
-  }
-  int3 tot;
-  const int3 ex = block_exclusive_scan3(make_int3(__popc(vi.mask), nt, nt > 0 ? 1 : 0), &tot);
-  const int3 b = blk[blockIdx.x];
-  const int vb = b.x + ex.x, tb = b.y + ex.y, cb = b.z + ex.z;
-  if (vi.mask) {
-    if (vb + __popc(vi.mask) <= mb.v_cap) {
-      mb.vbase[v] = ((uint32_t)vb << 3) | (uint32_t)vi.mask;
-      const DevGrid g = ctl->grid;
-      const int x = (int)(v % nx), y = (int)((v / nx) % ny), z = (int)(v / ((size_t)nx * ny));
-      const double v0 = (double)__ldg(A + v);
-      const size_t step[3] = {1, (size_t)nx, (size_t)nx * ny};
-      int id = vb;
-      for (int a = 0; a < 3; ++a) {
-        if (!(vi.mask & (1 << a))) continue;
-        const double v1 = (double)__ldg(A + v + step[a]);
-        double t = ddiv(dsub(L, v0), dsub(v1, v0));
-        t = t < 1e-6 ? 1e-6 : (t > 1.0 - 1e-6 ? 1.0 - 1e-6 : t);
-        double p[3] = {(double)x, (double)y, (double)z};
-        p[a] = dadd(p[a], t);
-        for (int c = 0; c < 3; ++c) mb.pos[3 * (size_t)id + c] = dadd(g.origin[c], dmul(g.edge, p[c]));
-        vertex_normal(A, nx, ny, nz, p[0], p[1], p[2], mb.nrm + 3 * (size_t)id);
-        mb.edge_id[id] = (uint64_t)v * 3 + a;
-        ++id;
-      }
-    }
-  }
-  if (nt > 0 && cb < mb.c_cap) {
-    mb.cells[cb] = (int32_t)v;
-    mb.cell_tri[cb] = tb;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < V; i += gridDim.x * blockDim.x) {
+    const uint64_t e = mb.edge_id[i];
+    const size_t v = (size_t)(e / 3);
+    const int a = (int)(e % 3);
+    const int x = (int)(v % nx), y = (int)((v / nx) % ny), z = (int)(v / ((size_t)nx * ny));
+    const size_t step = a == 0 ? 1 : (a == 1 ? (size_t)nx : (size_t)nx * ny);
+    const double v0 = (double)__ldg(A + v), v1 = (double)__ldg(A + v + step);
+    double t = ddiv(dsub(L, v0), dsub(v1, v0));
+    t = t < 1e-6 ? 1e-6 : (t > 1.0 - 1e-6 ? 1.0 - 1e-6 : t);
+    double p[3] = {(double)x, (double)y, (double)z};
+    p[a] = dadd(p[a], t);
+    vertex_normal(A, nx, ny, nz, p[0], p[1], p[2], mb.nrm + 3 * (size_t)i);
   }
 }
 
@@ -323,17 +427,30 @@ void launch_iso_level(const DevPoints& pts, const float* A, DevCtl* ctl, double*
   iso_final_kernel<<<1, 512, 0, st>>>(partial, kIsoBlocks, ctl);
 }
 
-int mc_blocks(int nx, int ny, int nz) {
-  const size_t N = (size_t)nx * ny * nz;
-  return (int)((N + kMcThreads - 1) / kMcThreads);
+int mc_blocks(int nx, int ny, int nz) {  // per-unit / per-block scratch entries
+  const int units = ny * nz;
+  return units + (units + kRowThreads - 1) / kRowThreads + 64;
+}
+
+void launch_row_minmax(const float* A, int nx, int ny, int nz, float2* rowmm, cudaStream_t st) {
+  const int rows = ny * nz;
+  row_minmax_kernel<<<(rows * 32 + 255) / 256, 256, 0, st>>>(A, nx, rows, rowmm);
 }
 
 void launch_marching_cubes(const float* A, DevCtl* ctl, MeshBufs mb, int nx, int ny, int nz, cudaStream_t st) {
-  const int nb = mc_blocks(nx, ny, nz);
-  int3* blk = reinterpret_cast<int3*>(mb.blk);
-  mc_count_kernel<<<nb, kMcThreads, 0, st>>>(A, ctl, nx, ny, nz, blk);
-  mc_scan_kernel<<<1, 1024, 0, st>>>(blk, nb, ctl, mb.v_cap, mb.t_cap, mb.c_cap);
-  mc_emit_kernel<<<nb, kMcThreads, 0, st>>>(A, ctl, nx, ny, nz, blk, mb);
+  const int units = ny * nz;
+  const int nblk = (units + kRowThreads - 1) / kRowThreads;
+  int32_t* blocklist = mb.blk;                 // units entries
+  int32_t* blkcnt = mb.blk + units;            // nblk entries
+  int32_t* ulist = mb.units;                   // units entries
+  int3* ucnt = reinterpret_cast<int3*>(mb.unitcnt);
+  const int threads = nx >= 256 ? 256 : (nx >= 128 ? 128 : (nx >= 64 ? 64 : 32));
+  mc_rows_kernel<<<nblk, kRowThreads, 0, st>>>(mb.rowmm, ctl, ny, nz, blocklist, blkcnt);
+  mc_units_kernel<<<1, 1024, 0, st>>>(blocklist, blkcnt, nblk, ulist, ctl);
+  mc_count_kernel<<<148 * 8, threads, 0, st>>>(A, ctl, nx, ny, nz, ulist, ucnt);
+  mc_scan_kernel<<<1, 1024, 0, st>>>(ucnt, ctl, ctl, mb.v_cap, mb.t_cap, mb.c_cap);
+  mc_emit_kernel<<<148 * 8, threads, 0, st>>>(A, ctl, nx, ny, nz, ulist, ucnt, mb);
+  mc_normals_kernel<<<148 * 4, 256, 0, st>>>(A, ctl, nx, ny, nz, mb);
   mc_tris_kernel<<<148 * 4, 256, 0, st>>>(A, ctl, nx, ny, nz, mb);
 }
 

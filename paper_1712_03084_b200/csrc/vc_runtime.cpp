@@ -58,7 +58,7 @@ struct vc_ctx {
 
   // grid-dependent
   int nx = 0, ny = 0, nz = 0;
-  Buf acc, spec, A, tw, vbase, blk;
+  Buf acc, spec, A, tw, vbase, blk, rowmm, units, unitcnt;
   // view staging + clouds
   Buf views, pts_pos, pts_nrm, pts_w, pts_pix, wmaps, pre_scratch, iso_partial;
   int pts_cap = 0;
@@ -265,13 +265,23 @@ vc_status ensure_mesh_caps(vc_ctx* ctx, int v_cap, int k) {
   return VC_OK;
 }
 
+vc_status ensure_mc_scratch(vc_ctx* ctx, int nx, int ny, int nz) {
+  (void)nx;
+  const size_t rows = (size_t)ny * nz;
+  VC_TRY(ensure(ctx, ctx->blk, (size_t)mc_blocks(nx, ny, nz) * sizeof(int32_t)));
+  VC_TRY(ensure(ctx, ctx->rowmm, rows * sizeof(float2)));
+  VC_TRY(ensure(ctx, ctx->units, rows * sizeof(int32_t)));
+  VC_TRY(ensure(ctx, ctx->unitcnt, rows * 3 * sizeof(int32_t)));
+  return VC_OK;
+}
+
 vc_status ensure_grid(vc_ctx* ctx, int nx, int ny, int nz) {
   const size_t N = (size_t)nx * ny * nz;
   VC_TRY(ensure(ctx, ctx->acc, N * sizeof(float4)));
   VC_TRY(ensure(ctx, ctx->spec, 3 * spectrum_elems(nx, ny, nz) * sizeof(float2)));
   VC_TRY(ensure(ctx, ctx->A, N * sizeof(float)));
   VC_TRY(ensure(ctx, ctx->vbase, N * sizeof(uint32_t)));
-  VC_TRY(ensure(ctx, ctx->blk, (size_t)mc_blocks(nx, ny, nz) * 3 * sizeof(int32_t)));
+  VC_TRY(ensure_mc_scratch(ctx, nx, ny, nz));
   VC_TRY(ensure(ctx, ctx->tw, twiddle_elems(nx, ny, nz) * sizeof(float2)));
   VC_TRY(ensure(ctx, ctx->iso_partial, 1024 * sizeof(double)));
   if (ctx->nx != nx || ctx->ny != ny || ctx->nz != nz) {
@@ -298,7 +308,10 @@ MeshBufs mesh_bufs(vc_ctx* ctx) {
   mb.cell_tri = P<int32_t>(ctx->m_celltri);
   mb.v_cap = ctx->v_cap, mb.t_cap = ctx->t_cap, mb.c_cap = ctx->c_cap;
   mb.blk = P<int32_t>(ctx->blk);
-  mb.nblk = mc_blocks(ctx->nx, ctx->ny, ctx->nz);
+  mb.nblk = 0;
+  mb.rowmm = P<float2>(ctx->rowmm);
+  mb.units = P<int32_t>(ctx->units);
+  mb.unitcnt = P<int32_t>(ctx->unitcnt);
   return mb;
 }
 
@@ -330,14 +343,14 @@ int enqueue_frame(vc_ctx* ctx, const FrameCfg& f) {
   n += 2;
   record(ctx, 2);
   launch_integrate(P<float4>(ctx->acc), P<float2>(ctx->spec), P<float>(ctx->A), f.nx, f.ny, f.nz, f.mode,
-                   P<float2>(ctx->tw), st, ctx->profiling ? &ctx->ev[14] : nullptr);
+                   P<float2>(ctx->tw), st, ctx->profiling ? &ctx->ev[14] : nullptr, P<float2>(ctx->rowmm));
   n += 5;
   record(ctx, 3);
   launch_iso_level(points(ctx), P<float>(ctx->A), ctx->ctl, P<double>(ctx->iso_partial), 1024, st);
   n += 2;
   record(ctx, 4);
   launch_marching_cubes(P<float>(ctx->A), ctx->ctl, mesh_bufs(ctx), f.nx, f.ny, f.nz, st);
-  n += 4;
+  n += 7;
   record(ctx, 5);
   launch_texture(ctx->ss, P<float>(ctx->wmaps), P<double>(ctx->m_pos), ctx->ctl, f.eps_vis, P<uint8_t>(ctx->t_vis),
                  P<float2>(ctx->t_uv), P<float>(ctx->t_w), P<uint8_t>(ctx->t_untex), P<uint8_t>(ctx->t_rgb),
@@ -771,7 +784,7 @@ vc_status vc_stage_integrate(vc_ctx* ctx, const float* field, int32_t nx, int32_
   for (size_t i = 0; i < N; ++i) h[i] = make_float4(-field[3 * i], -field[3 * i + 1], -field[3 * i + 2], 1.f);
   VC_CUDA(cudaMemcpyAsync(ctx->acc.p, h.data(), N * sizeof(float4), cudaMemcpyHostToDevice, ctx->st));
   launch_integrate(P<float4>(ctx->acc), P<float2>(ctx->spec), P<float>(ctx->A), nx, ny, nz, 1, P<float2>(ctx->tw),
-                   ctx->st, nullptr);
+                   ctx->st, nullptr, nullptr);
   VC_CUDA(cudaGetLastError());
   VC_CUDA(cudaMemcpyAsync(A, ctx->A.p, N * 4, cudaMemcpyDeviceToHost, ctx->st));
   VC_CUDA(cudaStreamSynchronize(ctx->st));
@@ -812,16 +825,16 @@ vc_status vc_stage_marching_cubes(vc_ctx* ctx, const float* A, const vc_grid_spe
   const size_t N = (size_t)nx * ny * nz;
   VC_TRY(ensure(ctx, ctx->A, N * 4));
   VC_TRY(ensure(ctx, ctx->vbase, N * 4));
-  VC_TRY(ensure(ctx, ctx->blk, (size_t)mc_blocks(nx, ny, nz) * 12));
+  VC_TRY(ensure_mc_scratch(ctx, nx, ny, nz));
   ctx->nx = ctx->ny = ctx->nz = 0;  // grid buffers no longer match a frame config
   if (ctx->v_cap == 0) VC_TRY(ensure_mesh_caps(ctx, (int)std::max<size_t>(N / 16, 1 << 16), kMaxViews));
   VC_CUDA(cudaMemcpyAsync(ctx->A.p, A, N * 4, cudaMemcpyHostToDevice, ctx->st));
   VC_TRY(upload_points(ctx, nullptr, nullptr, nullptr, 0, grid, 1));
   ctx->ctl_h->level = level;
   VC_CUDA(cudaMemcpyAsync(ctx->ctl, ctx->ctl_h, sizeof(DevCtl), cudaMemcpyHostToDevice, ctx->st));
+  launch_row_minmax(P<float>(ctx->A), nx, ny, nz, P<float2>(ctx->rowmm), ctx->st);
   for (int attempt = 0; attempt < 2; ++attempt) {
     MeshBufs mb = mesh_bufs(ctx);
-    mb.nblk = mc_blocks(nx, ny, nz);
     launch_marching_cubes(P<float>(ctx->A), ctx->ctl, mb, nx, ny, nz, ctx->st);
     VC_CUDA(cudaGetLastError());
     VC_TRY(read_ctl(ctx));

@@ -53,7 +53,8 @@ struct DevCtl {
   int32_t status;     // 0 ok, 2 empty scene
   int32_t V, T, C;    // vertices, triangles, active cells
   int32_t overflow;   // MC capacity exceeded
-  int32_t pad[2];
+  int32_t units;      // MC: active voxel-row units
+  int32_t pad;
   double bbox[6];
   DevGrid grid;
   double level;
@@ -77,8 +78,11 @@ struct MeshBufs {
   int32_t* cells;    // C: active cell linear index
   int32_t* cell_tri; // C: first triangle id
   int32_t v_cap, t_cap, c_cap;
-  int32_t* blk;      // per-block (nv, nt, nc) x nblocks, then scanned offsets
+  int32_t* blk;      // row-culling scratch (mc_blocks ints)
   int32_t nblk;
+  float2* rowmm;     // per voxel row (ny*nz): min, max of A
+  int32_t* units;    // ordered active row units (ny*nz)
+  int32_t* unitcnt;  // per active unit (nv, nt, nc), then exclusive offsets (3*ny*nz)
 };
 
 // Stage-timing events.  Profiled frames are launched directly (never from a
@@ -98,7 +102,8 @@ void launch_splat_finalize(const float4* acc, size_t n, int mode, int negate, do
 // k_fft.cu — integrate_fft chain: acc (float4 U,d) -> A
 size_t spectrum_elems(int nx, int ny, int nz);  // complex elements per component
 void launch_integrate(const float4* acc, float2* spec, float* A, int nx, int ny, int nz, int mode,
-                      const float2* twiddles, cudaStream_t st, cudaEvent_t* ev /*nullable, 6 events*/);
+                      const float2* twiddles, cudaStream_t st, cudaEvent_t* ev /*nullable, 6 events*/,
+                      float2* rowmm /*nullable: per-row min/max of A*/);
 void upload_twiddles(float2* dev, int nx, int ny, int nz, cudaStream_t st);
 void prepare_integrate(int nx, int ny, int nz);
 size_t twiddle_elems(int nx, int ny, int nz);
@@ -108,6 +113,7 @@ void launch_iso_level(const DevPoints& pts, const float* A, DevCtl* ctl, double*
                       cudaStream_t st);
 int mc_blocks(int nx, int ny, int nz);
 void launch_marching_cubes(const float* A, DevCtl* ctl, MeshBufs mb, int nx, int ny, int nz, cudaStream_t st);
+void launch_row_minmax(const float* A, int nx, int ny, int nz, float2* rowmm, cudaStream_t st);
 void upload_case_table_data(const int8_t* counts, const int8_t* tris, cudaStream_t st);
 // k_texture.cu
 void launch_texture(const SensorSet& ss, const float* weight_maps, const double* vpos, const DevCtl* ctl,
