@@ -134,14 +134,21 @@ __device__ __forceinline__ void relayout_for_inverse(float2* v) {
   }
 }
 
-// Exchange for teams of consecutive lanes (x passes): per-team padded tile.
+// Exchange for teams of consecutive lanes (x passes): per-team padded tile;
+// a team is T <= 32 adjacent lanes of one warp, so it syncs on its own lanes
+// and teams run independently (a team with two all-zero lines exits early).
 template <int N>
 struct ExTeam {
   float2* buf;  // R1 x (R2 + 1)
+  unsigned mask;
   __device__ void st(int j1, int k2, float2 v) { buf[j1 * (Shape<N>::R2 + 1) + k2] = v; }
   __device__ float2 ld(int j1, int k2) { return buf[j1 * (Shape<N>::R2 + 1) + k2]; }
-  __device__ void sync() { __syncthreads(); }
+  __device__ void sync() { __syncwarp(mask); }
 };
+template <int T>
+__device__ __forceinline__ unsigned team_mask(int team_lane0) {
+  return T >= 32 ? 0xffffffffu : (((1u << T) - 1u) << team_lane0);
+}
 // Exchange for column tiles (y/z passes): column index innermost.
 template <int N, int CW>
 struct ExCols {
@@ -179,25 +186,31 @@ struct CCfg {
 template <int NX>
 __global__ void __launch_bounds__(XCfg<NX>::THREADS, 2) fx_kernel(const float4* __restrict__ acc, float2* __restrict__ S0,
                                                        float2* __restrict__ S1, float2* __restrict__ S2, int rows,
-                                                       int H, size_t cstride, int mode,
+                                                       int H, const uint32_t* __restrict__ rowbits, int mode,
                                                        const float2* __restrict__ tw) {
   using S = Shape<NX>;
   constexpr int T = S::R2, R1 = S::R1, TEAMS = XCfg<NX>::TEAMS;
+  constexpr int CH = NX < 32 ? 0 : 5;  // log2 of the 32-voxel chunk (whole row when nx < 32)
   extern __shared__ float2 dyn_smem[];
   const int team = threadIdx.x / T, t = threadIdx.x % T;
   const int lane = threadIdx.x & 31, team_lane0 = lane - t;
-  ExTeam<NX> ex{dyn_smem + team * XCfg<NX>::TILE};
+  ExTeam<NX> ex{dyn_smem + team * XCfg<NX>::TILE, team_mask<T>(team_lane0)};
   const int pair = blockIdx.x * TEAMS + team;
   const int l0 = 2 * pair, l1 = l0 + 1;
-  const bool live = l1 < rows;
+  if (l1 >= rows) return;
+  const uint32_t bits0 = rowbits ? __ldg(rowbits + l0) : 0xffffffffu;
+  const uint32_t bits1 = rowbits ? __ldg(rowbits + l1) : 0xffffffffu;
+  if ((bits0 | bits1) == 0u) return;  // both rows empty: F-y treats them as zero
+  const bool live = true;
 
-  auto load_line = [&](int l, float2* xy, float* zc) {
+  auto load_line = [&](int l, uint32_t bits, float2* xy, float* zc) {
 #pragma unroll
     for (int q = 0; q < S::Q; ++q)
 #pragma unroll
       for (int j2 = 0; j2 < T; ++j2) {
         const int j = t + T * q + R1 * j2;
-        float4 a = live ? __ldcs(acc + (size_t)l * NX + j) : make_float4(0.f, 0.f, 0.f, 0.f);
+        const bool touched = CH == 0 ? bits != 0u : ((bits >> (j >> CH)) & 1u) != 0u;
+        float4 a = touched ? __ldcs(acc + (size_t)l * NX + j) : make_float4(0.f, 0.f, 0.f, 0.f);
         float s = 0.f;
         if (mode == 0) {
           if (a.w >= 1e-6f) s = -1.2247448713915890f / a.w;  // -sqrt(1.5)/d'
@@ -214,8 +227,8 @@ __global__ void __launch_bounds__(XCfg<NX>::THREADS, 2) fx_kernel(const float4* 
     const int src = team_lane0 + ((T - t) & (T - 1));
 #pragma unroll
     for (int k1 = 0; k1 <= R1 / 2; ++k1) {
-      const float2 pv = make_float2(__shfl_sync(0xffffffffu, v[R1 - 1 - k1].x, src),
-                                    __shfl_sync(0xffffffffu, v[R1 - 1 - k1].y, src));
+      const float2 pv = make_float2(__shfl_sync(ex.mask, v[R1 - 1 - k1].x, src),
+                                    __shfl_sync(ex.mask, v[R1 - 1 - k1].y, src));
       const float2 own = v[(R1 - k1) & (R1 - 1)];
       const float2 e = t == 0 ? own : pv;  // C[n-k]
       const float2 d = v[k1];
@@ -235,27 +248,47 @@ __global__ void __launch_bounds__(XCfg<NX>::THREADS, 2) fx_kernel(const float4* 
     }
   };
 
+  auto split_store_z = [&](float2* v, size_t offA, size_t offB, bool stA, bool stB) {
+    const int src = team_lane0 + ((T - t) & (T - 1));
+#pragma unroll
+    for (int k1 = 0; k1 <= R1 / 2; ++k1) {
+      const float2 pv = make_float2(__shfl_sync(ex.mask, v[R1 - 1 - k1].x, src),
+                                    __shfl_sync(ex.mask, v[R1 - 1 - k1].y, src));
+      const float2 own = v[(R1 - k1) & (R1 - 1)];
+      const float2 e = t == 0 ? own : pv;
+      const float2 d = v[k1];
+      const int k = t + T * k1;
+      if (k1 < R1 / 2 || t == 0) {
+        if (stA) __stcs(S2 + offA + k, make_float2(0.5f * (d.x + e.x), 0.5f * (d.y - e.y)));
+        if (stB) __stcs(S2 + offB + k, make_float2(0.5f * (d.y + e.y), -0.5f * (d.x - e.x)));
+      }
+    }
+  };
   float2 v[R1];
   float z0[R1];
-  load_line(l0, v, z0);
-  fft_line<NX, false>(v, t, tw, ex);
-  split_store(v, S0, (size_t)l0 * H, S1, (size_t)l0 * H, true);
+  load_line(l0, bits0, v, z0);
   float z1[R1];
-  load_line(l1, v, z1);
-  fft_line<NX, false>(v, t, tw, ex);
-  split_store(v, S0, (size_t)l1 * H, S1, (size_t)l1 * H, true);
+  if (bits0) {
+    fft_line<NX, false>(v, t, tw, ex);
+    split_store(v, S0, (size_t)l0 * H, S1, (size_t)l0 * H, true);
+  }
+  load_line(l1, bits1, v, z1);
+  if (bits1) {
+    fft_line<NX, false>(v, t, tw, ex);
+    split_store(v, S0, (size_t)l1 * H, S1, (size_t)l1 * H, true);
+  }
 #pragma unroll
   for (int i = 0; i < R1; ++i) v[i] = make_float2(z0[i], z1[i]);
   fft_line<NX, false>(v, t, tw, ex);
-  split_store(v, S2, (size_t)l0 * H, S2, (size_t)l1 * H, false);
-  (void)cstride;
+  split_store_z(v, (size_t)l0 * H, (size_t)l1 * H, bits0 != 0u, bits1 != 0u);
 }
 
 // ------------------------------------------------------------------ F-y
 template <int NY>
 __global__ void __launch_bounds__(CCfg<NY>::THREADS, 2) fy_kernel(float2* __restrict__ S0, float2* __restrict__ S1,
                                                                  const float2* __restrict__ S2, int nxh, int H,
-                                                                 const float2* __restrict__ tw) {
+                                                                 const float2* __restrict__ tw,
+                                                                 const uint32_t* __restrict__ rowbits) {
   using S = Shape<NY>;
   constexpr int T = S::R2, R1 = S::R1, kCW = CCfg<NY>::CW;
   extern __shared__ float2 sh[];
@@ -264,13 +297,23 @@ __global__ void __launch_bounds__(CCfg<NY>::THREADS, 2) fy_kernel(float2* __rest
   const bool live = kx < nxh;
   const size_t plane = (size_t)blockIdx.y * NY * H;
   ExCols<NY, kCW> ex{sh, c};
+  // rows F-x skipped (no splat contribution) are zero
+  uint32_t nz_rows = 0;  // bit (q*T + j2) set if row j is non-empty
+#pragma unroll
+  for (int q = 0; q < S::Q; ++q)
+#pragma unroll
+    for (int j2 = 0; j2 < T; ++j2) {
+      const int j = t + T * q + R1 * j2;
+      if (!rowbits || __ldg(rowbits + (size_t)blockIdx.y * NY + j)) nz_rows |= 1u << (q * T + j2);
+    }
   auto load = [&](const float2* src, float2* v) {
 #pragma unroll
     for (int q = 0; q < S::Q; ++q)
 #pragma unroll
       for (int j2 = 0; j2 < T; ++j2) {
         const int j = t + T * q + R1 * j2;
-        v[q * T + j2] = live ? __ldcs(src + plane + (size_t)j * H + kx) : make_float2(0.f, 0.f);
+        v[q * T + j2] = (live && ((nz_rows >> (q * T + j2)) & 1u)) ? __ldcs(src + plane + (size_t)j * H + kx)
+                                                                   : make_float2(0.f, 0.f);
       }
   };
   float2 d[R1], v[R1];
@@ -380,7 +423,7 @@ __global__ void __launch_bounds__(XCfg<NX>::THREADS, 2) ix_kernel(const float2* 
   extern __shared__ float2 dyn_smem[];
   const int team = threadIdx.x / T, t = threadIdx.x % T;
   float2* const tile = dyn_smem + team * XCfg<NX>::TILE;
-  ExTeam<NX> ex{tile};
+  ExTeam<NX> ex{tile, team_mask<T>((threadIdx.x & 31) - t)};
   const int pair = blockIdx.x * TEAMS + team;
   const int l0 = 2 * pair, l1 = l0 + 1;
   const bool live = l1 < rows;
@@ -390,7 +433,7 @@ __global__ void __launch_bounds__(XCfg<NX>::THREADS, 2) ix_kernel(const float2* 
     h0[k] = live ? __ldcs(S0 + (size_t)l0 * H + k) : make_float2(0.f, 0.f);
     h1[k] = live ? __ldcs(S0 + (size_t)l1 * H + k) : make_float2(0.f, 0.f);
   }
-  __syncthreads();
+  __syncwarp(ex.mask);
   // Hermitian extension with Re() of bins 0 and n/2 (numpy irfft / FFTW c2r)
   auto full = [&](const float2* h, int j) {
     if (j == 0) return make_float2(h[0].x, 0.f);
@@ -408,7 +451,7 @@ __global__ void __launch_bounds__(XCfg<NX>::THREADS, 2) ix_kernel(const float2* 
       const float2 f0 = full(h0, j), f1 = full(h1, j);
       v[q * T + j2] = make_float2(f0.x - f1.y, f0.y + f1.x);  // F0 + i F1
     }
-  __syncthreads();
+  __syncwarp(ex.mask);
   fft_line<NX, true>(v, t, tw, ex);
   float lo0 = 3.4e38f, hi0 = -3.4e38f, lo1 = 3.4e38f, hi1 = -3.4e38f;
 #pragma unroll
@@ -458,6 +501,7 @@ struct FftArgs {
   const float2 *twx, *twy, *twz;
   cudaStream_t st;
   float2* rowmm;
+  const uint32_t* rowbits;
 };
 
 inline int hpitch(int nx) { return ((nx / 2 + 1) + 3) & ~3; }
@@ -489,7 +533,7 @@ struct RunFx {
     using C = XCfg<N>;
     const int rows = a.ny * a.nz;
     const int grid = (rows / 2 + C::TEAMS - 1) / C::TEAMS;
-    fx_kernel<N><<<grid, C::THREADS, C::SMEM, a.st>>>(a.acc, a.S0, a.S1, a.S2, rows, a.H, 0, a.mode, a.twx);
+    fx_kernel<N><<<grid, C::THREADS, C::SMEM, a.st>>>(a.acc, a.S0, a.S1, a.S2, rows, a.H, a.rowbits, a.mode, a.twx);
   }
 };
 template <int N>
@@ -497,7 +541,7 @@ struct RunFy {
   static void run(const FftArgs& a) {
     using C = CCfg<N>;
     dim3 grid((a.nx / 2 + 1 + C::CW - 1) / C::CW, a.nz);
-    fy_kernel<N><<<grid, C::THREADS, C::SMEM, a.st>>>(a.S0, a.S1, a.S2, a.nx / 2 + 1, a.H, a.twy);
+    fy_kernel<N><<<grid, C::THREADS, C::SMEM, a.st>>>(a.S0, a.S1, a.S2, a.nx / 2 + 1, a.H, a.twy, a.rowbits);
   }
 };
 template <int N>
@@ -556,9 +600,10 @@ void upload_twiddles(float2* dev, int nx, int ny, int nz, cudaStream_t st) {
 }
 
 void launch_integrate(const float4* acc, float2* spec, float* A, int nx, int ny, int nz, int mode,
-                      const float2* tw, cudaStream_t st, cudaEvent_t* ev, float2* rowmm) {
+                      const float2* tw, cudaStream_t st, cudaEvent_t* ev, float2* rowmm, const uint32_t* rowbits) {
   FftArgs a;
   a.rowmm = rowmm;
+  a.rowbits = rowbits;
   const size_t cs = spectrum_elems(nx, ny, nz);
   a.acc = acc, a.S0 = spec, a.S1 = spec + cs, a.S2 = spec + 2 * cs, a.A = A;
   a.nx = nx, a.ny = ny, a.nz = nz, a.H = hpitch(nx), a.mode = mode;

@@ -14,6 +14,11 @@
 //
 // Binning is bit-exact: to_voxel (volume.hpp:44) and floor/lround are fp64
 // with the reference's operation order.
+//
+// Sparsity: the splat touches only a thin shell of the grid (~5% of 256^3).
+// Every scatter also sets the bit of its 32-voxel x-chunk in a per-row mask
+// (rowbits[(z*ny+y)], bit = x/32).  The next frame's clear zeroes only the
+// chunks those bits name, and the FFT's first pass loads only them.
 #include "vc_device.cuh"
 
 namespace vc {
@@ -25,6 +30,30 @@ __global__ void __launch_bounds__(256) clear_kernel(float4* acc, size_t n) {
   const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
     acc[i] = z;
+}
+
+// Zero the chunks the previous frame touched and reset their bits (one warp
+// per row, 32 lanes x float4 = one 512 B chunk per store instruction).
+__global__ void __launch_bounds__(256) sparse_clear_kernel(float4* acc, uint32_t* rowbits, int rows, int nx) {
+  const int lane = threadIdx.x & 31;
+  const int chunk = nx < 32 ? nx : 32;
+  for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < rows; r += (gridDim.x * blockDim.x) >> 5) {
+    uint32_t bits = rowbits[r];
+    if (!bits) continue;
+    const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+    while (bits) {
+      const int c = __ffs(bits) - 1;
+      bits &= bits - 1;
+      if (lane < chunk) acc[(size_t)r * nx + c * chunk + lane] = z;
+    }
+    __syncwarp();
+    if (lane == 0) rowbits[r] = 0u;
+  }
+}
+
+__device__ __forceinline__ void mark_chunks(uint32_t* rowbits, int row, int x0, int x1) {
+  const uint32_t m = (0xffffffffu >> (31 - (x1 >> 5))) & (0xffffffffu << (x0 >> 5));
+  atomicOr(rowbits + row, m);
 }
 
 __device__ __forceinline__ void red_add_v4(float4* addr, float4 v) {
@@ -39,7 +68,8 @@ __global__ void __launch_bounds__(kSplatThreads) splat_weighted_kernel(const dou
                                                                        const double* __restrict__ nrm,
                                                                        const double* __restrict__ wgt,
                                                                        const DevCtl* __restrict__ ctl,
-                                                                       float4* __restrict__ acc) {
+                                                                       float4* __restrict__ acc,
+                                                                       uint32_t* __restrict__ rowbits) {
   const int P = ctl->P;
   if (ctl->status != 0) return;
   const DevGrid g = ctl->grid;
@@ -51,7 +81,10 @@ __global__ void __launch_bounds__(kSplatThreads) splat_weighted_kernel(const dou
     const double cx = ddiv(dsub(__ldg(pos + 3 * p + 0), g.origin[0]), g.edge);
     const double cy = ddiv(dsub(__ldg(pos + 3 * p + 1), g.origin[1]), g.edge);
     const double cz = ddiv(dsub(__ldg(pos + 3 * p + 2), g.origin[2]), g.edge);
-    const int x = (int)floor(cx) - 1 + ox, y = (int)floor(cy) - 1 + oy, z = (int)floor(cz) - 1 + oz;
+    const int fx = (int)floor(cx);
+    const int x = fx - 1 + ox, y = (int)floor(cy) - 1 + oy, z = (int)floor(cz) - 1 + oz;
+    if (ox == 0 && y >= 0 && z >= 0 && y < g.ny && z < g.nz && fx + 2 >= 0 && fx - 1 < g.nx)
+      mark_chunks(rowbits, z * g.ny + y, max(fx - 1, 0), min(fx + 2, g.nx - 1));
     if (x < 0 || y < 0 || z < 0 || x >= g.nx || y >= g.ny || z >= g.nz) continue;
     const float dx = (float)(cx - (double)x), dy = (float)(cy - (double)y), dz = (float)(cz - (double)z);
     const float s = dx * dx + dy * dy + dz * dz;
@@ -66,7 +99,8 @@ __global__ void __launch_bounds__(kSplatThreads) splat_weighted_kernel(const dou
 // splat.cpp:40-56 simple mode: lround nearest voxel, (sum N, count)
 __global__ void __launch_bounds__(256) splat_simple_kernel(const double* __restrict__ pos,
                                                            const double* __restrict__ nrm,
-                                                           const DevCtl* __restrict__ ctl, float4* __restrict__ acc) {
+                                                           const DevCtl* __restrict__ ctl, float4* __restrict__ acc,
+                                                           uint32_t* __restrict__ rowbits) {
   const int P = ctl->P;
   if (ctl->status != 0) return;
   const DevGrid g = ctl->grid;
@@ -76,6 +110,7 @@ __global__ void __launch_bounds__(256) splat_simple_kernel(const double* __restr
     const double cz = ddiv(dsub(pos[3 * p + 2], g.origin[2]), g.edge);
     const long long x = lround_d(cx), y = lround_d(cy), z = lround_d(cz);
     if (!(x >= 0 && x < g.nx && y >= 0 && y < g.ny && z >= 0 && z < g.nz)) continue;
+    mark_chunks(rowbits, (int)(z * g.ny + y), (int)x, (int)x);
     red_add_v4(acc + ((size_t)z * g.ny + y) * g.nx + x,
                make_float4((float)nrm[3 * p + 0], (float)nrm[3 * p + 1], (float)nrm[3 * p + 2], 1.f));
   }
@@ -108,11 +143,16 @@ void launch_clear(float4* acc, size_t n, cudaStream_t st) {
   clear_kernel<<<148 * 8, 256, 0, st>>>(acc, n);
 }
 
-void launch_splat(const DevPoints& pts, const DevCtl* ctl, float4* acc, int mode, cudaStream_t st) {
+void launch_sparse_clear(float4* acc, uint32_t* rowbits, int rows, int nx, cudaStream_t st) {
+  sparse_clear_kernel<<<148 * 8, 256, 0, st>>>(acc, rowbits, rows, nx);
+}
+
+void launch_splat(const DevPoints& pts, const DevCtl* ctl, float4* acc, uint32_t* rowbits, int mode,
+                  cudaStream_t st) {
   if (mode == 0)
-    splat_weighted_kernel<<<148 * 8, kSplatThreads, 0, st>>>(pts.pos, pts.nrm, pts.weight, ctl, acc);
+    splat_weighted_kernel<<<148 * 8, kSplatThreads, 0, st>>>(pts.pos, pts.nrm, pts.weight, ctl, acc, rowbits);
   else
-    splat_simple_kernel<<<148 * 4, 256, 0, st>>>(pts.pos, pts.nrm, ctl, acc);
+    splat_simple_kernel<<<148 * 4, 256, 0, st>>>(pts.pos, pts.nrm, ctl, acc, rowbits);
 }
 
 void launch_splat_finalize(const float4* acc, size_t n, int mode, int negate, double sigma2, float* field,

@@ -58,7 +58,8 @@ struct vc_ctx {
 
   // grid-dependent
   int nx = 0, ny = 0, nz = 0;
-  Buf acc, spec, A, tw, vbase, blk, rowmm, units, unitcnt;
+  Buf acc, spec, A, tw, vbase, blk, rowmm, units, unitcnt, rowbits;
+  bool acc_dirty = true;  // accumulator contents unknown: next frame clears densely
   // view staging + clouds
   Buf views, pts_pos, pts_nrm, pts_w, pts_pix, wmaps, pre_scratch, iso_partial;
   int pts_cap = 0;
@@ -277,7 +278,10 @@ vc_status ensure_mc_scratch(vc_ctx* ctx, int nx, int ny, int nz) {
 
 vc_status ensure_grid(vc_ctx* ctx, int nx, int ny, int nz) {
   const size_t N = (size_t)nx * ny * nz;
+  const void* acc_before = ctx->acc.p;
   VC_TRY(ensure(ctx, ctx->acc, N * sizeof(float4)));
+  VC_TRY(ensure(ctx, ctx->rowbits, (size_t)ny * nz * sizeof(uint32_t)));
+  if (ctx->acc.p != acc_before || ctx->nx != nx || ctx->ny != ny || ctx->nz != nz) ctx->acc_dirty = true;
   VC_TRY(ensure(ctx, ctx->spec, 3 * spectrum_elems(nx, ny, nz) * sizeof(float2)));
   VC_TRY(ensure(ctx, ctx->A, N * sizeof(float)));
   VC_TRY(ensure(ctx, ctx->vbase, N * sizeof(uint32_t)));
@@ -335,15 +339,15 @@ int enqueue_frame(vc_ctx* ctx, const FrameCfg& f) {
                     f.nz, f.pad, f.disc, f.sil_r, st);
   n += 4;
   record(ctx, 1);
-  const size_t N = (size_t)f.nx * f.ny * f.nz;
   record(ctx, 12);
-  launch_clear(P<float4>(ctx->acc), N, st);
+  launch_sparse_clear(P<float4>(ctx->acc), P<uint32_t>(ctx->rowbits), f.ny * f.nz, f.nx, st);
   record(ctx, 13);
-  launch_splat(points(ctx), ctx->ctl, P<float4>(ctx->acc), f.mode, st);
+  launch_splat(points(ctx), ctx->ctl, P<float4>(ctx->acc), P<uint32_t>(ctx->rowbits), f.mode, st);
   n += 2;
   record(ctx, 2);
   launch_integrate(P<float4>(ctx->acc), P<float2>(ctx->spec), P<float>(ctx->A), f.nx, f.ny, f.nz, f.mode,
-                   P<float2>(ctx->tw), st, ctx->profiling ? &ctx->ev[14] : nullptr, P<float2>(ctx->rowmm));
+                   P<float2>(ctx->tw), st, ctx->profiling ? &ctx->ev[14] : nullptr, P<float2>(ctx->rowmm),
+                   P<uint32_t>(ctx->rowbits));
   n += 5;
   record(ctx, 3);
   launch_iso_level(points(ctx), P<float>(ctx->A), ctx->ctl, P<double>(ctx->iso_partial), 1024, st);
@@ -362,6 +366,12 @@ int enqueue_frame(vc_ctx* ctx, const FrameCfg& f) {
 }
 
 vc_status run_frame(vc_ctx* ctx, const FrameCfg& f) {
+  if (ctx->acc_dirty) {  // outside the graph: dense clear once, then sparse clears
+    launch_clear(P<float4>(ctx->acc), (size_t)f.nx * f.ny * f.nz, ctx->st);
+    VC_CUDA(cudaMemsetAsync(ctx->rowbits.p, 0, (size_t)f.ny * f.nz * sizeof(uint32_t), ctx->st));
+    VC_CUDA(cudaGetLastError());
+    ctx->acc_dirty = false;
+  }
   if (!ctx->graphs || ctx->profiling) {  // profiled frames: direct launches + events
     ctx->kernels_per_frame = enqueue_frame(ctx, f);
     VC_CUDA(cudaGetLastError());
@@ -471,7 +481,7 @@ vc_status vc_ctx_destroy(vc_ctx* ctx) {
   cudaSetDevice(ctx->device);
   if (ctx->st) cudaStreamSynchronize(ctx->st);
   if (ctx->gexec) cudaGraphExecDestroy(ctx->gexec);
-  for (Buf* b : {&ctx->acc, &ctx->spec, &ctx->A, &ctx->tw, &ctx->vbase, &ctx->blk, &ctx->views, &ctx->pts_pos,
+  for (Buf* b : {&ctx->acc, &ctx->spec, &ctx->A, &ctx->tw, &ctx->vbase, &ctx->blk, &ctx->rowmm, &ctx->units, &ctx->unitcnt, &ctx->rowbits, &ctx->views, &ctx->pts_pos,
                  &ctx->pts_nrm, &ctx->pts_w, &ctx->pts_pix, &ctx->wmaps, &ctx->pre_scratch, &ctx->iso_partial,
                  &ctx->m_pos, &ctx->m_nrm, &ctx->m_tri, &ctx->m_eid, &ctx->m_cells, &ctx->m_celltri, &ctx->m_posf,
                  &ctx->t_vis, &ctx->t_uv, &ctx->t_w, &ctx->t_untex, &ctx->t_rgb})
@@ -752,6 +762,9 @@ vc_status vc_stage_splat(vc_ctx* ctx, const double* pos, const double* nrm, cons
   cudaSetDevice(ctx->device);
   const size_t N = (size_t)grid->nx * grid->ny * grid->nz;
   VC_TRY(ensure(ctx, ctx->acc, N * sizeof(float4)));
+  VC_TRY(ensure(ctx, ctx->rowbits, (size_t)grid->ny * grid->nz * sizeof(uint32_t)));
+  ctx->acc_dirty = true;
+  VC_CUDA(cudaMemsetAsync(ctx->rowbits.p, 0, (size_t)grid->ny * grid->nz * sizeof(uint32_t), ctx->st));
   std::vector<double> ones;
   if (!weight) ones.assign(std::max<int64_t>(n, 1), 1.0), weight = ones.data();
   VC_TRY(upload_points(ctx, pos, nrm, weight, n, grid, 1));
@@ -759,7 +772,7 @@ vc_status vc_stage_splat(vc_ctx* ctx, const double* pos, const double* nrm, cons
   VC_TRY(ensure(ctx, fbuf, N * 12));
   VC_TRY(ensure(ctx, dbuf, N * 4));
   launch_clear(P<float4>(ctx->acc), N, ctx->st);
-  launch_splat(points(ctx), ctx->ctl, P<float4>(ctx->acc), mode, ctx->st);
+  launch_splat(points(ctx), ctx->ctl, P<float4>(ctx->acc), P<uint32_t>(ctx->rowbits), mode, ctx->st);
   const double sigma2 = std::sqrt(1.5) * (std::sqrt(3.0) / 2.0 * grid->edge_mm);  // splat.cpp:35-36
   launch_splat_finalize(P<float4>(ctx->acc), N, mode, negate, sigma2, P<float>(fbuf), P<float>(dbuf), ctx->st);
   cudaError_t e = cudaGetLastError();
@@ -783,8 +796,9 @@ vc_status vc_stage_integrate(vc_ctx* ctx, const float* field, int32_t nx, int32_
   std::vector<float4> h(N);
   for (size_t i = 0; i < N; ++i) h[i] = make_float4(-field[3 * i], -field[3 * i + 1], -field[3 * i + 2], 1.f);
   VC_CUDA(cudaMemcpyAsync(ctx->acc.p, h.data(), N * sizeof(float4), cudaMemcpyHostToDevice, ctx->st));
+  ctx->acc_dirty = true;  // dense contents from the host
   launch_integrate(P<float4>(ctx->acc), P<float2>(ctx->spec), P<float>(ctx->A), nx, ny, nz, 1, P<float2>(ctx->tw),
-                   ctx->st, nullptr, nullptr);
+                   ctx->st, nullptr, nullptr, nullptr);
   VC_CUDA(cudaGetLastError());
   VC_CUDA(cudaMemcpyAsync(A, ctx->A.p, N * 4, cudaMemcpyDeviceToHost, ctx->st));
   VC_CUDA(cudaStreamSynchronize(ctx->st));

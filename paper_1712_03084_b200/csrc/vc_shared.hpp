@@ -96,14 +96,17 @@ void launch_preprocess(const SensorSet& ss, DevPoints pts, float* weight_maps, i
                        int dims_x, int dims_y, int dims_z, int padding, double disc_mm, int sil_r, cudaStream_t st);
 // k_splat.cu
 void launch_clear(float4* acc, size_t n, cudaStream_t st);
-void launch_splat(const DevPoints& pts, const DevCtl* ctl, float4* acc, int mode, cudaStream_t st);
+void launch_splat(const DevPoints& pts, const DevCtl* ctl, float4* acc, uint32_t* rowbits, int mode,
+                  cudaStream_t st);
+void launch_sparse_clear(float4* acc, uint32_t* rowbits, int rows, int nx, cudaStream_t st);
 void launch_splat_finalize(const float4* acc, size_t n, int mode, int negate, double sigma2, float* field,
                            float* density, cudaStream_t st);
 // k_fft.cu — integrate_fft chain: acc (float4 U,d) -> A
 size_t spectrum_elems(int nx, int ny, int nz);  // complex elements per component
 void launch_integrate(const float4* acc, float2* spec, float* A, int nx, int ny, int nz, int mode,
                       const float2* twiddles, cudaStream_t st, cudaEvent_t* ev /*nullable, 6 events*/,
-                      float2* rowmm /*nullable: per-row min/max of A*/);
+                      float2* rowmm /*nullable: per-row min/max of A*/,
+                      const uint32_t* rowbits /*nullable: touched 32-voxel chunks per row; null = dense*/);
 void upload_twiddles(float2* dev, int nx, int ny, int nz, cudaStream_t st);
 void prepare_integrate(int nx, int ny, int nz);
 size_t twiddle_elems(int nx, int ny, int nz);
