@@ -162,14 +162,39 @@ def cpu_baseline_sample():
 
 
 # ------------------------------------------------------------------ GPU arm
-def alg_bytes(nx, ny, nz, P, V, T, k):
-    """Algorithmic bytes per launch (fp32 device layout, each tensor read once
-    and written once) — SURVEY §8(d), adapted to the fused kernels."""
+def sparse_stats(pos, origin, edge, nx, ny, nz):
+    """Touched 32-voxel x-chunks and non-empty voxel rows of the splat
+    accumulator (the same marking rule as k_splat.cu: rows floor(c)-1..+2 in
+    y and z, chunks of x in [floor(cx)-1, floor(cx)+2])."""
+    c = (np.asarray(pos) - np.asarray(origin)) / edge
+    f = np.floor(c).astype(np.int64)
+    keys = []
+    for oy in range(4):
+        for oz in range(4):
+            y = f[:, 1] - 1 + oy
+            z = f[:, 2] - 1 + oz
+            ok = (y >= 0) & (y < ny) & (z >= 0) & (z < nz) & (f[:, 0] + 2 >= 0) & (f[:, 0] - 1 < nx)
+            row = (z * ny + y)[ok]
+            c0 = np.maximum(f[ok, 0] - 1, 0) // 32
+            c1 = np.minimum(f[ok, 0] + 2, nx - 1) // 32
+            keys += [row * 64 + c0, row * 64 + c1]
+    keys = np.unique(np.concatenate(keys)) if keys else np.zeros(0, np.int64)
+    return len(keys), len(np.unique(keys // 64))
+
+
+def alg_bytes(nx, ny, nz, P, V, T, k, chunks, nzrows):
+    """Compulsory bytes per launch in the fp32 device layout (each tensor read
+    once and written once; the sparse clear / F-x / F-y touch only the splat's
+    32-voxel chunks and non-empty rows) — SURVEY §8(d) adapted, see DESIGN.md."""
     N = nx * ny * nz
     Nh = nz * ny * (nx // 2 + 1)
-    return {"clear": 16 * N, "splat": 16 * 64 * P, "fft_x": 16 * N + 3 * 8 * Nh, "fft_y": 3 * 8 * Nh + 2 * 8 * Nh,
-            "fft_z": 2 * 8 * Nh + 8 * Nh, "ifft_y": 2 * 8 * Nh, "ifft_x": 8 * Nh + 4 * N, "mc": 2 * 4 * N,
-            "preprocess": k * W * H * 7 + P * 60, "iso": P * 32, "texture": V * (24 + 13 * k) + T * 0}
+    rows = ny * nz
+    line = 8 * (nx // 2 + 1)
+    return {"clear": 16 * 32 * chunks + 8 * rows, "splat": 16 * 64 * P + 4 * 16 * P,
+            "fft_x": 16 * 32 * chunks + 4 * rows + 3 * line * nzrows,
+            "fft_y": 3 * line * nzrows + 4 * rows + 2 * 8 * Nh,
+            "fft_z": 2 * 8 * Nh + 8 * Nh, "ifft_y": 2 * 8 * Nh, "ifft_x": 8 * Nh + 4 * N + 8 * rows,
+            "mc": 8 * rows, "preprocess": k * W * H * 7 + P * 60, "iso": P * 32, "texture": V * (24 + 13 * k)}
 
 
 def run_gpu(args):
@@ -276,7 +301,10 @@ def run_gpu(args):
     names = ["preprocess", "clear", "splat", "fft_x", "fft_y", "fft_z", "ifft_y", "ifft_x", "iso", "mc", "texture"]
     kernel_ms = dict(zip(names, ker.tolist()))
     P, V, T = out.point_count, out.vertex_count, out.triangle_count
-    ab = alg_bytes(*DIMS, P, V, T, K_VIEWS)
+    pos = np.zeros((P, 3))
+    L.check(lib.vc_export_points(h, C.c_void_p(pos.ctypes.data), None, None, None, None), h)
+    chunks, nzrows = sparse_stats(pos, out.grid.origin[:], out.grid.edge_mm, *DIMS)
+    ab = alg_bytes(*DIMS, P, V, T, K_VIEWS, chunks, nzrows)
     bw = {n: ab[n] / (kernel_ms[n] * 1e-3) / 1e9 for n in names if kernel_ms[n] > 0}
     if not all(n in bw for n in ["clear", "fft_x", "fft_y", "fft_z", "ifft_y", "ifft_x"]):
         raise RuntimeError(f"per-kernel event timings missing: {kernel_ms}")
@@ -314,6 +342,9 @@ def run_gpu(args):
             "kernel_ms": {k: round(v, 4) for k, v in kernel_ms.items()},
             "kernel_gbs": {k: round(v, 1) for k, v in bw.items()},
             "mesh": {"points": P, "vertices": V, "triangles": T},
+            "sparsity": {"touched_chunks": chunks, "chunks_total": DIMS[1] * DIMS[2] * (DIMS[0] // 32),
+                         "nonzero_rows": nzrows, "rows_total": DIMS[1] * DIMS[2]},
+            "algorithmic_bytes": ab,
             "clocks": clk.summary(),
             "wall_s": wall,
         }

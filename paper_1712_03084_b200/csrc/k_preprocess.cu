@@ -4,13 +4,19 @@
 // (/root/reference/proj/core/src/recon/cloud.cpp:19-117), the foreground
 // bounding box and fit_grid (reconstruct.cpp:16-35, 56-68).
 //
-// One CTA per depth row (rows of all views concatenated), so the CTA order is
-// the reference's point order (views in sensor order, pixels row-major):
-//   pre_count  -> points per row
-//   pre_scan   -> exclusive scan over rows (single CTA), P
-//   pre_emit   -> recompute, compact in order, write SoA points + weight map
-//                 row + per-row bbox
-//   pre_fit    -> reduce bbox, fit_grid, empty-scene status
+//   pre_prefix  one warp per depth row: inclusive prefix count of the mask
+//               along x (the 21x21 silhouette box count of cloud.cpp:89-106
+//               becomes 2 loads per window row)
+//   pre_points  one CTA per depth row (rows of all views concatenated, so CTA
+//               order = the reference's point order): the rows y-1..y+1 are
+//               staged in shared memory, each pixel evaluates its six incident
+//               triangles in the reference's accumulation order
+//               (cloud.cpp:53-71), W = W1*W2 (cloud.cpp:108-114); points are
+//               compacted in row order into a per-row staging slot, the
+//               weight-map row and the row bbox are written
+//   pre_scan    exclusive scan of the per-row counts (single CTA) -> P
+//   pre_gather  one warp per row: staged points -> final SoA at the row offset
+//   pre_fit     bbox reduction + fit_grid + empty-scene status
 // fp64 with the reference's operation order and no FMA (vc_device.cuh), so
 // positions — hence every downstream binning decision — are bit-exact.
 #include <cfloat>
@@ -22,29 +28,57 @@ namespace {
 
 constexpr int kThreads = 256;
 
-struct RowCtx {
-  const DevSensor* s;
-  const ViewPtrs* v;
+__device__ __forceinline__ void row_of_block(const SensorSet& ss, int b, int* k, int* y) {
+  int kk = 0;
+  while (kk + 1 < ss.k && b >= ss.row_offset[kk + 1]) ++kk;
+  *k = kk;
+  *y = b - ss.row_offset[kk];
+}
+
+// inclusive prefix of (mask != 0) along each row: pref[row][x]
+__global__ void __launch_bounds__(256) pre_prefix_kernel(const __grid_constant__ SensorSet ss, int rows,
+                                                         uint16_t* __restrict__ pref, int pitch) {
+  const int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (r >= rows) return;
+  int k, y;
+  row_of_block(ss, r, &k, &y);
+  const ViewPtrs& v = ss.v[k];
+  const int w = ss.s[k].w;
+  const uint8_t* m = v.mask + (size_t)y * v.mpitch;
+  uint16_t* o = pref + (size_t)r * pitch;
+  int carry = 0;
+  for (int x0 = 0; x0 < w; x0 += 32) {
+    const int x = x0 + lane;
+    int c = (x < w && m[x]) ? 1 : 0;
+    for (int d = 1; d < 32; d <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, c, d);
+      if (lane >= d) c += t;
+    }
+    if (x < w) o[x] = (uint16_t)(carry + c);
+    carry += __shfl_sync(0xffffffffu, c, 31);
+  }
+}
+
+struct Rows3 {
+  const uint16_t* d;  // [3][w] depth of rows y-1, y, y+1 (0 = invalid or out of image)
   int w, h, y;
+  const DevSensor* s;
+  __device__ bool valid(int x, int yy) const {
+    if (x < 0 || x >= w || yy < 0 || yy >= h || yy < y - 1 || yy > y + 1) return false;
+    return d[(yy - y + 1) * w + x] != 0;
+  }
+  // camera.cpp:12-17 backproject_local with u = (x, yy)
+  __device__ d3 local(int x, int yy) const {
+    const double z = (double)d[(yy - y + 1) * w + x];
+    return {ddiv(dmul(dsub((double)x, s->cx), z), s->fx), ddiv(dmul(dsub((double)yy, s->cy), z), s->fy), z};
+  }
 };
 
-__device__ __forceinline__ bool valid_px(const RowCtx& c, int x, int y) {
-  if (x < 0 || y < 0 || x >= c.w || y >= c.h) return false;
-  return __ldg(c.v->mask + (size_t)y * c.v->mpitch + x) != 0 && __ldg(c.v->depth + (size_t)y * c.v->dpitch + x) != 0;
-}
-
-// camera.cpp:12-17 backproject_local with u = (x, y) and z = depth
-__device__ __forceinline__ d3 local_px(const RowCtx& c, int x, int y) {
-  const double z = (double)__ldg(c.v->depth + (size_t)y * c.v->dpitch + x);
-  const DevSensor& s = *c.s;
-  return {ddiv(dmul(dsub((double)x, s.cx), z), s.fx), ddiv(dmul(dsub((double)y, s.cy), z), s.fy), z};
-}
-
-// cloud.cpp:38-51 add_triangle(ia, ib, ic), accumulated into (sum, count)
-__device__ __forceinline__ void add_tri(const RowCtx& c, int ax, int ay, int bx, int by, int cx, int cy,
-                                        double disc, d3& sum, int& cnt) {
-  if (!valid_px(c, ax, ay) || !valid_px(c, bx, by) || !valid_px(c, cx, cy)) return;
-  const d3 a = local_px(c, ax, ay), b = local_px(c, bx, by), cc = local_px(c, cx, cy);
+// cloud.cpp:38-51 add_triangle(ia, ib, ic)
+__device__ __forceinline__ void add_tri(const Rows3& c, int ax, int ay, int bx, int by, int cx, int cy, double disc,
+                                        d3& sum, int& cnt) {
+  if (!c.valid(ax, ay) || !c.valid(bx, by) || !c.valid(cx, cy)) return;
+  const d3 a = c.local(ax, ay), b = c.local(bx, by), cc = c.local(cx, cy);
   const double lo = fmin(fmin(a.z, b.z), cc.z), hi = fmax(fmax(a.z, b.z), cc.z);
   if (dsub(hi, lo) > disc) return;
   d3 n = cross3(sub3(cc, a), sub3(b, a));
@@ -55,61 +89,129 @@ __device__ __forceinline__ void add_tri(const RowCtx& c, int ax, int ay, int bx,
   ++cnt;
 }
 
-// cloud.cpp:53-71 for pixel (x, y): the six incident triangles in the
-// reference's accumulation order, then mean, normalise, camera-facing flip.
-__device__ bool point_at(const RowCtx& c, int x, int y, double disc, d3* local_out, d3* n_out) {
-  if (!valid_px(c, x, y)) return false;
+// cloud.cpp:53-71: the six incident triangles of pixel (x, y) in the
+// reference's order Q(x-1,y-1).T2, Q(x,y-1).T1, Q(x,y-1).T2, Q(x-1,y).T1,
+// Q(x-1,y).T2, Q(x,y).T1; mean, normalise, camera-facing flip.
+__device__ bool point_at(const Rows3& c, int x, double disc, d3* local_out, d3* n_out) {
+  const int y = c.y, w = c.w, h = c.h;
+  if (!c.valid(x, y)) return false;
   d3 sum{0.0, 0.0, 0.0};
   int cnt = 0;
-  const int w = c.w, h = c.h;
-  if (x >= 1 && y >= 1) add_tri(c, x, y - 1, x, y, x - 1, y, disc, sum, cnt);                // Q(x-1,y-1).T2
+  if (x >= 1 && y >= 1) add_tri(c, x, y - 1, x, y, x - 1, y, disc, sum, cnt);
   if (x <= w - 2 && y >= 1) {
-    add_tri(c, x, y - 1, x + 1, y - 1, x, y, disc, sum, cnt);                                 // Q(x,y-1).T1
-    add_tri(c, x + 1, y - 1, x + 1, y, x, y, disc, sum, cnt);                                 // Q(x,y-1).T2
+    add_tri(c, x, y - 1, x + 1, y - 1, x, y, disc, sum, cnt);
+    add_tri(c, x + 1, y - 1, x + 1, y, x, y, disc, sum, cnt);
   }
   if (x >= 1 && y <= h - 2) {
-    add_tri(c, x - 1, y, x, y, x - 1, y + 1, disc, sum, cnt);                                 // Q(x-1,y).T1
-    add_tri(c, x, y, x, y + 1, x - 1, y + 1, disc, sum, cnt);                                 // Q(x-1,y).T2
+    add_tri(c, x - 1, y, x, y, x - 1, y + 1, disc, sum, cnt);
+    add_tri(c, x, y, x, y + 1, x - 1, y + 1, disc, sum, cnt);
   }
-  if (x <= w - 2 && y <= h - 2) add_tri(c, x, y, x + 1, y, x, y + 1, disc, sum, cnt);         // Q(x,y).T1
+  if (x <= w - 2 && y <= h - 2) add_tri(c, x, y, x + 1, y, x, y + 1, disc, sum, cnt);
   if (cnt == 0) return false;
   d3 n = div3(sum, (double)cnt);
   const double len = norm3(n);
   if (len < 1e-12) return false;
   n = div3(n, len);
-  const d3 local = local_px(c, x, y);
+  const d3 local = c.local(x, y);
   if (dot3(n, local) > 0) n = neg3(n);
   *local_out = local;
   *n_out = n;
   return true;
 }
 
-__device__ __forceinline__ void row_of_block(const SensorSet& ss, int b, int* k, int* y) {
-  int kk = 0;
-  while (kk + 1 < ss.k && b >= ss.row_offset[kk + 1]) ++kk;
-  *k = kk;
-  *y = b - ss.row_offset[kk];
-}
+struct Staged {  // per-point staging record (row-local order)
+  double pos[3], nrm[3], w;
+  int32_t px;
+};
 
-__global__ void __launch_bounds__(kThreads) pre_count_kernel(const __grid_constant__ SensorSet ss, double disc,
-                                                             int32_t* row_counts) {
+__global__ void __launch_bounds__(kThreads) pre_points_kernel(const __grid_constant__ SensorSet ss, double disc,
+                                                              int sil_r, const uint16_t* __restrict__ pref, int ppitch,
+                                                              Staged* __restrict__ stage, int spitch,
+                                                              int32_t* __restrict__ row_counts,
+                                                              float* __restrict__ weight_maps,
+                                                              double* __restrict__ row_bbox) {
+  extern __shared__ uint16_t rows3[];  // [3][w]
+  __shared__ int warp_cnt[kThreads / 32];
+  __shared__ double bb[kThreads / 32][6];
   int k, y;
   row_of_block(ss, blockIdx.x, &k, &y);
-  RowCtx c{&ss.s[k], &ss.v[k], ss.s[k].w, ss.s[k].h, y};
-  int n = 0;
-  for (int x = threadIdx.x; x < c.w; x += kThreads) {
-    d3 l, nn;
-    n += point_at(c, x, y, disc, &l, &nn) ? 1 : 0;
+  const DevSensor& s = ss.s[k];
+  const ViewPtrs& v = ss.v[k];
+  const int w = s.w, h = s.h;
+  // stage rows y-1..y+1: depth where the mask is set, else 0 (cloud.cpp:28-30)
+  for (int i = threadIdx.x; i < 3 * w; i += kThreads) {
+    const int r = i / w, x = i - r * w, yy = y - 1 + r;
+    uint16_t d = 0;
+    if (yy >= 0 && yy < h && v.mask[(size_t)yy * v.mpitch + x]) d = v.depth[(size_t)yy * v.dpitch + x];
+    rows3[i] = d;
   }
-  __shared__ int red[kThreads / 32];
-  n = __reduce_add_sync(0xffffffffu, n);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = n;
   __syncthreads();
-  if (threadIdx.x == 0) {
-    int t = 0;
-    for (int i = 0; i < kThreads / 32; ++i) t += red[i];
-    row_counts[blockIdx.x] = t;
+  const Rows3 c{rows3, w, h, y, &s};
+  const double window = (double)(2 * sil_r + 1) * (double)(2 * sil_r + 1);
+  const int wy0 = max(0, y - sil_r), wy1 = min(h - 1, y + sil_r);
+  const uint16_t* prow0 = pref + (size_t)(blockIdx.x - y) * ppitch;  // row 0 of this view
+  const double inf = DBL_MAX * 2.0;
+  double lo0 = inf, lo1 = inf, lo2 = inf, hi0 = -inf, hi1 = -inf, hi2 = -inf;
+  int base = 0;
+  Staged* srow = stage + (size_t)blockIdx.x * spitch;
+  float* wrow = weight_maps + ss.pix_offset[k] + (size_t)y * w;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int x0 = 0; x0 < w; x0 += kThreads) {
+    const int x = x0 + threadIdx.x;
+    d3 local{0, 0, 0}, n{0, 0, 0};
+    const bool is_pt = x < w && point_at(c, x, disc, &local, &n);
+    const unsigned ball = __ballot_sync(0xffffffffu, is_pt);
+    if (lane == 0) warp_cnt[wid] = __popc(ball);
+    __syncthreads();
+    int wpre = 0, tot = 0;
+    for (int i = 0; i < kThreads / 32; ++i) wpre += i < wid ? warp_cnt[i] : 0, tot += warp_cnt[i];
+    float wmap = 0.f;
+    if (is_pt) {
+      // cloud.cpp:73-74 world position / normal
+      const d3 p = add3(mat3(s.R, local), ld3(s.t));
+      const d3 nw = mat3(s.R, n);
+      // cloud.cpp:108-114: W1 from the re-transformed local frame, W2 coverage
+      const d3 l2 = add3(mat3(s.Ri, p), ld3(s.ti));
+      const d3 nl = mat3(s.Ri, nw);
+      const double w1raw = dot3(neg3(normalized3(l2)), nl);
+      const double w1 = w1raw < 0.0 ? 0.0 : w1raw;
+      const int xa = max(0, x - sil_r), xb = min(w - 1, x + sil_r);
+      uint32_t cnt = 0;
+      for (int yy = wy0; yy <= wy1; ++yy) {
+        const uint16_t* pr = prow0 + (size_t)yy * ppitch;
+        cnt += (uint32_t)pr[xb] - (xa > 0 ? (uint32_t)pr[xa - 1] : 0u);
+      }
+      const double wt = dmul(w1, ddiv((double)cnt, window));
+      Staged& o = srow[base + wpre + __popc(ball & ((1u << lane) - 1u))];
+      o.pos[0] = p.x, o.pos[1] = p.y, o.pos[2] = p.z;
+      o.nrm[0] = nw.x, o.nrm[1] = nw.y, o.nrm[2] = nw.z;
+      o.w = wt;
+      o.px = x;
+      wmap = (float)wt;
+      lo0 = fmin(lo0, p.x), lo1 = fmin(lo1, p.y), lo2 = fmin(lo2, p.z);
+      hi0 = fmax(hi0, p.x), hi1 = fmax(hi1, p.y), hi2 = fmax(hi2, p.z);
+    }
+    if (x < w) wrow[x] = wmap;
+    base += tot;
+    __syncthreads();
   }
+  for (int o = 16; o > 0; o >>= 1) {
+    lo0 = fmin(lo0, __shfl_xor_sync(0xffffffffu, lo0, o)), hi0 = fmax(hi0, __shfl_xor_sync(0xffffffffu, hi0, o));
+    lo1 = fmin(lo1, __shfl_xor_sync(0xffffffffu, lo1, o)), hi1 = fmax(hi1, __shfl_xor_sync(0xffffffffu, hi1, o));
+    lo2 = fmin(lo2, __shfl_xor_sync(0xffffffffu, lo2, o)), hi2 = fmax(hi2, __shfl_xor_sync(0xffffffffu, hi2, o));
+  }
+  if (lane == 0) {
+    bb[wid][0] = lo0, bb[wid][1] = lo1, bb[wid][2] = lo2;
+    bb[wid][3] = hi0, bb[wid][4] = hi1, bb[wid][5] = hi2;
+  }
+  __syncthreads();
+  if (threadIdx.x < 6) {
+    double r = bb[0][threadIdx.x];
+    for (int i = 1; i < kThreads / 32; ++i)
+      r = threadIdx.x < 3 ? fmin(r, bb[i][threadIdx.x]) : fmax(r, bb[i][threadIdx.x]);
+    row_bbox[(size_t)blockIdx.x * 6 + threadIdx.x] = r;
+  }
+  if (threadIdx.x == 0) row_counts[blockIdx.x] = base;
 }
 
 // single-CTA exclusive scan of the per-row counts
@@ -151,114 +253,57 @@ __global__ void __launch_bounds__(1024) pre_scan_kernel(const int32_t* counts, i
   }
 }
 
-__global__ void __launch_bounds__(kThreads) pre_emit_kernel(const __grid_constant__ SensorSet ss, double disc,
-                                                            int sil_r, const int32_t* row_offsets, DevPoints pts,
-                                                            float* weight_maps, double* row_bbox) {
-  extern __shared__ uint32_t colsum[];  // w entries
-  __shared__ int warp_cnt[kThreads / 32];
-  __shared__ double bb[kThreads / 32][6];
+// one warp per row: staged points -> final SoA (pos, nrm, weight, pix)
+__global__ void __launch_bounds__(256) pre_gather_kernel(const __grid_constant__ SensorSet ss, int rows,
+                                                         const Staged* __restrict__ stage, int spitch,
+                                                         const int32_t* __restrict__ counts,
+                                                         const int32_t* __restrict__ offsets, DevPoints pts) {
+  const int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (r >= rows) return;
+  const int n = counts[r];
+  if (!n) return;
   int k, y;
-  row_of_block(ss, blockIdx.x, &k, &y);
-  const DevSensor& s = ss.s[k];
-  const ViewPtrs& v = ss.v[k];
-  RowCtx c{&s, &v, s.w, s.h, y};
-  const int w = s.w, h = s.h;
-
-  // cloud.cpp:89-106: foreground count of the (2r+1)^2 window, clipped to the
-  // image (off-image area counts as background), as column sums + row window.
-  const int y0 = max(0, y - sil_r), y1 = min(h - 1, y + sil_r);
-  for (int x = threadIdx.x; x < w; x += kThreads) {
-    uint32_t cs = 0;
-    for (int yy = y0; yy <= y1; ++yy) cs += __ldg(v.mask + (size_t)yy * v.mpitch + x) ? 1u : 0u;
-    colsum[x] = cs;
-  }
-  __syncthreads();
-  const double window = (double)(2 * sil_r + 1) * (double)(2 * sil_r + 1);
-
-  const double inf = DBL_MAX * 2.0;
-  double lo[3] = {inf, inf, inf}, hi[3] = {-inf, -inf, -inf};
-  int base = row_offsets[blockIdx.x];
-  float* wrow = weight_maps + ss.pix_offset[k] + (size_t)y * w;
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-
-  for (int x0 = 0; x0 < w; x0 += kThreads) {
-    const int x = x0 + threadIdx.x;
-    d3 local{0, 0, 0}, n{0, 0, 0};
-    const bool is_pt = x < w && point_at(c, x, y, disc, &local, &n);
-    const unsigned ball = __ballot_sync(0xffffffffu, is_pt);
-    if (lane == 0) warp_cnt[wid] = __popc(ball);
-    __syncthreads();
-    int wpre = 0, tot = 0;
-    for (int i = 0; i < kThreads / 32; ++i) {
-      wpre += i < wid ? warp_cnt[i] : 0;
-      tot += warp_cnt[i];
-    }
-    float wmap = 0.f;
-    if (is_pt) {
-      const int idx = base + wpre + __popc(ball & ((1u << lane) - 1u));
-      // cloud.cpp:73-74: world position / normal
-      const d3 p = add3(mat3(s.R, local), ld3(s.t));
-      const d3 nw = mat3(s.R, n);
-      // cloud.cpp:108-114: W1 from the re-transformed local frame, W2 coverage
-      const d3 l2 = add3(mat3(s.Ri, p), ld3(s.ti));
-      const d3 nl = mat3(s.Ri, nw);
-      const double w1raw = dot3(neg3(normalized3(l2)), nl);
-      const double w1 = w1raw < 0.0 ? 0.0 : w1raw;
-      const int xa = max(0, x - sil_r), xb = min(w - 1, x + sil_r);
-      uint32_t cnt = 0;
-      for (int xx = xa; xx <= xb; ++xx) cnt += colsum[xx];
-      const double w2 = ddiv((double)cnt, window);
-      const double wt = dmul(w1, w2);
-      pts.pos[3 * idx + 0] = p.x;
-      pts.pos[3 * idx + 1] = p.y;
-      pts.pos[3 * idx + 2] = p.z;
-      pts.nrm[3 * idx + 0] = nw.x;
-      pts.nrm[3 * idx + 1] = nw.y;
-      pts.nrm[3 * idx + 2] = nw.z;
-      pts.weight[idx] = wt;
-      pts.pix[3 * idx + 0] = x;
-      pts.pix[3 * idx + 1] = y;
-      pts.pix[3 * idx + 2] = k;
-      wmap = (float)wt;
-      lo[0] = fmin(lo[0], p.x), lo[1] = fmin(lo[1], p.y), lo[2] = fmin(lo[2], p.z);
-      hi[0] = fmax(hi[0], p.x), hi[1] = fmax(hi[1], p.y), hi[2] = fmax(hi[2], p.z);
-    }
-    if (x < w) wrow[x] = wmap;
-    base += tot;
-    __syncthreads();
-  }
-  // per-row bbox (exact min/max, order-independent)
-  for (int a = 0; a < 3; ++a)
-    for (int o = 16; o > 0; o >>= 1) {
-      lo[a] = fmin(lo[a], __shfl_xor_sync(0xffffffffu, lo[a], o));
-      hi[a] = fmax(hi[a], __shfl_xor_sync(0xffffffffu, hi[a], o));
-    }
-  if (lane == 0)
-    for (int a = 0; a < 3; ++a) bb[wid][a] = lo[a], bb[wid][3 + a] = hi[a];
-  __syncthreads();
-  if (threadIdx.x < 6) {
-    double r = bb[0][threadIdx.x];
-    for (int i = 1; i < kThreads / 32; ++i)
-      r = threadIdx.x < 3 ? fmin(r, bb[i][threadIdx.x]) : fmax(r, bb[i][threadIdx.x]);
-    row_bbox[(size_t)blockIdx.x * 6 + threadIdx.x] = r;
+  row_of_block(ss, r, &k, &y);
+  const int off = offsets[r];
+  const Staged* srow = stage + (size_t)r * spitch;
+  for (int i = lane; i < n; i += 32) {
+    const Staged s = srow[i];
+    const int idx = off + i;
+    pts.pos[3 * idx + 0] = s.pos[0], pts.pos[3 * idx + 1] = s.pos[1], pts.pos[3 * idx + 2] = s.pos[2];
+    pts.nrm[3 * idx + 0] = s.nrm[0], pts.nrm[3 * idx + 1] = s.nrm[1], pts.nrm[3 * idx + 2] = s.nrm[2];
+    pts.weight[idx] = s.w;
+    pts.pix[3 * idx + 0] = s.px, pts.pix[3 * idx + 1] = y, pts.pix[3 * idx + 2] = k;
   }
 }
 
 // reconstruct.cpp:56-68 (bbox) + fit_grid (reconstruct.cpp:16-35, dims given)
 __global__ void __launch_bounds__(256) pre_fit_kernel(const double* row_bbox, int rows, int nx, int ny, int nz,
                                                       int pad, DevCtl* ctl) {
-  __shared__ double sh[256][6];
+  __shared__ double sh[6][256];
   const double inf = DBL_MAX * 2.0;
   double r[6] = {inf, inf, inf, -inf, -inf, -inf};
-  for (int i = threadIdx.x; i < rows; i += 256)
-    for (int a = 0; a < 6; ++a)
-      r[a] = a < 3 ? fmin(r[a], row_bbox[(size_t)i * 6 + a]) : fmax(r[a], row_bbox[(size_t)i * 6 + a]);
-  for (int a = 0; a < 6; ++a) sh[threadIdx.x][a] = r[a];
+  for (int i = threadIdx.x; i < rows; i += 256) {
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      r[a] = fmin(r[a], row_bbox[(size_t)i * 6 + a]);
+      r[3 + a] = fmax(r[3 + a], row_bbox[(size_t)i * 6 + 3 + a]);
+    }
+  }
+#pragma unroll
+  for (int a = 0; a < 6; ++a) sh[a][threadIdx.x] = r[a];
   __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if (threadIdx.x < o) {
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        sh[a][threadIdx.x] = fmin(sh[a][threadIdx.x], sh[a][threadIdx.x + o]);
+        sh[3 + a][threadIdx.x] = fmax(sh[3 + a][threadIdx.x], sh[3 + a][threadIdx.x + o]);
+      }
+    }
+    __syncthreads();
+  }
   if (threadIdx.x != 0) return;
-  for (int i = 1; i < 256; ++i)
-    for (int a = 0; a < 6; ++a) r[a] = a < 3 ? fmin(r[a], sh[i][a]) : fmax(r[a], sh[i][a]);
-  for (int a = 0; a < 6; ++a) ctl->bbox[a] = r[a];
+  for (int a = 0; a < 6; ++a) r[a] = sh[a][0], ctl->bbox[a] = r[a];
   DevGrid g;
   g.nx = nx, g.ny = ny, g.nz = nz;
   if (ctl->status != 0) {
@@ -282,26 +327,59 @@ __global__ void __launch_bounds__(256) pre_fit_kernel(const double* row_bbox, in
   ctl->grid = g;
 }
 
+struct Scratch {
+  int32_t* counts;
+  int32_t* offsets;
+  double* bbox;
+  uint16_t* pref;
+  Staged* stage;
+  int ppitch, spitch;
+};
+
+Scratch carve(const SensorSet& ss, void* base) {
+  const int rows = ss.row_offset[ss.k];
+  int maxw = 0;
+  for (int k = 0; k < ss.k; ++k) maxw = maxw > ss.s[k].w ? maxw : ss.s[k].w;
+  auto up = [](uintptr_t p) { return (p + 255) & ~uintptr_t(255); };
+  Scratch s;
+  uintptr_t p = up(reinterpret_cast<uintptr_t>(base));
+  s.counts = reinterpret_cast<int32_t*>(p);
+  p = up(p + rows * sizeof(int32_t));
+  s.offsets = reinterpret_cast<int32_t*>(p);
+  p = up(p + rows * sizeof(int32_t));
+  s.bbox = reinterpret_cast<double*>(p);
+  p = up(p + rows * 6 * sizeof(double));
+  s.ppitch = (maxw + 127) & ~127;
+  s.pref = reinterpret_cast<uint16_t*>(p);
+  p = up(p + (size_t)rows * s.ppitch * sizeof(uint16_t));
+  s.spitch = maxw;
+  s.stage = reinterpret_cast<Staged*>(p);
+  p = up(p + (size_t)rows * s.spitch * sizeof(Staged));
+  return s;
+}
+
 }  // namespace
 
 size_t preprocess_scratch_bytes(const SensorSet& ss) {
-  const size_t rows = (size_t)ss.row_offset[ss.k];
-  return rows * (2 * sizeof(int32_t)) + rows * 6 * sizeof(double) + 64;
+  const Scratch s = carve(ss, nullptr);
+  const int rows = ss.row_offset[ss.k];
+  return reinterpret_cast<uintptr_t>(s.stage) + (size_t)rows * s.spitch * sizeof(Staged) + 512;
 }
 
 void launch_preprocess(const SensorSet& ss, DevPoints pts, float* weight_maps, int32_t* scratch, DevCtl* ctl,
                        int nx, int ny, int nz, int padding, double disc_mm, int sil_r, cudaStream_t st) {
   const int rows = ss.row_offset[ss.k];
-  int32_t* counts = scratch;
-  int32_t* offsets = scratch + rows;
-  double* bbox = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(offsets + rows) + 63) & ~uintptr_t(63));
+  const Scratch s = carve(ss, scratch);
   int maxw = 0;
   for (int k = 0; k < ss.k; ++k) maxw = maxw > ss.s[k].w ? maxw : ss.s[k].w;
-  pre_count_kernel<<<rows, kThreads, 0, st>>>(ss, disc_mm, counts);
-  pre_scan_kernel<<<1, 1024, 0, st>>>(counts, offsets, rows, pts.cap, ctl);
-  pre_emit_kernel<<<rows, kThreads, maxw * sizeof(uint32_t), st>>>(ss, disc_mm, sil_r, offsets, pts, weight_maps,
-                                                                   bbox);
-  pre_fit_kernel<<<1, 256, 0, st>>>(bbox, rows, nx, ny, nz, padding, ctl);
+  const int warp_grid = (rows * 32 + 255) / 256;
+  pre_prefix_kernel<<<warp_grid, 256, 0, st>>>(ss, rows, s.pref, s.ppitch);
+  pre_points_kernel<<<rows, kThreads, 3 * maxw * sizeof(uint16_t), st>>>(ss, disc_mm, sil_r, s.pref, s.ppitch,
+                                                                         s.stage, s.spitch, s.counts, weight_maps,
+                                                                         s.bbox);
+  pre_scan_kernel<<<1, 1024, 0, st>>>(s.counts, s.offsets, rows, pts.cap, ctl);
+  pre_gather_kernel<<<warp_grid, 256, 0, st>>>(ss, rows, s.stage, s.spitch, s.counts, s.offsets, pts);
+  pre_fit_kernel<<<1, 256, 0, st>>>(s.bbox, rows, nx, ny, nz, padding, ctl);
 }
 
 }  // namespace vc
