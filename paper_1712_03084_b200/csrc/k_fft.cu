@@ -179,7 +179,7 @@ template <int N>
 struct CCfg {
   static constexpr int CW = N >= 512 ? 8 : 16;
   static constexpr int THREADS = CW * Shape<N>::R2;
-  static constexpr int SMEM = N * CW * 8;
+  static constexpr int SMEM = N * CW * 8;  // one staged tile (= exchange buffer)
 };
 
 // ------------------------------------------------------------------ F-x
@@ -283,6 +283,44 @@ __global__ void __launch_bounds__(XCfg<NX>::THREADS, 2) fx_kernel(const float4* 
   split_store_z(v, (size_t)l0 * H, (size_t)l1 * H, bits0 != 0u, bits1 != 0u);
 }
 
+// ------------------------------------------------------------------ tile staging
+// Column tiles (n rows x CW complex columns, row stride `stride` elements) are
+// staged into shared memory with cp.async (16 B = 2 columns per request,
+// L1-bypassing), so every component of a CTA is in flight while the previous
+// one is transformed; the staged tile then doubles as that component's
+// exchange buffer.  Rows flagged empty (or columns past the pitch) zero-fill.
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool pred) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(pred ? 16 : 0) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+template <int N, int CW, int THREADS>
+__device__ __forceinline__ void stage_tile(float2* tile, const float2* src, size_t stride, int kx0, int H,
+                                           const uint32_t* rowbits) {
+  constexpr int CPR = CW / 2;  // 16-byte chunks per row
+#pragma unroll 4
+  for (int i = threadIdx.x; i < N * CPR; i += THREADS) {
+    const int j = i / CPR, c2 = i - j * CPR;
+    const int kx = kx0 + 2 * c2;
+    const bool ok = kx < H && (!rowbits || __ldg(rowbits + j) != 0u);
+    cp_async16(tile + j * CW + 2 * c2, ok ? (const void*)(src + (size_t)j * stride + kx) : (const void*)src, ok);
+  }
+}
+
+template <int N, int CW>
+__device__ __forceinline__ void tile_to_regs(const float2* tile, int c, int t, float2* v) {
+  using S = Shape<N>;
+#pragma unroll
+  for (int q = 0; q < S::Q; ++q)
+#pragma unroll
+    for (int j2 = 0; j2 < S::R2; ++j2) v[q * S::R2 + j2] = tile[(t + S::R2 * q + S::R1 * j2) * CW + c];
+}
+
 // ------------------------------------------------------------------ F-y
 template <int NY>
 __global__ void __launch_bounds__(CCfg<NY>::THREADS, 2) fy_kernel(float2* __restrict__ S0, float2* __restrict__ S1,
@@ -290,44 +328,46 @@ __global__ void __launch_bounds__(CCfg<NY>::THREADS, 2) fy_kernel(float2* __rest
                                                                  const float2* __restrict__ tw,
                                                                  const uint32_t* __restrict__ rowbits) {
   using S = Shape<NY>;
-  constexpr int T = S::R2, R1 = S::R1, kCW = CCfg<NY>::CW;
-  extern __shared__ float2 sh[];
+  constexpr int T = S::R2, R1 = S::R1, kCW = CCfg<NY>::CW, TH = CCfg<NY>::THREADS;
+  extern __shared__ float2 sh[];  // 3 tiles of NY x kCW
+  float2* b0 = sh;
+  float2* b1 = sh + NY * kCW;
+  float2* b2 = sh + 2 * NY * kCW;
   const int c = threadIdx.x % kCW, t = threadIdx.x / kCW;
-  const int kx = blockIdx.x * kCW + c;
+  const int kx0 = blockIdx.x * kCW, kx = kx0 + c;
   const bool live = kx < nxh;
   const size_t plane = (size_t)blockIdx.y * NY * H;
-  ExCols<NY, kCW> ex{sh, c};
-  // rows F-x skipped (no splat contribution) are zero
-  uint32_t nz_rows = 0;  // bit (q*T + j2) set if row j is non-empty
-#pragma unroll
-  for (int q = 0; q < S::Q; ++q)
-#pragma unroll
-    for (int j2 = 0; j2 < T; ++j2) {
-      const int j = t + T * q + R1 * j2;
-      if (!rowbits || __ldg(rowbits + (size_t)blockIdx.y * NY + j)) nz_rows |= 1u << (q * T + j2);
-    }
-  auto load = [&](const float2* src, float2* v) {
-#pragma unroll
-    for (int q = 0; q < S::Q; ++q)
-#pragma unroll
-      for (int j2 = 0; j2 < T; ++j2) {
-        const int j = t + T * q + R1 * j2;
-        v[q * T + j2] = (live && ((nz_rows >> (q * T + j2)) & 1u)) ? __ldcs(src + plane + (size_t)j * H + kx)
-                                                                   : make_float2(0.f, 0.f);
-      }
-  };
+  const uint32_t* rb = rowbits ? rowbits + (size_t)blockIdx.y * NY : nullptr;  // empty rows (F-x skipped) are zero
+  stage_tile<NY, kCW, TH>(b0, S0 + plane, H, kx0, H, rb);
+  cp_async_commit();
+  stage_tile<NY, kCW, TH>(b1, S1 + plane, H, kx0, H, rb);
+  cp_async_commit();
+  stage_tile<NY, kCW, TH>(b2, S2 + plane, H, kx0, H, rb);
+  cp_async_commit();
   float2 d[R1], v[R1];
-  load(S0, d);
-  fft_line<NY, false>(d, t, tw, ex);
-  load(S1, v);
-  fft_line<NY, false>(v, t, tw, ex);
+  cp_async_wait<2>();
+  __syncthreads();
+  tile_to_regs<NY, kCW>(b0, c, t, d);
+  __syncthreads();
+  ExCols<NY, kCW> e0{b0, c};
+  fft_line<NY, false>(d, t, tw, e0);
+  cp_async_wait<1>();
+  __syncthreads();
+  tile_to_regs<NY, kCW>(b1, c, t, v);
+  __syncthreads();
+  ExCols<NY, kCW> e1{b1, c};
+  fft_line<NY, false>(v, t, tw, e1);
 #pragma unroll
   for (int k1 = 0; k1 < R1; ++k1) {
     const float wy = signed_freq(t + T * k1, NY);
     d[k1] = make_float2(d[k1].x + wy * v[k1].x, d[k1].y + wy * v[k1].y);
   }
-  load(S2, v);
-  fft_line<NY, false>(v, t, tw, ex);
+  cp_async_wait<0>();
+  __syncthreads();
+  tile_to_regs<NY, kCW>(b2, c, t, v);
+  __syncthreads();
+  ExCols<NY, kCW> e2{b2, c};
+  fft_line<NY, false>(v, t, tw, e2);
   if (live) {
 #pragma unroll
     for (int k1 = 0; k1 < R1; ++k1) {
@@ -344,29 +384,33 @@ __global__ void __launch_bounds__(CCfg<NZ>::THREADS, 2) z_kernel(float2* __restr
                                                                 const float2* __restrict__ S1, int nx, int ny,
                                                                 int H, const float2* __restrict__ tw) {
   using S = Shape<NZ>;
-  constexpr int T = S::R2, R1 = S::R1, kCW = CCfg<NZ>::CW;
-  extern __shared__ float2 sh[];
+  constexpr int T = S::R2, R1 = S::R1, kCW = CCfg<NZ>::CW, TH = CCfg<NZ>::THREADS;
+  extern __shared__ float2 sh[];  // 2 tiles of NZ x kCW
+  float2* b0 = sh;
+  float2* b1 = sh + NZ * kCW;
   const int c = threadIdx.x % kCW, t = threadIdx.x / kCW;
-  const int kx = blockIdx.x * kCW + c;
+  const int kx0 = blockIdx.x * kCW, kx = kx0 + c;
   const int ky = blockIdx.y;
   const bool live = kx <= nx / 2;
   const size_t zstride = (size_t)ny * H;
   const size_t base = (size_t)ky * H + kx;
-  ExCols<NZ, kCW> ex{sh, c};
-  auto load = [&](const float2* src, float2* v) {
-#pragma unroll
-    for (int q = 0; q < S::Q; ++q)
-#pragma unroll
-      for (int j2 = 0; j2 < T; ++j2) {
-        const int j = t + T * q + R1 * j2;
-        v[q * T + j2] = live ? __ldcs(src + base + (size_t)j * zstride) : make_float2(0.f, 0.f);
-      }
-  };
+  stage_tile<NZ, kCW, TH>(b0, S0 + (size_t)ky * H, zstride, kx0, H, nullptr);
+  cp_async_commit();
+  stage_tile<NZ, kCW, TH>(b1, S1 + (size_t)ky * H, zstride, kx0, H, nullptr);
+  cp_async_commit();
   float2 d[R1], z[R1];
-  load(S0, d);
-  fft_line<NZ, false>(d, t, tw, ex);
-  load(S1, z);
-  fft_line<NZ, false>(z, t, tw, ex);
+  cp_async_wait<1>();
+  __syncthreads();
+  tile_to_regs<NZ, kCW>(b0, c, t, d);
+  __syncthreads();
+  ExCols<NZ, kCW> e0{b0, c};
+  fft_line<NZ, false>(d, t, tw, e0);
+  cp_async_wait<0>();
+  __syncthreads();
+  tile_to_regs<NZ, kCW>(b1, c, t, z);
+  __syncthreads();
+  ExCols<NZ, kCW> e1{b1, c};
+  fft_line<NZ, false>(z, t, tw, e1);
   const float wx = signed_freq(kx, nx), wy = signed_freq(ky, ny);
   const float wxy = wx * wx + wy * wy;
 #pragma unroll
@@ -379,7 +423,7 @@ __global__ void __launch_bounds__(CCfg<NZ>::THREADS, 2) z_kernel(float2* __restr
     d[k1] = make_float2(s.y * inv, -s.x * inv);  // (-i/|w|^2) * s
   }
   relayout_for_inverse<NZ>(d);
-  fft_line<NZ, true>(d, t, tw, ex);
+  fft_line<NZ, true>(d, t, tw, e0);
   if (live) {
 #pragma unroll
     for (int k1 = 0; k1 < R1; ++k1) __stcs(S0 + base + (size_t)(t + T * k1) * zstride, d[k1]);
@@ -388,29 +432,29 @@ __global__ void __launch_bounds__(CCfg<NZ>::THREADS, 2) z_kernel(float2* __restr
 
 // ------------------------------------------------------------------ I-y
 template <int NY>
-__global__ void __launch_bounds__(CCfg<NY>::THREADS, 2) iy_kernel(float2* __restrict__ S0, int nxh, int H,
+__global__ void __launch_bounds__(CCfg<NY>::THREADS, 3) iy_kernel(float2* __restrict__ S0, int nxh, int H,
                                                                  const float2* __restrict__ tw) {
   using S = Shape<NY>;
-  constexpr int T = S::R2, R1 = S::R1, kCW = CCfg<NY>::CW;
+  constexpr int T = S::R2, R1 = S::R1, kCW = CCfg<NY>::CW, TH = CCfg<NY>::THREADS;
   extern __shared__ float2 sh[];
   const int c = threadIdx.x % kCW, t = threadIdx.x / kCW;
-  const int kx = blockIdx.x * kCW + c;
+  const int kx0 = blockIdx.x * kCW, kx = kx0 + c;
   const bool live = kx < nxh;
   const size_t plane = (size_t)blockIdx.y * NY * H;
-  ExCols<NY, kCW> ex{sh, c};
+  stage_tile<NY, kCW, TH>(sh, S0 + plane, H, kx0, H, nullptr);
+  cp_async_commit();
   float2 v[R1];
-#pragma unroll
-  for (int q = 0; q < S::Q; ++q)
-#pragma unroll
-    for (int j2 = 0; j2 < T; ++j2) {
-      const int j = t + T * q + R1 * j2;
-      v[q * T + j2] = live ? __ldcs(S0 + plane + (size_t)j * H + kx) : make_float2(0.f, 0.f);
-    }
+  cp_async_wait<0>();
+  __syncthreads();
+  tile_to_regs<NY, kCW>(sh, c, t, v);
+  __syncthreads();
+  ExCols<NY, kCW> ex{sh, c};
   fft_line<NY, true>(v, t, tw, ex);
   if (live) {
 #pragma unroll
     for (int k1 = 0; k1 < R1; ++k1) __stcs(S0 + plane + (size_t)(t + T * k1) * H + kx, v[k1]);
   }
+  (void)T;
 }
 
 // ------------------------------------------------------------------ I-x
@@ -519,10 +563,10 @@ struct Prep {
       allow_smem(fx_kernel<N>, XCfg<N>::SMEM);
       allow_smem(ix_kernel<N>, XCfg<N>::SMEM);
     } else if (axis == 1) {
-      allow_smem(fy_kernel<N>, CCfg<N>::SMEM);
+      allow_smem(fy_kernel<N>, 3 * CCfg<N>::SMEM);
       allow_smem(iy_kernel<N>, CCfg<N>::SMEM);
     } else {
-      allow_smem(z_kernel<N>, CCfg<N>::SMEM);
+      allow_smem(z_kernel<N>, 2 * CCfg<N>::SMEM);
     }
   }
 };
@@ -541,7 +585,7 @@ struct RunFy {
   static void run(const FftArgs& a) {
     using C = CCfg<N>;
     dim3 grid((a.nx / 2 + 1 + C::CW - 1) / C::CW, a.nz);
-    fy_kernel<N><<<grid, C::THREADS, C::SMEM, a.st>>>(a.S0, a.S1, a.S2, a.nx / 2 + 1, a.H, a.twy, a.rowbits);
+    fy_kernel<N><<<grid, C::THREADS, 3 * C::SMEM, a.st>>>(a.S0, a.S1, a.S2, a.nx / 2 + 1, a.H, a.twy, a.rowbits);
   }
 };
 template <int N>
@@ -549,7 +593,7 @@ struct RunZ {
   static void run(const FftArgs& a) {
     using C = CCfg<N>;
     dim3 grid((a.nx / 2 + 1 + C::CW - 1) / C::CW, a.ny);
-    z_kernel<N><<<grid, C::THREADS, C::SMEM, a.st>>>(a.S0, a.S1, a.nx, a.ny, a.H, a.twz);
+    z_kernel<N><<<grid, C::THREADS, 2 * C::SMEM, a.st>>>(a.S0, a.S1, a.nx, a.ny, a.H, a.twz);
   }
 };
 template <int N>

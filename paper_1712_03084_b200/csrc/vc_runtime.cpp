@@ -168,7 +168,7 @@ vc_status check_sensors(vc_ctx* ctx, const vc_sensor* s, int k) {
     if (d.width <= 0 || d.height <= 0 || r.width <= 0 || r.height <= 0 || d.fx <= 0 || d.fy <= 0 || r.fx <= 0 ||
         r.fy <= 0)
       return fail(ctx, VC_ERR_INVALID_ARGUMENT, "Intrinsics: focal lengths / image sizes must be positive");
-    if (d.width > 8192) return fail(ctx, VC_ERR_INVALID_ARGUMENT, "depth width > 8192");
+    if (d.width > 1024) return fail(ctx, VC_ERR_INVALID_ARGUMENT, "depth width > 1024 (pre_points stages 3 rows in shared memory)");
   }
   return VC_OK;
 }
@@ -228,6 +228,8 @@ vc_status setup_sensorset(vc_ctx* ctx, const vc_sensor* sensors, int k) {
   VC_TRY(ensure(ctx, ctx->pts_pix, npix * 3 * sizeof(int32_t)));
   VC_TRY(ensure(ctx, ctx->wmaps, npix * sizeof(float)));
   VC_TRY(ensure(ctx, ctx->pre_scratch, preprocess_scratch_bytes(ss)));
+  prepare_preprocess(ss);
+  VC_CUDA(cudaGetLastError());
   ctx->pts_cap = (int)npix;
   ctx->last_k = k;
   return VC_OK;

@@ -92,6 +92,7 @@ inline void record_event(cudaEvent_t e, cudaStream_t s) { cudaEventRecord(e, s);
 // ----------------------------------------------------------------- launchers
 // k_preprocess.cu — build_cloud + confidence_weights + bbox + fit_grid
 size_t preprocess_scratch_bytes(const SensorSet& ss);
+void prepare_preprocess(const SensorSet& ss);  // smem opt-in; call outside graph capture
 void launch_preprocess(const SensorSet& ss, DevPoints pts, float* weight_maps, int32_t* scratch, DevCtl* ctl,
                        int dims_x, int dims_y, int dims_z, int padding, double disc_mm, int sil_r, cudaStream_t st);
 // k_splat.cu
