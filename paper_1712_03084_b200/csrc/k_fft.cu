@@ -159,9 +159,16 @@ struct ExCols {
   __device__ void sync() { __syncthreads(); }
 };
 
-__device__ __forceinline__ float signed_freq(int i, int n) {  // integrate.cpp:37-40
+// integrate.cpp:37-40: w = 2 pi m / n, m = i (i <= n/2) else i - n (Nyquist -> +pi);
+// evaluated as m * (2 pi / n) in fp32 (one multiply; the filter runs in fp32)
+template <int N>
+__device__ __forceinline__ float signed_freq(int i) {
+  constexpr float k = (float)(2.0 * 3.14159265358979323846 / N);
+  return (float)(i <= N / 2 ? i : i - N) * k;
+}
+__device__ __forceinline__ float signed_freq(int i, int n) {
   const int m = i <= n / 2 ? i : i - n;
-  return (float)(2.0 * 3.14159265358979323846 * (double)m / (double)n);
+  return (float)m * __fdiv_rn(6.283185307179586f, (float)n);
 }
 
 // x passes: TEAMS teams of T lanes; keep the exchange tiles under ~48 KB.
@@ -237,7 +244,7 @@ __global__ void __launch_bounds__(XCfg<NX>::THREADS, 2) fx_kernel(const float4* 
         float2 A = make_float2(0.5f * (d.x + e.x), 0.5f * (d.y - e.y));  // (d + conj e)/2
         const float2 B = make_float2(0.5f * (d.y + e.y), -0.5f * (d.x - e.x));  // (d - conj e)/(2i)
         if (scale_wx) {
-          const float wx = (float)(2.0 * 3.14159265358979323846 * (double)k / (double)NX);
+          const float wx = signed_freq<NX>(k);  // k <= NX/2
           A.x *= wx, A.y *= wx;
         }
         if (live) {
@@ -299,15 +306,29 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
 
+// Thread i stages chunk c2 = i % CPR of rows j = i / CPR + k * (THREADS / CPR);
+// `rowmask` (bit k) says which of those rows are non-empty (row_flags()).
+template <int N, int CW, int THREADS>
+__device__ __forceinline__ uint32_t row_flags(const uint32_t* rowbits) {
+  constexpr int CPR = CW / 2, RSTEP = THREADS / CPR, NR = N / RSTEP;
+  static_assert(NR <= 32, "row mask");
+  if (!rowbits) return 0xffffffffu;
+  uint32_t m = 0;
+  const int j0 = threadIdx.x / CPR;
+#pragma unroll
+  for (int k = 0; k < NR; ++k) m |= (__ldg(rowbits + j0 + k * RSTEP) != 0u ? 1u : 0u) << k;
+  return m;
+}
 template <int N, int CW, int THREADS>
 __device__ __forceinline__ void stage_tile(float2* tile, const float2* src, size_t stride, int kx0, int H,
-                                           const uint32_t* rowbits) {
-  constexpr int CPR = CW / 2;  // 16-byte chunks per row
-#pragma unroll 4
-  for (int i = threadIdx.x; i < N * CPR; i += THREADS) {
-    const int j = i / CPR, c2 = i - j * CPR;
-    const int kx = kx0 + 2 * c2;
-    const bool ok = kx < H && (!rowbits || __ldg(rowbits + j) != 0u);
+                                           uint32_t rowmask) {
+  constexpr int CPR = CW / 2, RSTEP = THREADS / CPR, NR = N / RSTEP;
+  const int j0 = threadIdx.x / CPR, c2 = threadIdx.x % CPR;
+  const int kx = kx0 + 2 * c2;
+#pragma unroll
+  for (int k = 0; k < NR; ++k) {
+    const int j = j0 + k * RSTEP;
+    const bool ok = kx < H && ((rowmask >> k) & 1u);
     cp_async16(tile + j * CW + 2 * c2, ok ? (const void*)(src + (size_t)j * stride + kx) : (const void*)src, ok);
   }
 }
@@ -337,12 +358,13 @@ __global__ void __launch_bounds__(CCfg<NY>::THREADS, 2) fy_kernel(float2* __rest
   const int kx0 = blockIdx.x * kCW, kx = kx0 + c;
   const bool live = kx < nxh;
   const size_t plane = (size_t)blockIdx.y * NY * H;
-  const uint32_t* rb = rowbits ? rowbits + (size_t)blockIdx.y * NY : nullptr;  // empty rows (F-x skipped) are zero
-  stage_tile<NY, kCW, TH>(b0, S0 + plane, H, kx0, H, rb);
+  // empty rows (F-x skipped them) are zero-filled
+  const uint32_t rm = row_flags<NY, kCW, TH>(rowbits ? rowbits + (size_t)blockIdx.y * NY : nullptr);
+  stage_tile<NY, kCW, TH>(b0, S0 + plane, H, kx0, H, rm);
   cp_async_commit();
-  stage_tile<NY, kCW, TH>(b1, S1 + plane, H, kx0, H, rb);
+  stage_tile<NY, kCW, TH>(b1, S1 + plane, H, kx0, H, rm);
   cp_async_commit();
-  stage_tile<NY, kCW, TH>(b2, S2 + plane, H, kx0, H, rb);
+  stage_tile<NY, kCW, TH>(b2, S2 + plane, H, kx0, H, rm);
   cp_async_commit();
   float2 d[R1], v[R1];
   cp_async_wait<2>();
@@ -359,7 +381,7 @@ __global__ void __launch_bounds__(CCfg<NY>::THREADS, 2) fy_kernel(float2* __rest
   fft_line<NY, false>(v, t, tw, e1);
 #pragma unroll
   for (int k1 = 0; k1 < R1; ++k1) {
-    const float wy = signed_freq(t + T * k1, NY);
+    const float wy = signed_freq<NY>(t + T * k1);
     d[k1] = make_float2(d[k1].x + wy * v[k1].x, d[k1].y + wy * v[k1].y);
   }
   cp_async_wait<0>();
@@ -394,9 +416,9 @@ __global__ void __launch_bounds__(CCfg<NZ>::THREADS, 2) z_kernel(float2* __restr
   const bool live = kx <= nx / 2;
   const size_t zstride = (size_t)ny * H;
   const size_t base = (size_t)ky * H + kx;
-  stage_tile<NZ, kCW, TH>(b0, S0 + (size_t)ky * H, zstride, kx0, H, nullptr);
+  stage_tile<NZ, kCW, TH>(b0, S0 + (size_t)ky * H, zstride, kx0, H, 0xffffffffu);
   cp_async_commit();
-  stage_tile<NZ, kCW, TH>(b1, S1 + (size_t)ky * H, zstride, kx0, H, nullptr);
+  stage_tile<NZ, kCW, TH>(b1, S1 + (size_t)ky * H, zstride, kx0, H, 0xffffffffu);
   cp_async_commit();
   float2 d[R1], z[R1];
   cp_async_wait<1>();
@@ -416,10 +438,10 @@ __global__ void __launch_bounds__(CCfg<NZ>::THREADS, 2) z_kernel(float2* __restr
 #pragma unroll
   for (int k1 = 0; k1 < R1; ++k1) {
     const int kz = t + T * k1;
-    const float wz = signed_freq(kz, NZ);
+    const float wz = signed_freq<NZ>(kz);
     const float w2 = wxy + wz * wz;
     const float2 s = make_float2(d[k1].x + wz * z[k1].x, d[k1].y + wz * z[k1].y);
-    const float inv = (kx == 0 && ky == 0 && kz == 0) ? 0.f : 1.f / w2;
+    const float inv = (kx == 0 && ky == 0 && kz == 0) ? 0.f : __frcp_rn(w2);
     d[k1] = make_float2(s.y * inv, -s.x * inv);  // (-i/|w|^2) * s
   }
   relayout_for_inverse<NZ>(d);
@@ -441,7 +463,7 @@ __global__ void __launch_bounds__(CCfg<NY>::THREADS, 3) iy_kernel(float2* __rest
   const int kx0 = blockIdx.x * kCW, kx = kx0 + c;
   const bool live = kx < nxh;
   const size_t plane = (size_t)blockIdx.y * NY * H;
-  stage_tile<NY, kCW, TH>(sh, S0 + plane, H, kx0, H, nullptr);
+  stage_tile<NY, kCW, TH>(sh, S0 + plane, H, kx0, H, 0xffffffffu);
   cp_async_commit();
   float2 v[R1];
   cp_async_wait<0>();

@@ -99,26 +99,35 @@ struct VoxelInfo {
   int cfg;   // cell case, -1 if no cell
 };
 
-__device__ __forceinline__ VoxelInfo classify(const float* A, int nx, int ny, int nz, size_t v, double L) {
-  const int x = (int)(v % nx), y = (int)((v / nx) % ny), z = (int)(v / ((size_t)nx * ny));
+// Cut-edge mask and cell case of voxel (x, y, z) (linear index v).  The
+// reference tests vals >= level in fp64 (marching_cubes.cpp:168-171); for an
+// fp32 value a and double L that equals a >= Lf with Lf = L rounded up to fp32
+// (__double2float_ru), so the test runs in fp32 bit-exactly.
+__device__ __forceinline__ VoxelInfo classify(const float* A, int nx, int ny, int nz, int x, int y, int z, size_t v,
+                                              float Lf) {
   const size_t plane = (size_t)nx * ny;
-  const bool a0 = (double)__ldg(A + v) >= L;
+  const bool a0 = __ldg(A + v) >= Lf;
   VoxelInfo r{0, -1};
-  if (x + 1 < nx && (((double)__ldg(A + v + 1) >= L) != a0)) r.mask |= 1;
-  if (y + 1 < ny && (((double)__ldg(A + v + nx) >= L) != a0)) r.mask |= 2;
-  if (z + 1 < nz && (((double)__ldg(A + v + plane) >= L) != a0)) r.mask |= 4;
-  if (x + 1 < nx && y + 1 < ny && z + 1 < nz) {
-    int cfg = a0 ? 1 : 0;
-    cfg |= ((double)__ldg(A + v + 1) >= L) << 1;
-    cfg |= ((double)__ldg(A + v + nx) >= L) << 2;
-    cfg |= ((double)__ldg(A + v + nx + 1) >= L) << 3;
-    cfg |= ((double)__ldg(A + v + plane) >= L) << 4;
-    cfg |= ((double)__ldg(A + v + plane + 1) >= L) << 5;
-    cfg |= ((double)__ldg(A + v + plane + nx) >= L) << 6;
-    cfg |= ((double)__ldg(A + v + plane + nx + 1) >= L) << 7;
+  const bool hx = x + 1 < nx, hy = y + 1 < ny, hz = z + 1 < nz;
+  const bool a1 = hx && __ldg(A + v + 1) >= Lf;
+  const bool a2 = hy && __ldg(A + v + nx) >= Lf;
+  const bool a4 = hz && __ldg(A + v + plane) >= Lf;
+  if (hx && a1 != a0) r.mask |= 1;
+  if (hy && a2 != a0) r.mask |= 2;
+  if (hz && a4 != a0) r.mask |= 4;
+  if (hx && hy && hz) {
+    int cfg = (a0 ? 1 : 0) | (a1 ? 2 : 0) | (a2 ? 4 : 0) | (a4 ? 16 : 0);
+    cfg |= (__ldg(A + v + nx + 1) >= Lf) << 3;
+    cfg |= (__ldg(A + v + plane + 1) >= Lf) << 5;
+    cfg |= (__ldg(A + v + plane + nx) >= Lf) << 6;
+    cfg |= (__ldg(A + v + plane + nx + 1) >= Lf) << 7;
     r.cfg = cfg;
   }
   return r;
+}
+__device__ __forceinline__ VoxelInfo classify(const float* A, int nx, int ny, int nz, size_t v, float Lf) {
+  const int x = (int)(v % nx), y = (int)((v / nx) % ny), z = (int)(v / ((size_t)nx * ny));
+  return classify(A, nx, ny, nz, x, y, z, v, Lf);
 }
 
 __device__ __forceinline__ int3 block_exclusive_scan3(int3 v, int3* total) {
@@ -191,12 +200,40 @@ __global__ void __launch_bounds__(kRowThreads) mc_rows_kernel(const float2* __re
 __global__ void __launch_bounds__(1024) mc_units_kernel(const int32_t* blocklist, const int32_t* blkcnt, int nblk,
                                                         int32_t* units, DevCtl* ctl) {
   __shared__ int off[4097];  // nblk <= 4096 (ny*nz <= 1M)
-  if (threadIdx.x == 0) {
-    int s = 0;
-    for (int b = 0; b < nblk; ++b) off[b] = s, s += blkcnt[b];
-    off[nblk] = s;
-    ctl->units = s;  // active unit count
+  __shared__ int wsum[32];
+  // exclusive scan of blkcnt: 4 entries per thread, warp + block scan
+  int v[4], tot = 0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int b = threadIdx.x * 4 + i;
+    v[i] = b < nblk ? blkcnt[b] : 0;
+    tot += v[i];
   }
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  int inc = tot;
+  for (int o = 1; o < 32; o <<= 1) {
+    const int t = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += t;
+  }
+  if (lane == 31) wsum[wid] = inc;
+  __syncthreads();
+  if (wid == 0) {
+    int w = wsum[lane];
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += t;
+    }
+    wsum[lane] = w;
+  }
+  __syncthreads();
+  int run = (wid ? wsum[wid - 1] : 0) + inc - tot;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int b = threadIdx.x * 4 + i;
+    if (b <= nblk) off[b] = run;
+    run += v[i];
+  }
+  if (threadIdx.x == 1023) ctl->units = wsum[31];
   __syncthreads();
   for (int b = threadIdx.x >> 5; b < nblk; b += 32)
     for (int j = threadIdx.x & 31; j < blkcnt[b]; j += 32) units[off[b] + j] = blocklist[b * kRowThreads + j];
@@ -220,12 +257,14 @@ __global__ void __launch_bounds__(256) mc_count_kernel(const float* __restrict__
                                                        int nz, const int32_t* __restrict__ units, int3* unitcnt) {
   if (ctl->status != 0) return;
   const int U = ctl->units;
-  const double L = ctl->level;
+  const float Lf = __double2float_ru(ctl->level);
   for (int i = blockIdx.x; i < U; i += gridDim.x) {
-    const size_t row0 = (size_t)units[i] * nx;
+    const int u = units[i];
+    const int y = u % ny, z = u / ny;
+    const size_t row0 = (size_t)u * nx;
     int3 c = make_int3(0, 0, 0);
     for (int x = threadIdx.x; x < nx; x += blockDim.x) {
-      const VoxelInfo vi = classify(A, nx, ny, nz, row0 + x, L);
+      const VoxelInfo vi = classify(A, nx, ny, nz, x, y, z, row0 + x, Lf);
       const int nt = vi.cfg >= 0 ? c_mc_count[vi.cfg] : 0;
       c.x += __popc(vi.mask), c.y += nt, c.z += nt > 0 ? 1 : 0;
     }
@@ -236,42 +275,43 @@ __global__ void __launch_bounds__(256) mc_count_kernel(const float* __restrict__
 
 __global__ void __launch_bounds__(1024) mc_scan_kernel(int3* blk, const DevCtl* ctl_in, DevCtl* ctl, int v_cap,
                                                        int t_cap, int c_cap) {
-  __shared__ int3 warp_sums[32];
-  __shared__ int3 carry;
+  __shared__ int3 wsum[32];
   const int n = ctl_in->status == 0 ? ctl_in->units : 0;
-  if (threadIdx.x == 0) carry = make_int3(0, 0, 0);
-  __syncthreads();
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  for (int base = 0; base < n; base += 1024) {
-    const int i = base + threadIdx.x;
-    const int3 v = i < n ? blk[i] : make_int3(0, 0, 0);
-    int3 inc = v;
-    for (int o = 1; o < 32; o <<= 1) {
-      const int a = __shfl_up_sync(0xffffffffu, inc.x, o), b = __shfl_up_sync(0xffffffffu, inc.y, o),
-                c = __shfl_up_sync(0xffffffffu, inc.z, o);
-      if (lane >= o) inc.x += a, inc.y += b, inc.z += c;
-    }
-    if (lane == 31) warp_sums[wid] = inc;
-    __syncthreads();
-    if (threadIdx.x < 32) {
-      int3 ws = warp_sums[threadIdx.x];
-      for (int o = 1; o < 32; o <<= 1) {
-        const int a = __shfl_up_sync(0xffffffffu, ws.x, o), b = __shfl_up_sync(0xffffffffu, ws.y, o),
-                  c = __shfl_up_sync(0xffffffffu, ws.z, o);
-        if (threadIdx.x >= o) ws.x += a, ws.y += b, ws.z += c;
-      }
-      warp_sums[threadIdx.x] = ws;
-    }
-    __syncthreads();
-    const int3 wp = wid ? warp_sums[wid - 1] : make_int3(0, 0, 0);
-    const int3 cr = carry;
-    if (i < n) blk[i] = make_int3(cr.x + wp.x + inc.x - v.x, cr.y + wp.y + inc.y - v.y, cr.z + wp.z + inc.z - v.z);
-    __syncthreads();
-    if (threadIdx.x == 1023) carry = make_int3(cr.x + wp.x + inc.x, cr.y + wp.y + inc.y, cr.z + wp.z + inc.z);
-    __syncthreads();
+  const int per = (n + 1023) / 1024;
+  const int b0 = min(n, threadIdx.x * per), b1 = min(n, b0 + per);
+  int3 tot = make_int3(0, 0, 0);
+  for (int i = b0; i < b1; ++i) {
+    const int3 v = blk[i];
+    tot.x += v.x, tot.y += v.y, tot.z += v.z;
   }
-  if (threadIdx.x == 0) {
-    const int3 t = carry;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  int3 inc = tot;
+  for (int o = 1; o < 32; o <<= 1) {
+    const int a = __shfl_up_sync(0xffffffffu, inc.x, o), b = __shfl_up_sync(0xffffffffu, inc.y, o),
+              c = __shfl_up_sync(0xffffffffu, inc.z, o);
+    if (lane >= o) inc.x += a, inc.y += b, inc.z += c;
+  }
+  if (lane == 31) wsum[wid] = inc;
+  __syncthreads();
+  if (wid == 0) {
+    int3 w = wsum[lane];
+    for (int o = 1; o < 32; o <<= 1) {
+      const int a = __shfl_up_sync(0xffffffffu, w.x, o), b = __shfl_up_sync(0xffffffffu, w.y, o),
+                c = __shfl_up_sync(0xffffffffu, w.z, o);
+      if (lane >= o) w.x += a, w.y += b, w.z += c;
+    }
+    wsum[lane] = w;
+  }
+  __syncthreads();
+  const int3 wp = wid ? wsum[wid - 1] : make_int3(0, 0, 0);
+  int3 run = make_int3(wp.x + inc.x - tot.x, wp.y + inc.y - tot.y, wp.z + inc.z - tot.z);
+  for (int i = b0; i < b1; ++i) {
+    const int3 v = blk[i];
+    blk[i] = run;
+    run.x += v.x, run.y += v.y, run.z += v.z;
+  }
+  if (threadIdx.x == 1023) {
+    const int3 t = wsum[31];
     ctl->V = t.x, ctl->T = t.y, ctl->C = t.z;
     ctl->overflow = (t.x > v_cap || t.y > t_cap || t.z > c_cap) ? 1 : 0;
   }
@@ -285,6 +325,7 @@ __global__ void __launch_bounds__(256) mc_emit_kernel(const float* __restrict__ 
   if (ctl->status != 0 || ctl->overflow) return;
   const int U = ctl->units;
   const double L = ctl->level;
+  const float Lf = __double2float_ru(L);
   const DevGrid g = ctl->grid;
   const size_t step[3] = {1, (size_t)nx, (size_t)nx * ny};
   for (int i = blockIdx.x; i < U; i += gridDim.x) {
@@ -295,7 +336,7 @@ __global__ void __launch_bounds__(256) mc_emit_kernel(const float* __restrict__ 
     for (int x0 = 0; x0 < nx; x0 += blockDim.x) {
       const int x = x0 + threadIdx.x;
       VoxelInfo vi{0, -1};
-      if (x < nx) vi = classify(A, nx, ny, nz, row0 + x, L);
+      if (x < nx) vi = classify(A, nx, ny, nz, x, y, z, row0 + x, Lf);
       const int nt = vi.cfg >= 0 ? c_mc_count[vi.cfg] : 0;
       int3 tot;
       const int3 ex = block_exclusive_scan3(make_int3(__popc(vi.mask), nt, nt > 0 ? 1 : 0), &tot);
@@ -386,12 +427,12 @@ __global__ void __launch_bounds__(256) mc_tris_kernel(const float* __restrict__ 
                                                       int nz, MeshBufs mb) {
   if (ctl->status != 0 || ctl->overflow) return;
   const int C = ctl->C;
-  const double L = ctl->level;
+  const float Lf = __double2float_ru(ctl->level);
   const size_t plane = (size_t)nx * ny;
   for (int i = blockIdx.x * 256 + threadIdx.x; i < C; i += gridDim.x * 256) {
     const size_t v = (size_t)mb.cells[i];
     const int tb = mb.cell_tri[i];
-    const VoxelInfo vi = classify(A, nx, ny, nz, v, L);
+    const VoxelInfo vi = classify(A, nx, ny, nz, v, Lf);
     const int n = c_mc_count[vi.cfg];
     for (int tri = 0; tri < n; ++tri) {
       int ids[3];

@@ -59,72 +59,90 @@ __global__ void __launch_bounds__(256) pre_prefix_kernel(const __grid_constant__
   }
 }
 
-// Rows y-1..y+1 staged in shared memory: validity, fp64 local positions
-// (backprojected once per pixel) and the T1/T2 triangle normals of the quads
-// touching row y (computed once per triangle instead of once per vertex).
-struct RowCache {
-  int w, h, y;
-  const uint16_t* dep;  // [3][w]
-  double* pos;          // [3][w][3]
-  double* tri;          // [2 quad rows][w][2 tris][4]: nx, ny, nz, valid (0/1)
-  __device__ bool valid(int x, int yy) const {
-    if (x < 0 || x >= w || yy < y - 1 || yy > y + 1) return false;
-    return dep[(yy - y + 1) * w + x] != 0;
-  }
-  __device__ d3 local(int x, int yy) const {
-    const double* p = pos + ((size_t)(yy - y + 1) * w + x) * 3;
-    return {p[0], p[1], p[2]};
-  }
-  // quad row qr = qy - (y - 1) in {0, 1}; triangle t in {0: T1, 1: T2}
-  __device__ const double* tri_at(int qr, int qx, int t) const { return tri + (((size_t)qr * w + qx) * 2 + t) * 4; }
-};
-
-// cloud.cpp:38-51 add_triangle(ia, ib, ic) -> normalised normal or invalid
-__device__ void triangle_normal(const RowCache& c, int ax, int ay, int bx, int by, int cx, int cy, double disc,
-                                double* out) {
-  out[3] = 0.0;
-  if (!c.valid(ax, ay) || !c.valid(bx, by) || !c.valid(cx, cy)) return;
-  const d3 a = c.local(ax, ay), b = c.local(bx, by), cc = c.local(cx, cy);
-  const double lo = fmin(fmin(a.z, b.z), cc.z), hi = fmax(fmax(a.z, b.z), cc.z);
-  if (dsub(hi, lo) > disc) return;
-  d3 n = cross3(sub3(cc, a), sub3(b, a));
-  const double len = norm3(n);
-  if (len < 1e-12) return;
-  n = div3(n, len);
-  out[0] = n.x, out[1] = n.y, out[2] = n.z, out[3] = 1.0;
+__device__ __forceinline__ bool valid_px(const ViewPtrs& v, int w, int h, int x, int y) {
+  if (x < 0 || y < 0 || x >= w || y >= h) return false;
+  return __ldg(v.mask + (size_t)y * v.mpitch + x) != 0 && __ldg(v.depth + (size_t)y * v.dpitch + x) != 0;
+}
+// camera.cpp:12-17 backproject_local with u = (x, y), z = depth
+__device__ __forceinline__ d3 local_px(const DevSensor& s, const ViewPtrs& v, int x, int y) {
+  const double z = (double)__ldg(v.depth + (size_t)y * v.dpitch + x);
+  return {ddiv(dmul(dsub((double)x, s.cx), z), s.fx), ddiv(dmul(dsub((double)y, s.cy), z), s.fy), z};
 }
 
-__device__ __forceinline__ void add_cached(const RowCache& c, int qr, int qx, int t, d3& sum, int& cnt) {
-  const double* tn = c.tri_at(qr, qx, t);
-  if (tn[3] == 0.0) return;
-  sum = add3(sum, mk3(tn[0], tn[1], tn[2]));
+// cloud.cpp:38-51 add_triangle(ia, ib, ic): the normalised normal, or NaN
+// when the triangle is rejected (invalid vertex, depth step > disc, len < 1e-12)
+__device__ d3 triangle_normal(bool ok, d3 a, d3 b, d3 c, double disc) {
+  const d3 bad{__longlong_as_double(0x7ff8000000000000ll), 0.0, 0.0};
+  if (!ok) return bad;
+  const double lo = fmin(fmin(a.z, b.z), c.z), hi = fmax(fmax(a.z, b.z), c.z);
+  if (dsub(hi, lo) > disc) return bad;
+  const d3 n = cross3(sub3(c, a), sub3(b, a));
+  const double len = norm3(n);
+  if (len < 1e-12) return bad;
+  return div3(n, len);
+}
+
+// One thread per quad (qx, qy) with a valid corner: T1 = (i00, i10, i01) and
+// T2 = (i10, i11, i01) (cloud.cpp:53-59), each normal computed once.
+__global__ void __launch_bounds__(256) pre_tri_kernel(const __grid_constant__ SensorSet ss, double disc,
+                                                      double* __restrict__ tri) {
+  const int64_t npix = ss.pix_offset[ss.k];
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < npix; q += (int64_t)gridDim.x * blockDim.x) {
+    int k = 0;
+    while (k + 1 < ss.k && q >= ss.pix_offset[k + 1]) ++k;
+    const DevSensor& s = ss.s[k];
+    const ViewPtrs& v = ss.v[k];
+    const int64_t r = q - ss.pix_offset[k];
+    const int qy = (int)(r / s.w), qx = (int)(r - (int64_t)qy * s.w);
+    if (qx + 1 >= s.w || qy + 1 >= s.h) continue;
+    const bool v00 = valid_px(v, s.w, s.h, qx, qy), v10 = valid_px(v, s.w, s.h, qx + 1, qy);
+    const bool v01 = valid_px(v, s.w, s.h, qx, qy + 1), v11 = valid_px(v, s.w, s.h, qx + 1, qy + 1);
+    if (!(v00 || v10 || v01 || v11)) continue;
+    const d3 z{0, 0, 0};
+    const d3 p00 = v00 ? local_px(s, v, qx, qy) : z, p10 = v10 ? local_px(s, v, qx + 1, qy) : z;
+    const d3 p01 = v01 ? local_px(s, v, qx, qy + 1) : z, p11 = v11 ? local_px(s, v, qx + 1, qy + 1) : z;
+    const d3 t1 = triangle_normal(v00 && v10 && v01, p00, p10, p01, disc);
+    const d3 t2 = triangle_normal(v10 && v11 && v01, p10, p11, p01, disc);
+    double* o = tri + 6 * q;
+    o[0] = t1.x, o[1] = t1.y, o[2] = t1.z, o[3] = t2.x, o[4] = t2.y, o[5] = t2.z;
+  }
+}
+
+__device__ __forceinline__ void add_tri(const double* tri, int64_t q, int t, d3& sum, int& cnt) {
+  const double* n = tri + 6 * q + 3 * t;
+  const double nx = n[0];
+  if (nx != nx) return;  // rejected triangle
+  sum = add3(sum, mk3(nx, n[1], n[2]));
   ++cnt;
 }
 
 // cloud.cpp:53-71: the six incident triangles of pixel (x, y) in the
 // reference's order Q(x-1,y-1).T2, Q(x,y-1).T1, Q(x,y-1).T2, Q(x-1,y).T1,
 // Q(x-1,y).T2, Q(x,y).T1; mean, normalise, camera-facing flip.
-__device__ bool point_at(const RowCache& c, int x, d3* local_out, d3* n_out) {
-  const int y = c.y, w = c.w, h = c.h;
-  if (!c.valid(x, y)) return false;
+__device__ bool point_at(const SensorSet& ss, int k, const double* tri, int x, int y, d3* local_out, d3* n_out) {
+  const DevSensor& s = ss.s[k];
+  const ViewPtrs& v = ss.v[k];
+  const int w = s.w, h = s.h;
+  if (!valid_px(v, w, h, x, y)) return false;
+  const int64_t q = ss.pix_offset[k] + (int64_t)y * w + x;  // quad (x, y)
   d3 sum{0.0, 0.0, 0.0};
   int cnt = 0;
-  if (x >= 1 && y >= 1) add_cached(c, 0, x - 1, 1, sum, cnt);
+  if (x >= 1 && y >= 1) add_tri(tri, q - w - 1, 1, sum, cnt);
   if (x <= w - 2 && y >= 1) {
-    add_cached(c, 0, x, 0, sum, cnt);
-    add_cached(c, 0, x, 1, sum, cnt);
+    add_tri(tri, q - w, 0, sum, cnt);
+    add_tri(tri, q - w, 1, sum, cnt);
   }
   if (x >= 1 && y <= h - 2) {
-    add_cached(c, 1, x - 1, 0, sum, cnt);
-    add_cached(c, 1, x - 1, 1, sum, cnt);
+    add_tri(tri, q - 1, 0, sum, cnt);
+    add_tri(tri, q - 1, 1, sum, cnt);
   }
-  if (x <= w - 2 && y <= h - 2) add_cached(c, 1, x, 0, sum, cnt);
+  if (x <= w - 2 && y <= h - 2) add_tri(tri, q, 0, sum, cnt);
   if (cnt == 0) return false;
   d3 n = div3(sum, (double)cnt);
   const double len = norm3(n);
   if (len < 1e-12) return false;
   n = div3(n, len);
-  const d3 local = c.local(x, y);
+  const d3 local = local_px(s, v, x, y);
   if (dot3(n, local) > 0) n = neg3(n);
   *local_out = local;
   *n_out = n;
@@ -136,63 +154,19 @@ struct Staged {  // per-point staging record (row-local order)
   int32_t px;
 };
 
-__global__ void __launch_bounds__(kThreads) pre_points_kernel(const __grid_constant__ SensorSet ss, double disc,
-                                                              int sil_r, const uint16_t* __restrict__ pref, int ppitch,
+__global__ void __launch_bounds__(kThreads) pre_points_kernel(const __grid_constant__ SensorSet ss, int sil_r,
+                                                              const double* __restrict__ tri,
+                                                              const uint16_t* __restrict__ pref, int ppitch,
                                                               Staged* __restrict__ stage, int spitch,
                                                               int32_t* __restrict__ row_counts,
                                                               float* __restrict__ weight_maps,
                                                               double* __restrict__ row_bbox) {
-  extern __shared__ double smem_d[];  // pos [3][w][3] | tri [2][w][2][4] | depth [3][w] (uint16)
   __shared__ int warp_cnt[kThreads / 32];
-  __shared__ int any_valid;
   __shared__ double bb[kThreads / 32][6];
   int k, y;
   row_of_block(ss, blockIdx.x, &k, &y);
   const DevSensor& s = ss.s[k];
-  const ViewPtrs& v = ss.v[k];
   const int w = s.w, h = s.h;
-  double* spos = smem_d;
-  double* stri = smem_d + (size_t)9 * w;
-  uint16_t* rows3 = reinterpret_cast<uint16_t*>(smem_d + (size_t)9 * w + (size_t)16 * w);
-  if (threadIdx.x == 0) any_valid = 0;
-  __syncthreads();
-  // stage rows y-1..y+1: depth where the mask is set, else 0 (cloud.cpp:28-30),
-  // and backproject each valid pixel once (camera.cpp:12-17)
-  int mine = 0;
-  for (int i = threadIdx.x; i < 3 * w; i += kThreads) {
-    const int r = i / w, x = i - r * w, yy = y - 1 + r;
-    uint16_t d = 0;
-    if (yy >= 0 && yy < h && v.mask[(size_t)yy * v.mpitch + x]) d = v.depth[(size_t)yy * v.dpitch + x];
-    rows3[i] = d;
-    if (d) {
-      const double z = (double)d;
-      spos[3 * i + 0] = ddiv(dmul(dsub((double)x, s.cx), z), s.fx);
-      spos[3 * i + 1] = ddiv(dmul(dsub((double)yy, s.cy), z), s.fy);
-      spos[3 * i + 2] = z;
-      if (r == 1) mine = 1;
-    }
-  }
-  if (mine) any_valid = 1;
-  __syncthreads();
-  float* wrow0 = weight_maps + ss.pix_offset[k] + (size_t)y * w;
-  if (!any_valid) {  // no foreground on this row: no points
-    for (int x = threadIdx.x; x < w; x += kThreads) wrow0[x] = 0.f;
-    if (threadIdx.x < 6) row_bbox[(size_t)blockIdx.x * 6 + threadIdx.x] = threadIdx.x < 3 ? DBL_MAX * 2.0 : -DBL_MAX * 2.0;
-    if (threadIdx.x == 0) row_counts[blockIdx.x] = 0;
-    return;
-  }
-  const RowCache c{w, h, y, rows3, spos, stri};
-  // triangle normals of quads (qx, qy), qy in {y-1, y}: T1 = (i00,i10,i01), T2 = (i10,i11,i01)
-  for (int i = threadIdx.x; i < 2 * w; i += kThreads) {
-    const int qr = i / w, qx = i - qr * w, qy = y - 1 + qr;
-    double* t1 = stri + ((size_t)(qr * w + qx) * 2 + 0) * 4;
-    double* t2 = t1 + 4;
-    t1[3] = 0.0, t2[3] = 0.0;
-    if (qx + 1 >= w || qy < 0 || qy + 1 >= h) continue;
-    triangle_normal(c, qx, qy, qx + 1, qy, qx, qy + 1, disc, t1);
-    triangle_normal(c, qx + 1, qy, qx + 1, qy + 1, qx, qy + 1, disc, t2);
-  }
-  __syncthreads();
   const double window = (double)(2 * sil_r + 1) * (double)(2 * sil_r + 1);
   const int wy0 = max(0, y - sil_r), wy1 = min(h - 1, y + sil_r);
   const uint16_t* prow0 = pref + (size_t)(blockIdx.x - y) * ppitch;  // row 0 of this view
@@ -200,12 +174,12 @@ __global__ void __launch_bounds__(kThreads) pre_points_kernel(const __grid_const
   double lo0 = inf, lo1 = inf, lo2 = inf, hi0 = -inf, hi1 = -inf, hi2 = -inf;
   int base = 0;
   Staged* srow = stage + (size_t)blockIdx.x * spitch;
-  float* wrow = wrow0;
+  float* wrow = weight_maps + ss.pix_offset[k] + (size_t)y * w;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   for (int x0 = 0; x0 < w; x0 += kThreads) {
     const int x = x0 + threadIdx.x;
     d3 local{0, 0, 0}, n{0, 0, 0};
-    const bool is_pt = x < w && point_at(c, x, &local, &n);
+    const bool is_pt = x < w && point_at(ss, k, tri, x, y, &local, &n);
     const unsigned ball = __ballot_sync(0xffffffffu, is_pt);
     if (lane == 0) warp_cnt[wid] = __popc(ball);
     __syncthreads();
@@ -374,6 +348,7 @@ __global__ void __launch_bounds__(256) pre_fit_kernel(const double* row_bbox, in
 }
 
 struct Scratch {
+  double* tri;  // 6 doubles per quad (indexed by its i00 pixel)
   int32_t* counts;
   int32_t* offsets;
   double* bbox;
@@ -389,6 +364,8 @@ Scratch carve(const SensorSet& ss, void* base) {
   auto up = [](uintptr_t p) { return (p + 255) & ~uintptr_t(255); };
   Scratch s;
   uintptr_t p = up(reinterpret_cast<uintptr_t>(base));
+  s.tri = reinterpret_cast<double*>(p);
+  p = up(p + (size_t)ss.pix_offset[ss.k] * 6 * sizeof(double));
   s.counts = reinterpret_cast<int32_t*>(p);
   p = up(p + rows * sizeof(int32_t));
   s.offsets = reinterpret_cast<int32_t*>(p);
@@ -406,15 +383,7 @@ Scratch carve(const SensorSet& ss, void* base) {
 
 }  // namespace
 
-static size_t points_smem(int maxw) {
-  return (size_t)maxw * (9 + 16) * sizeof(double) + 3 * (size_t)maxw * sizeof(uint16_t) + 16;
-}
-
-void prepare_preprocess(const SensorSet& ss) {  // outside any graph capture
-  int maxw = 0;
-  for (int k = 0; k < ss.k; ++k) maxw = maxw > ss.s[k].w ? maxw : ss.s[k].w;
-  cudaFuncSetAttribute(pre_points_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)points_smem(maxw));
-}
+void prepare_preprocess(const SensorSet&) {}  // no opt-in shared memory needed
 
 size_t preprocess_scratch_bytes(const SensorSet& ss) {
   const Scratch s = carve(ss, nullptr);
@@ -430,10 +399,9 @@ void launch_preprocess(const SensorSet& ss, DevPoints pts, float* weight_maps, i
   for (int k = 0; k < ss.k; ++k) maxw = maxw > ss.s[k].w ? maxw : ss.s[k].w;
   const int warp_grid = (rows * 32 + 255) / 256;
   pre_prefix_kernel<<<warp_grid, 256, 0, st>>>(ss, rows, s.pref, s.ppitch);
-  const size_t smem = points_smem(maxw);
-  pre_points_kernel<<<rows, kThreads, smem, st>>>(ss, disc_mm, sil_r, s.pref, s.ppitch,
-                                                                         s.stage, s.spitch, s.counts, weight_maps,
-                                                                         s.bbox);
+  pre_tri_kernel<<<148 * 8, 256, 0, st>>>(ss, disc_mm, s.tri);
+  pre_points_kernel<<<rows, kThreads, 0, st>>>(ss, sil_r, s.tri, s.pref, s.ppitch, s.stage, s.spitch, s.counts,
+                                               weight_maps, s.bbox);
   pre_scan_kernel<<<1, 1024, 0, st>>>(s.counts, s.offsets, rows, pts.cap, ctl);
   pre_gather_kernel<<<warp_grid, 256, 0, st>>>(ss, rows, s.stage, s.spitch, s.counts, s.offsets, pts);
   pre_fit_kernel<<<1, 256, 0, st>>>(s.bbox, rows, nx, ny, nz, padding, ctl);

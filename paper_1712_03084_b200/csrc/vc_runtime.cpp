@@ -339,7 +339,7 @@ int enqueue_frame(vc_ctx* ctx, const FrameCfg& f) {
   record(ctx, 0);
   launch_preprocess(ctx->ss, points(ctx), P<float>(ctx->wmaps), P<int32_t>(ctx->pre_scratch), ctx->ctl, f.nx, f.ny,
                     f.nz, f.pad, f.disc, f.sil_r, st);
-  n += 5;
+  n += 6;
   record(ctx, 1);
   record(ctx, 12);
   launch_sparse_clear(P<float4>(ctx->acc), P<uint32_t>(ctx->rowbits), f.ny * f.nz, f.nx, st);
