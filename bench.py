@@ -244,9 +244,10 @@ def run_gpu(args):
 
     dev_views = [views_for(dbuf.value, f, L.VC_MEM_DEVICE) for f in range(STREAM)]
     host_views = [views_for(hbuf.value, f, L.VC_MEM_HOST) for f in range(STREAM)]
+    from paper_1712_03084_b200.frame_parallel import max_over_ranks, shard_frames
     cfg = vc.ReconConfig(dims=DIMS).to_c()
     out = L.TexturedMesh()
-    my_frames = list(range(rank, STREAM, world)) or [0]
+    my_frames = shard_frames(STREAM, rank, world) or [0]
 
     def frame(i, views):
         L.check(lib.vc_reconstruct_frame(h, sensors, views[my_frames[i % len(my_frames)]], K_VIEWS, C.byref(cfg),
@@ -266,11 +267,7 @@ def run_gpu(args):
         ev1.record(stream)
         torch.cuda.synchronize()
         wall = time.perf_counter() - t0
-        ms = ev0.elapsed_time(ev1)
-        if world > 1:
-            t = torch.tensor([ms], device="cuda")
-            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-            ms = float(t.item())
+        ms = max_over_ranks(ev0.elapsed_time(ev1), device="cuda")
         return ms, wall, d2h / steps
 
     # ---- device-resident (value)

@@ -401,8 +401,10 @@ __global__ void __launch_bounds__(CCfg<NY>::THREADS, 2) fy_kernel(float2* __rest
 }
 
 // ------------------------------------------------------------------ Z (fused)
+// FFT_z(D) is parked in its staged tile while FFT_z(Z) runs (one register
+// array live, three CTAs per SM).
 template <int NZ>
-__global__ void __launch_bounds__(CCfg<NZ>::THREADS, 2) z_kernel(float2* __restrict__ S0,
+__global__ void __launch_bounds__(CCfg<NZ>::THREADS, 3) z_kernel(float2* __restrict__ S0,
                                                                 const float2* __restrict__ S1, int nx, int ny,
                                                                 int H, const float2* __restrict__ tw) {
   using S = Shape<NZ>;
@@ -420,19 +422,22 @@ __global__ void __launch_bounds__(CCfg<NZ>::THREADS, 2) z_kernel(float2* __restr
   cp_async_commit();
   stage_tile<NZ, kCW, TH>(b1, S1 + (size_t)ky * H, zstride, kx0, H, 0xffffffffu);
   cp_async_commit();
-  float2 d[R1], z[R1];
+  float2 v[R1];
   cp_async_wait<1>();
   __syncthreads();
-  tile_to_regs<NZ, kCW>(b0, c, t, d);
+  tile_to_regs<NZ, kCW>(b0, c, t, v);
   __syncthreads();
   ExCols<NZ, kCW> e0{b0, c};
-  fft_line<NZ, false>(d, t, tw, e0);
+  fft_line<NZ, false>(v, t, tw, e0);
+  // park FFT_z(D): thread (c, t) owns slots (t + T*k1, c) of b0 (free again)
+#pragma unroll
+  for (int k1 = 0; k1 < R1; ++k1) b0[(t + T * k1) * kCW + c] = v[k1];
   cp_async_wait<0>();
   __syncthreads();
-  tile_to_regs<NZ, kCW>(b1, c, t, z);
+  tile_to_regs<NZ, kCW>(b1, c, t, v);
   __syncthreads();
   ExCols<NZ, kCW> e1{b1, c};
-  fft_line<NZ, false>(z, t, tw, e1);
+  fft_line<NZ, false>(v, t, tw, e1);
   const float wx = signed_freq(kx, nx), wy = signed_freq(ky, ny);
   const float wxy = wx * wx + wy * wy;
 #pragma unroll
@@ -440,15 +445,17 @@ __global__ void __launch_bounds__(CCfg<NZ>::THREADS, 2) z_kernel(float2* __restr
     const int kz = t + T * k1;
     const float wz = signed_freq<NZ>(kz);
     const float w2 = wxy + wz * wz;
-    const float2 s = make_float2(d[k1].x + wz * z[k1].x, d[k1].y + wz * z[k1].y);
+    const float2 d = b0[kz * kCW + c];
+    const float2 s = make_float2(d.x + wz * v[k1].x, d.y + wz * v[k1].y);
     const float inv = (kx == 0 && ky == 0 && kz == 0) ? 0.f : __frcp_rn(w2);
-    d[k1] = make_float2(s.y * inv, -s.x * inv);  // (-i/|w|^2) * s
+    v[k1] = make_float2(s.y * inv, -s.x * inv);  // (-i/|w|^2) * s
   }
-  relayout_for_inverse<NZ>(d);
-  fft_line<NZ, true>(d, t, tw, e0);
+  __syncthreads();  // everyone has read its parked D before b0 becomes the exchange
+  relayout_for_inverse<NZ>(v);
+  fft_line<NZ, true>(v, t, tw, e0);
   if (live) {
 #pragma unroll
-    for (int k1 = 0; k1 < R1; ++k1) __stcs(S0 + base + (size_t)(t + T * k1) * zstride, d[k1]);
+    for (int k1 = 0; k1 < R1; ++k1) __stcs(S0 + base + (size_t)(t + T * k1) * zstride, v[k1]);
   }
 }
 

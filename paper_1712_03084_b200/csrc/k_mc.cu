@@ -172,7 +172,7 @@ __global__ void row_minmax_kernel(const float* __restrict__ A, int nx, int rows,
 constexpr int kRowThreads = 256;
 
 __global__ void __launch_bounds__(kRowThreads) mc_rows_kernel(const float2* __restrict__ rowmm, const DevCtl* ctl,
-                                                              int ny, int nz, int32_t* blocklist, int32_t* blkcnt) {
+                                                              int ny, int nz, uint32_t* rowmask) {
   const int u = blockIdx.x * kRowThreads + threadIdx.x;
   bool active = false;
   if (u < ny * nz && ctl->status == 0) {
@@ -185,30 +185,18 @@ __global__ void __launch_bounds__(kRowThreads) mc_rows_kernel(const float2* __re
     if (y + 1 < ny && z + 1 < nz) m = rowmm[u + ny + 1], lo = fminf(lo, m.x), hi = fmaxf(hi, m.y);
     active = (double)hi >= L && (double)lo < L;
   }
-  __shared__ int wc[kRowThreads / 32];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const unsigned b = __ballot_sync(0xffffffffu, active);
-  if (lane == 0) wc[wid] = __popc(b);
-  __syncthreads();
-  int pre = 0, tot = 0;
-  for (int i = 0; i < kRowThreads / 32; ++i) pre += i < wid ? wc[i] : 0, tot += wc[i];
-  if (active) blocklist[blockIdx.x * kRowThreads + pre + __popc(b & ((1u << lane) - 1u))] = u;
-  if (threadIdx.x == 0) blkcnt[blockIdx.x] = tot;
+  if ((threadIdx.x & 31) == 0) rowmask[u >> 5] = b;
 }
 
-// single CTA: gather the active units into one ordered list
-__global__ void __launch_bounds__(1024) mc_units_kernel(const int32_t* blocklist, const int32_t* blkcnt, int nblk,
+// single CTA: ordered list of the active units from the bit mask
+__global__ void __launch_bounds__(1024) mc_units_kernel(const uint32_t* __restrict__ rowmask, int nwords,
                                                         int32_t* units, DevCtl* ctl) {
-  __shared__ int off[4097];  // nblk <= 4096 (ny*nz <= 1M)
   __shared__ int wsum[32];
-  // exclusive scan of blkcnt: 4 entries per thread, warp + block scan
-  int v[4], tot = 0;
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int b = threadIdx.x * 4 + i;
-    v[i] = b < nblk ? blkcnt[b] : 0;
-    tot += v[i];
-  }
+  const int per = (nwords + 1023) / 1024;
+  const int w0 = min(nwords, (int)threadIdx.x * per), w1 = min(nwords, w0 + per);
+  int tot = 0;
+  for (int i = w0; i < w1; ++i) tot += __popc(rowmask[i]);
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   int inc = tot;
   for (int o = 1; o < 32; o <<= 1) {
@@ -226,17 +214,16 @@ __global__ void __launch_bounds__(1024) mc_units_kernel(const int32_t* blocklist
     wsum[lane] = w;
   }
   __syncthreads();
-  int run = (wid ? wsum[wid - 1] : 0) + inc - tot;
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int b = threadIdx.x * 4 + i;
-    if (b <= nblk) off[b] = run;
-    run += v[i];
+  int pos = (wid ? wsum[wid - 1] : 0) + inc - tot;
+  for (int i = w0; i < w1; ++i) {
+    uint32_t m = rowmask[i];
+    while (m) {
+      const int b = __ffs(m) - 1;
+      m &= m - 1;
+      units[pos++] = i * 32 + b;
+    }
   }
   if (threadIdx.x == 1023) ctl->units = wsum[31];
-  __syncthreads();
-  for (int b = threadIdx.x >> 5; b < nblk; b += 32)
-    for (int j = threadIdx.x & 31; j < blkcnt[b]; j += 32) units[off[b] + j] = blocklist[b * kRowThreads + j];
 }
 
 __device__ __forceinline__ int3 block_reduce3(int3 v) {
@@ -278,9 +265,15 @@ __global__ void __launch_bounds__(1024) mc_scan_kernel(int3* blk, const DevCtl* 
   __shared__ int3 wsum[32];
   const int n = ctl_in->status == 0 ? ctl_in->units : 0;
   const int per = (n + 1023) / 1024;
-  const int b0 = min(n, threadIdx.x * per), b1 = min(n, b0 + per);
+  const int b0 = min(n, (int)threadIdx.x * per), b1 = min(n, b0 + per);
+  int3 vals[16];
   int3 tot = make_int3(0, 0, 0);
-  for (int i = b0; i < b1; ++i) {
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    vals[i] = b0 + i < b1 ? blk[b0 + i] : make_int3(0, 0, 0);
+    tot.x += vals[i].x, tot.y += vals[i].y, tot.z += vals[i].z;
+  }
+  for (int i = b0 + 16; i < b1; ++i) {
     const int3 v = blk[i];
     tot.x += v.x, tot.y += v.y, tot.z += v.z;
   }
@@ -305,7 +298,13 @@ __global__ void __launch_bounds__(1024) mc_scan_kernel(int3* blk, const DevCtl* 
   __syncthreads();
   const int3 wp = wid ? wsum[wid - 1] : make_int3(0, 0, 0);
   int3 run = make_int3(wp.x + inc.x - tot.x, wp.y + inc.y - tot.y, wp.z + inc.z - tot.z);
-  for (int i = b0; i < b1; ++i) {
+#pragma unroll
+  for (int i = 0; i < 16; ++i)
+    if (b0 + i < b1) {
+      blk[b0 + i] = run;
+      run.x += vals[i].x, run.y += vals[i].y, run.z += vals[i].z;
+    }
+  for (int i = b0 + 16; i < b1; ++i) {
     const int3 v = blk[i];
     blk[i] = run;
     run.x += v.x, run.y += v.y, run.z += v.z;
@@ -481,13 +480,12 @@ void launch_row_minmax(const float* A, int nx, int ny, int nz, float2* rowmm, cu
 void launch_marching_cubes(const float* A, DevCtl* ctl, MeshBufs mb, int nx, int ny, int nz, cudaStream_t st) {
   const int units = ny * nz;
   const int nblk = (units + kRowThreads - 1) / kRowThreads;
-  int32_t* blocklist = mb.blk;                 // units entries
-  int32_t* blkcnt = mb.blk + units;            // nblk entries
-  int32_t* ulist = mb.units;                   // units entries
+  uint32_t* rowmask = reinterpret_cast<uint32_t*>(mb.blk);  // ceil(units/32) words
+  int32_t* ulist = mb.units;                                  // units entries
   int3* ucnt = reinterpret_cast<int3*>(mb.unitcnt);
   const int threads = nx >= 256 ? 256 : (nx >= 128 ? 128 : (nx >= 64 ? 64 : 32));
-  mc_rows_kernel<<<nblk, kRowThreads, 0, st>>>(mb.rowmm, ctl, ny, nz, blocklist, blkcnt);
-  mc_units_kernel<<<1, 1024, 0, st>>>(blocklist, blkcnt, nblk, ulist, ctl);
+  mc_rows_kernel<<<nblk, kRowThreads, 0, st>>>(mb.rowmm, ctl, ny, nz, rowmask);
+  mc_units_kernel<<<1, 1024, 0, st>>>(rowmask, (units + 31) / 32, ulist, ctl);
   mc_count_kernel<<<148 * 8, threads, 0, st>>>(A, ctl, nx, ny, nz, ulist, ucnt);
   mc_scan_kernel<<<1, 1024, 0, st>>>(ucnt, ctl, ctl, mb.v_cap, mb.t_cap, mb.c_cap);
   mc_emit_kernel<<<148 * 8, threads, 0, st>>>(A, ctl, nx, ny, nz, ulist, ucnt, mb);

@@ -168,7 +168,7 @@ vc_status check_sensors(vc_ctx* ctx, const vc_sensor* s, int k) {
     if (d.width <= 0 || d.height <= 0 || r.width <= 0 || r.height <= 0 || d.fx <= 0 || d.fy <= 0 || r.fx <= 0 ||
         r.fy <= 0)
       return fail(ctx, VC_ERR_INVALID_ARGUMENT, "Intrinsics: focal lengths / image sizes must be positive");
-    if (d.width > 1024) return fail(ctx, VC_ERR_INVALID_ARGUMENT, "depth width > 1024 (pre_points stages 3 rows in shared memory)");
+    if (d.width > 8192) return fail(ctx, VC_ERR_INVALID_ARGUMENT, "depth width > 8192");
   }
   return VC_OK;
 }
