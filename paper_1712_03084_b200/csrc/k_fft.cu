@@ -487,66 +487,98 @@ __global__ void __launch_bounds__(CCfg<NY>::THREADS, 3) iy_kernel(float2* __rest
 }
 
 // ------------------------------------------------------------------ I-x
+// Persistent teams: each team (T adjacent lanes) walks line pairs with a
+// double-buffered cp.async stage of the next pair's half spectra, so the
+// loads of pair i+1 overlap the C2R of pair i with no CTA-wide barrier.
 template <int NX>
-__global__ void __launch_bounds__(XCfg<NX>::THREADS, 2) ix_kernel(const float2* __restrict__ S0, float* __restrict__ A,
+struct IXCfg {
+  static constexpr int T = Shape<NX>::R2;
+  static constexpr int LINE = ((NX / 2 + 4) + 7) & ~7;  // >= pitch, 64 B aligned slots
+  static constexpr int BUF0 = 2 * LINE;
+  static constexpr int TILE = Shape<NX>::R1 * (T + 1);
+  static constexpr int BUF = BUF0 > TILE ? BUF0 : TILE;  // staged pair, then the exchange
+  static constexpr int T0 = 256 / T;
+  static constexpr int TEAMS = (T0 * 2 * BUF * 8 <= 96 * 1024) ? T0 : (T0 / 2 * 2 * BUF * 8 <= 96 * 1024 ? T0 / 2 : T0 / 4);
+  static constexpr int THREADS = T * TEAMS;
+  static constexpr int SMEM = TEAMS * 2 * BUF * 8;
+};
+
+template <int NX>
+__global__ void __launch_bounds__(IXCfg<NX>::THREADS, 2) ix_kernel(const float2* __restrict__ S0, float* __restrict__ A,
                                                        int rows, int H, float scale,
                                                        const float2* __restrict__ tw, float2* __restrict__ rowmm) {
   using S = Shape<NX>;
-  constexpr int T = S::R2, R1 = S::R1, TEAMS = XCfg<NX>::TEAMS, NH = NX / 2;
+  using CF = IXCfg<NX>;
+  constexpr int T = S::R2, R1 = S::R1, NH = NX / 2;
   extern __shared__ float2 dyn_smem[];
   const int team = threadIdx.x / T, t = threadIdx.x % T;
-  float2* const tile = dyn_smem + team * XCfg<NX>::TILE;
-  ExTeam<NX> ex{tile, team_mask<T>((threadIdx.x & 31) - t)};
-  const int pair = blockIdx.x * TEAMS + team;
-  const int l0 = 2 * pair, l1 = l0 + 1;
-  const bool live = l1 < rows;
-  float2* h0 = tile;
-  float2* h1 = tile + (NH + 1);
-  for (int k = t; k <= NH; k += T) {
-    h0[k] = live ? __ldcs(S0 + (size_t)l0 * H + k) : make_float2(0.f, 0.f);
-    h1[k] = live ? __ldcs(S0 + (size_t)l1 * H + k) : make_float2(0.f, 0.f);
-  }
-  __syncwarp(ex.mask);
-  // Hermitian extension with Re() of bins 0 and n/2 (numpy irfft / FFTW c2r)
-  auto full = [&](const float2* h, int j) {
-    if (j == 0) return make_float2(h[0].x, 0.f);
-    if (j == NH) return make_float2(h[NH].x, 0.f);
-    if (j < NH) return h[j];
-    const float2 c = h[NX - j];
-    return make_float2(c.x, -c.y);
-  };
-  float2 v[R1];
-#pragma unroll
-  for (int q = 0; q < S::Q; ++q)
-#pragma unroll
-    for (int j2 = 0; j2 < T; ++j2) {
-      const int j = t + T * q + R1 * j2;
-      const float2 f0 = full(h0, j), f1 = full(h1, j);
-      v[q * T + j2] = make_float2(f0.x - f1.y, f0.y + f1.x);  // F0 + i F1
+  const unsigned mask = team_mask<T>((threadIdx.x & 31) - t);
+  float2* const bufs = dyn_smem + (size_t)team * 2 * CF::BUF;
+  const int pairs = rows / 2;
+  const int stride = gridDim.x * CF::TEAMS;
+  const int chunks = (H * 8) / 16;  // 16 B per cp.async; H is a multiple of 4
+  auto stage = [&](int pr, float2* b) {
+    const float2* src = S0 + (size_t)(2 * pr) * H;
+    for (int i = t; i < 2 * chunks; i += T) {
+      const int l = i / chunks, c = i - l * chunks;
+      cp_async16(b + l * CF::LINE + 2 * c, src + (size_t)l * H + 2 * c, true);
     }
-  __syncwarp(ex.mask);
-  fft_line<NX, true>(v, t, tw, ex);
-  float lo0 = 3.4e38f, hi0 = -3.4e38f, lo1 = 3.4e38f, hi1 = -3.4e38f;
+  };
+  int pr = blockIdx.x * CF::TEAMS + team;
+  if (pr < pairs) stage(pr, bufs);
+  cp_async_commit();
+  for (int it = 0; pr < pairs; ++it, pr += stride) {
+    float2* cur = bufs + (it & 1) * CF::BUF;
+    const int nx_pr = pr + stride;
+    if (nx_pr < pairs) stage(nx_pr, bufs + ((it + 1) & 1) * CF::BUF);
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncwarp(mask);
+    const float2* h0 = cur;
+    const float2* h1 = cur + CF::LINE;
+    // Hermitian extension with Re() of bins 0 and n/2 (numpy irfft / FFTW c2r)
+    auto full = [&](const float2* h, int j) {
+      if (j == 0) return make_float2(h[0].x, 0.f);
+      if (j == NH) return make_float2(h[NH].x, 0.f);
+      if (j < NH) return h[j];
+      const float2 c = h[NX - j];
+      return make_float2(c.x, -c.y);
+    };
+    float2 v[R1];
 #pragma unroll
-  for (int k1 = 0; k1 < R1; ++k1) {
-    const int k = t + T * k1;
-    const float a0 = v[k1].x * scale, a1 = v[k1].y * scale;
-    lo0 = fminf(lo0, a0), hi0 = fmaxf(hi0, a0), lo1 = fminf(lo1, a1), hi1 = fmaxf(hi1, a1);
-    if (live) {
+    for (int q = 0; q < S::Q; ++q)
+#pragma unroll
+      for (int j2 = 0; j2 < T; ++j2) {
+        const int j = t + T * q + R1 * j2;
+        const float2 f0 = full(h0, j), f1 = full(h1, j);
+        v[q * T + j2] = make_float2(f0.x - f1.y, f0.y + f1.x);  // F0 + i F1
+      }
+    __syncwarp(mask);
+    ExTeam<NX> ex{cur, mask};
+    fft_line<NX, true>(v, t, tw, ex);
+    const int l0 = 2 * pr, l1 = l0 + 1;
+    float lo0 = 3.4e38f, hi0 = -3.4e38f, lo1 = 3.4e38f, hi1 = -3.4e38f;
+#pragma unroll
+    for (int k1 = 0; k1 < R1; ++k1) {
+      const int k = t + T * k1;
+      const float a0 = v[k1].x * scale, a1 = v[k1].y * scale;
+      lo0 = fminf(lo0, a0), hi0 = fmaxf(hi0, a0), lo1 = fminf(lo1, a1), hi1 = fmaxf(hi1, a1);
       __stcs(A + (size_t)l0 * NX + k, a0);
       __stcs(A + (size_t)l1 * NX + k, a1);
     }
-  }
-  // per-row min/max for marching-cubes row culling (team = T adjacent lanes)
+    // per-row min/max for marching-cubes row culling
 #pragma unroll
-  for (int o = T / 2; o > 0; o >>= 1) {
-    lo0 = fminf(lo0, __shfl_xor_sync(0xffffffffu, lo0, o)), hi0 = fmaxf(hi0, __shfl_xor_sync(0xffffffffu, hi0, o));
-    lo1 = fminf(lo1, __shfl_xor_sync(0xffffffffu, lo1, o)), hi1 = fmaxf(hi1, __shfl_xor_sync(0xffffffffu, hi1, o));
+    for (int o = T / 2; o > 0; o >>= 1) {
+      lo0 = fminf(lo0, __shfl_xor_sync(mask, lo0, o)), hi0 = fmaxf(hi0, __shfl_xor_sync(mask, hi0, o));
+      lo1 = fminf(lo1, __shfl_xor_sync(mask, lo1, o)), hi1 = fmaxf(hi1, __shfl_xor_sync(mask, hi1, o));
+    }
+    if (rowmm && t == 0) {
+      rowmm[l0] = make_float2(lo0, hi0);
+      rowmm[l1] = make_float2(lo1, hi1);
+    }
+    __syncwarp(mask);  // `cur` is re-staged two iterations later
   }
-  if (rowmm && live && t == 0) {
-    rowmm[l0] = make_float2(lo0, hi0);
-    rowmm[l1] = make_float2(lo1, hi1);
-  }
+  cp_async_wait<0>();
 }
 
 // ------------------------------------------------------------------ dispatch
@@ -590,7 +622,7 @@ struct Prep {
   static void run(int axis) {
     if (axis == 0) {
       allow_smem(fx_kernel<N>, XCfg<N>::SMEM);
-      allow_smem(ix_kernel<N>, XCfg<N>::SMEM);
+      allow_smem(ix_kernel<N>, IXCfg<N>::SMEM);
     } else if (axis == 1) {
       allow_smem(fy_kernel<N>, 3 * CCfg<N>::SMEM);
       allow_smem(iy_kernel<N>, CCfg<N>::SMEM);
@@ -636,9 +668,10 @@ struct RunIy {
 template <int N>
 struct RunIx {
   static void run(const FftArgs& a) {
-    using C = XCfg<N>;
+    using C = IXCfg<N>;
     const int rows = a.ny * a.nz;
-    const int grid = (rows / 2 + C::TEAMS - 1) / C::TEAMS;
+    const int need = (rows / 2 + C::TEAMS - 1) / C::TEAMS;
+    const int grid = need < 148 * 4 ? need : 148 * 4;  // persistent teams
     const float scale = (float)(1.0 / ((double)a.nx * a.ny * a.nz));
     ix_kernel<N><<<grid, C::THREADS, C::SMEM, a.st>>>(a.S0, a.A, rows, a.H, scale, a.twx, a.rowmm);
   }

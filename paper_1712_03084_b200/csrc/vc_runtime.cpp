@@ -832,6 +832,7 @@ vc_status vc_stage_marching_cubes(vc_ctx* ctx, const float* A, const vc_grid_spe
                                   const float** normals, const int32_t** triangles, const uint64_t** edge_ids) {
   if (!ctx || !A || !grid || !n_vertices || !n_triangles) return fail(ctx, VC_ERR_INVALID_ARGUMENT, "null");
   const int nx = grid->nx, ny = grid->ny, nz = grid->nz;
+  if (nx > 1024) return fail(ctx, VC_ERR_INVALID_ARGUMENT, "marching cubes: nx > 1024");
   if (nx < 2 || ny < 2 || nz < 2) {  // marching_cubes.cpp:135
     *n_vertices = *n_triangles = 0;
     return VC_OK;
