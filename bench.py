@@ -179,10 +179,11 @@ def sparse_stats(pos, origin, edge, nx, ny, nz):
             c1 = np.minimum(f[ok, 0] + 2, nx - 1) // 32
             keys += [row * 64 + c0, row * 64 + c1]
     keys = np.unique(np.concatenate(keys)) if keys else np.zeros(0, np.int64)
-    return len(keys), len(np.unique(keys // 64))
+    rows = np.unique(keys // 64)
+    return len(keys), len(rows), len(np.unique(rows // ny))
 
 
-def alg_bytes(nx, ny, nz, P, V, T, k, chunks, nzrows):
+def alg_bytes(nx, ny, nz, P, V, T, k, chunks, nzrows, nzplanes):
     """Compulsory bytes per launch in the fp32 device layout (each tensor read
     once and written once; the sparse clear / F-x / F-y touch only the splat's
     32-voxel chunks and non-empty rows) — SURVEY §8(d) adapted, see DESIGN.md."""
@@ -192,8 +193,8 @@ def alg_bytes(nx, ny, nz, P, V, T, k, chunks, nzrows):
     line = 8 * (nx // 2 + 1)
     return {"clear": 16 * 32 * chunks + 8 * rows, "splat": 16 * 64 * P + 4 * 16 * P,
             "fft_x": 16 * 32 * chunks + 4 * rows + 3 * line * nzrows,
-            "fft_y": 3 * line * nzrows + 4 * rows + 2 * 8 * Nh,
-            "fft_z": 2 * 8 * Nh + 8 * Nh, "ifft_y": 2 * 8 * Nh, "ifft_x": 8 * Nh + 4 * N + 8 * rows,
+            "fft_y": 3 * line * nzrows + 4 * rows + 2 * line * ny * nzplanes,
+            "fft_z": 2 * line * ny * nzplanes + 8 * Nh, "ifft_y": 2 * 8 * Nh, "ifft_x": 8 * Nh + 4 * N + 8 * rows,
             "mc": 8 * rows, "preprocess": k * W * H * 7 + P * 60, "iso": P * 32, "texture": V * (24 + 13 * k)}
 
 
@@ -335,8 +336,8 @@ def run_gpu(args):
     P, V, T = out.point_count, out.vertex_count, out.triangle_count
     pos = np.zeros((P, 3))
     L.check(lib.vc_export_points(h, C.c_void_p(pos.ctypes.data), None, None, None, None), h)
-    chunks, nzrows = sparse_stats(pos, out.grid.origin[:], out.grid.edge_mm, *DIMS)
-    ab = alg_bytes(*DIMS, P, V, T, K_VIEWS, chunks, nzrows)
+    chunks, nzrows, nzplanes = sparse_stats(pos, out.grid.origin[:], out.grid.edge_mm, *DIMS)
+    ab = alg_bytes(*DIMS, P, V, T, K_VIEWS, chunks, nzrows, nzplanes)
     bw = {n: ab[n] / (kernel_ms[n] * 1e-3) / 1e9 for n in names if kernel_ms[n] > 0}
     if not all(n in bw for n in ["clear", "fft_x", "fft_y", "fft_z", "ifft_y", "ifft_x"]):
         raise RuntimeError(f"per-kernel event timings missing: {kernel_ms}")
@@ -376,7 +377,8 @@ def run_gpu(args):
             "kernel_gbs": {k: round(v, 1) for k, v in bw.items()},
             "mesh": {"points": P, "vertices": V, "triangles": T},
             "sparsity": {"touched_chunks": chunks, "chunks_total": DIMS[1] * DIMS[2] * (DIMS[0] // 32),
-                         "nonzero_rows": nzrows, "rows_total": DIMS[1] * DIMS[2]},
+                         "nonzero_rows": nzrows, "rows_total": DIMS[1] * DIMS[2],
+                         "nonzero_planes": nzplanes, "planes_total": DIMS[2]},
             "algorithmic_bytes": ab,
             "clocks": clk.summary(),
             "wall_s": wall,

@@ -347,7 +347,8 @@ template <int NY>
 __global__ void __launch_bounds__(CCfg<NY>::THREADS, 2) fy_kernel(float2* __restrict__ S0, float2* __restrict__ S1,
                                                                  const float2* __restrict__ S2, int nxh, int H,
                                                                  const float2* __restrict__ tw,
-                                                                 const uint32_t* __restrict__ rowbits) {
+                                                                 const uint32_t* __restrict__ rowbits,
+                                                                 uint32_t* __restrict__ planeflag) {
   using S = Shape<NY>;
   constexpr int T = S::R2, R1 = S::R1, kCW = CCfg<NY>::CW, TH = CCfg<NY>::THREADS;
   extern __shared__ float2 sh[];  // 3 tiles of NY x kCW
@@ -358,8 +359,12 @@ __global__ void __launch_bounds__(CCfg<NY>::THREADS, 2) fy_kernel(float2* __rest
   const int kx0 = blockIdx.x * kCW, kx = kx0 + c;
   const bool live = kx < nxh;
   const size_t plane = (size_t)blockIdx.y * NY * H;
-  // empty rows (F-x skipped them) are zero-filled
+  // empty rows (F-x skipped them) are zero-filled; a plane with no splat
+  // contribution at all has zero spectra: it is skipped and flagged for Z
   const uint32_t rm = row_flags<NY, kCW, TH>(rowbits ? rowbits + (size_t)blockIdx.y * NY : nullptr);
+  const int nonempty = __syncthreads_or(rm != 0u);
+  if (blockIdx.x == 0 && threadIdx.x == 0) planeflag[blockIdx.y] = nonempty ? 1u : 0u;
+  if (!nonempty) return;
   stage_tile<NY, kCW, TH>(b0, S0 + plane, H, kx0, H, rm);
   cp_async_commit();
   stage_tile<NY, kCW, TH>(b1, S1 + plane, H, kx0, H, rm);
@@ -406,7 +411,8 @@ __global__ void __launch_bounds__(CCfg<NY>::THREADS, 2) fy_kernel(float2* __rest
 template <int NZ>
 __global__ void __launch_bounds__(CCfg<NZ>::THREADS, 3) z_kernel(float2* __restrict__ S0,
                                                                 const float2* __restrict__ S1, int nx, int ny,
-                                                                int H, const float2* __restrict__ tw) {
+                                                                int H, const float2* __restrict__ tw,
+                                                                const uint32_t* __restrict__ planeflag) {
   using S = Shape<NZ>;
   constexpr int T = S::R2, R1 = S::R1, kCW = CCfg<NZ>::CW, TH = CCfg<NZ>::THREADS;
   extern __shared__ float2 sh[];  // 2 tiles of NZ x kCW
@@ -418,9 +424,10 @@ __global__ void __launch_bounds__(CCfg<NZ>::THREADS, 3) z_kernel(float2* __restr
   const bool live = kx <= nx / 2;
   const size_t zstride = (size_t)ny * H;
   const size_t base = (size_t)ky * H + kx;
-  stage_tile<NZ, kCW, TH>(b0, S0 + (size_t)ky * H, zstride, kx0, H, 0xffffffffu);
+  const uint32_t pm = row_flags<NZ, kCW, TH>(planeflag);  // planes F-y skipped are zero
+  stage_tile<NZ, kCW, TH>(b0, S0 + (size_t)ky * H, zstride, kx0, H, pm);
   cp_async_commit();
-  stage_tile<NZ, kCW, TH>(b1, S1 + (size_t)ky * H, zstride, kx0, H, 0xffffffffu);
+  stage_tile<NZ, kCW, TH>(b1, S1 + (size_t)ky * H, zstride, kx0, H, pm);
   cp_async_commit();
   float2 v[R1];
   cp_async_wait<1>();
@@ -607,6 +614,7 @@ struct FftArgs {
   cudaStream_t st;
   float2* rowmm;
   const uint32_t* rowbits;
+  uint32_t* planeflag;
 };
 
 inline int hpitch(int nx) { return ((nx / 2 + 1) + 3) & ~3; }
@@ -646,7 +654,8 @@ struct RunFy {
   static void run(const FftArgs& a) {
     using C = CCfg<N>;
     dim3 grid((a.nx / 2 + 1 + C::CW - 1) / C::CW, a.nz);
-    fy_kernel<N><<<grid, C::THREADS, 3 * C::SMEM, a.st>>>(a.S0, a.S1, a.S2, a.nx / 2 + 1, a.H, a.twy, a.rowbits);
+    fy_kernel<N><<<grid, C::THREADS, 3 * C::SMEM, a.st>>>(a.S0, a.S1, a.S2, a.nx / 2 + 1, a.H, a.twy, a.rowbits,
+                                                          a.planeflag);
   }
 };
 template <int N>
@@ -654,7 +663,7 @@ struct RunZ {
   static void run(const FftArgs& a) {
     using C = CCfg<N>;
     dim3 grid((a.nx / 2 + 1 + C::CW - 1) / C::CW, a.ny);
-    z_kernel<N><<<grid, C::THREADS, 2 * C::SMEM, a.st>>>(a.S0, a.S1, a.nx, a.ny, a.H, a.twz);
+    z_kernel<N><<<grid, C::THREADS, 2 * C::SMEM, a.st>>>(a.S0, a.S1, a.nx, a.ny, a.H, a.twz, a.planeflag);
   }
 };
 template <int N>
@@ -706,8 +715,10 @@ void upload_twiddles(float2* dev, int nx, int ny, int nz, cudaStream_t st) {
 }
 
 void launch_integrate(const float4* acc, float2* spec, float* A, int nx, int ny, int nz, int mode,
-                      const float2* tw, cudaStream_t st, cudaEvent_t* ev, float2* rowmm, const uint32_t* rowbits) {
+                      const float2* tw, cudaStream_t st, cudaEvent_t* ev, float2* rowmm, const uint32_t* rowbits,
+                      uint32_t* planeflag) {
   FftArgs a;
+  a.planeflag = planeflag;
   a.rowmm = rowmm;
   a.rowbits = rowbits;
   const size_t cs = spectrum_elems(nx, ny, nz);

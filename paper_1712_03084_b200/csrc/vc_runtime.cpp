@@ -58,7 +58,7 @@ struct vc_ctx {
 
   // grid-dependent
   int nx = 0, ny = 0, nz = 0;
-  Buf acc, spec, A, tw, vbase, blk, rowmm, units, unitcnt, rowbits;
+  Buf acc, spec, A, tw, vbase, blk, rowmm, units, unitcnt, rowbits, planeflag;
   bool acc_dirty = true;  // accumulator contents unknown: next frame clears densely
   // view staging + clouds
   Buf views, pts_pos, pts_nrm, pts_w, pts_pix, wmaps, pre_scratch, iso_partial;
@@ -283,6 +283,7 @@ vc_status ensure_grid(vc_ctx* ctx, int nx, int ny, int nz) {
   const void* acc_before = ctx->acc.p;
   VC_TRY(ensure(ctx, ctx->acc, N * sizeof(float4)));
   VC_TRY(ensure(ctx, ctx->rowbits, (size_t)ny * nz * sizeof(uint32_t)));
+  VC_TRY(ensure(ctx, ctx->planeflag, (size_t)nz * sizeof(uint32_t) + 256));
   if (ctx->acc.p != acc_before || ctx->nx != nx || ctx->ny != ny || ctx->nz != nz) ctx->acc_dirty = true;
   VC_TRY(ensure(ctx, ctx->spec, 3 * spectrum_elems(nx, ny, nz) * sizeof(float2)));
   VC_TRY(ensure(ctx, ctx->A, N * sizeof(float)));
@@ -349,7 +350,7 @@ int enqueue_frame(vc_ctx* ctx, const FrameCfg& f) {
   record(ctx, 2);
   launch_integrate(P<float4>(ctx->acc), P<float2>(ctx->spec), P<float>(ctx->A), f.nx, f.ny, f.nz, f.mode,
                    P<float2>(ctx->tw), st, ctx->profiling ? &ctx->ev[14] : nullptr, P<float2>(ctx->rowmm),
-                   P<uint32_t>(ctx->rowbits));
+                   P<uint32_t>(ctx->rowbits), P<uint32_t>(ctx->planeflag));
   n += 5;
   record(ctx, 3);
   launch_iso_level(points(ctx), P<float>(ctx->A), ctx->ctl, P<double>(ctx->iso_partial), 1024, st);
@@ -483,7 +484,7 @@ vc_status vc_ctx_destroy(vc_ctx* ctx) {
   cudaSetDevice(ctx->device);
   if (ctx->st) cudaStreamSynchronize(ctx->st);
   if (ctx->gexec) cudaGraphExecDestroy(ctx->gexec);
-  for (Buf* b : {&ctx->acc, &ctx->spec, &ctx->A, &ctx->tw, &ctx->vbase, &ctx->blk, &ctx->rowmm, &ctx->units, &ctx->unitcnt, &ctx->rowbits, &ctx->views, &ctx->pts_pos,
+  for (Buf* b : {&ctx->acc, &ctx->spec, &ctx->A, &ctx->tw, &ctx->vbase, &ctx->blk, &ctx->rowmm, &ctx->units, &ctx->unitcnt, &ctx->rowbits, &ctx->planeflag, &ctx->views, &ctx->pts_pos,
                  &ctx->pts_nrm, &ctx->pts_w, &ctx->pts_pix, &ctx->wmaps, &ctx->pre_scratch, &ctx->iso_partial,
                  &ctx->m_pos, &ctx->m_nrm, &ctx->m_tri, &ctx->m_eid, &ctx->m_cells, &ctx->m_celltri, &ctx->m_posf,
                  &ctx->t_vis, &ctx->t_uv, &ctx->t_w, &ctx->t_untex, &ctx->t_rgb})
@@ -800,7 +801,7 @@ vc_status vc_stage_integrate(vc_ctx* ctx, const float* field, int32_t nx, int32_
   VC_CUDA(cudaMemcpyAsync(ctx->acc.p, h.data(), N * sizeof(float4), cudaMemcpyHostToDevice, ctx->st));
   ctx->acc_dirty = true;  // dense contents from the host
   launch_integrate(P<float4>(ctx->acc), P<float2>(ctx->spec), P<float>(ctx->A), nx, ny, nz, 1, P<float2>(ctx->tw),
-                   ctx->st, nullptr, nullptr, nullptr);
+                   ctx->st, nullptr, nullptr, nullptr, P<uint32_t>(ctx->planeflag));
   VC_CUDA(cudaGetLastError());
   VC_CUDA(cudaMemcpyAsync(A, ctx->A.p, N * 4, cudaMemcpyDeviceToHost, ctx->st));
   VC_CUDA(cudaStreamSynchronize(ctx->st));

@@ -107,7 +107,8 @@ size_t spectrum_elems(int nx, int ny, int nz);  // complex elements per componen
 void launch_integrate(const float4* acc, float2* spec, float* A, int nx, int ny, int nz, int mode,
                       const float2* twiddles, cudaStream_t st, cudaEvent_t* ev /*nullable, 6 events*/,
                       float2* rowmm /*nullable: per-row min/max of A*/,
-                      const uint32_t* rowbits /*nullable: touched 32-voxel chunks per row; null = dense*/);
+                      const uint32_t* rowbits /*nullable: touched 32-voxel chunks per row; null = dense*/,
+                      uint32_t* planeflag /*nz words: F-y marks planes with any splat contribution*/);
 void upload_twiddles(float2* dev, int nx, int ny, int nz, cudaStream_t st);
 void prepare_integrate(int nx, int ny, int nz);
 size_t twiddle_elems(int nx, int ny, int nz);
