@@ -308,3 +308,63 @@ def test_repeatability_and_graph_replay(scene, ctx):
     b = vc.reconstruct_frame(frames, rig, cfg, ctx=ctx, want_volume=True)
     assert rel_l2(a.volume.values, b.volume.values) < 1e-6
     assert ctx.kernels_per_frame() >= 19
+
+
+# ------------------------------------------------------------------ larger configurations (BASELINE C3 / C5)
+def hd_rig(vc, k=6):
+    """C3: K=6 Kinect2 depth 512x424 (f=365) + 1920x1080 colour (f~1060,
+    cx=959.5, cy=539.5) offset by 52 mm along x."""
+    rig = vc.make_circle_rig(k, 0, 2500, 512, 424, 365)
+    for s in rig.sensors:
+        s.rgb_intr = vc.Intrinsics(1060.0, 1060.0, 959.5, 539.5, 1920, 1080)
+        s.rgb_relative = vc.Pose(np.eye(3), np.array([52.0, 0.0, 0.0]))
+    return rig
+
+
+def to_oracle_rig(O, rig):
+    arr = (O.Sensor * len(rig.sensors))()
+    for i, s in enumerate(rig.sensors):
+        arr[i] = O.Sensor.from_buffer_copy(bytes(s.to_c()))
+    return arr
+
+
+@pytest.mark.slow
+def test_c3_six_views_hd_colour_512(O, ctx):
+    rig = hd_rig(vc)
+    orig = to_oracle_rig(O, rig)
+    body = vc.kick_body(300, 90)
+    frames = [vc.render_frame(rig, body, k, ctx=ctx) for k in range(6)]
+    obody = O.kick_body(300, 90)
+    o0 = O.render_frame(orig[0], obody, 0, 0)
+    assert np.array_equal(o0.rgb, frames[0].color) and np.array_equal(o0.depth, frames[0].depth)
+    dims = (512, 512, 512)
+    rec = vc.reconstruct_frame(frames, rig, vc.ReconConfig(dims=dims), ctx=ctx, want_volume=True)
+    ref = oracle_frame(O, orig, frames, dims=dims)
+    assert rel_l2(rec.volume.values, ref.volume) < REL_L2_A
+    d1, _ = cKDTree(ref.mesh.vertices).query(rec.mesh.vertices)
+    d2, _ = cKDTree(rec.mesh.vertices).query(ref.mesh.vertices)
+    assert max(d1.max(), d2.max()) <= HAUSDORFF_VOX * ref.grid.edge
+    assert O.analyze_topology(rec.mesh.triangles, len(rec.mesh.vertices))["edge_manifold"]
+    tm = vc.texture(ref.mesh.vertices, rig, frames, ref.weight_maps, ctx=ctx)
+    assert np.array_equal(tm.visible, ref.vis) and np.array_equal(tm.weight, ref.weight)
+    assert np.max(np.abs(tm.rgb.astype(int) - ref.rgb8.astype(int))) <= COLOR_TOL
+
+
+@pytest.mark.slow
+def test_c5_1024_single_gpu(ctx):
+    """C5 on one B200 (~40 GB working set): watertight textured mesh."""
+    rig = vc.make_circle_rig(4, 0, 2500, 512, 424, 365)
+    frames = [vc.render_frame(rig, vc.xpose_body(), k, ctx=ctx) for k in range(4)]
+    t = vc.StageTimings()
+    rec = vc.reconstruct_frame(frames, rig, vc.ReconConfig(dims=(1024, 1024, 1024)), ctx=ctx, timings=t)
+    assert len(rec.mesh.vertices) > 500_000
+    assert vc_topology_ok(rec.mesh)
+    assert rec.textured.visible.any(0).mean() > 0.8
+
+
+def vc_topology_ok(mesh):
+    t = np.asarray(mesh.triangles, np.int64)
+    e = np.concatenate([t[:, [0, 1]], t[:, [1, 2]], t[:, [2, 0]]])
+    e.sort(axis=1)
+    _, counts = np.unique(e[:, 0] * (1 << 32) + e[:, 1], return_counts=True)
+    return bool(np.all(counts == 2))
