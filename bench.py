@@ -345,8 +345,12 @@ def run_gpu(args):
     hbm = float(pk.get("hbm_gbs", 6650.0))
     fft_names = ["fft_x", "fft_y", "fft_z", "ifft_y", "ifft_x"]
     dom = max(fft_names + ["clear"], key=lambda n: kernel_ms[n])
+    try:  # dram bytes per launch of the same kernel from the committed ncu --set full capture
+        traffic = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))[dom]["dram_bytes_per_launch"]
+    except Exception:
+        traffic = None
     roofline = {"bound": "hbm", "kernel": dom, "achieved": bw[dom], "peak": hbm, "unit": "GB/s",
-                "frac": bw[dom] / hbm, "traffic": None,
+                "frac": bw[dom] / hbm, "traffic": traffic,
                 "algorithmic_bytes": ab[dom], "avg_launch_ms": kernel_ms[dom],
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)" if "_fallback" not in pk else "fallback"}
 
