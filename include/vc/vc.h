@@ -187,6 +187,48 @@ vc_status vc_export_volume(vc_ctx* ctx, float* dst, int32_t dst_kind);
 vc_status vc_export_points(vc_ctx* ctx, double* pos, double* nrm, double* weight, int32_t* pix,
                            float* weight_maps);
 
+/* ------------------------------------------------ z-slab decomposition (C5)
+ * One frame on P GPUs (SURVEY.md §8(e) "large grids"): rank r owns voxel
+ * planes [r*nz/P, (r+1)*nz/P).  Every rank preprocesses all views and splats
+ * only its slab (the reference's own slab split, splat.cpp:61-77); the 3-D FFT
+ * of integrate.cpp:19-74 runs as local x/y passes, one all-to-all to ky-slabs,
+ * the fused z pass, one all-to-all back, local inverse y/x passes; the iso
+ * level (splat.cpp:91-101) sums per-point samples across ranks; marching
+ * cubes (marching_cubes.cpp:131-210) runs per slab with a 1-plane (below) /
+ * 2-plane (above) halo of A and global vertex ids, so the concatenation of
+ * the ranks' pieces in rank order IS the single-GPU mesh.
+ *
+ * Exchanges go through NCCL (libnccl.so.2, loaded at run time; one process
+ * per GPU) or, for testing on one device, a loopback exchanger that runs P
+ * virtual ranks (P contexts) in one process with device copies. */
+typedef struct vc_dist vc_dist;
+
+typedef struct vc_dist_info {
+  int32_t rank, world;
+  int32_t z_begin, z_end;          /* owned voxel planes */
+  int32_t vertex_offset;           /* global id of this piece's first vertex */
+  int32_t vertex_total, triangle_offset, triangle_total;
+} vc_dist_info;
+
+/* 128-byte NCCL unique id (rank 0 makes it; the caller broadcasts it). */
+vc_status vc_dist_nccl_unique_id(uint8_t id[128]);
+/* One rank of a P-process job over NCCL on ctx's device. */
+vc_status vc_dist_create_nccl(vc_ctx* ctx, int32_t world, int32_t rank, const uint8_t id[128], vc_dist** out);
+/* P virtual ranks in this process (ctxs[0..world), usually one device). */
+vc_status vc_dist_create_loopback(vc_ctx* const* ctxs, int32_t world, vc_dist** out);
+vc_status vc_dist_destroy(vc_dist* d);
+/* Local ranks of d (1 for NCCL, world for loopback). */
+int32_t vc_dist_local_ranks(const vc_dist* d);
+/* vc_reconstruct_frame on the slab decomposition.  out/info: one entry per
+ * local rank; out[i] is that rank's piece (its vertices, global indices in its
+ * triangles; outputs owned by that rank's context).  nz divisible by world,
+ * nz/world >= 2. */
+vc_status vc_reconstruct_frame_dist(vc_dist* d, const vc_sensor* sensors, const vc_view* views, int32_t k,
+                                    const vc_recon_config* config, vc_textured_mesh* out, vc_dist_info* info,
+                                    vc_stage_timings* timings);
+/* The owned planes of A of local rank i: (z_end-z_begin)*ny*nx floats. */
+vc_status vc_dist_export_volume(vc_dist* d, int32_t local_rank, float* dst, int32_t dst_kind);
+
 /* ------------------------------------------------ per-stage entry points
  * Host arrays in, host arrays out; each runs the same kernels as the frame
  * path on the context's stream.  For parity tests against the reference's

@@ -77,6 +77,11 @@ class TexturedMesh(C.Structure):
                 ("iso_level", C.c_double), ("grid", GridSpec), ("mem_kind", C.c_int32)]
 
 
+class DistInfo(C.Structure):
+    _fields_ = [(n, C.c_int32) for n in ("rank", "world", "z_begin", "z_end", "vertex_offset", "vertex_total",
+                                         "triangle_offset", "triangle_total")]
+
+
 class Body(C.Structure):
     _fields_ = [("joints", C.c_double * 45), ("radii", C.c_double * 14), ("colors", C.c_uint8 * 42)]
 

@@ -319,8 +319,18 @@ __device__ __forceinline__ uint32_t row_flags(const uint32_t* rowbits) {
   for (int k = 0; k < NR; ++k) m |= (__ldg(rowbits + j0 + k * RSTEP) != 0u ? 1u : 0u) << k;
   return m;
 }
+// Row j of a tile lives at src + (j >> lp) * blkstride + (j & ((1 << lp) - 1)) * stride:
+// one uniform stride (lp = 31) for the single-GPU layouts, blocks of 2^lp rows
+// for the slab exchange layouts of the distributed transform.
+struct RowMap {
+  size_t stride, blkstride;
+  int lp;
+  __device__ __forceinline__ size_t off(int j) const {
+    return (size_t)(j >> lp) * blkstride + (size_t)(j & ((1 << lp) - 1)) * stride;
+  }
+};
 template <int N, int CW, int THREADS>
-__device__ __forceinline__ void stage_tile(float2* tile, const float2* src, size_t stride, int kx0, int H,
+__device__ __forceinline__ void stage_tile(float2* tile, const float2* src, RowMap rm, int kx0, int H,
                                            uint32_t rowmask) {
   constexpr int CPR = CW / 2, RSTEP = THREADS / CPR, NR = N / RSTEP;
   const int j0 = threadIdx.x / CPR, c2 = threadIdx.x % CPR;
@@ -329,8 +339,13 @@ __device__ __forceinline__ void stage_tile(float2* tile, const float2* src, size
   for (int k = 0; k < NR; ++k) {
     const int j = j0 + k * RSTEP;
     const bool ok = kx < H && ((rowmask >> k) & 1u);
-    cp_async16(tile + j * CW + 2 * c2, ok ? (const void*)(src + (size_t)j * stride + kx) : (const void*)src, ok);
+    cp_async16(tile + j * CW + 2 * c2, ok ? (const void*)(src + rm.off(j) + kx) : (const void*)src, ok);
   }
+}
+template <int N, int CW, int THREADS>
+__device__ __forceinline__ void stage_tile(float2* tile, const float2* src, size_t stride, int kx0, int H,
+                                           uint32_t rowmask) {
+  stage_tile<N, CW, THREADS>(tile, src, RowMap{stride, 0, 31}, kx0, H, rowmask);
 }
 
 template <int N, int CW>
@@ -343,9 +358,14 @@ __device__ __forceinline__ void tile_to_regs(const float2* tile, int c, int t, f
 }
 
 // ------------------------------------------------------------------ F-y
+// Outputs D, Z go to O0, O1 (in place over S0, S1 on one GPU).  Row ky of
+// plane zl is stored at ((s*nzl + zl)*kyl + yl)*H with s = ky / kyl, yl = ky % kyl:
+// for the slab transform that is the send layout of the forward all-to-all
+// (block s = the ky-slab of rank s); with kyl = ny it is the plain layout.
 template <int NY>
-__global__ void __launch_bounds__(CCfg<NY>::THREADS, 2) fy_kernel(float2* __restrict__ S0, float2* __restrict__ S1,
-                                                                 const float2* __restrict__ S2, int nxh, int H,
+__global__ void __launch_bounds__(CCfg<NY>::THREADS, 2) fy_kernel(const float2* S0, const float2* S1,
+                                                                 const float2* __restrict__ S2, float2* O0, float2* O1,
+                                                                 int nxh, int H, int lk,
                                                                  const float2* __restrict__ tw,
                                                                  const uint32_t* __restrict__ rowbits,
                                                                  uint32_t* __restrict__ planeflag) {
@@ -396,11 +416,13 @@ __global__ void __launch_bounds__(CCfg<NY>::THREADS, 2) fy_kernel(float2* __rest
   ExCols<NY, kCW> e2{b2, c};
   fft_line<NY, false>(v, t, tw, e2);
   if (live) {
+    const int kyl = 1 << lk, nzl = gridDim.y;
 #pragma unroll
     for (int k1 = 0; k1 < R1; ++k1) {
-      const size_t o = plane + (size_t)(t + T * k1) * H + kx;
-      __stcs(S0 + o, d[k1]);
-      __stcs(S1 + o, v[k1]);
+      const int ky = t + T * k1;
+      const size_t o = ((size_t)((ky >> lk) * nzl + blockIdx.y) * kyl + (ky & (kyl - 1))) * H + kx;
+      __stcs(O0 + o, d[k1]);
+      __stcs(O1 + o, v[k1]);
     }
   }
 }
@@ -408,10 +430,13 @@ __global__ void __launch_bounds__(CCfg<NY>::THREADS, 2) fy_kernel(float2* __rest
 // ------------------------------------------------------------------ Z (fused)
 // FFT_z(D) is parked in its staged tile while FFT_z(Z) runs (one register
 // array live, three CTAs per SM).
+// Input: D, Z as [z][kyl][H] (kyl = ny on one GPU; a ky-slab starting at ky0
+// after the forward all-to-all).  The result overwrites S0 in place.
 template <int NZ>
 __global__ void __launch_bounds__(CCfg<NZ>::THREADS, 3) z_kernel(float2* __restrict__ S0,
                                                                 const float2* __restrict__ S1, int nx, int ny,
-                                                                int H, const float2* __restrict__ tw,
+                                                                int kyl, int ky0, int H,
+                                                                const float2* __restrict__ tw,
                                                                 const uint32_t* __restrict__ planeflag) {
   using S = Shape<NZ>;
   constexpr int T = S::R2, R1 = S::R1, kCW = CCfg<NZ>::CW, TH = CCfg<NZ>::THREADS;
@@ -420,14 +445,14 @@ __global__ void __launch_bounds__(CCfg<NZ>::THREADS, 3) z_kernel(float2* __restr
   float2* b1 = sh + NZ * kCW;
   const int c = threadIdx.x % kCW, t = threadIdx.x / kCW;
   const int kx0 = blockIdx.x * kCW, kx = kx0 + c;
-  const int ky = blockIdx.y;
+  const int kyr = blockIdx.y, ky = ky0 + kyr;
   const bool live = kx <= nx / 2;
-  const size_t zstride = (size_t)ny * H;
-  const size_t base = (size_t)ky * H + kx;
+  const size_t zstride = (size_t)kyl * H;
+  const size_t base = (size_t)kyr * H + kx;
   const uint32_t pm = row_flags<NZ, kCW, TH>(planeflag);  // planes F-y skipped are zero
-  stage_tile<NZ, kCW, TH>(b0, S0 + (size_t)ky * H, zstride, kx0, H, pm);
+  stage_tile<NZ, kCW, TH>(b0, S0 + (size_t)kyr * H, zstride, kx0, H, pm);
   cp_async_commit();
-  stage_tile<NZ, kCW, TH>(b1, S1 + (size_t)ky * H, zstride, kx0, H, pm);
+  stage_tile<NZ, kCW, TH>(b1, S1 + (size_t)kyr * H, zstride, kx0, H, pm);
   cp_async_commit();
   float2 v[R1];
   cp_async_wait<1>();
@@ -467,9 +492,12 @@ __global__ void __launch_bounds__(CCfg<NZ>::THREADS, 3) z_kernel(float2* __restr
 }
 
 // ------------------------------------------------------------------ I-y
+// Input rows in the layout fy_kernel writes (the receive layout of the
+// backward all-to-all on several GPUs); output in the plain [zl][ky][H]
+// layout (in place on one GPU: Rin == Rout, lk = log2 ny).
 template <int NY>
-__global__ void __launch_bounds__(CCfg<NY>::THREADS, 3) iy_kernel(float2* __restrict__ S0, int nxh, int H,
-                                                                 const float2* __restrict__ tw) {
+__global__ void __launch_bounds__(CCfg<NY>::THREADS, 3) iy_kernel(const float2* Rin, float2* Rout, int nxh, int H,
+                                                                 int lk, const float2* __restrict__ tw) {
   using S = Shape<NY>;
   constexpr int T = S::R2, R1 = S::R1, kCW = CCfg<NY>::CW, TH = CCfg<NY>::THREADS;
   extern __shared__ float2 sh[];
@@ -477,7 +505,9 @@ __global__ void __launch_bounds__(CCfg<NY>::THREADS, 3) iy_kernel(float2* __rest
   const int kx0 = blockIdx.x * kCW, kx = kx0 + c;
   const bool live = kx < nxh;
   const size_t plane = (size_t)blockIdx.y * NY * H;
-  stage_tile<NY, kCW, TH>(sh, S0 + plane, H, kx0, H, 0xffffffffu);
+  const size_t kyl = (size_t)1 << lk;
+  const RowMap rm{(size_t)H, gridDim.y * kyl * H, lk};
+  stage_tile<NY, kCW, TH>(sh, Rin + blockIdx.y * kyl * H, rm, kx0, H, 0xffffffffu);
   cp_async_commit();
   float2 v[R1];
   cp_async_wait<0>();
@@ -488,9 +518,8 @@ __global__ void __launch_bounds__(CCfg<NY>::THREADS, 3) iy_kernel(float2* __rest
   fft_line<NY, true>(v, t, tw, ex);
   if (live) {
 #pragma unroll
-    for (int k1 = 0; k1 < R1; ++k1) __stcs(S0 + plane + (size_t)(t + T * k1) * H + kx, v[k1]);
+    for (int k1 = 0; k1 < R1; ++k1) __stcs(Rout + plane + (size_t)(t + T * k1) * H + kx, v[k1]);
   }
-  (void)T;
 }
 
 // ------------------------------------------------------------------ I-x
@@ -605,19 +634,8 @@ void dispatch_n(int n, Args&&... args) {
   }
 }
 
-struct FftArgs {
-  const float4* acc;
-  float2 *S0, *S1, *S2;
-  float* A;
-  int nx, ny, nz, H, mode;
-  const float2 *twx, *twy, *twz;
-  cudaStream_t st;
-  float2* rowmm;
-  const uint32_t* rowbits;
-  uint32_t* planeflag;
-};
-
 inline int hpitch(int nx) { return ((nx / 2 + 1) + 3) & ~3; }
+
 
 // Opt-in dynamic shared memory above 48 KB.  Called from prepare_integrate
 // (whenever the grid dims change), never inside a graph capture.
@@ -642,47 +660,48 @@ struct Prep {
 
 template <int N>
 struct RunFx {
-  static void run(const FftArgs& a) {
+  static void run(const SlabFft& a) {
     using C = XCfg<N>;
-    const int rows = a.ny * a.nz;
+    const int rows = a.ny * a.nzl;
     const int grid = (rows / 2 + C::TEAMS - 1) / C::TEAMS;
     fx_kernel<N><<<grid, C::THREADS, C::SMEM, a.st>>>(a.acc, a.S0, a.S1, a.S2, rows, a.H, a.rowbits, a.mode, a.twx);
   }
 };
 template <int N>
 struct RunFy {
-  static void run(const FftArgs& a) {
+  static void run(const SlabFft& a) {
     using C = CCfg<N>;
-    dim3 grid((a.nx / 2 + 1 + C::CW - 1) / C::CW, a.nz);
-    fy_kernel<N><<<grid, C::THREADS, 3 * C::SMEM, a.st>>>(a.S0, a.S1, a.S2, a.nx / 2 + 1, a.H, a.twy, a.rowbits,
-                                                          a.planeflag);
+    dim3 grid((a.nx / 2 + 1 + C::CW - 1) / C::CW, a.nzl);
+    fy_kernel<N><<<grid, C::THREADS, 3 * C::SMEM, a.st>>>(a.S0, a.S1, a.S2, a.O0, a.O1, a.nx / 2 + 1, a.H,
+                                                          ilog2(a.kyl), a.twy, a.rowbits, a.planeflag + a.zoff);
   }
 };
 template <int N>
 struct RunZ {
-  static void run(const FftArgs& a) {
+  static void run(const SlabFft& a) {
     using C = CCfg<N>;
-    dim3 grid((a.nx / 2 + 1 + C::CW - 1) / C::CW, a.ny);
-    z_kernel<N><<<grid, C::THREADS, 2 * C::SMEM, a.st>>>(a.S0, a.S1, a.nx, a.ny, a.H, a.twz, a.planeflag);
+    dim3 grid((a.nx / 2 + 1 + C::CW - 1) / C::CW, a.kyl);
+    z_kernel<N><<<grid, C::THREADS, 2 * C::SMEM, a.st>>>(a.R0, a.R1, a.nx, a.ny, a.kyl, a.ky0, a.H, a.twz,
+                                                         a.planeflag);
   }
 };
 template <int N>
 struct RunIy {
-  static void run(const FftArgs& a) {
+  static void run(const SlabFft& a) {
     using C = CCfg<N>;
-    dim3 grid((a.nx / 2 + 1 + C::CW - 1) / C::CW, a.nz);
-    iy_kernel<N><<<grid, C::THREADS, C::SMEM, a.st>>>(a.S0, a.nx / 2 + 1, a.H, a.twy);
+    dim3 grid((a.nx / 2 + 1 + C::CW - 1) / C::CW, a.nzl);
+    iy_kernel<N><<<grid, C::THREADS, C::SMEM, a.st>>>(a.Rin, a.Rout, a.nx / 2 + 1, a.H, ilog2(a.kyl), a.twy);
   }
 };
 template <int N>
 struct RunIx {
-  static void run(const FftArgs& a) {
+  static void run(const SlabFft& a) {
     using C = IXCfg<N>;
-    const int rows = a.ny * a.nz;
+    const int rows = a.ny * a.nzl;
     const int need = (rows / 2 + C::TEAMS - 1) / C::TEAMS;
     const int grid = need < 148 * 4 ? need : 148 * 4;  // persistent teams
     const float scale = (float)(1.0 / ((double)a.nx * a.ny * a.nz));
-    ix_kernel<N><<<grid, C::THREADS, C::SMEM, a.st>>>(a.S0, a.A, rows, a.H, scale, a.twx, a.rowmm);
+    ix_kernel<N><<<grid, C::THREADS, C::SMEM, a.st>>>(a.Rout, a.A, rows, a.H, scale, a.twx, a.rowmm);
   }
 };
 
@@ -714,17 +733,26 @@ void upload_twiddles(float2* dev, int nx, int ny, int nz, cudaStream_t st) {
   cudaStreamSynchronize(st);
 }
 
+void launch_fft_forward_xy(const SlabFft& a) {
+  dispatch_n<RunFx>(a.nx, a);
+  dispatch_n<RunFy>(a.ny, a);
+}
+void launch_fft_z(const SlabFft& a) { dispatch_n<RunZ>(a.nz, a); }
+void launch_fft_inverse_yx(const SlabFft& a) {
+  dispatch_n<RunIy>(a.ny, a);
+  dispatch_n<RunIx>(a.nx, a);
+}
+
 void launch_integrate(const float4* acc, float2* spec, float* A, int nx, int ny, int nz, int mode,
                       const float2* tw, cudaStream_t st, cudaEvent_t* ev, float2* rowmm, const uint32_t* rowbits,
                       uint32_t* planeflag) {
-  FftArgs a;
-  a.planeflag = planeflag;
-  a.rowmm = rowmm;
-  a.rowbits = rowbits;
+  SlabFft a;
   const size_t cs = spectrum_elems(nx, ny, nz);
   a.acc = acc, a.S0 = spec, a.S1 = spec + cs, a.S2 = spec + 2 * cs, a.A = A;
-  a.nx = nx, a.ny = ny, a.nz = nz, a.H = hpitch(nx), a.mode = mode;
+  a.O0 = a.S0, a.O1 = a.S1, a.R0 = a.S0, a.R1 = a.S1, a.Rin = a.S0, a.Rout = a.S0;
+  a.nx = nx, a.ny = ny, a.nz = nz, a.nzl = nz, a.zoff = 0, a.kyl = ny, a.ky0 = 0, a.H = hpitch(nx), a.mode = mode;
   a.twx = tw, a.twy = tw + nx, a.twz = tw + nx + ny, a.st = st;
+  a.rowmm = rowmm, a.rowbits = rowbits, a.planeflag = planeflag;
   if (ev) record_event(ev[0], st);
   dispatch_n<RunFx>(nx, a);
   if (ev) record_event(ev[1], st);

@@ -83,6 +83,41 @@ __global__ void __launch_bounds__(256) iso_partial_kernel(const double* __restri
   if (threadIdx.x == 0) partial[blockIdx.x] = sh[0];
 }
 
+// trilinear()'s lower z plane of the point, owned by exactly one slab
+__global__ void __launch_bounds__(256) iso_sample_kernel(const double* __restrict__ pos, const float* __restrict__ A,
+                                                         const DevCtl* __restrict__ ctl, int zoff, int nzl,
+                                                         double* samples) {
+  if (ctl->status != 0) return;
+  const DevGrid g = ctl->grid;
+  const int P = ctl->P;
+  for (int p = blockIdx.x * 256 + threadIdx.x; p < P; p += gridDim.x * 256) {
+    const double vx = ddiv(dsub(pos[3 * p + 0], g.origin[0]), g.edge);
+    const double vy = ddiv(dsub(pos[3 * p + 1], g.origin[1]), g.edge);
+    const double vz = ddiv(dsub(pos[3 * p + 2], g.origin[2]), g.edge);
+    const double fz = vz < 0.0 ? 0.0 : (vz > g.nz - 1.0 ? g.nz - 1.0 : vz);
+    const int z0 = min((int)fz, g.nz - 2 >= 0 ? g.nz - 2 : 0);
+    samples[p] = (z0 >= zoff && z0 < zoff + nzl) ? trilinear(A, g, vx, vy, vz) : 0.0;
+  }
+}
+
+// iso_partial_kernel's reduction order over precomputed samples
+__global__ void __launch_bounds__(256) iso_partial_samples_kernel(const double* __restrict__ samples,
+                                                                  const DevCtl* __restrict__ ctl, double* partial) {
+  __shared__ double sh[256];
+  double sum = 0.0;
+  if (ctl->status == 0) {
+    const int P = ctl->P;
+    for (int p = blockIdx.x * 256 + threadIdx.x; p < P; p += gridDim.x * 256) sum = dadd(sum, samples[p]);
+  }
+  sh[threadIdx.x] = sum;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if (threadIdx.x < o) sh[threadIdx.x] = dadd(sh[threadIdx.x], sh[threadIdx.x + o]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) partial[blockIdx.x] = sh[0];
+}
+
 __global__ void iso_final_kernel(const double* partial, int n, DevCtl* ctl) {
   __shared__ double sh[512];
   sh[threadIdx.x] = threadIdx.x < n ? partial[threadIdx.x] : 0.0;
@@ -172,12 +207,12 @@ __global__ void row_minmax_kernel(const float* __restrict__ A, int nx, int rows,
 constexpr int kRowThreads = 256;
 
 __global__ void __launch_bounds__(kRowThreads) mc_rows_kernel(const float2* __restrict__ rowmm, const DevCtl* ctl,
-                                                              int ny, int nz, uint32_t* rowmask) {
+                                                              int ny, int nz, McSlab sl, uint32_t* rowmask) {
   const int u = blockIdx.x * kRowThreads + threadIdx.x;
   bool active = false;
-  if (u < ny * nz && ctl->status == 0) {
+  if (u < ny * sl.nzu && ctl->status == 0) {
     const double L = ctl->level;
-    const int y = u % ny, z = u / ny;
+    const int y = u % ny, z = sl.z0 + u / ny;
     float2 m = rowmm[u];
     float lo = m.x, hi = m.y;
     if (y + 1 < ny) m = rowmm[u + 1], lo = fminf(lo, m.x), hi = fmaxf(hi, m.y);
@@ -223,7 +258,7 @@ __global__ void __launch_bounds__(1024) mc_units_kernel(const uint32_t* __restri
       units[pos++] = i * 32 + b;
     }
   }
-  if (threadIdx.x == 1023) ctl->units = wsum[31];
+  if (threadIdx.x == 1023) ctl->units = wsum[31], ctl->v_extra = 0;
 }
 
 __device__ __forceinline__ int3 block_reduce3(int3 v) {
@@ -240,23 +275,28 @@ __device__ __forceinline__ int3 block_reduce3(int3 v) {
 }
 
 // per active unit: (owned cut edges, triangles, non-trivial cells)
-__global__ void __launch_bounds__(256) mc_count_kernel(const float* __restrict__ A, const DevCtl* ctl, int nx, int ny,
-                                                       int nz, const int32_t* __restrict__ units, int3* unitcnt) {
+__global__ void __launch_bounds__(256) mc_count_kernel(const float* __restrict__ A, DevCtl* ctl, int nx, int ny,
+                                                       int nz, McSlab sl, const int32_t* __restrict__ units,
+                                                       int3* unitcnt) {
   if (ctl->status != 0) return;
   const int U = ctl->units;
   const float Lf = __double2float_ru(ctl->level);
   for (int i = blockIdx.x; i < U; i += gridDim.x) {
     const int u = units[i];
-    const int y = u % ny, z = u / ny;
-    const size_t row0 = (size_t)u * nx;
+    const int y = u % ny, z = sl.z0 + u / ny;
+    const bool own = z < sl.zend;
+    const size_t row0 = ((size_t)z * ny + y) * nx;
     int3 c = make_int3(0, 0, 0);
     for (int x = threadIdx.x; x < nx; x += blockDim.x) {
       const VoxelInfo vi = classify(A, nx, ny, nz, x, y, z, row0 + x, Lf);
-      const int nt = vi.cfg >= 0 ? c_mc_count[vi.cfg] : 0;
+      const int nt = vi.cfg >= 0 && own ? c_mc_count[vi.cfg] : 0;
       c.x += __popc(vi.mask), c.y += nt, c.z += nt > 0 ? 1 : 0;
     }
     const int3 t = block_reduce3(c);
-    if (threadIdx.x == 0) unitcnt[i] = t;
+    if (threadIdx.x == 0) {
+      unitcnt[i] = t;
+      if (!own) atomicAdd(&ctl->v_extra, t.x);
+    }
   }
 }
 
@@ -311,7 +351,7 @@ __global__ void __launch_bounds__(1024) mc_scan_kernel(int3* blk, const DevCtl* 
   }
   if (threadIdx.x == 1023) {
     const int3 t = wsum[31];
-    ctl->V = t.x, ctl->T = t.y, ctl->C = t.z;
+    ctl->V = t.x - ctl->v_extra, ctl->T = t.y, ctl->C = t.z;
     ctl->overflow = (t.x > v_cap || t.y > t_cap || t.z > c_cap) ? 1 : 0;
   }
 }
@@ -319,7 +359,7 @@ __global__ void __launch_bounds__(1024) mc_scan_kernel(int3* blk, const DevCtl* 
 // per active unit, in order: vertex ids = rank of the cut edge in global edge
 // id order; fp64 positions (marching_cubes.cpp:153-155, volume.hpp:45)
 __global__ void __launch_bounds__(256) mc_emit_kernel(const float* __restrict__ A, const DevCtl* ctl, int nx, int ny,
-                                                      int nz, const int32_t* __restrict__ units,
+                                                      int nz, McSlab sl, const int32_t* __restrict__ units,
                                                       const int3* __restrict__ unitoff, MeshBufs mb) {
   if (ctl->status != 0 || ctl->overflow) return;
   const int U = ctl->units;
@@ -329,8 +369,9 @@ __global__ void __launch_bounds__(256) mc_emit_kernel(const float* __restrict__ 
   const size_t step[3] = {1, (size_t)nx, (size_t)nx * ny};
   for (int i = blockIdx.x; i < U; i += gridDim.x) {
     const int u = units[i];
-    const size_t row0 = (size_t)u * nx;
-    const int y = u % ny, z = u / ny;
+    const int y = u % ny, z = sl.z0 + u / ny;
+    const bool own = z < sl.zend;  // else: only number the next rank's edges
+    const size_t row0 = ((size_t)z * ny + y) * nx;
     int3 carry = unitoff[i];
     for (int x0 = 0; x0 < nx; x0 += blockDim.x) {
       const int x = x0 + threadIdx.x;
@@ -341,8 +382,8 @@ __global__ void __launch_bounds__(256) mc_emit_kernel(const float* __restrict__ 
       const int3 ex = block_exclusive_scan3(make_int3(__popc(vi.mask), nt, nt > 0 ? 1 : 0), &tot);
       const int vb = carry.x + ex.x, tb = carry.y + ex.y, cb = carry.z + ex.z;
       const size_t v = row0 + x;
-      if (vi.mask) {
-        mb.vbase[v] = ((uint32_t)vb << 3) | (uint32_t)vi.mask;
+      if (vi.mask) mb.vbase[v] = ((uint32_t)vb << 3) | (uint32_t)vi.mask;
+      if (vi.mask && own) {
         const double v0 = (double)__ldg(A + v);
         int id = vb;
         for (int a = 0; a < 3; ++a) {
@@ -426,6 +467,7 @@ __global__ void __launch_bounds__(256) mc_tris_kernel(const float* __restrict__ 
                                                       int nz, MeshBufs mb) {
   if (ctl->status != 0 || ctl->overflow) return;
   const int C = ctl->C;
+  const int voff = ctl->voff;
   const float Lf = __double2float_ru(ctl->level);
   const size_t plane = (size_t)nx * ny;
   for (int i = blockIdx.x * 256 + threadIdx.x; i < C; i += gridDim.x * 256) {
@@ -440,7 +482,7 @@ __global__ void __launch_bounds__(256) mc_tris_kernel(const float* __restrict__ 
         const int c0 = c_edge_c0[e], axis = c_edge_axis[e];
         const size_t owner = v + (c0 & 1) + ((c0 >> 1) & 1) * (size_t)nx + ((c0 >> 2) & 1) * plane;
         const uint32_t pk = mb.vbase[owner];
-        ids[m] = (int)(pk >> 3) + __popc(pk & 7u & ((1u << axis) - 1u));
+        ids[m] = voff + (int)(pk >> 3) + __popc(pk & 7u & ((1u << axis) - 1u));
       }
       int32_t* o = mb.tri + 3 * (size_t)(tb + tri);
       o[0] = ids[0], o[1] = ids[1], o[2] = ids[2];
@@ -448,7 +490,28 @@ __global__ void __launch_bounds__(256) mc_tris_kernel(const float* __restrict__ 
   }
 }
 
+// slab ranks: this rank's first global vertex id = sum of the vertex counts
+// of the ranks below it (counts: (V, T, C) per rank, all-gathered)
+__global__ void mc_set_voff_kernel(const int3* counts, int rank, DevCtl* ctl) {
+  int s = 0;
+  for (int r = 0; r < rank; ++r) s += counts[r].x;
+  ctl->voff = s;
+}
+
+__global__ void add_f64_kernel(double* dst, const double* src, size_t n) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+    dst[i] = dadd(dst[i], src[i]);
+}
+
 }  // namespace
+
+void launch_add_f64(double* dst, const double* src, size_t n, cudaStream_t st) {
+  add_f64_kernel<<<148 * 4, 256, 0, st>>>(dst, src, n);
+}
+
+void launch_mc_set_voff(const int32_t* counts, int rank, DevCtl* ctl, cudaStream_t st) {
+  mc_set_voff_kernel<<<1, 1, 0, st>>>(reinterpret_cast<const int3*>(counts), rank, ctl);
+}
 
 void upload_case_table_data(const int8_t* counts, const int8_t* tris, cudaStream_t st) {
   cudaMemcpyToSymbolAsync(c_mc_count, counts, 256, 0, cudaMemcpyHostToDevice, st);
@@ -477,20 +540,44 @@ void launch_row_minmax(const float* A, int nx, int ny, int nz, float2* rowmm, cu
   row_minmax_kernel<<<(rows * 32 + 255) / 256, 256, 0, st>>>(A, nx, rows, rowmm);
 }
 
-void launch_marching_cubes(const float* A, DevCtl* ctl, MeshBufs mb, int nx, int ny, int nz, cudaStream_t st) {
-  const int units = ny * nz;
+namespace {
+int mc_threads(int nx) { return nx >= 256 ? 256 : (nx >= 128 ? 128 : (nx >= 64 ? 64 : 32)); }
+}  // namespace
+
+void launch_marching_cubes_count(const float* A, DevCtl* ctl, MeshBufs mb, int nx, int ny, int nz, McSlab sl,
+                                 cudaStream_t st) {
+  const int units = ny * sl.nzu;
   const int nblk = (units + kRowThreads - 1) / kRowThreads;
   uint32_t* rowmask = reinterpret_cast<uint32_t*>(mb.blk);  // ceil(units/32) words
-  int32_t* ulist = mb.units;                                  // units entries
   int3* ucnt = reinterpret_cast<int3*>(mb.unitcnt);
-  const int threads = nx >= 256 ? 256 : (nx >= 128 ? 128 : (nx >= 64 ? 64 : 32));
-  mc_rows_kernel<<<nblk, kRowThreads, 0, st>>>(mb.rowmm, ctl, ny, nz, rowmask);
-  mc_units_kernel<<<1, 1024, 0, st>>>(rowmask, (units + 31) / 32, ulist, ctl);
-  mc_count_kernel<<<148 * 8, threads, 0, st>>>(A, ctl, nx, ny, nz, ulist, ucnt);
+  mc_rows_kernel<<<nblk, kRowThreads, 0, st>>>(mb.rowmm, ctl, ny, nz, sl, rowmask);
+  mc_units_kernel<<<1, 1024, 0, st>>>(rowmask, (units + 31) / 32, mb.units, ctl);
+  mc_count_kernel<<<148 * 8, mc_threads(nx), 0, st>>>(A, ctl, nx, ny, nz, sl, mb.units, ucnt);
   mc_scan_kernel<<<1, 1024, 0, st>>>(ucnt, ctl, ctl, mb.v_cap, mb.t_cap, mb.c_cap);
-  mc_emit_kernel<<<148 * 8, threads, 0, st>>>(A, ctl, nx, ny, nz, ulist, ucnt, mb);
+}
+
+void launch_marching_cubes_emit(const float* A, DevCtl* ctl, MeshBufs mb, int nx, int ny, int nz, McSlab sl,
+                                cudaStream_t st) {
+  int3* ucnt = reinterpret_cast<int3*>(mb.unitcnt);
+  mc_emit_kernel<<<148 * 8, mc_threads(nx), 0, st>>>(A, ctl, nx, ny, nz, sl, mb.units, ucnt, mb);
   mc_normals_kernel<<<148 * 4, 256, 0, st>>>(A, ctl, nx, ny, nz, mb);
   mc_tris_kernel<<<148 * 4, 256, 0, st>>>(A, ctl, nx, ny, nz, mb);
+}
+
+void launch_marching_cubes(const float* A, DevCtl* ctl, MeshBufs mb, int nx, int ny, int nz, cudaStream_t st) {
+  const McSlab whole{0, nz, nz};
+  launch_marching_cubes_count(A, ctl, mb, nx, ny, nz, whole, st);
+  launch_marching_cubes_emit(A, ctl, mb, nx, ny, nz, whole, st);
+}
+
+void launch_iso_samples(const DevPoints& pts, const float* A, const DevCtl* ctl, int zoff, int nzl, double* samples,
+                        cudaStream_t st) {
+  iso_sample_kernel<<<148 * 4, 256, 0, st>>>(pts.pos, A, ctl, zoff, nzl, samples);
+}
+
+void launch_iso_final_samples(const double* samples, DevCtl* ctl, double* partial, cudaStream_t st) {
+  iso_partial_samples_kernel<<<kIsoBlocks, 256, 0, st>>>(samples, ctl, partial);
+  iso_final_kernel<<<1, 512, 0, st>>>(partial, kIsoBlocks, ctl);
 }
 
 }  // namespace vc

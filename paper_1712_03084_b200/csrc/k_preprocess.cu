@@ -291,6 +291,7 @@ __global__ void __launch_bounds__(1024) pre_scan_kernel(const int32_t* counts, i
     const int P = wsum[31];
     ctl->P = P;
     ctl->status = P == 0 ? 2 : (P > cap ? 3 : 0);
+    ctl->voff = 0;
   }
 }
 

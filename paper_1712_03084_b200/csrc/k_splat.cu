@@ -69,7 +69,8 @@ __global__ void __launch_bounds__(kSplatThreads) splat_weighted_kernel(const dou
                                                                        const double* __restrict__ wgt,
                                                                        const DevCtl* __restrict__ ctl,
                                                                        float4* __restrict__ acc,
-                                                                       uint32_t* __restrict__ rowbits) {
+                                                                       uint32_t* __restrict__ rowbits, int zoff,
+                                                                       int nzl) {
   const int P = ctl->P;
   if (ctl->status != 0) return;
   const DevGrid g = ctl->grid;
@@ -83,16 +84,18 @@ __global__ void __launch_bounds__(kSplatThreads) splat_weighted_kernel(const dou
     const double cz = ddiv(dsub(__ldg(pos + 3 * p + 2), g.origin[2]), g.edge);
     const int fx = (int)floor(cx);
     const int x = fx - 1 + ox, y = (int)floor(cy) - 1 + oy, z = (int)floor(cz) - 1 + oz;
-    if (ox == 0 && y >= 0 && z >= 0 && y < g.ny && z < g.nz && fx + 2 >= 0 && fx - 1 < g.nx)
-      mark_chunks(rowbits, z * g.ny + y, max(fx - 1, 0), min(fx + 2, g.nx - 1));
-    if (x < 0 || y < 0 || z < 0 || x >= g.nx || y >= g.ny || z >= g.nz) continue;
+    // z-slab [zoff, zoff+nzl) of this rank (the reference's own slab split, splat.cpp:61-77)
+    const int zl = z - zoff;
+    if (ox == 0 && y >= 0 && zl >= 0 && y < g.ny && zl < nzl && z < g.nz && fx + 2 >= 0 && fx - 1 < g.nx)
+      mark_chunks(rowbits, zl * g.ny + y, max(fx - 1, 0), min(fx + 2, g.nx - 1));
+    if (x < 0 || y < 0 || zl < 0 || x >= g.nx || y >= g.ny || zl >= nzl || z >= g.nz) continue;
     const float dx = (float)(cx - (double)x), dy = (float)(cy - (double)y), dz = (float)(cz - (double)z);
     const float s = dx * dx + dy * dy + dz * dz;
     const float w = (float)__ldg(wgt + p);
     const float g1w = exp2f(s * k1) * w, g2w = exp2f(s * k2) * w;
     const float4 v = make_float4(g1w * (float)__ldg(nrm + 3 * p + 0), g1w * (float)__ldg(nrm + 3 * p + 1),
                                  g1w * (float)__ldg(nrm + 3 * p + 2), g2w);
-    red_add_v4(acc + ((size_t)z * g.ny + y) * g.nx + x, v);
+    red_add_v4(acc + ((size_t)zl * g.ny + y) * g.nx + x, v);
   }
 }
 
@@ -100,7 +103,7 @@ __global__ void __launch_bounds__(kSplatThreads) splat_weighted_kernel(const dou
 __global__ void __launch_bounds__(256) splat_simple_kernel(const double* __restrict__ pos,
                                                            const double* __restrict__ nrm,
                                                            const DevCtl* __restrict__ ctl, float4* __restrict__ acc,
-                                                           uint32_t* __restrict__ rowbits) {
+                                                           uint32_t* __restrict__ rowbits, int zoff, int nzl) {
   const int P = ctl->P;
   if (ctl->status != 0) return;
   const DevGrid g = ctl->grid;
@@ -110,8 +113,10 @@ __global__ void __launch_bounds__(256) splat_simple_kernel(const double* __restr
     const double cz = ddiv(dsub(pos[3 * p + 2], g.origin[2]), g.edge);
     const long long x = lround_d(cx), y = lround_d(cy), z = lround_d(cz);
     if (!(x >= 0 && x < g.nx && y >= 0 && y < g.ny && z >= 0 && z < g.nz)) continue;
-    mark_chunks(rowbits, (int)(z * g.ny + y), (int)x, (int)x);
-    red_add_v4(acc + ((size_t)z * g.ny + y) * g.nx + x,
+    const long long zl = z - zoff;
+    if (zl < 0 || zl >= nzl) continue;
+    mark_chunks(rowbits, (int)(zl * g.ny + y), (int)x, (int)x);
+    red_add_v4(acc + ((size_t)zl * g.ny + y) * g.nx + x,
                make_float4((float)nrm[3 * p + 0], (float)nrm[3 * p + 1], (float)nrm[3 * p + 2], 1.f));
   }
 }
@@ -148,11 +153,12 @@ void launch_sparse_clear(float4* acc, uint32_t* rowbits, int rows, int nx, cudaS
 }
 
 void launch_splat(const DevPoints& pts, const DevCtl* ctl, float4* acc, uint32_t* rowbits, int mode,
-                  cudaStream_t st) {
+                  cudaStream_t st, int zoff, int nzl) {
   if (mode == 0)
-    splat_weighted_kernel<<<148 * 8, kSplatThreads, 0, st>>>(pts.pos, pts.nrm, pts.weight, ctl, acc, rowbits);
+    splat_weighted_kernel<<<148 * 8, kSplatThreads, 0, st>>>(pts.pos, pts.nrm, pts.weight, ctl, acc, rowbits, zoff,
+                                                             nzl);
   else
-    splat_simple_kernel<<<148 * 4, 256, 0, st>>>(pts.pos, pts.nrm, ctl, acc, rowbits);
+    splat_simple_kernel<<<148 * 4, 256, 0, st>>>(pts.pos, pts.nrm, ctl, acc, rowbits, zoff, nzl);
 }
 
 void launch_splat_finalize(const float4* acc, size_t n, int mode, int negate, double sigma2, float* field,

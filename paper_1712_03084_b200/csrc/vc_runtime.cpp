@@ -21,7 +21,7 @@
 #include <vector>
 
 #include "vc/vc.h"
-#include "vc_shared.hpp"
+#include "vc_ctx.hpp"
 
 namespace vc {
 void circle_rig(int recon, int held_out, double radius, double target_h, int w, int h, double f, vc_sensor* out);
@@ -31,79 +31,12 @@ void kick_body(int frames, int f, vc_body* b);
 
 using namespace vc;
 
-namespace {
-
-struct Buf {
-  void* p = nullptr;
-  size_t bytes = 0;
-};
-
-struct HostBuf {
-  void* p = nullptr;
-  size_t bytes = 0;
-};
-
-constexpr int kEvents = 24;
-constexpr int kKernelGroups = 13;  // events 12..24 bracket the kernel groups
-
-}  // namespace
-
-struct vc_ctx {
-  int device = 0;
-  cudaStream_t st = nullptr;
-  std::string err;
-  int out_kind = VC_MEM_HOST;
-  bool profiling = false;
-  bool graphs = true;
-
-  // grid-dependent
-  int nx = 0, ny = 0, nz = 0;
-  Buf acc, spec, A, tw, vbase, blk, rowmm, units, unitcnt, rowbits, planeflag;
-  bool acc_dirty = true;  // accumulator contents unknown: next frame clears densely
-  // view staging + clouds
-  Buf views, pts_pos, pts_nrm, pts_w, pts_pix, wmaps, pre_scratch, iso_partial;
-  int pts_cap = 0;
-  SensorSet ss{};
-  // control block
-  DevCtl* ctl = nullptr;
-  DevCtl* ctl_h = nullptr;
-  // mesh + texture
-  Buf m_pos, m_nrm, m_tri, m_eid, m_cells, m_celltri, m_posf, t_vis, t_uv, t_w, t_untex, t_rgb;
-  int v_cap = 0, t_cap = 0, c_cap = 0;
-  // host outputs (pinned)
-  HostBuf h_posf, h_nrm, h_tri, h_vis, h_uv, h_w, h_untex, h_rgb, h_pos, h_eid;
-  // stage-API host scratch
-  std::vector<uint8_t> scratch;
-  // graph
-  cudaGraphExec_t gexec = nullptr;
-  std::vector<uint8_t> gkey;
-  cudaEvent_t ev[kEvents] = {};
-  bool table_ready = false;
-  int last_k = 0;
-  int kernels_per_frame = 0;
-};
-
-namespace {
+namespace vc::rt {
 
 vc_status fail(vc_ctx* c, vc_status s, const std::string& msg) {
   if (c) c->err = msg;
   return s;
 }
-
-#define VC_CUDA(call)                                                                             \
-  do {                                                                                            \
-    const cudaError_t e_ = (call);                                                                \
-    if (e_ != cudaSuccess) {                                                                      \
-      return fail(ctx, e_ == cudaErrorMemoryAllocation ? VC_ERR_OOM : VC_ERR_CUDA,                \
-                  std::string(#call) + ": " + cudaGetErrorString(e_));                            \
-    }                                                                                             \
-  } while (0)
-
-#define VC_TRY(expr)                  \
-  do {                                \
-    const vc_status s_ = (expr);      \
-    if (s_ != VC_OK) return s_;       \
-  } while (0)
 
 vc_status ensure(vc_ctx* ctx, Buf& b, size_t bytes) {
   if (b.bytes >= bytes && b.p) return VC_OK;
@@ -129,11 +62,6 @@ vc_status ensure_host(vc_ctx* ctx, HostBuf& b, size_t bytes) {
   VC_CUDA(cudaHostAlloc(&b.p, want, cudaHostAllocDefault));
   b.bytes = want;
   return VC_OK;
-}
-
-template <class T>
-T* P(const Buf& b) {
-  return static_cast<T*>(b.p);
 }
 
 bool pow2_ok(int n) { return n >= 4 && n <= 1024 && (n & (n - 1)) == 0; }
@@ -322,11 +250,6 @@ MeshBufs mesh_bufs(vc_ctx* ctx) {
   return mb;
 }
 
-struct FrameCfg {
-  int nx, ny, nz, mode, pad, sil_r;
-  double disc, eps_vis;
-};
-
 void record(vc_ctx* ctx, int i) {
   if (ctx->profiling) record_event(ctx->ev[i], ctx->st);
 }
@@ -345,7 +268,7 @@ int enqueue_frame(vc_ctx* ctx, const FrameCfg& f) {
   record(ctx, 12);
   launch_sparse_clear(P<float4>(ctx->acc), P<uint32_t>(ctx->rowbits), f.ny * f.nz, f.nx, st);
   record(ctx, 13);
-  launch_splat(points(ctx), ctx->ctl, P<float4>(ctx->acc), P<uint32_t>(ctx->rowbits), f.mode, st);
+  launch_splat(points(ctx), ctx->ctl, P<float4>(ctx->acc), P<uint32_t>(ctx->rowbits), f.mode, st, 0, f.nz);
   n += 2;
   record(ctx, 2);
   launch_integrate(P<float4>(ctx->acc), P<float2>(ctx->spec), P<float>(ctx->A), f.nx, f.ny, f.nz, f.mode,
@@ -437,7 +360,48 @@ vc_status read_ctl(vc_ctx* ctx) {
   return VC_OK;
 }
 
-}  // namespace
+// Hand the context's mesh + texture buffers to the caller: device pointers,
+// or pinned host copies (enqueued on the context stream, not synchronised).
+vc_status copy_out(vc_ctx* ctx, int V, int T, int k, vc_textured_mesh* out) {
+  if (ctx->out_kind == VC_MEM_DEVICE) {
+    out->positions = P<float>(ctx->m_posf), out->normals = P<float>(ctx->m_nrm), out->triangles = P<int32_t>(ctx->m_tri);
+    out->visible = P<uint8_t>(ctx->t_vis), out->uv = P<float>(ctx->t_uv), out->weight = P<float>(ctx->t_w);
+    out->untextured = P<uint8_t>(ctx->t_untex), out->rgb = P<uint8_t>(ctx->t_rgb);
+    out->positions_f64 = P<double>(ctx->m_pos);
+  } else {
+    VC_TRY(ensure_host(ctx, ctx->h_posf, (size_t)V * 12));
+    VC_TRY(ensure_host(ctx, ctx->h_nrm, (size_t)V * 12));
+    VC_TRY(ensure_host(ctx, ctx->h_tri, (size_t)T * 12));
+    VC_TRY(ensure_host(ctx, ctx->h_vis, (size_t)V * k));
+    VC_TRY(ensure_host(ctx, ctx->h_uv, (size_t)V * k * 8));
+    VC_TRY(ensure_host(ctx, ctx->h_w, (size_t)V * k * 4));
+    VC_TRY(ensure_host(ctx, ctx->h_untex, (size_t)V));
+    VC_TRY(ensure_host(ctx, ctx->h_rgb, (size_t)V * 3));
+    VC_TRY(ensure_host(ctx, ctx->h_pos, (size_t)V * 24));
+    auto d2h = [&](HostBuf& h, const Buf& d, size_t bytes) {
+      return bytes ? cudaMemcpyAsync(h.p, d.p, bytes, cudaMemcpyDeviceToHost, ctx->st) : cudaSuccess;
+    };
+    VC_CUDA(d2h(ctx->h_posf, ctx->m_posf, (size_t)V * 12));
+    VC_CUDA(d2h(ctx->h_nrm, ctx->m_nrm, (size_t)V * 12));
+    VC_CUDA(d2h(ctx->h_tri, ctx->m_tri, (size_t)T * 12));
+    VC_CUDA(d2h(ctx->h_vis, ctx->t_vis, (size_t)V * k));
+    VC_CUDA(d2h(ctx->h_uv, ctx->t_uv, (size_t)V * k * 8));
+    VC_CUDA(d2h(ctx->h_w, ctx->t_w, (size_t)V * k * 4));
+    VC_CUDA(d2h(ctx->h_untex, ctx->t_untex, (size_t)V));
+    VC_CUDA(d2h(ctx->h_rgb, ctx->t_rgb, (size_t)V * 3));
+    VC_CUDA(d2h(ctx->h_pos, ctx->m_pos, (size_t)V * 24));
+    out->positions = (const float*)ctx->h_posf.p, out->normals = (const float*)ctx->h_nrm.p;
+    out->triangles = (const int32_t*)ctx->h_tri.p, out->visible = (const uint8_t*)ctx->h_vis.p;
+    out->uv = (const float*)ctx->h_uv.p, out->weight = (const float*)ctx->h_w.p;
+    out->untextured = (const uint8_t*)ctx->h_untex.p, out->rgb = (const uint8_t*)ctx->h_rgb.p;
+    out->positions_f64 = (const double*)ctx->h_pos.p;
+  }
+  return VC_OK;
+}
+
+}  // namespace vc::rt
+
+using namespace vc::rt;
 
 extern "C" {
 
@@ -472,7 +436,9 @@ vc_status vc_ctx_create(int device, vc_ctx** out) {
   if (cudaSetDevice(device) != cudaSuccess) return cleanup(VC_ERR_CUDA);
   if (cudaStreamCreateWithFlags(&ctx->st, cudaStreamNonBlocking) != cudaSuccess) return cleanup(VC_ERR_CUDA);
   if (cudaMalloc(&ctx->ctl, sizeof(DevCtl)) != cudaSuccess) return cleanup(VC_ERR_OOM);
+  if (cudaMemset(ctx->ctl, 0, sizeof(DevCtl)) != cudaSuccess) return cleanup(VC_ERR_CUDA);
   if (cudaHostAlloc(&ctx->ctl_h, sizeof(DevCtl), cudaHostAllocDefault) != cudaSuccess) return cleanup(VC_ERR_OOM);
+  std::memset(ctx->ctl_h, 0, sizeof(DevCtl));
   for (auto& e : ctx->ev)
     if (cudaEventCreate(&e) != cudaSuccess) return cleanup(VC_ERR_CUDA);
   *out = ctx;
@@ -617,39 +583,7 @@ vc_status vc_reconstruct_frame(vc_ctx* ctx, const vc_sensor* sensors, const vc_v
   out->grid.edge_mm = ctx->ctl_h->grid.edge;
   out->mem_kind = ctx->out_kind;
   if (prof) record_event(ctx->ev[10], ctx->st);
-  if (ctx->out_kind == VC_MEM_DEVICE) {
-    out->positions = P<float>(ctx->m_posf), out->normals = P<float>(ctx->m_nrm), out->triangles = P<int32_t>(ctx->m_tri);
-    out->visible = P<uint8_t>(ctx->t_vis), out->uv = P<float>(ctx->t_uv), out->weight = P<float>(ctx->t_w);
-    out->untextured = P<uint8_t>(ctx->t_untex), out->rgb = P<uint8_t>(ctx->t_rgb);
-    out->positions_f64 = P<double>(ctx->m_pos);
-  } else {
-    VC_TRY(ensure_host(ctx, ctx->h_posf, (size_t)V * 12));
-    VC_TRY(ensure_host(ctx, ctx->h_nrm, (size_t)V * 12));
-    VC_TRY(ensure_host(ctx, ctx->h_tri, (size_t)T * 12));
-    VC_TRY(ensure_host(ctx, ctx->h_vis, (size_t)V * k));
-    VC_TRY(ensure_host(ctx, ctx->h_uv, (size_t)V * k * 8));
-    VC_TRY(ensure_host(ctx, ctx->h_w, (size_t)V * k * 4));
-    VC_TRY(ensure_host(ctx, ctx->h_untex, (size_t)V));
-    VC_TRY(ensure_host(ctx, ctx->h_rgb, (size_t)V * 3));
-    VC_TRY(ensure_host(ctx, ctx->h_pos, (size_t)V * 24));
-    auto d2h = [&](HostBuf& h, const Buf& d, size_t bytes) {
-      return bytes ? cudaMemcpyAsync(h.p, d.p, bytes, cudaMemcpyDeviceToHost, ctx->st) : cudaSuccess;
-    };
-    VC_CUDA(d2h(ctx->h_posf, ctx->m_posf, (size_t)V * 12));
-    VC_CUDA(d2h(ctx->h_nrm, ctx->m_nrm, (size_t)V * 12));
-    VC_CUDA(d2h(ctx->h_tri, ctx->m_tri, (size_t)T * 12));
-    VC_CUDA(d2h(ctx->h_vis, ctx->t_vis, (size_t)V * k));
-    VC_CUDA(d2h(ctx->h_uv, ctx->t_uv, (size_t)V * k * 8));
-    VC_CUDA(d2h(ctx->h_w, ctx->t_w, (size_t)V * k * 4));
-    VC_CUDA(d2h(ctx->h_untex, ctx->t_untex, (size_t)V));
-    VC_CUDA(d2h(ctx->h_rgb, ctx->t_rgb, (size_t)V * 3));
-    VC_CUDA(d2h(ctx->h_pos, ctx->m_pos, (size_t)V * 24));
-    out->positions = (const float*)ctx->h_posf.p, out->normals = (const float*)ctx->h_nrm.p;
-    out->triangles = (const int32_t*)ctx->h_tri.p, out->visible = (const uint8_t*)ctx->h_vis.p;
-    out->uv = (const float*)ctx->h_uv.p, out->weight = (const float*)ctx->h_w.p;
-    out->untextured = (const uint8_t*)ctx->h_untex.p, out->rgb = (const uint8_t*)ctx->h_rgb.p;
-    out->positions_f64 = (const double*)ctx->h_pos.p;
-  }
+  VC_TRY(copy_out(ctx, V, T, k, out));
   if (prof) record_event(ctx->ev[11], ctx->st);
   VC_CUDA(cudaStreamSynchronize(ctx->st));
   if (timings) {
@@ -775,7 +709,7 @@ vc_status vc_stage_splat(vc_ctx* ctx, const double* pos, const double* nrm, cons
   VC_TRY(ensure(ctx, fbuf, N * 12));
   VC_TRY(ensure(ctx, dbuf, N * 4));
   launch_clear(P<float4>(ctx->acc), N, ctx->st);
-  launch_splat(points(ctx), ctx->ctl, P<float4>(ctx->acc), P<uint32_t>(ctx->rowbits), mode, ctx->st);
+  launch_splat(points(ctx), ctx->ctl, P<float4>(ctx->acc), P<uint32_t>(ctx->rowbits), mode, ctx->st, 0, grid->nz);
   const double sigma2 = std::sqrt(1.5) * (std::sqrt(3.0) / 2.0 * grid->edge_mm);  // splat.cpp:35-36
   launch_splat_finalize(P<float4>(ctx->acc), N, mode, negate, sigma2, P<float>(fbuf), P<float>(dbuf), ctx->st);
   cudaError_t e = cudaGetLastError();
@@ -849,6 +783,7 @@ vc_status vc_stage_marching_cubes(vc_ctx* ctx, const float* A, const vc_grid_spe
   VC_CUDA(cudaMemcpyAsync(ctx->A.p, A, N * 4, cudaMemcpyHostToDevice, ctx->st));
   VC_TRY(upload_points(ctx, nullptr, nullptr, nullptr, 0, grid, 1));
   ctx->ctl_h->level = level;
+  ctx->ctl_h->voff = 0;
   VC_CUDA(cudaMemcpyAsync(ctx->ctl, ctx->ctl_h, sizeof(DevCtl), cudaMemcpyHostToDevice, ctx->st));
   launch_row_minmax(P<float>(ctx->A), nx, ny, nz, P<float2>(ctx->rowmm), ctx->st);
   for (int attempt = 0; attempt < 2; ++attempt) {

@@ -54,6 +54,8 @@ struct DevCtl {
   int32_t V, T, C;    // vertices, triangles, active cells
   int32_t overflow;   // MC capacity exceeded
   int32_t units;      // MC: active voxel-row units
+  int32_t v_extra;    // MC slab: cut edges counted on the next rank's first plane
+  int32_t voff;       // MC slab: global id of this rank's first vertex
   int32_t pad;
   double bbox[6];
   DevGrid grid;
@@ -97,13 +99,36 @@ void launch_preprocess(const SensorSet& ss, DevPoints pts, float* weight_maps, i
                        int dims_x, int dims_y, int dims_z, int padding, double disc_mm, int sil_r, cudaStream_t st);
 // k_splat.cu
 void launch_clear(float4* acc, size_t n, cudaStream_t st);
+// zoff/nzl: the z-slab [zoff, zoff+nzl) this rank accumulates (whole grid: 0, nz)
 void launch_splat(const DevPoints& pts, const DevCtl* ctl, float4* acc, uint32_t* rowbits, int mode,
-                  cudaStream_t st);
+                  cudaStream_t st, int zoff, int nzl);
 void launch_sparse_clear(float4* acc, uint32_t* rowbits, int rows, int nx, cudaStream_t st);
 void launch_splat_finalize(const float4* acc, size_t n, int mode, int negate, double sigma2, float* field,
                            float* density, cudaStream_t st);
 // k_fft.cu — integrate_fft chain: acc (float4 U,d) -> A
 size_t spectrum_elems(int nx, int ny, int nz);  // complex elements per component
+// One z-slab of the spectral integration (SURVEY §8(e) "large grids").  On a
+// single GPU every pointer pair aliases (O0 = R0 = Rin = Rout = S0, O1 = R1 =
+// S1) and nzl = nz, kyl = ny.  On P ranks: local x-R2C + y-C2C over planes
+// [zoff, zoff+nzl) -> O0/O1 in send layout; all-to-all -> R0/R1 ([z][kyl][H],
+// ky in [ky0, ky0+kyl)); z pass in place on R0; all-to-all R0 -> Rin; y/x
+// inverse -> Rout (plain layout) -> A (the rank's planes).
+struct SlabFft {
+  const float4* acc;
+  float2 *S0, *S1, *S2, *O0, *O1, *R0, *R1;
+  const float2* Rin;
+  float2* Rout;
+  float* A;
+  int nx, ny, nz, nzl, zoff, kyl, ky0, H, mode;
+  const float2 *twx, *twy, *twz;
+  cudaStream_t st;
+  float2* rowmm;
+  const uint32_t* rowbits;
+  uint32_t* planeflag;  // nz entries (global); F-y writes [zoff, zoff+nzl)
+};
+void launch_fft_forward_xy(const SlabFft& a);
+void launch_fft_z(const SlabFft& a);
+void launch_fft_inverse_yx(const SlabFft& a);
 void launch_integrate(const float4* acc, float2* spec, float* A, int nx, int ny, int nz, int mode,
                       const float2* twiddles, cudaStream_t st, cudaEvent_t* ev /*nullable, 6 events*/,
                       float2* rowmm /*nullable: per-row min/max of A*/,
@@ -118,6 +143,26 @@ void launch_iso_level(const DevPoints& pts, const float* A, DevCtl* ctl, double*
                       cudaStream_t st);
 int mc_blocks(int nx, int ny, int nz);
 void launch_marching_cubes(const float* A, DevCtl* ctl, MeshBufs mb, int nx, int ny, int nz, cudaStream_t st);
+// Slab variant: units (voxel rows) of planes [z0, z0+nzu); planes >= zend
+// belong to the next rank: their cut edges are numbered (vbase) but neither
+// emitted nor meshed.  A, vbase are indexed with GLOBAL voxel ids (callers
+// pass pointers shifted by the slab origin); rowmm is indexed from plane z0.
+// The scan stops before the emit: launch_marching_cubes_count, then (after
+// ctl->voff is known) launch_marching_cubes_emit.
+struct McSlab {
+  int z0, nzu, zend;
+};
+void launch_marching_cubes_count(const float* A, DevCtl* ctl, MeshBufs mb, int nx, int ny, int nz, McSlab sl,
+                                 cudaStream_t st);
+void launch_marching_cubes_emit(const float* A, DevCtl* ctl, MeshBufs mb, int nx, int ny, int nz, McSlab sl,
+                                cudaStream_t st);
+// Slab iso level: samples[p] = trilinear(A, point p) if this rank owns the
+// point's lower z plane, else 0 (summed over ranks, then launch_iso_final_samples)
+void launch_iso_samples(const DevPoints& pts, const float* A, const DevCtl* ctl, int zoff, int nzl, double* samples,
+                        cudaStream_t st);
+void launch_add_f64(double* dst, const double* src, size_t n, cudaStream_t st);
+void launch_mc_set_voff(const int32_t* counts, int rank, DevCtl* ctl, cudaStream_t st);
+void launch_iso_final_samples(const double* samples, DevCtl* ctl, double* partial, cudaStream_t st);
 void launch_row_minmax(const float* A, int nx, int ny, int nz, float2* rowmm, cudaStream_t st);
 void upload_case_table_data(const int8_t* counts, const int8_t* tris, cudaStream_t st);
 // k_texture.cu
