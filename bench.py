@@ -198,6 +198,52 @@ def alg_bytes(nx, ny, nz, P, V, T, k, chunks, nzrows, nzplanes):
             "mc": 8 * rows, "preprocess": k * W * H * 7 + P * 60, "iso": P * 32, "texture": V * (24 + 13 * k)}
 
 
+def profile_kernels(lib, h, sensors, views_list, cfg, dims, out):
+    """Per-stage and per-kernel-group CUDA-event times (profiling replay on
+    context h, outside the timed loop) + the roofline of the dominant kernel."""
+    from paper_1712_03084_b200 import _lib as L
+    lib.vc_ctx_set_output(h, L.VC_MEM_DEVICE)
+    lib.vc_ctx_set_profiling(h, 1)
+    tm = L.StageTimings()
+    kt = (C.c_double * 16)()
+    acc = {}
+    n = len(views_list)
+    ker = np.zeros(11)
+    for views in views_list:
+        L.check(lib.vc_reconstruct_frame(h, sensors, views, K_VIEWS, C.byref(cfg), C.byref(out), C.byref(tm)), h)
+        for nm, _ in L.StageTimings._fields_:
+            acc[nm] = acc.get(nm, 0.0) + getattr(tm, nm) / n
+        lib.vc_ctx_kernel_times(h, kt, 16)
+        ker += np.array(kt[:11]) / n
+    lib.vc_ctx_set_profiling(h, 0)
+    names = ["preprocess", "clear", "splat", "fft_x", "fft_y", "fft_z", "ifft_y", "ifft_x", "iso", "mc", "texture"]
+    kernel_ms = dict(zip(names, ker.tolist()))
+    P, V, T = out.point_count, out.vertex_count, out.triangle_count
+    pos = np.zeros((P, 3))
+    L.check(lib.vc_export_points(h, C.c_void_p(pos.ctypes.data), None, None, None, None), h)
+    sp = sparse_stats(pos, out.grid.origin[:], out.grid.edge_mm, *dims)
+    ab = alg_bytes(*dims, P, V, T, K_VIEWS, *sp)
+    bw = {nm: ab[nm] / (kernel_ms[nm] * 1e-3) / 1e9 for nm in names if kernel_ms[nm] > 0}
+    if not all(nm in bw for nm in ["clear", "fft_x", "fft_y", "fft_z", "ifft_y", "ifft_x"]):
+        raise RuntimeError(f"per-kernel event timings missing: {kernel_ms}")
+    pk = peaks()
+    hbm = float(pk.get("hbm_gbs", 6650.0))
+    fft_names = ["fft_x", "fft_y", "fft_z", "ifft_y", "ifft_x"]
+    dom = max(fft_names + ["clear"], key=lambda nm: kernel_ms[nm])
+    traffic = None
+    if tuple(dims) == DIMS:
+        try:  # dram bytes per launch of the same kernel from the committed ncu --set full capture
+            traffic = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))[dom]["dram_bytes_per_launch"]
+        except Exception:
+            traffic = None
+    roofline = {"bound": "hbm", "kernel": dom, "achieved": bw[dom], "peak": hbm, "unit": "GB/s",
+                "frac": bw[dom] / hbm, "traffic": traffic,
+                "algorithmic_bytes": ab[dom], "avg_launch_ms": kernel_ms[dom],
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)" if "_fallback" not in pk else "fallback"}
+    return {"stages": acc, "kernel_ms": kernel_ms, "bw": bw, "ab": ab, "roofline": roofline, "P": P, "V": V, "T": T,
+            "sparse": sp}
+
+
 def run_gpu(args):
     rank, world, local = dist_env()
     import torch
@@ -317,42 +363,11 @@ def run_gpu(args):
     kernels = lib.vc_ctx_kernels_per_frame(h)
 
     # ---- per-stage / per-kernel timings (profiling replay, separate from the timed loop)
-    lib.vc_ctx_set_profiling(h, 1)
-    tm = L.StageTimings()
-    kt = (C.c_double * 16)()
-    acc = {}
-    prof_frames = min(20, STREAM)
-    ker = np.zeros(11)
-    for i in range(prof_frames):
-        L.check(lib.vc_reconstruct_frame(h, sensors, dev_views[(i * 13) % STREAM], K_VIEWS, C.byref(cfg),
-                                         C.byref(out), C.byref(tm)), h)
-        for n, _ in L.StageTimings._fields_:
-            acc[n] = acc.get(n, 0.0) + getattr(tm, n) / prof_frames
-        lib.vc_ctx_kernel_times(h, kt, 16)
-        ker += np.array(kt[:11]) / prof_frames
-    lib.vc_ctx_set_profiling(h, 0)
-    names = ["preprocess", "clear", "splat", "fft_x", "fft_y", "fft_z", "ifft_y", "ifft_x", "iso", "mc", "texture"]
-    kernel_ms = dict(zip(names, ker.tolist()))
-    P, V, T = out.point_count, out.vertex_count, out.triangle_count
-    pos = np.zeros((P, 3))
-    L.check(lib.vc_export_points(h, C.c_void_p(pos.ctypes.data), None, None, None, None), h)
-    chunks, nzrows, nzplanes = sparse_stats(pos, out.grid.origin[:], out.grid.edge_mm, *DIMS)
-    ab = alg_bytes(*DIMS, P, V, T, K_VIEWS, chunks, nzrows, nzplanes)
-    bw = {n: ab[n] / (kernel_ms[n] * 1e-3) / 1e9 for n in names if kernel_ms[n] > 0}
-    if not all(n in bw for n in ["clear", "fft_x", "fft_y", "fft_z", "ifft_y", "ifft_x"]):
-        raise RuntimeError(f"per-kernel event timings missing: {kernel_ms}")
-    pk = peaks()
-    hbm = float(pk.get("hbm_gbs", 6650.0))
-    fft_names = ["fft_x", "fft_y", "fft_z", "ifft_y", "ifft_x"]
-    dom = max(fft_names + ["clear"], key=lambda n: kernel_ms[n])
-    try:  # dram bytes per launch of the same kernel from the committed ncu --set full capture
-        traffic = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))[dom]["dram_bytes_per_launch"]
-    except Exception:
-        traffic = None
-    roofline = {"bound": "hbm", "kernel": dom, "achieved": bw[dom], "peak": hbm, "unit": "GB/s",
-                "frac": bw[dom] / hbm, "traffic": traffic,
-                "algorithmic_bytes": ab[dom], "avg_launch_ms": kernel_ms[dom],
-                "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)" if "_fallback" not in pk else "fallback"}
+    prof = profile_kernels(lib, h, sensors, [dev_views[(i * 13) % STREAM] for i in range(min(20, STREAM))], cfg,
+                           DIMS, out)
+    acc, kernel_ms, bw, ab, roofline = prof["stages"], prof["kernel_ms"], prof["bw"], prof["ab"], prof["roofline"]
+    P, V, T = prof["P"], prof["V"], prof["T"]
+    chunks, nzrows, nzplanes = prof["sparse"]
 
     # ---- e2e through the C-ABI with host buffers
     for c in ctxs:
@@ -398,6 +413,149 @@ def run_gpu(args):
         torch.distributed.destroy_process_group()
 
 
+C5_DIMS = (1024, 1024, 1024)
+C5_FRAMES = 4
+C5_METRIC = "reconstructed frames/sec at 1024^3 grid, 4x512x424 RGB-D views"
+
+
+def run_c5(args):
+    """Config C5: one 1024^3 frame per step.  N=1: the single-GPU frame path
+    (fits: ~40 GB); N>1 (torchrun): the z-slab decomposition over NCCL
+    (vc_reconstruct_frame_dist), strong scaling, time = max over ranks."""
+    rank, world, local = dist_env()
+    import torch
+    from paper_1712_03084_b200 import _lib as L
+    from paper_1712_03084_b200 import volcap as vc
+    from paper_1712_03084_b200.frame_parallel import max_over_ranks
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    lib = L.lib()
+    sr = None
+    if world > 1:
+        import torch.distributed as dist
+        from paper_1712_03084_b200.slab import SlabReconstructor, nccl_unique_id
+        dist.init_process_group("nccl", device_id=dev)
+        obj = [nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        sr = SlabReconstructor.nccl(world, rank, local, obj[0])
+        ctx = sr.contexts[0]
+    else:
+        ctx = vc.Context(local)
+    h = ctx.handle
+    stream = torch.cuda.ExternalStream(ctx.stream(), device=dev)
+    rig = vc.make_circle_rig(K_VIEWS, 0, 2500, W, H, F)
+    sensors = rig.c_array(K_VIEWS)
+    n_pix = W * H
+    per_view = n_pix * 6
+    frame_bytes = K_VIEWS * per_view
+    dbuf, hbuf = C.c_void_p(), C.c_void_p()
+    L.check(lib.vc_device_alloc(h, C.c_size_t(C5_FRAMES * frame_bytes), C.byref(dbuf)), h)
+    L.check(lib.vc_host_alloc(h, C.c_size_t(C5_FRAMES * frame_bytes), C.byref(hbuf)), h)
+
+    def vp(base, f, k):
+        o = base + f * frame_bytes + k * per_view
+        return o, o + 2 * n_pix, o + 3 * n_pix
+
+    for f in range(C5_FRAMES):
+        body = vc.kick_body(STREAM, f * STREAM // C5_FRAMES)
+        for k in range(K_VIEWS):
+            d, m, c = vp(dbuf.value, f, k)
+            L.check(lib.vc_synth_render(h, C.byref(sensors[k]), C.byref(body), C.c_double(0.0), C.c_uint64(1),
+                                        C.c_double(1.0), k, f, C.c_void_p(d), C.c_void_p(m), C.c_void_p(c),
+                                        L.VC_MEM_DEVICE), h)
+    L.check(lib.vc_memcpy(h, hbuf, dbuf, C.c_size_t(C5_FRAMES * frame_bytes), L.VC_MEM_HOST, L.VC_MEM_DEVICE), h)
+
+    def views_for(base, f, kind):
+        arr = (L.View * K_VIEWS)()
+        for k in range(K_VIEWS):
+            d, m, c = vp(base, f, k)
+            arr[k] = L.View(d, m, c, 0, 0, 0, kind)
+        return arr
+
+    dev_views = [views_for(dbuf.value, f, L.VC_MEM_DEVICE) for f in range(C5_FRAMES)]
+    host_views = [views_for(hbuf.value, f, L.VC_MEM_HOST) for f in range(C5_FRAMES)]
+    cfg = vc.ReconConfig(dims=C5_DIMS).to_c()
+    out = L.TexturedMesh()
+    info = L.DistInfo()
+    d2h = [0]
+
+    def frame(i, views):
+        if sr is None:
+            L.check(lib.vc_reconstruct_frame(h, sensors, views[i % C5_FRAMES], K_VIEWS, C.byref(cfg), C.byref(out),
+                                             None), h)
+        else:
+            L.check(lib.vc_reconstruct_frame_dist(sr._h, sensors, views[i % C5_FRAMES], K_VIEWS, C.byref(cfg),
+                                                  C.byref(out), C.byref(info), None), h)
+        d2h[0] += out.vertex_count * (12 + 12 + 24 + 3 + 1 + K_VIEWS * 13) + out.triangle_count * 12
+
+    def timed(views, steps):
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+        d2h[0] = 0
+        ev0.record(stream)
+        for i in range(steps):
+            frame(i, views)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        return max_over_ranks(ev0.elapsed_time(ev1), device="cuda"), d2h[0] / steps
+
+    lib.vc_ctx_set_output(h, L.VC_MEM_DEVICE)
+    for i in range(args.warmup):
+        frame(i, dev_views)
+    with Clocks(local) as clk:
+        ms, _ = timed(dev_views, args.steps)
+    value = args.steps / (ms / 1000.0)
+    tm = L.StageTimings()
+    if sr is None:
+        prof = profile_kernels(lib, h, sensors, dev_views[:2], cfg, C5_DIMS, out)
+        roofline, stages, kernel_ms = prof["roofline"], prof["stages"], prof["kernel_ms"]
+        launches = lib.vc_ctx_kernels_per_frame(h) * args.steps
+        mesh = {"points": prof["P"], "vertices": prof["V"], "triangles": prof["T"]}
+    else:
+        L.check(lib.vc_reconstruct_frame_dist(sr._h, sensors, dev_views[0], K_VIEWS, C.byref(cfg), C.byref(out),
+                                              C.byref(info), C.byref(tm)), h)
+        stages = {nm: getattr(tm, nm) for nm, _ in L.StageTimings._fields_}
+        kernel_ms = None
+        # slab integrate: this rank's share of the whole-grid FFT chain bytes over fft_ms (incl. the exchanges)
+        nx, ny, nz = C5_DIMS
+        Nh = nz * ny * (nx // 2 + 1)
+        fft_bytes = (16 * nx * ny * nz + 3 * 8 * Nh + 2 * 3 * 8 * Nh + 4 * 8 * Nh + 2 * 8 * Nh + 8 * Nh
+                     + 4 * nx * ny * nz) / world
+        pk = peaks()
+        hbm = float(pk.get("hbm_gbs", 6650.0))
+        ach = fft_bytes / (tm.fft_ms * 1e-3) / 1e9
+        roofline = {"bound": "hbm", "kernel": "slab integrate (x/y, all-to-all, z, all-to-all, y/x)",
+                    "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm, "traffic": None,
+                    "algorithmic_bytes": fft_bytes, "avg_launch_ms": tm.fft_ms}
+        launches = None
+        mesh = {"vertices_total": info.vertex_total, "triangles_total": info.triangle_total}
+    lib.vc_ctx_set_output(h, L.VC_MEM_HOST)
+    for i in range(min(args.warmup, 2)):
+        frame(i, host_views)
+    e2e_ms, d2h_per = timed(host_views, args.steps)
+    if rank == 0:
+        line = {"metric": C5_METRIC, "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+                "config": {"workload": "C5: 4 views 512x424 of the kick stream, 1024^3 grid, weighted splat",
+                           "grid": list(C5_DIMS), "parallelism": "single GPU" if world == 1 else f"z-slab x{world}",
+                           "l2": "working set ~40 GB >> 126 MB L2"},
+                "e2e": {"value": args.steps / (e2e_ms / 1000.0), "unit": "frames/s",
+                        "h2d_bytes_per_step": frame_bytes, "d2h_bytes_per_step": int(d2h_per)},
+                "gpu_launches": launches, "roofline": roofline,
+                "stages_ms": {k: round(v, 3) for k, v in stages.items()},
+                "kernel_ms": {k: round(v, 3) for k, v in kernel_ms.items()} if kernel_ms else None,
+                "mesh": mesh, "clocks": clk.summary()}
+        print(json.dumps(line), flush=True)
+    lib.vc_device_free(h, dbuf)
+    lib.vc_host_free(h, hbuf)
+    if sr is not None:
+        sr.close()
+        torch.distributed.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -405,6 +563,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--workload", default="c2", choices=["c2", "c5"],
+                    help="c2: the BASELINE metric (256^3 stream, frame-parallel); c5: 1024^3 frames (z-slabs on N>1)")
     ap.add_argument("--streams", type=int, default=3,
                     help="concurrent frames per GPU (one context + host thread each)")
     args = ap.parse_args()
@@ -412,6 +572,8 @@ def main():
         args.warmup = 3
     if args.impl == "reference":
         run_reference(args)
+    elif args.workload == "c5":
+        run_c5(args)
     else:
         run_gpu(args)
 
