@@ -21,6 +21,7 @@
 // = R1/R2 register DFTs of length R2 per thread + twiddle W_n^(j1 k2), one
 // shared-memory exchange, step 2 = one register DFT of length R1.
 #include <cmath>
+#include <cstdlib>
 #include <vector>
 
 #include "vc_shared.hpp"
@@ -166,10 +167,6 @@ __device__ __forceinline__ float signed_freq(int i) {
   constexpr float k = (float)(2.0 * 3.14159265358979323846 / N);
   return (float)(i <= N / 2 ? i : i - N) * k;
 }
-__device__ __forceinline__ float signed_freq(int i, int n) {
-  const int m = i <= n / 2 ? i : i - n;
-  return (float)m * __fdiv_rn(6.283185307179586f, (float)n);
-}
 
 // x passes: TEAMS teams of T lanes; keep the exchange tiles under ~48 KB.
 template <int N>
@@ -300,6 +297,10 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool pr
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(pred ? 16 : 0) : "memory");
 }
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool pred) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(pred ? 8 : 0) : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() {
@@ -348,6 +349,28 @@ __device__ __forceinline__ void stage_tile(float2* tile, const float2* src, size
   stage_tile<N, CW, THREADS>(tile, src, RowMap{stride, 0, 31}, kx0, H, rowmask);
 }
 
+// Nyquist tile: column c is the kx = nx/2 column of line group c (another
+// plane / ky row), at src + c*colstride, rows by `rm`; element (j, c) is
+// zero-filled when c >= ncol or its flag word flags[c*fstride + j] is 0.
+template <int N, int CW, int THREADS>
+__device__ __forceinline__ void stage_nyq(float2* tile, const float2* src, RowMap rm, size_t colstride, int ncol,
+                                          const uint32_t* flags, int fstride) {
+  constexpr int NI = N * CW / THREADS;
+  static_assert(NI * THREADS == N * CW && NI <= 32, "tile");
+  uint32_t ok = 0;
+#pragma unroll
+  for (int k = 0; k < NI; ++k) {  // all flag loads in flight before any copy
+    const int i = threadIdx.x + k * THREADS, j = i / CW, c = i % CW;
+    ok |= (c < ncol && (!flags || __ldg(flags + (size_t)c * fstride + j) != 0u) ? 1u : 0u) << k;
+  }
+#pragma unroll
+  for (int k = 0; k < NI; ++k) {
+    const int i = threadIdx.x + k * THREADS, j = i / CW, c = i % CW;
+    const bool p = (ok >> k) & 1u;
+    cp_async8(tile + j * CW + c, p ? (const void*)(src + (size_t)c * colstride + rm.off(j)) : (const void*)src, p);
+  }
+}
+
 template <int N, int CW>
 __device__ __forceinline__ void tile_to_regs(const float2* tile, int c, int t, float2* v) {
   using S = Shape<N>;
@@ -363,7 +386,7 @@ __device__ __forceinline__ void tile_to_regs(const float2* tile, int c, int t, f
 // for the slab transform that is the send layout of the forward all-to-all
 // (block s = the ky-slab of rank s); with kyl = ny it is the plain layout.
 template <int NY>
-__global__ void __launch_bounds__(CCfg<NY>::THREADS, 2) fy_kernel(const float2* S0, const float2* S1,
+__global__ void __launch_bounds__(CCfg<NY>::THREADS, NY >= 1024 ? 1 : 2) fy_kernel(const float2* S0, const float2* S1,
                                                                  const float2* __restrict__ S2, float2* O0, float2* O1,
                                                                  int nxh, int H, int lk,
                                                                  const float2* __restrict__ tw,
@@ -430,30 +453,36 @@ __global__ void __launch_bounds__(CCfg<NY>::THREADS, 2) fy_kernel(const float2* 
 // ------------------------------------------------------------------ Z (fused)
 // FFT_z(D) is parked in its staged tile while FFT_z(Z) runs (one register
 // array live, three CTAs per SM).
-// Input: D, Z as [z][kyl][H] (kyl = ny on one GPU; a ky-slab starting at ky0
-// after the forward all-to-all).  The result overwrites S0 in place.
-template <int NZ>
-__global__ void __launch_bounds__(CCfg<NZ>::THREADS, 3) z_kernel(float2* __restrict__ S0,
-                                                                const float2* __restrict__ S1, int nx, int ny,
-                                                                int kyl, int ky0, int H,
-                                                                const float2* __restrict__ tw,
-                                                                const uint32_t* __restrict__ planeflag) {
+template <int NZ, bool NYQ>
+__device__ __forceinline__ void z_body(float2* __restrict__ S0, const float2* __restrict__ S1, int nx, int ny, int kyl,
+                                       int ky0, int H, float fx_step, float fy_step, const float2* __restrict__ tw,
+                                       const uint32_t* __restrict__ planeflag) {
   using S = Shape<NZ>;
   constexpr int T = S::R2, R1 = S::R1, kCW = CCfg<NZ>::CW, TH = CCfg<NZ>::THREADS;
   extern __shared__ float2 sh[];  // 2 tiles of NZ x kCW
   float2* b0 = sh;
   float2* b1 = sh + NZ * kCW;
   const int c = threadIdx.x % kCW, t = threadIdx.x / kCW;
-  const int kx0 = blockIdx.x * kCW, kx = kx0 + c;
-  const int kyr = blockIdx.y, ky = ky0 + kyr;
-  const bool live = kx <= nx / 2;
   const size_t zstride = (size_t)kyl * H;
-  const size_t base = (size_t)kyr * H + kx;
-  const uint32_t pm = row_flags<NZ, kCW, TH>(planeflag);  // planes F-y skipped are zero
-  stage_tile<NZ, kCW, TH>(b0, S0 + (size_t)kyr * H, zstride, kx0, H, pm);
-  cp_async_commit();
-  stage_tile<NZ, kCW, TH>(b1, S1 + (size_t)kyr * H, zstride, kx0, H, pm);
-  cp_async_commit();
+  // column c: (kx, local ky row); the Nyquist tile packs kx = nx/2 of kCW ky rows
+  const int kx = NYQ ? nx / 2 : blockIdx.x * kCW + c;
+  const int kyr = NYQ ? blockIdx.y * kCW + c : blockIdx.y;
+  if (NYQ) {
+    const int y0 = blockIdx.y * kCW;
+    if (y0 >= kyl) return;
+    const size_t off = (size_t)y0 * H + nx / 2;
+    const RowMap rm{zstride, 0, 31};
+    stage_nyq<NZ, kCW, TH>(b0, S0 + off, rm, (size_t)H, min(kCW, kyl - y0), planeflag, 0);
+    cp_async_commit();
+    stage_nyq<NZ, kCW, TH>(b1, S1 + off, rm, (size_t)H, min(kCW, kyl - y0), planeflag, 0);
+    cp_async_commit();
+  } else {
+    const uint32_t pm = row_flags<NZ, kCW, TH>(planeflag);  // planes F-y skipped are zero
+    stage_tile<NZ, kCW, TH>(b0, S0 + (size_t)kyr * H, zstride, blockIdx.x * kCW, H, pm);
+    cp_async_commit();
+    stage_tile<NZ, kCW, TH>(b1, S1 + (size_t)kyr * H, zstride, blockIdx.x * kCW, H, pm);
+    cp_async_commit();
+  }
   float2 v[R1];
   cp_async_wait<1>();
   __syncthreads();
@@ -470,7 +499,10 @@ __global__ void __launch_bounds__(CCfg<NZ>::THREADS, 3) z_kernel(float2* __restr
   __syncthreads();
   ExCols<NZ, kCW> e1{b1, c};
   fft_line<NZ, false>(v, t, tw, e1);
-  const float wx = signed_freq(kx, nx), wy = signed_freq(ky, ny);
+  // integrate.cpp:37-40 frequencies 2 pi m / n (fp32: m * (2 pi / n))
+  const int ky = ky0 + kyr;
+  const float wx = (float)(kx <= nx / 2 ? kx : kx - nx) * fx_step;
+  const float wy = (float)(ky <= ny / 2 ? ky : ky - ny) * fy_step;
   const float wxy = wx * wx + wy * wy;
 #pragma unroll
   for (int k1 = 0; k1 < R1; ++k1) {
@@ -485,29 +517,46 @@ __global__ void __launch_bounds__(CCfg<NZ>::THREADS, 3) z_kernel(float2* __restr
   __syncthreads();  // everyone has read its parked D before b0 becomes the exchange
   relayout_for_inverse<NZ>(v);
   fft_line<NZ, true>(v, t, tw, e0);
+  const bool live = NYQ ? kyr < kyl : kx <= nx / 2;
   if (live) {
+    const size_t base = (size_t)kyr * H + kx;
 #pragma unroll
     for (int k1 = 0; k1 < R1; ++k1) __stcs(S0 + base + (size_t)(t + T * k1) * zstride, v[k1]);
   }
 }
 
+// Input: D, Z as [z][kyl][H] (kyl = ny on one GPU; a ky-slab starting at ky0
+// after the forward all-to-all).  The result overwrites S0 in place.
+template <int NZ>
+__global__ void __launch_bounds__(CCfg<NZ>::THREADS, NZ >= 1024 ? 1 : 3)
+    z_kernel(float2* __restrict__ S0, const float2* __restrict__ S1, int nx, int ny, int kyl, int ky0, int H, int nyq,
+             float fx_step, float fy_step, const float2* __restrict__ tw, const uint32_t* __restrict__ planeflag) {
+  if (blockIdx.x == nyq)
+    z_body<NZ, true>(S0, S1, nx, ny, kyl, ky0, H, fx_step, fy_step, tw, planeflag);
+  else
+    z_body<NZ, false>(S0, S1, nx, ny, kyl, ky0, H, fx_step, fy_step, tw, planeflag);
+}
+
 // ------------------------------------------------------------------ I-y
-// Input rows in the layout fy_kernel writes (the receive layout of the
-// backward all-to-all on several GPUs); output in the plain [zl][ky][H]
-// layout (in place on one GPU: Rin == Rout, lk = log2 ny).
-template <int NY>
-__global__ void __launch_bounds__(CCfg<NY>::THREADS, 3) iy_kernel(const float2* Rin, float2* Rout, int nxh, int H,
-                                                                 int lk, const float2* __restrict__ tw) {
+template <int NY, bool NYQ>
+__device__ __forceinline__ void iy_body(const float2* Rin, float2* Rout, int nxh, int H, int lk,
+                                        const float2* __restrict__ tw) {
   using S = Shape<NY>;
   constexpr int T = S::R2, R1 = S::R1, kCW = CCfg<NY>::CW, TH = CCfg<NY>::THREADS;
   extern __shared__ float2 sh[];
   const int c = threadIdx.x % kCW, t = threadIdx.x / kCW;
-  const int kx0 = blockIdx.x * kCW, kx = kx0 + c;
-  const bool live = kx < nxh;
-  const size_t plane = (size_t)blockIdx.y * NY * H;
+  const int nzl = gridDim.y;
   const size_t kyl = (size_t)1 << lk;
-  const RowMap rm{(size_t)H, gridDim.y * kyl * H, lk};
-  stage_tile<NY, kCW, TH>(sh, Rin + blockIdx.y * kyl * H, rm, kx0, H, 0xffffffffu);
+  const RowMap rm{(size_t)H, nzl * kyl * H, lk};
+  const int zl = NYQ ? blockIdx.y * kCW + c : blockIdx.y;
+  const int kx = NYQ ? nxh - 1 : blockIdx.x * kCW + c;
+  if (NYQ) {  // the kx = nx/2 column of planes blockIdx.y*kCW + c
+    const int z0 = blockIdx.y * kCW;
+    if (z0 >= nzl) return;
+    stage_nyq<NY, kCW, TH>(sh, Rin + z0 * kyl * H + (nxh - 1), rm, kyl * H, min(kCW, nzl - z0), nullptr, 0);
+  } else {
+    stage_tile<NY, kCW, TH>(sh, Rin + zl * kyl * H, rm, blockIdx.x * kCW, H, 0xffffffffu);
+  }
   cp_async_commit();
   float2 v[R1];
   cp_async_wait<0>();
@@ -516,10 +565,24 @@ __global__ void __launch_bounds__(CCfg<NY>::THREADS, 3) iy_kernel(const float2* 
   __syncthreads();
   ExCols<NY, kCW> ex{sh, c};
   fft_line<NY, true>(v, t, tw, ex);
+  const bool live = NYQ ? zl < nzl : kx < nxh;
   if (live) {
+    const size_t plane = (size_t)zl * NY * H;
 #pragma unroll
     for (int k1 = 0; k1 < R1; ++k1) __stcs(Rout + plane + (size_t)(t + T * k1) * H + kx, v[k1]);
   }
+}
+
+// Input rows in the layout fy_kernel writes (the receive layout of the
+// backward all-to-all on several GPUs); output in the plain [zl][ky][H]
+// layout (in place on one GPU: Rin == Rout, lk = log2 ny).
+template <int NY>
+__global__ void __launch_bounds__(CCfg<NY>::THREADS, NY >= 1024 ? 2 : 3)
+    iy_kernel(const float2* Rin, float2* Rout, int nxh, int H, int lk, int nyq, const float2* __restrict__ tw) {
+  if (blockIdx.x == nyq)
+    iy_body<NY, true>(Rin, Rout, nxh, H, lk, tw);
+  else
+    iy_body<NY, false>(Rin, Rout, nxh, H, lk, tw);
 }
 
 // ------------------------------------------------------------------ I-x
@@ -667,10 +730,29 @@ struct RunFx {
     fx_kernel<N><<<grid, C::THREADS, C::SMEM, a.st>>>(a.acc, a.S0, a.S1, a.S2, rows, a.H, a.rowbits, a.mode, a.twx);
   }
 };
+// Column tiles of CW kx columns.  When nx/2 is a multiple of CW the single
+// kx = nx/2 (Nyquist) column would fill a whole tile alone: the last grid
+// column instead packs it from CW planes / ky rows (tile index `nyq`).
+inline int nyq_mode() {  // VC_NYQ_PACK: bit 1 z, bit 2 iy (A/B switch; default both)
+  static const int m = [] {
+    const char* e = std::getenv("VC_NYQ_PACK");
+    return e ? std::atoi(e) : 6;
+  }();
+  return m;
+}
+inline void col_grid(int nx, int cw, int* tiles, int* nyq, int bit) {
+  if ((nx / 2) % cw == 0 && (nyq_mode() >> bit & 1)) {
+    *tiles = nx / 2 / cw + 1, *nyq = nx / 2 / cw;
+  } else {
+    *tiles = (nx / 2 + 1 + cw - 1) / cw, *nyq = -1;
+  }
+}
 template <int N>
 struct RunFy {
   static void run(const SlabFft& a) {
     using C = CCfg<N>;
+    // (no Nyquist packing here: F-y's per-row empty flags make the packed
+    // gather slower than the one wasted tile, measured)
     dim3 grid((a.nx / 2 + 1 + C::CW - 1) / C::CW, a.nzl);
     fy_kernel<N><<<grid, C::THREADS, 3 * C::SMEM, a.st>>>(a.S0, a.S1, a.S2, a.O0, a.O1, a.nx / 2 + 1, a.H,
                                                           ilog2(a.kyl), a.twy, a.rowbits, a.planeflag + a.zoff);
@@ -680,17 +762,22 @@ template <int N>
 struct RunZ {
   static void run(const SlabFft& a) {
     using C = CCfg<N>;
-    dim3 grid((a.nx / 2 + 1 + C::CW - 1) / C::CW, a.kyl);
-    z_kernel<N><<<grid, C::THREADS, 2 * C::SMEM, a.st>>>(a.R0, a.R1, a.nx, a.ny, a.kyl, a.ky0, a.H, a.twz,
-                                                         a.planeflag);
+    int tiles, nyq;
+    col_grid(a.nx, C::CW, &tiles, &nyq, 1);
+    dim3 grid(tiles, a.kyl);
+    const float fxs = (float)(2.0 * M_PI / a.nx), fys = (float)(2.0 * M_PI / a.ny);
+    z_kernel<N><<<grid, C::THREADS, 2 * C::SMEM, a.st>>>(a.R0, a.R1, a.nx, a.ny, a.kyl, a.ky0, a.H, nyq, fxs, fys,
+                                                         a.twz, a.planeflag);
   }
 };
 template <int N>
 struct RunIy {
   static void run(const SlabFft& a) {
     using C = CCfg<N>;
-    dim3 grid((a.nx / 2 + 1 + C::CW - 1) / C::CW, a.nzl);
-    iy_kernel<N><<<grid, C::THREADS, C::SMEM, a.st>>>(a.Rin, a.Rout, a.nx / 2 + 1, a.H, ilog2(a.kyl), a.twy);
+    int tiles, nyq;
+    col_grid(a.nx, C::CW, &tiles, &nyq, 2);
+    dim3 grid(tiles, a.nzl);
+    iy_kernel<N><<<grid, C::THREADS, C::SMEM, a.st>>>(a.Rin, a.Rout, a.nx / 2 + 1, a.H, ilog2(a.kyl), nyq, a.twy);
   }
 };
 template <int N>
