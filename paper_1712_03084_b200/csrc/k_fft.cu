@@ -186,12 +186,22 @@ struct CCfg {
   static constexpr int SMEM = N * CW * 8;  // one staged tile (= exchange buffer)
 };
 
+// Predicated streaming load (no branch): zero when !pred.
+__device__ __forceinline__ float4 ld_pred_cs(const float4* p, bool pred) {
+  float4 r = make_float4(0.f, 0.f, 0.f, 0.f);
+  asm("{\n .reg .pred q;\n setp.ne.u32 q, %5, 0;\n @q ld.global.cs.v4.f32 {%0, %1, %2, %3}, [%4];\n}"
+      : "+f"(r.x), "+f"(r.y), "+f"(r.z), "+f"(r.w)
+      : "l"(p), "r"((unsigned)pred));
+  return r;
+}
+
 // ------------------------------------------------------------------ F-x
 template <int NX>
 __global__ void __launch_bounds__(XCfg<NX>::THREADS, 2) fx_kernel(const float4* __restrict__ acc, float2* __restrict__ S0,
                                                        float2* __restrict__ S1, float2* __restrict__ S2, int rows,
                                                        int H, const uint32_t* __restrict__ rowbits, int mode,
-                                                       const float2* __restrict__ tw) {
+                                                       const float2* __restrict__ tw,
+                                                       const int32_t* __restrict__ rowlist) {
   using S = Shape<NX>;
   constexpr int T = S::R2, R1 = S::R1, TEAMS = XCfg<NX>::TEAMS;
   constexpr int CH = NX < 32 ? 0 : 5;  // log2 of the 32-voxel chunk (whole row when nx < 32)
@@ -199,22 +209,37 @@ __global__ void __launch_bounds__(XCfg<NX>::THREADS, 2) fx_kernel(const float4* 
   const int team = threadIdx.x / T, t = threadIdx.x % T;
   const int lane = threadIdx.x & 31, team_lane0 = lane - t;
   ExTeam<NX> ex{dyn_smem + team * XCfg<NX>::TILE, team_mask<T>(team_lane0)};
-  const int pair = blockIdx.x * TEAMS + team;
-  const int l0 = 2 * pair, l1 = l0 + 1;
-  if (l1 >= rows) return;
+  // rows: the splat's touched-row list, two per team (any two rows: the z
+  // components of a pair share one complex FFT), persistent teams over the
+  // list; without a list, row pairs (2p, 2p+1) of the whole slab
+  const int n = rowlist ? rowlist[0] : rows;
+  const int pairs = (n + 1) / 2;
+  const int step = rowlist ? gridDim.x * TEAMS : pairs;
+  for (int pair = blockIdx.x * TEAMS + team; pair < pairs; pair += step) {
+  const int l0 = rowlist ? __ldg(rowlist + 1 + 2 * pair) : 2 * pair;
+  const int l1 = 2 * pair + 1 < n ? (rowlist ? __ldg(rowlist + 2 + 2 * pair) : 2 * pair + 1) : -1;
   const uint32_t bits0 = rowbits ? __ldg(rowbits + l0) : 0xffffffffu;
-  const uint32_t bits1 = rowbits ? __ldg(rowbits + l1) : 0xffffffffu;
-  if ((bits0 | bits1) == 0u) return;  // both rows empty: F-y treats them as zero
+  const uint32_t bits1 = l1 < 0 ? 0u : (rowbits ? __ldg(rowbits + l1) : 0xffffffffu);
+  if ((bits0 | bits1) == 0u) continue;  // both rows empty: F-y treats them as zero
   const bool live = true;
 
   auto load_line = [&](int l, uint32_t bits, float2* xy, float* zc) {
+    // all R1 predicated loads in flight before the first use (untouched
+    // chunks hold stale data and are neither read nor used)
+    float4 av[R1];
 #pragma unroll
     for (int q = 0; q < S::Q; ++q)
 #pragma unroll
       for (int j2 = 0; j2 < T; ++j2) {
         const int j = t + T * q + R1 * j2;
         const bool touched = CH == 0 ? bits != 0u : ((bits >> (j >> CH)) & 1u) != 0u;
-        float4 a = touched ? __ldcs(acc + (size_t)l * NX + j) : make_float4(0.f, 0.f, 0.f, 0.f);
+        av[q * T + j2] = ld_pred_cs(acc + (size_t)l * NX + j, touched);
+      }
+#pragma unroll
+    for (int q = 0; q < S::Q; ++q)
+#pragma unroll
+      for (int j2 = 0; j2 < T; ++j2) {
+        const float4 a = av[q * T + j2];
         float s = 0.f;
         if (mode == 0) {
           if (a.w >= 1e-6f) s = -1.2247448713915890f / a.w;  // -sqrt(1.5)/d'
@@ -285,6 +310,7 @@ __global__ void __launch_bounds__(XCfg<NX>::THREADS, 2) fx_kernel(const float4* 
   for (int i = 0; i < R1; ++i) v[i] = make_float2(z0[i], z1[i]);
   fft_line<NX, false>(v, t, tw, ex);
   split_store_z(v, (size_t)l0 * H, (size_t)l1 * H, bits0 != 0u, bits1 != 0u);
+  }
 }
 
 // ------------------------------------------------------------------ tile staging
@@ -726,8 +752,10 @@ struct RunFx {
   static void run(const SlabFft& a) {
     using C = XCfg<N>;
     const int rows = a.ny * a.nzl;
-    const int grid = (rows / 2 + C::TEAMS - 1) / C::TEAMS;
-    fx_kernel<N><<<grid, C::THREADS, C::SMEM, a.st>>>(a.acc, a.S0, a.S1, a.S2, rows, a.H, a.rowbits, a.mode, a.twx);
+    const int need = (rows / 2 + C::TEAMS - 1) / C::TEAMS;
+    const int grid = a.rowlist && need > 148 * 2 ? 148 * 2 : need;  // persistent teams over the row list
+    fx_kernel<N><<<grid, C::THREADS, C::SMEM, a.st>>>(a.acc, a.S0, a.S1, a.S2, rows, a.H, a.rowbits, a.mode, a.twx,
+                                                      a.rowlist);
   }
 };
 // Column tiles of CW kx columns.  When nx/2 is a multiple of CW the single
@@ -832,8 +860,9 @@ void launch_fft_inverse_yx(const SlabFft& a) {
 
 void launch_integrate(const float4* acc, float2* spec, float* A, int nx, int ny, int nz, int mode,
                       const float2* tw, cudaStream_t st, cudaEvent_t* ev, float2* rowmm, const uint32_t* rowbits,
-                      uint32_t* planeflag) {
+                      uint32_t* planeflag, const int32_t* rowlist) {
   SlabFft a;
+  a.rowlist = rowlist;
   const size_t cs = spectrum_elems(nx, ny, nz);
   a.acc = acc, a.S0 = spec, a.S1 = spec + cs, a.S2 = spec + 2 * cs, a.A = A;
   a.O0 = a.S0, a.O1 = a.S1, a.R0 = a.S0, a.R1 = a.S1, a.Rin = a.S0, a.Rout = a.S0;

@@ -253,7 +253,7 @@ __global__ void __launch_bounds__(kSeg) pre_points_kernel(const __grid_constant_
 
 // single CTA: exclusive scan of the segment counts (contiguous runs per thread)
 __global__ void __launch_bounds__(1024) pre_scan_kernel(const int32_t* counts, int32_t* offsets, int n, int cap,
-                                                        DevCtl* ctl) {
+                                                        DevCtl* ctl, int32_t* rowlist_reset) {
   __shared__ int wsum[32];
   const int per = (n + 1023) / 1024;
   const int b0 = min(n, (int)threadIdx.x * per), b1 = min(n, b0 + per);
@@ -292,6 +292,7 @@ __global__ void __launch_bounds__(1024) pre_scan_kernel(const int32_t* counts, i
     ctl->P = P;
     ctl->status = P == 0 ? 2 : (P > cap ? 3 : 0);
     ctl->voff = 0;
+    if (rowlist_reset) *rowlist_reset = 0;  // the frame's clear (launched before) has read the previous list
   }
 }
 
@@ -422,7 +423,8 @@ size_t preprocess_scratch_bytes(const SensorSet& ss) {
 }
 
 void launch_preprocess(const SensorSet& ss, DevPoints pts, float* weight_maps, int32_t* scratch, DevCtl* ctl,
-                       int nx, int ny, int nz, int padding, double disc_mm, int sil_r, cudaStream_t st) {
+                       int nx, int ny, int nz, int padding, double disc_mm, int sil_r, cudaStream_t st,
+                       int32_t* rowlist_reset) {
   const int rows = ss.row_offset[ss.k];
   const Scratch s = carve(ss, scratch);
   const dim3 grid(s.spr, rows);
@@ -430,7 +432,7 @@ void launch_preprocess(const SensorSet& ss, DevPoints pts, float* weight_maps, i
   pre_tri_kernel<<<grid, kSeg, 0, st>>>(ss, disc_mm, s.tri);
   pre_points_kernel<<<grid, kSeg, 0, st>>>(ss, sil_r, s.tri, s.pref, s.ppitch, s.stage, s.flags, s.counts, s.bbox,
                                            weight_maps);
-  pre_scan_kernel<<<1, 1024, 0, st>>>(s.counts, s.offsets, s.nseg, pts.cap, ctl);
+  pre_scan_kernel<<<1, 1024, 0, st>>>(s.counts, s.offsets, s.nseg, pts.cap, ctl, rowlist_reset);
   pre_gather_kernel<<<grid, kSeg, 0, st>>>(ss, s.stage, s.flags, s.offsets, pts);
   pre_fit_kernel<<<1, 1024, 0, st>>>(s.bbox, s.nseg, nx, ny, nz, padding, ctl);
 }

@@ -17,8 +17,10 @@
 //
 // Sparsity: the splat touches only a thin shell of the grid (~5% of 256^3).
 // Every scatter also sets the bit of its 32-voxel x-chunk in a per-row mask
-// (rowbits[(z*ny+y)], bit = x/32).  The next frame's clear zeroes only the
-// chunks those bits name, and the FFT's first pass loads only them.
+// (rowbits[(z*ny+y)], bit = x/32); the first marking of a row appends it to
+// a compact row list.  The next frame's clear zeroes only the chunks of the
+// listed rows, and the FFT's first pass works through the list, loading only
+// the marked chunks.
 #include "vc_device.cuh"
 
 namespace vc {
@@ -34,10 +36,13 @@ __global__ void __launch_bounds__(256) clear_kernel(float4* acc, size_t n) {
 
 // Zero the chunks the previous frame touched and reset their bits (one warp
 // per row, 32 lanes x float4 = one 512 B chunk per store instruction).
-__global__ void __launch_bounds__(256) sparse_clear_kernel(float4* acc, uint32_t* rowbits, int rows, int nx) {
+__global__ void __launch_bounds__(256) sparse_clear_kernel(float4* acc, uint32_t* rowbits,
+                                                           const int32_t* __restrict__ rowlist, int nx) {
   const int lane = threadIdx.x & 31;
   const int chunk = nx < 32 ? nx : 32;
-  for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < rows; r += (gridDim.x * blockDim.x) >> 5) {
+  const int n = rowlist[0];
+  for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n; i += (gridDim.x * blockDim.x) >> 5) {
+    const int r = rowlist[1 + i];
     uint32_t bits = rowbits[r];
     if (!bits) continue;
     const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -51,9 +56,9 @@ __global__ void __launch_bounds__(256) sparse_clear_kernel(float4* acc, uint32_t
   }
 }
 
-__device__ __forceinline__ void mark_chunks(uint32_t* rowbits, int row, int x0, int x1) {
+__device__ __forceinline__ void mark_chunks(uint32_t* rowbits, int32_t* rowlist, int row, int x0, int x1) {
   const uint32_t m = (0xffffffffu >> (31 - (x1 >> 5))) & (0xffffffffu << (x0 >> 5));
-  atomicOr(rowbits + row, m);
+  if (atomicOr(rowbits + row, m) == 0u) rowlist[1 + atomicAdd(rowlist, 1)] = row;  // first touch of the row
 }
 
 __device__ __forceinline__ void red_add_v4(float4* addr, float4 v) {
@@ -69,7 +74,8 @@ __global__ void __launch_bounds__(kSplatThreads) splat_weighted_kernel(const dou
                                                                        const double* __restrict__ wgt,
                                                                        const DevCtl* __restrict__ ctl,
                                                                        float4* __restrict__ acc,
-                                                                       uint32_t* __restrict__ rowbits, int zoff,
+                                                                       uint32_t* __restrict__ rowbits,
+                                                                       int32_t* __restrict__ rowlist, int zoff,
                                                                        int nzl) {
   const int P = ctl->P;
   if (ctl->status != 0) return;
@@ -87,7 +93,7 @@ __global__ void __launch_bounds__(kSplatThreads) splat_weighted_kernel(const dou
     // z-slab [zoff, zoff+nzl) of this rank (the reference's own slab split, splat.cpp:61-77)
     const int zl = z - zoff;
     if (ox == 0 && y >= 0 && zl >= 0 && y < g.ny && zl < nzl && z < g.nz && fx + 2 >= 0 && fx - 1 < g.nx)
-      mark_chunks(rowbits, zl * g.ny + y, max(fx - 1, 0), min(fx + 2, g.nx - 1));
+      mark_chunks(rowbits, rowlist, zl * g.ny + y, max(fx - 1, 0), min(fx + 2, g.nx - 1));
     if (x < 0 || y < 0 || zl < 0 || x >= g.nx || y >= g.ny || zl >= nzl || z >= g.nz) continue;
     const float dx = (float)(cx - (double)x), dy = (float)(cy - (double)y), dz = (float)(cz - (double)z);
     const float s = dx * dx + dy * dy + dz * dz;
@@ -103,7 +109,8 @@ __global__ void __launch_bounds__(kSplatThreads) splat_weighted_kernel(const dou
 __global__ void __launch_bounds__(256) splat_simple_kernel(const double* __restrict__ pos,
                                                            const double* __restrict__ nrm,
                                                            const DevCtl* __restrict__ ctl, float4* __restrict__ acc,
-                                                           uint32_t* __restrict__ rowbits, int zoff, int nzl) {
+                                                           uint32_t* __restrict__ rowbits,
+                                                           int32_t* __restrict__ rowlist, int zoff, int nzl) {
   const int P = ctl->P;
   if (ctl->status != 0) return;
   const DevGrid g = ctl->grid;
@@ -115,7 +122,7 @@ __global__ void __launch_bounds__(256) splat_simple_kernel(const double* __restr
     if (!(x >= 0 && x < g.nx && y >= 0 && y < g.ny && z >= 0 && z < g.nz)) continue;
     const long long zl = z - zoff;
     if (zl < 0 || zl >= nzl) continue;
-    mark_chunks(rowbits, (int)(zl * g.ny + y), (int)x, (int)x);
+    mark_chunks(rowbits, rowlist, (int)(zl * g.ny + y), (int)x, (int)x);
     red_add_v4(acc + ((size_t)zl * g.ny + y) * g.nx + x,
                make_float4((float)nrm[3 * p + 0], (float)nrm[3 * p + 1], (float)nrm[3 * p + 2], 1.f));
   }
@@ -148,17 +155,17 @@ void launch_clear(float4* acc, size_t n, cudaStream_t st) {
   clear_kernel<<<148 * 8, 256, 0, st>>>(acc, n);
 }
 
-void launch_sparse_clear(float4* acc, uint32_t* rowbits, int rows, int nx, cudaStream_t st) {
-  sparse_clear_kernel<<<148 * 8, 256, 0, st>>>(acc, rowbits, rows, nx);
+void launch_sparse_clear(float4* acc, uint32_t* rowbits, const int32_t* rowlist, int nx, cudaStream_t st) {
+  sparse_clear_kernel<<<148 * 4, 256, 0, st>>>(acc, rowbits, rowlist, nx);
 }
 
-void launch_splat(const DevPoints& pts, const DevCtl* ctl, float4* acc, uint32_t* rowbits, int mode,
+void launch_splat(const DevPoints& pts, DevCtl* ctl, float4* acc, uint32_t* rowbits, int32_t* rowlist, int mode,
                   cudaStream_t st, int zoff, int nzl) {
   if (mode == 0)
-    splat_weighted_kernel<<<148 * 8, kSplatThreads, 0, st>>>(pts.pos, pts.nrm, pts.weight, ctl, acc, rowbits, zoff,
-                                                             nzl);
+    splat_weighted_kernel<<<148 * 8, kSplatThreads, 0, st>>>(pts.pos, pts.nrm, pts.weight, ctl, acc, rowbits,
+                                                             rowlist, zoff, nzl);
   else
-    splat_simple_kernel<<<148 * 4, 256, 0, st>>>(pts.pos, pts.nrm, ctl, acc, rowbits, zoff, nzl);
+    splat_simple_kernel<<<148 * 4, 256, 0, st>>>(pts.pos, pts.nrm, ctl, acc, rowbits, rowlist, zoff, nzl);
 }
 
 void launch_splat_finalize(const float4* acc, size_t n, int mode, int negate, double sigma2, float* field,

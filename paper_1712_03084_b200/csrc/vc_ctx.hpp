@@ -42,8 +42,9 @@ struct vc_ctx {
 
   // grid-dependent
   int nx = 0, ny = 0, nz = 0;
-  Buf acc, spec, A, tw, vbase, blk, rowmm, units, unitcnt, rowbits, planeflag;
+  Buf acc, spec, A, tw, vbase, blk, rowmm, units, unitcnt, rowbits, planeflag, rowlist;
   bool acc_dirty = true;  // accumulator contents unknown: next frame clears densely
+  int layout = 0;         // what acc/rowbits/rowlist hold: 1 whole-grid frame, 2 z-slab frame
   // view staging + clouds
   Buf views, pts_pos, pts_nrm, pts_w, pts_pix, wmaps, pre_scratch, iso_partial;
   int pts_cap = 0;

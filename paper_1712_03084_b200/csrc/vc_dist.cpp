@@ -273,6 +273,7 @@ SlabFft slab_fft(DistRank& rk, const Geo& g, int mode) {
   a.rowmm = P<float2>(ctx->rowmm);
   a.rowbits = P<uint32_t>(ctx->rowbits);
   a.planeflag = P<uint32_t>(ctx->planeflag);
+  a.rowlist = P<int32_t>(ctx->rowlist);
   return a;
 }
 
@@ -284,6 +285,7 @@ vc_status ensure_rank(DistRank& rk, const Geo& g, const vc_sensor* sensors, cons
   const void* acc_before = ctx->acc.p;
   VC_TRY(ensure(ctx, ctx->acc, Nl * sizeof(float4)));
   VC_TRY(ensure(ctx, ctx->rowbits, (size_t)g.ny * g.nzl * sizeof(uint32_t)));
+  VC_TRY(ensure(ctx, ctx->rowlist, ((size_t)g.ny * g.nzl + 1) * sizeof(int32_t)));
   VC_TRY(ensure(ctx, ctx->planeflag, (size_t)g.nz * sizeof(uint32_t) + 256));
   VC_TRY(ensure(ctx, ctx->spec, 3 * g.E * sizeof(float2)));
   VC_TRY(ensure(ctx, rk.sd, 2 * g.E * sizeof(float2)));
@@ -293,7 +295,8 @@ vc_status ensure_rank(DistRank& rk, const Geo& g, const vc_sensor* sensors, cons
   VC_TRY(ensure(ctx, ctx->tw, twiddle_elems(g.nx, g.ny, g.nz) * sizeof(float2)));
   VC_TRY(ensure(ctx, ctx->iso_partial, 1024 * sizeof(double)));
   VC_TRY(ensure(ctx, rk.counts, (size_t)3 * g.P * sizeof(int32_t)));
-  if (ctx->acc.p != acc_before) rk.dirty = true;
+  if (ctx->acc.p != acc_before || ctx->layout != 2) rk.dirty = true;
+  ctx->layout = 2;
   if (rk.dims[0] != g.nx || rk.dims[1] != g.ny || rk.dims[2] != g.nz) {
     upload_twiddles(P<float2>(ctx->tw), g.nx, g.ny, g.nz, ctx->st);
     prepare_integrate(g.nx, g.ny, g.nz);
@@ -343,17 +346,19 @@ vc_status run_dist_frame(vc_dist* d, const Geo& g, const vc_recon_config* c, boo
   mark(0);
   // P1: preprocess + splat + forward x/y
   VC_TRY(each([&](DistRank& rk, vc_ctx* ctx) -> vc_status {
-    launch_preprocess(ctx->ss, points(ctx), P<float>(ctx->wmaps), P<int32_t>(ctx->pre_scratch), ctx->ctl, g.nx, g.ny,
-                      g.nz, c->padding_voxels, c->discontinuity_mm, c->silhouette_radius_px, ctx->st);
     if (rk.dirty) {
       launch_clear(P<float4>(ctx->acc), g.plane * g.nzl, ctx->st);
       VC_CUDA(cudaMemsetAsync(ctx->rowbits.p, 0, (size_t)g.ny * g.nzl * sizeof(uint32_t), ctx->st));
+      VC_CUDA(cudaMemsetAsync(ctx->rowlist.p, 0, sizeof(int32_t), ctx->st));
       rk.dirty = false;
-    } else {
-      launch_sparse_clear(P<float4>(ctx->acc), P<uint32_t>(ctx->rowbits), g.ny * g.nzl, g.nx, ctx->st);
+    } else {  // the previous frame's touched rows (before the preprocess resets the list)
+      launch_sparse_clear(P<float4>(ctx->acc), P<uint32_t>(ctx->rowbits), P<int32_t>(ctx->rowlist), g.nx, ctx->st);
     }
-    launch_splat(points(ctx), ctx->ctl, P<float4>(ctx->acc), P<uint32_t>(ctx->rowbits), c->mode, ctx->st,
-                 rk.rank * g.nzl, g.nzl);
+    launch_preprocess(ctx->ss, points(ctx), P<float>(ctx->wmaps), P<int32_t>(ctx->pre_scratch), ctx->ctl, g.nx, g.ny,
+                      g.nz, c->padding_voxels, c->discontinuity_mm, c->silhouette_radius_px, ctx->st,
+                      P<int32_t>(ctx->rowlist));
+    launch_splat(points(ctx), ctx->ctl, P<float4>(ctx->acc), P<uint32_t>(ctx->rowbits), P<int32_t>(ctx->rowlist),
+                 c->mode, ctx->st, rk.rank * g.nzl, g.nzl);
     return VC_OK;
   }));
   mark(1);

@@ -211,8 +211,11 @@ vc_status ensure_grid(vc_ctx* ctx, int nx, int ny, int nz) {
   const void* acc_before = ctx->acc.p;
   VC_TRY(ensure(ctx, ctx->acc, N * sizeof(float4)));
   VC_TRY(ensure(ctx, ctx->rowbits, (size_t)ny * nz * sizeof(uint32_t)));
+  VC_TRY(ensure(ctx, ctx->rowlist, ((size_t)ny * nz + 1) * sizeof(int32_t)));
   VC_TRY(ensure(ctx, ctx->planeflag, (size_t)nz * sizeof(uint32_t) + 256));
-  if (ctx->acc.p != acc_before || ctx->nx != nx || ctx->ny != ny || ctx->nz != nz) ctx->acc_dirty = true;
+  if (ctx->acc.p != acc_before || ctx->nx != nx || ctx->ny != ny || ctx->nz != nz || ctx->layout != 1)
+    ctx->acc_dirty = true;
+  ctx->layout = 1;
   VC_TRY(ensure(ctx, ctx->spec, 3 * spectrum_elems(nx, ny, nz) * sizeof(float2)));
   VC_TRY(ensure(ctx, ctx->A, N * sizeof(float)));
   VC_TRY(ensure(ctx, ctx->vbase, N * sizeof(uint32_t)));
@@ -260,20 +263,23 @@ void record(vc_ctx* ctx, int i) {
 int enqueue_frame(vc_ctx* ctx, const FrameCfg& f) {
   cudaStream_t st = ctx->st;
   int n = 0;
+  // the clear walks the previous frame's touched-row list: before the
+  // preprocess, whose scan resets the list for this frame's splat
+  record(ctx, 12);
+  launch_sparse_clear(P<float4>(ctx->acc), P<uint32_t>(ctx->rowbits), P<int32_t>(ctx->rowlist), f.nx, st);
+  record(ctx, 13);
   record(ctx, 0);
   launch_preprocess(ctx->ss, points(ctx), P<float>(ctx->wmaps), P<int32_t>(ctx->pre_scratch), ctx->ctl, f.nx, f.ny,
-                    f.nz, f.pad, f.disc, f.sil_r, st);
+                    f.nz, f.pad, f.disc, f.sil_r, st, P<int32_t>(ctx->rowlist));
   n += 6;
   record(ctx, 1);
-  record(ctx, 12);
-  launch_sparse_clear(P<float4>(ctx->acc), P<uint32_t>(ctx->rowbits), f.ny * f.nz, f.nx, st);
-  record(ctx, 13);
-  launch_splat(points(ctx), ctx->ctl, P<float4>(ctx->acc), P<uint32_t>(ctx->rowbits), f.mode, st, 0, f.nz);
+  launch_splat(points(ctx), ctx->ctl, P<float4>(ctx->acc), P<uint32_t>(ctx->rowbits), P<int32_t>(ctx->rowlist),
+               f.mode, st, 0, f.nz);
   n += 2;
   record(ctx, 2);
   launch_integrate(P<float4>(ctx->acc), P<float2>(ctx->spec), P<float>(ctx->A), f.nx, f.ny, f.nz, f.mode,
                    P<float2>(ctx->tw), st, ctx->profiling ? &ctx->ev[14] : nullptr, P<float2>(ctx->rowmm),
-                   P<uint32_t>(ctx->rowbits), P<uint32_t>(ctx->planeflag));
+                   P<uint32_t>(ctx->rowbits), P<uint32_t>(ctx->planeflag), P<int32_t>(ctx->rowlist));
   n += 5;
   record(ctx, 3);
   launch_iso_level(points(ctx), P<float>(ctx->A), ctx->ctl, P<double>(ctx->iso_partial), 1024, st);
@@ -295,6 +301,7 @@ vc_status run_frame(vc_ctx* ctx, const FrameCfg& f) {
   if (ctx->acc_dirty) {  // outside the graph: dense clear once, then sparse clears
     launch_clear(P<float4>(ctx->acc), (size_t)f.nx * f.ny * f.nz, ctx->st);
     VC_CUDA(cudaMemsetAsync(ctx->rowbits.p, 0, (size_t)f.ny * f.nz * sizeof(uint32_t), ctx->st));
+    VC_CUDA(cudaMemsetAsync(ctx->rowlist.p, 0, sizeof(int32_t), ctx->st));  // empty touched-row list
     VC_CUDA(cudaGetLastError());
     ctx->acc_dirty = false;
   }
@@ -491,7 +498,7 @@ int32_t vc_ctx_kernel_times(const vc_ctx* ctx, double* ms, int32_t max_n) {
   if (!ctx || !ms) return 0;
   vc_ctx* c = const_cast<vc_ctx*>(ctx);
   // preprocess, clear, splat, fx, fy, z, iy, ix, iso, mc, texture
-  const int pairs[11][2] = {{0, 1}, {12, 13}, {13, 2}, {14, 15}, {15, 16}, {16, 17}, {17, 18}, {18, 19},
+  const int pairs[11][2] = {{0, 1}, {12, 13}, {1, 2}, {14, 15}, {15, 16}, {16, 17}, {17, 18}, {18, 19},
                             {3, 4}, {4, 5}, {5, 6}};
   int n = 0;
   for (; n < 11 && n < max_n; ++n) ms[n] = ev_ms(c, pairs[n][0], pairs[n][1]);
@@ -700,8 +707,10 @@ vc_status vc_stage_splat(vc_ctx* ctx, const double* pos, const double* nrm, cons
   const size_t N = (size_t)grid->nx * grid->ny * grid->nz;
   VC_TRY(ensure(ctx, ctx->acc, N * sizeof(float4)));
   VC_TRY(ensure(ctx, ctx->rowbits, (size_t)grid->ny * grid->nz * sizeof(uint32_t)));
-  ctx->acc_dirty = true;
+  VC_TRY(ensure(ctx, ctx->rowlist, ((size_t)grid->ny * grid->nz + 1) * sizeof(int32_t)));
+  ctx->acc_dirty = true, ctx->layout = 0;
   VC_CUDA(cudaMemsetAsync(ctx->rowbits.p, 0, (size_t)grid->ny * grid->nz * sizeof(uint32_t), ctx->st));
+  VC_CUDA(cudaMemsetAsync(ctx->rowlist.p, 0, sizeof(int32_t), ctx->st));
   std::vector<double> ones;
   if (!weight) ones.assign(std::max<int64_t>(n, 1), 1.0), weight = ones.data();
   VC_TRY(upload_points(ctx, pos, nrm, weight, n, grid, 1));
@@ -709,7 +718,8 @@ vc_status vc_stage_splat(vc_ctx* ctx, const double* pos, const double* nrm, cons
   VC_TRY(ensure(ctx, fbuf, N * 12));
   VC_TRY(ensure(ctx, dbuf, N * 4));
   launch_clear(P<float4>(ctx->acc), N, ctx->st);
-  launch_splat(points(ctx), ctx->ctl, P<float4>(ctx->acc), P<uint32_t>(ctx->rowbits), mode, ctx->st, 0, grid->nz);
+  launch_splat(points(ctx), ctx->ctl, P<float4>(ctx->acc), P<uint32_t>(ctx->rowbits), P<int32_t>(ctx->rowlist), mode,
+               ctx->st, 0, grid->nz);
   const double sigma2 = std::sqrt(1.5) * (std::sqrt(3.0) / 2.0 * grid->edge_mm);  // splat.cpp:35-36
   launch_splat_finalize(P<float4>(ctx->acc), N, mode, negate, sigma2, P<float>(fbuf), P<float>(dbuf), ctx->st);
   cudaError_t e = cudaGetLastError();
@@ -733,7 +743,7 @@ vc_status vc_stage_integrate(vc_ctx* ctx, const float* field, int32_t nx, int32_
   std::vector<float4> h(N);
   for (size_t i = 0; i < N; ++i) h[i] = make_float4(-field[3 * i], -field[3 * i + 1], -field[3 * i + 2], 1.f);
   VC_CUDA(cudaMemcpyAsync(ctx->acc.p, h.data(), N * sizeof(float4), cudaMemcpyHostToDevice, ctx->st));
-  ctx->acc_dirty = true;  // dense contents from the host
+  ctx->acc_dirty = true, ctx->layout = 0;  // dense contents from the host
   launch_integrate(P<float4>(ctx->acc), P<float2>(ctx->spec), P<float>(ctx->A), nx, ny, nz, 1, P<float2>(ctx->tw),
                    ctx->st, nullptr, nullptr, nullptr, P<uint32_t>(ctx->planeflag));
   VC_CUDA(cudaGetLastError());

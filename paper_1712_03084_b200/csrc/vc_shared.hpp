@@ -96,13 +96,21 @@ inline void record_event(cudaEvent_t e, cudaStream_t s) { cudaEventRecord(e, s);
 size_t preprocess_scratch_bytes(const SensorSet& ss);
 void prepare_preprocess(const SensorSet& ss);  // smem opt-in; call outside graph capture
 void launch_preprocess(const SensorSet& ss, DevPoints pts, float* weight_maps, int32_t* scratch, DevCtl* ctl,
-                       int dims_x, int dims_y, int dims_z, int padding, double disc_mm, int sil_r, cudaStream_t st);
+                       int dims_x, int dims_y, int dims_z, int padding, double disc_mm, int sil_r, cudaStream_t st,
+                       int32_t* rowlist_reset = nullptr /*frame path: zero the touched-row count*/);
 // k_splat.cu
 void launch_clear(float4* acc, size_t n, cudaStream_t st);
-// zoff/nzl: the z-slab [zoff, zoff+nzl) this rank accumulates (whole grid: 0, nz)
-void launch_splat(const DevPoints& pts, const DevCtl* ctl, float4* acc, uint32_t* rowbits, int mode,
+// zoff/nzl: the z-slab [zoff, zoff+nzl) this rank accumulates (whole grid: 0, nz).
+// Every voxel row the splat touches is appended once to the touched-row list
+// rowlist = [count, rows...] (the first marking of the row's chunk mask
+// appends it).  The list lives outside DevCtl: only the frame path's clear,
+// preprocess (reset) and splat touch it, so stage calls cannot desynchronise
+// it from the accumulator.
+void launch_splat(const DevPoints& pts, DevCtl* ctl, float4* acc, uint32_t* rowbits, int32_t* rowlist, int mode,
                   cudaStream_t st, int zoff, int nzl);
-void launch_sparse_clear(float4* acc, uint32_t* rowbits, int rows, int nx, cudaStream_t st);
+// Zero the chunks of the rows the previous frame listed, reset their masks.
+// Runs before the frame's preprocess (which resets the list count).
+void launch_sparse_clear(float4* acc, uint32_t* rowbits, const int32_t* rowlist, int nx, cudaStream_t st);
 void launch_splat_finalize(const float4* acc, size_t n, int mode, int negate, double sigma2, float* field,
                            float* density, cudaStream_t st);
 // k_fft.cu — integrate_fft chain: acc (float4 U,d) -> A
@@ -124,7 +132,8 @@ struct SlabFft {
   cudaStream_t st;
   float2* rowmm;
   const uint32_t* rowbits;
-  uint32_t* planeflag;  // nz entries (global); F-y writes [zoff, zoff+nzl)
+  uint32_t* planeflag;     // nz entries (global); F-y writes [zoff, zoff+nzl)
+  const int32_t* rowlist;  // touched-row list [count, rows...] (F-x works through it), or null: all rows
 };
 void launch_fft_forward_xy(const SlabFft& a);
 void launch_fft_z(const SlabFft& a);
@@ -132,8 +141,9 @@ void launch_fft_inverse_yx(const SlabFft& a);
 void launch_integrate(const float4* acc, float2* spec, float* A, int nx, int ny, int nz, int mode,
                       const float2* twiddles, cudaStream_t st, cudaEvent_t* ev /*nullable, 6 events*/,
                       float2* rowmm /*nullable: per-row min/max of A*/,
-                      const uint32_t* rowbits /*nullable: touched 32-voxel chunks per row; null = dense*/,
-                      uint32_t* planeflag /*nz words: F-y marks planes with any splat contribution*/);
+                      const uint32_t* rowbits /*nullable: touched 32-voxel chunks per row (null = dense)*/,
+                      uint32_t* planeflag /*nz words: F-y marks planes with any splat contribution*/,
+                      const int32_t* rowlist = nullptr /*touched-row list for F-x (null = all rows)*/);
 void upload_twiddles(float2* dev, int nx, int ny, int nz, cudaStream_t st);
 void prepare_integrate(int nx, int ny, int nz);
 size_t twiddle_elems(int nx, int ny, int nz);

@@ -301,6 +301,27 @@ def test_six_views_and_single_view(O, ctx):
     assert rel_l2(rec1.volume.values, ref1.volume) < REL_L2_A
 
 
+def test_accumulator_state_survives_stage_calls(scene, ctx):
+    """The frame path's sparse clear walks the previous frame's touched-row
+    list: stage calls, other bodies and other view counts in between must not
+    leave stale accumulator contents (field equal to a fresh context's)."""
+    rig, _, frames, _ = scene
+    cfg = vc.ReconConfig(dims=(128, 128, 128))
+    fresh = vc.Context(0)
+    ref = vc.reconstruct_frame(frames, rig, cfg, ctx=fresh, want_volume=True).volume.values
+    kick = [vc.render_frame(rig, vc.kick_body(300, 60), k) for k in range(4)]
+    vc.reconstruct_frame(kick, rig, cfg, ctx=ctx)
+    vc.preprocess(frames, rig, cfg, ctx=ctx)  # stage call: resets the control block, not the accumulator
+    a = vc.reconstruct_frame(frames, rig, cfg, ctx=ctx, want_volume=True).volume.values
+    assert rel_l2(a, ref) < 1e-5
+    rig6 = vc.make_circle_rig(6, 0, 2500, 512, 424, 365)
+    f6 = [vc.render_frame(rig6, vc.kick_body(300, 200), k) for k in range(6)]
+    vc.reconstruct_frame(f6, rig6, cfg, ctx=ctx)
+    b = vc.reconstruct_frame(frames, rig, cfg, ctx=ctx, want_volume=True).volume.values
+    assert rel_l2(b, ref) < 1e-5
+    fresh.close()
+
+
 def test_repeatability_and_graph_replay(scene, ctx):
     rig, _, frames, _ = scene
     cfg = vc.ReconConfig(dims=(128, 128, 128))
