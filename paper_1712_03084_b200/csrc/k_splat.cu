@@ -67,7 +67,7 @@ __device__ __forceinline__ void red_add_v4(float4* addr, float4 v) {
                : "memory");
 }
 
-// splat.cpp:58-87 weighted mode: 64 threads per point, one per support voxel
+// splat.cpp:58-87 weighted mode: 64 threads (two warps) per point, one per support voxel
 // floor(c)-1 .. floor(c)+2 per axis (support_around, splat.cpp:19-29).
 __global__ void __launch_bounds__(kSplatThreads) splat_weighted_kernel(const double* __restrict__ pos,
                                                                        const double* __restrict__ nrm,
@@ -85,9 +85,16 @@ __global__ void __launch_bounds__(kSplatThreads) splat_weighted_kernel(const dou
   // exp(-s/0.75) = exp2(s * k1), exp(-s/1.125) = exp2(s * k2)
   const float k1 = -1.4426950408889634f / 0.75f, k2 = -1.4426950408889634f / 1.125f;
   for (int p = blockIdx.x * (kSplatThreads / 64) + (threadIdx.x >> 6); p < P; p += gridDim.x * (kSplatThreads / 64)) {
-    const double cx = ddiv(dsub(__ldg(pos + 3 * p + 0), g.origin[0]), g.edge);
-    const double cy = ddiv(dsub(__ldg(pos + 3 * p + 1), g.origin[1]), g.edge);
-    const double cz = ddiv(dsub(__ldg(pos + 3 * p + 2), g.origin[2]), g.edge);
+    // to_voxel (volume.hpp:44) once per warp: lanes 0-2 divide one coordinate
+    // each (IEEE fp64, bit-exact), the warp shares them by shuffle
+    const int lane = threadIdx.x & 31;
+    double c = 0.0;
+    if (lane < 3) {
+      const double o = lane == 0 ? g.origin[0] : (lane == 1 ? g.origin[1] : g.origin[2]);
+      c = ddiv(dsub(__ldg(pos + 3 * p + lane), o), g.edge);
+    }
+    const double cx = __shfl_sync(0xffffffffu, c, 0), cy = __shfl_sync(0xffffffffu, c, 1),
+                 cz = __shfl_sync(0xffffffffu, c, 2);
     const int fx = (int)floor(cx);
     const int x = fx - 1 + ox, y = (int)floor(cy) - 1 + oy, z = (int)floor(cz) - 1 + oz;
     // z-slab [zoff, zoff+nzl) of this rank (the reference's own slab split, splat.cpp:61-77)
