@@ -300,21 +300,36 @@ __global__ void __launch_bounds__(256) mc_count_kernel(const float* __restrict__
   }
 }
 
+// Single CTA: exclusive scan of the per-unit (V, T, C) counts, contiguous
+// runs per thread; when they fit, the runs are staged through shared memory
+// so the global loads/stores are coalesced (a single SM otherwise issues one
+// L2 transaction per thread per element).
+constexpr int kScanStage = 12288;  // int3 entries staged (144 KB, opt-in)
+
 __global__ void __launch_bounds__(1024) mc_scan_kernel(int3* blk, const DevCtl* ctl_in, DevCtl* ctl, int v_cap,
                                                        int t_cap, int c_cap) {
   __shared__ int3 wsum[32];
+  extern __shared__ int3 sstage[];
   const int n = ctl_in->status == 0 ? ctl_in->units : 0;
+  const bool staged = n <= kScanStage;
+  if (staged) {
+    int* si = reinterpret_cast<int*>(sstage);
+    const int* gi = reinterpret_cast<const int*>(blk);
+    for (int i = threadIdx.x; i < 3 * n; i += 1024) si[i] = gi[i];
+    __syncthreads();
+  }
+  int3* buf = staged ? sstage : blk;
   const int per = (n + 1023) / 1024;
   const int b0 = min(n, (int)threadIdx.x * per), b1 = min(n, b0 + per);
   int3 vals[16];
   int3 tot = make_int3(0, 0, 0);
 #pragma unroll
   for (int i = 0; i < 16; ++i) {
-    vals[i] = b0 + i < b1 ? blk[b0 + i] : make_int3(0, 0, 0);
+    vals[i] = b0 + i < b1 ? buf[b0 + i] : make_int3(0, 0, 0);
     tot.x += vals[i].x, tot.y += vals[i].y, tot.z += vals[i].z;
   }
   for (int i = b0 + 16; i < b1; ++i) {
-    const int3 v = blk[i];
+    const int3 v = buf[i];
     tot.x += v.x, tot.y += v.y, tot.z += v.z;
   }
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -341,13 +356,19 @@ __global__ void __launch_bounds__(1024) mc_scan_kernel(int3* blk, const DevCtl* 
 #pragma unroll
   for (int i = 0; i < 16; ++i)
     if (b0 + i < b1) {
-      blk[b0 + i] = run;
+      buf[b0 + i] = run;
       run.x += vals[i].x, run.y += vals[i].y, run.z += vals[i].z;
     }
   for (int i = b0 + 16; i < b1; ++i) {
-    const int3 v = blk[i];
-    blk[i] = run;
+    const int3 v = buf[i];
+    buf[i] = run;
     run.x += v.x, run.y += v.y, run.z += v.z;
+  }
+  if (staged) {
+    __syncthreads();
+    int* gi = reinterpret_cast<int*>(blk);
+    const int* si = reinterpret_cast<const int*>(sstage);
+    for (int i = threadIdx.x; i < 3 * n; i += 1024) gi[i] = si[i];
   }
   if (threadIdx.x == 1023) {
     const int3 t = wsum[31];
@@ -514,6 +535,7 @@ void launch_mc_set_voff(const int32_t* counts, int rank, DevCtl* ctl, cudaStream
 }
 
 void upload_case_table_data(const int8_t* counts, const int8_t* tris, cudaStream_t st) {
+  cudaFuncSetAttribute(mc_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kScanStage * sizeof(int3)));
   cudaMemcpyToSymbolAsync(c_mc_count, counts, 256, 0, cudaMemcpyHostToDevice, st);
   cudaMemcpyToSymbolAsync(c_mc_tris, tris, 256 * 15, 0, cudaMemcpyHostToDevice, st);
   const int8_t c0[12] = {0, 2, 4, 6, 0, 1, 4, 5, 0, 1, 2, 3};  // marching_cubes.cpp:15-19
@@ -553,7 +575,7 @@ void launch_marching_cubes_count(const float* A, DevCtl* ctl, MeshBufs mb, int n
   mc_rows_kernel<<<nblk, kRowThreads, 0, st>>>(mb.rowmm, ctl, ny, nz, sl, rowmask);
   mc_units_kernel<<<1, 1024, 0, st>>>(rowmask, (units + 31) / 32, mb.units, ctl);
   mc_count_kernel<<<148 * 8, mc_threads(nx), 0, st>>>(A, ctl, nx, ny, nz, sl, mb.units, ucnt);
-  mc_scan_kernel<<<1, 1024, 0, st>>>(ucnt, ctl, ctl, mb.v_cap, mb.t_cap, mb.c_cap);
+  mc_scan_kernel<<<1, 1024, kScanStage * sizeof(int3), st>>>(ucnt, ctl, ctl, mb.v_cap, mb.t_cap, mb.c_cap);
 }
 
 void launch_marching_cubes_emit(const float* A, DevCtl* ctl, MeshBufs mb, int nx, int ny, int nz, McSlab sl,

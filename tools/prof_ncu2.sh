@@ -1,5 +1,5 @@
 # ncu launch list + full capture of the listed kernels for one bench frame set
-CMD="python bench.py --steps 5 --warmup 3 --no-cpu-baseline"
+CMD="python bench.py --steps 5 --warmup 3 --no-cpu-baseline --streams 1"
 $CMD > gpurun_out/prof_plain.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"${LIST_RE:-fx_kernel|fy_kernel|z_kernel|iy_kernel|ix_kernel|mc_|pre_|splat|clear_kernel|iso_|texture_kernel|mesh_f32}" -s 50 -c 75 --csv --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu_launch.log 2>&1 && \
 ncu --set full --clock-control none --import-source on -k regex:"${FULL_RE}" -s ${FULL_SKIP:-20} -c ${FULL_COUNT:-8} -o gpurun_out/prof_full $CMD > gpurun_out/ncu_full.log 2>&1
