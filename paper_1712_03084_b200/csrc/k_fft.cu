@@ -186,6 +186,13 @@ struct CCfg {
   static constexpr int SMEM = N * CW * 8;  // one staged tile (= exchange buffer)
 };
 
+// Pass outputs are read by the next pass right away: plain (L2-allocating)
+// stores, so what fits in the 126 MB L2 is not re-read from HBM.
+template <class T>
+__device__ __forceinline__ void st_out(T* p, T v) {
+  *p = v;
+}
+
 // Predicated streaming load (no branch): zero when !pred.
 __device__ __forceinline__ float4 ld_pred_cs(const float4* p, bool pred) {
   float4 r = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -270,8 +277,8 @@ __global__ void __launch_bounds__(XCfg<NX>::THREADS, 2) fx_kernel(const float4* 
           A.x *= wx, A.y *= wx;
         }
         if (live) {
-          __stcs(outA + offA + k, A);
-          __stcs(outB + offB + k, B);
+          st_out(outA + offA + k, A);
+          st_out(outB + offB + k, B);
         }
       }
     }
@@ -288,8 +295,8 @@ __global__ void __launch_bounds__(XCfg<NX>::THREADS, 2) fx_kernel(const float4* 
       const float2 d = v[k1];
       const int k = t + T * k1;
       if (k1 < R1 / 2 || t == 0) {
-        if (stA) __stcs(S2 + offA + k, make_float2(0.5f * (d.x + e.x), 0.5f * (d.y - e.y)));
-        if (stB) __stcs(S2 + offB + k, make_float2(0.5f * (d.y + e.y), -0.5f * (d.x - e.x)));
+        if (stA) st_out(S2 + offA + k, make_float2(0.5f * (d.x + e.x), 0.5f * (d.y - e.y)));
+        if (stB) st_out(S2 + offB + k, make_float2(0.5f * (d.y + e.y), -0.5f * (d.x - e.x)));
       }
     }
   };
@@ -470,8 +477,8 @@ __global__ void __launch_bounds__(CCfg<NY>::THREADS, NY >= 1024 ? 1 : 2) fy_kern
     for (int k1 = 0; k1 < R1; ++k1) {
       const int ky = t + T * k1;
       const size_t o = ((size_t)((ky >> lk) * nzl + blockIdx.y) * kyl + (ky & (kyl - 1))) * H + kx;
-      __stcs(O0 + o, d[k1]);
-      __stcs(O1 + o, v[k1]);
+      st_out(O0 + o, d[k1]);
+      st_out(O1 + o, v[k1]);
     }
   }
 }
@@ -547,7 +554,7 @@ __device__ __forceinline__ void z_body(float2* __restrict__ S0, const float2* __
   if (live) {
     const size_t base = (size_t)kyr * H + kx;
 #pragma unroll
-    for (int k1 = 0; k1 < R1; ++k1) __stcs(S0 + base + (size_t)(t + T * k1) * zstride, v[k1]);
+    for (int k1 = 0; k1 < R1; ++k1) st_out(S0 + base + (size_t)(t + T * k1) * zstride, v[k1]);
   }
 }
 
@@ -595,7 +602,7 @@ __device__ __forceinline__ void iy_body(const float2* Rin, float2* Rout, int nxh
   if (live) {
     const size_t plane = (size_t)zl * NY * H;
 #pragma unroll
-    for (int k1 = 0; k1 < R1; ++k1) __stcs(Rout + plane + (size_t)(t + T * k1) * H + kx, v[k1]);
+    for (int k1 = 0; k1 < R1; ++k1) st_out(Rout + plane + (size_t)(t + T * k1) * H + kx, v[k1]);
   }
 }
 
@@ -688,8 +695,8 @@ __global__ void __launch_bounds__(IXCfg<NX>::THREADS, 2) ix_kernel(const float2*
       const int k = t + T * k1;
       const float a0 = v[k1].x * scale, a1 = v[k1].y * scale;
       lo0 = fminf(lo0, a0), hi0 = fmaxf(hi0, a0), lo1 = fminf(lo1, a1), hi1 = fmaxf(hi1, a1);
-      __stcs(A + (size_t)l0 * NX + k, a0);
-      __stcs(A + (size_t)l1 * NX + k, a1);
+      st_out(A + (size_t)l0 * NX + k, a0);
+      st_out(A + (size_t)l1 * NX + k, a1);
     }
     // per-row min/max for marching-cubes row culling
 #pragma unroll
