@@ -160,10 +160,6 @@ __device__ __forceinline__ VoxelInfo classify(const float* A, int nx, int ny, in
   }
   return r;
 }
-__device__ __forceinline__ VoxelInfo classify(const float* A, int nx, int ny, int nz, size_t v, float Lf) {
-  const int x = (int)(v % nx), y = (int)((v / nx) % ny), z = (int)(v / ((size_t)nx * ny));
-  return classify(A, nx, ny, nz, x, y, z, v, Lf);
-}
 
 __device__ __forceinline__ int3 block_exclusive_scan3(int3 v, int3* total) {
   __shared__ int3 warp_tot[kMcThreads / 32];
@@ -277,7 +273,7 @@ __device__ __forceinline__ int3 block_reduce3(int3 v) {
 // per active unit: (owned cut edges, triangles, non-trivial cells)
 __global__ void __launch_bounds__(256) mc_count_kernel(const float* __restrict__ A, DevCtl* ctl, int nx, int ny,
                                                        int nz, McSlab sl, const int32_t* __restrict__ units,
-                                                       int3* unitcnt) {
+                                                       int3* unitcnt, MeshBufs mb) {
   if (ctl->status != 0) return;
   const int U = ctl->units;
   const float Lf = __double2float_ru(ctl->level);
@@ -291,6 +287,8 @@ __global__ void __launch_bounds__(256) mc_count_kernel(const float* __restrict__
       const VoxelInfo vi = classify(A, nx, ny, nz, x, y, z, row0 + x, Lf);
       const int nt = vi.cfg >= 0 && own ? c_mc_count[vi.cfg] : 0;
       c.x += __popc(vi.mask), c.y += nt, c.z += nt > 0 ? 1 : 0;
+      // the emit pass reads this instead of classifying again
+      mb.vinfo[(size_t)i * nx + x] = (uint16_t)(vi.mask | (nt > 0 ? (vi.cfg << 3) | (1 << 11) : 0));
     }
     const int3 t = block_reduce3(c);
     if (threadIdx.x == 0) {
@@ -397,7 +395,10 @@ __global__ void __launch_bounds__(256) mc_emit_kernel(const float* __restrict__ 
     for (int x0 = 0; x0 < nx; x0 += blockDim.x) {
       const int x = x0 + threadIdx.x;
       VoxelInfo vi{0, -1};
-      if (x < nx) vi = classify(A, nx, ny, nz, x, y, z, row0 + x, Lf);
+      if (x < nx) {
+        const unsigned in = mb.vinfo[(size_t)i * nx + x];
+        vi.mask = (int)(in & 7u), vi.cfg = (in >> 11) & 1u ? (int)((in >> 3) & 255u) : -1;
+      }
       const int nt = vi.cfg >= 0 ? c_mc_count[vi.cfg] : 0;
       int3 tot;
       const int3 ex = block_exclusive_scan3(make_int3(__popc(vi.mask), nt, nt > 0 ? 1 : 0), &tot);
@@ -422,6 +423,7 @@ __global__ void __launch_bounds__(256) mc_emit_kernel(const float* __restrict__ 
       if (nt > 0) {
         mb.cells[cb] = (int32_t)v;
         mb.cell_tri[cb] = tb;
+        mb.cell_cfg[cb] = (uint8_t)vi.cfg;
       }
       carry = make_int3(carry.x + tot.x, carry.y + tot.y, carry.z + tot.z);
     }
@@ -494,7 +496,8 @@ __global__ void __launch_bounds__(256) mc_tris_kernel(const float* __restrict__ 
   for (int i = blockIdx.x * 256 + threadIdx.x; i < C; i += gridDim.x * 256) {
     const size_t v = (size_t)mb.cells[i];
     const int tb = mb.cell_tri[i];
-    const VoxelInfo vi = classify(A, nx, ny, nz, v, Lf);
+    VoxelInfo vi;
+    vi.cfg = mb.cell_cfg[i];
     const int n = c_mc_count[vi.cfg];
     for (int tri = 0; tri < n; ++tri) {
       int ids[3];
@@ -574,7 +577,7 @@ void launch_marching_cubes_count(const float* A, DevCtl* ctl, MeshBufs mb, int n
   int3* ucnt = reinterpret_cast<int3*>(mb.unitcnt);
   mc_rows_kernel<<<nblk, kRowThreads, 0, st>>>(mb.rowmm, ctl, ny, nz, sl, rowmask);
   mc_units_kernel<<<1, 1024, 0, st>>>(rowmask, (units + 31) / 32, mb.units, ctl);
-  mc_count_kernel<<<148 * 8, mc_threads(nx), 0, st>>>(A, ctl, nx, ny, nz, sl, mb.units, ucnt);
+  mc_count_kernel<<<148 * 8, mc_threads(nx), 0, st>>>(A, ctl, nx, ny, nz, sl, mb.units, ucnt, mb);
   mc_scan_kernel<<<1, 1024, kScanStage * sizeof(int3), st>>>(ucnt, ctl, ctl, mb.v_cap, mb.t_cap, mb.c_cap);
 }
 

@@ -42,7 +42,7 @@ struct vc_ctx {
 
   // grid-dependent
   int nx = 0, ny = 0, nz = 0;
-  Buf acc, spec, A, tw, vbase, blk, rowmm, units, unitcnt, rowbits, planeflag, rowlist;
+  Buf acc, spec, A, tw, vbase, blk, rowmm, units, unitcnt, rowbits, planeflag, rowlist, vinfo;
   bool acc_dirty = true;  // accumulator contents unknown: next frame clears densely
   int layout = 0;         // what acc/rowbits/rowlist hold: 1 whole-grid frame, 2 z-slab frame
   // view staging + clouds
@@ -53,7 +53,7 @@ struct vc_ctx {
   vc::DevCtl* ctl = nullptr;
   vc::DevCtl* ctl_h = nullptr;
   // mesh + texture
-  Buf m_pos, m_nrm, m_tri, m_eid, m_cells, m_celltri, m_posf, t_vis, t_uv, t_w, t_untex, t_rgb;
+  Buf m_pos, m_nrm, m_tri, m_eid, m_cells, m_celltri, m_cellcfg, m_posf, t_vis, t_uv, t_w, t_untex, t_rgb;
   int v_cap = 0, t_cap = 0, c_cap = 0;
   // host outputs (pinned)
   HostBuf h_posf, h_nrm, h_tri, h_vis, h_uv, h_w, h_untex, h_rgb, h_pos, h_eid;

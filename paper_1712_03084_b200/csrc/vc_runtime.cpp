@@ -187,6 +187,7 @@ vc_status ensure_mesh_caps(vc_ctx* ctx, int v_cap, int k) {
   VC_TRY(ensure(ctx, ctx->m_tri, (size_t)t_cap * 3 * sizeof(int32_t)));
   VC_TRY(ensure(ctx, ctx->m_cells, (size_t)c_cap * sizeof(int32_t)));
   VC_TRY(ensure(ctx, ctx->m_celltri, (size_t)c_cap * sizeof(int32_t)));
+  VC_TRY(ensure(ctx, ctx->m_cellcfg, (size_t)c_cap));
   VC_TRY(ensure(ctx, ctx->t_vis, (size_t)v_cap * k));
   VC_TRY(ensure(ctx, ctx->t_uv, (size_t)v_cap * k * sizeof(float2)));
   VC_TRY(ensure(ctx, ctx->t_w, (size_t)v_cap * k * sizeof(float)));
@@ -203,6 +204,7 @@ vc_status ensure_mc_scratch(vc_ctx* ctx, int nx, int ny, int nz) {
   VC_TRY(ensure(ctx, ctx->rowmm, rows * sizeof(float2)));
   VC_TRY(ensure(ctx, ctx->units, rows * sizeof(int32_t)));
   VC_TRY(ensure(ctx, ctx->unitcnt, rows * 3 * sizeof(int32_t)));
+  VC_TRY(ensure(ctx, ctx->vinfo, rows * (size_t)nx * sizeof(uint16_t)));
   return VC_OK;
 }
 
@@ -244,6 +246,8 @@ MeshBufs mesh_bufs(vc_ctx* ctx) {
   mb.vbase = P<uint32_t>(ctx->vbase);
   mb.cells = P<int32_t>(ctx->m_cells);
   mb.cell_tri = P<int32_t>(ctx->m_celltri);
+  mb.cell_cfg = P<uint8_t>(ctx->m_cellcfg);
+  mb.vinfo = P<uint16_t>(ctx->vinfo);
   mb.v_cap = ctx->v_cap, mb.t_cap = ctx->t_cap, mb.c_cap = ctx->c_cap;
   mb.blk = P<int32_t>(ctx->blk);
   mb.nblk = 0;
@@ -457,9 +461,9 @@ vc_status vc_ctx_destroy(vc_ctx* ctx) {
   cudaSetDevice(ctx->device);
   if (ctx->st) cudaStreamSynchronize(ctx->st);
   if (ctx->gexec) cudaGraphExecDestroy(ctx->gexec);
-  for (Buf* b : {&ctx->acc, &ctx->spec, &ctx->A, &ctx->tw, &ctx->vbase, &ctx->blk, &ctx->rowmm, &ctx->units, &ctx->unitcnt, &ctx->rowbits, &ctx->planeflag, &ctx->views, &ctx->pts_pos,
+  for (Buf* b : {&ctx->acc, &ctx->spec, &ctx->A, &ctx->tw, &ctx->vbase, &ctx->blk, &ctx->rowmm, &ctx->units, &ctx->unitcnt, &ctx->rowbits, &ctx->planeflag, &ctx->rowlist, &ctx->vinfo, &ctx->views, &ctx->pts_pos,
                  &ctx->pts_nrm, &ctx->pts_w, &ctx->pts_pix, &ctx->wmaps, &ctx->pre_scratch, &ctx->iso_partial,
-                 &ctx->m_pos, &ctx->m_nrm, &ctx->m_tri, &ctx->m_eid, &ctx->m_cells, &ctx->m_celltri, &ctx->m_posf,
+                 &ctx->m_pos, &ctx->m_nrm, &ctx->m_tri, &ctx->m_eid, &ctx->m_cells, &ctx->m_celltri, &ctx->m_cellcfg, &ctx->m_posf,
                  &ctx->t_vis, &ctx->t_uv, &ctx->t_w, &ctx->t_untex, &ctx->t_rgb})
     if (b->p) cudaFree(b->p);
   for (HostBuf* b : {&ctx->h_posf, &ctx->h_nrm, &ctx->h_tri, &ctx->h_vis, &ctx->h_uv, &ctx->h_w, &ctx->h_untex,

@@ -79,6 +79,8 @@ struct MeshBufs {
   uint32_t* vbase;   // N (sparse): first vertex id * 8 | cut mask
   int32_t* cells;    // C: active cell linear index
   int32_t* cell_tri; // C: first triangle id
+  uint8_t* cell_cfg; // C: cube case
+  uint16_t* vinfo;   // per voxel of the active units (unit slot * nx + x): cut mask | case << 3 | has-cell << 11
   int32_t v_cap, t_cap, c_cap;
   int32_t* blk;      // row-culling scratch (mc_blocks ints)
   int32_t nblk;
