@@ -7,13 +7,14 @@
 //
 //   mc_rows     per voxel row (y,z): can it hold a cut edge or cell?  (row
 //               min/max from the last FFT pass vs the level) -> ordered list
-//   mc_count    one CTA per active row, one thread per voxel: owned cut edges
+//   mc_count    one warp per active row, 8 voxels per lane: owned cut edges
 //               (+x,+y,+z, sign test vals >= level in fp64, :168-171) and the
-//               cell's triangle count from the generated table
+//               cell's triangle count from the generated table; caches each
+//               voxel's (mask, case)
 //   mc_scan     single-CTA exclusive scan of the per-row totals
-//   mc_emit     recompute; vertex ids = rank of the cut edge in global edge id
-//               order ((z*ny+y)*nx+x)*3+axis (:139-142); fp64 positions
-//               (:153-155, volume.hpp:45); compact list of active cells
+//   mc_emit     one warp per active row; vertex ids = rank of the cut edge in
+//               global edge id order ((z*ny+y)*nx+x)*3+axis (:139-142); fp64
+//               positions (:153-155, volume.hpp:45); compact list of cells
 //   mc_normals  one thread per vertex: gradient normals (:180-207)
 //   mc_tris     one thread per active cell: triangles in the reference's cell
 //               scan order (z, y, x), table order within the cell
@@ -29,7 +30,6 @@ __constant__ int8_t c_mc_tris[256][5][3];
 __constant__ int8_t c_edge_c0[12];  // low corner of each cube edge
 __constant__ int8_t c_edge_axis[12];
 
-constexpr int kMcThreads = 256;
 
 __device__ __forceinline__ float vol_at(const float* A, int nx, int ny, int x, int y, int z) {
   return __ldg(A + ((size_t)z * ny + y) * nx + x);
@@ -134,53 +134,10 @@ struct VoxelInfo {
   int cfg;   // cell case, -1 if no cell
 };
 
-// Cut-edge mask and cell case of voxel (x, y, z) (linear index v).  The
+// classify_regs below: cut-edge mask and cell case of a voxel.  The
 // reference tests vals >= level in fp64 (marching_cubes.cpp:168-171); for an
 // fp32 value a and double L that equals a >= Lf with Lf = L rounded up to fp32
 // (__double2float_ru), so the test runs in fp32 bit-exactly.
-__device__ __forceinline__ VoxelInfo classify(const float* A, int nx, int ny, int nz, int x, int y, int z, size_t v,
-                                              float Lf) {
-  const size_t plane = (size_t)nx * ny;
-  const bool a0 = __ldg(A + v) >= Lf;
-  VoxelInfo r{0, -1};
-  const bool hx = x + 1 < nx, hy = y + 1 < ny, hz = z + 1 < nz;
-  const bool a1 = hx && __ldg(A + v + 1) >= Lf;
-  const bool a2 = hy && __ldg(A + v + nx) >= Lf;
-  const bool a4 = hz && __ldg(A + v + plane) >= Lf;
-  if (hx && a1 != a0) r.mask |= 1;
-  if (hy && a2 != a0) r.mask |= 2;
-  if (hz && a4 != a0) r.mask |= 4;
-  if (hx && hy && hz) {
-    int cfg = (a0 ? 1 : 0) | (a1 ? 2 : 0) | (a2 ? 4 : 0) | (a4 ? 16 : 0);
-    cfg |= (__ldg(A + v + nx + 1) >= Lf) << 3;
-    cfg |= (__ldg(A + v + plane + 1) >= Lf) << 5;
-    cfg |= (__ldg(A + v + plane + nx) >= Lf) << 6;
-    cfg |= (__ldg(A + v + plane + nx + 1) >= Lf) << 7;
-    r.cfg = cfg;
-  }
-  return r;
-}
-
-__device__ __forceinline__ int3 block_exclusive_scan3(int3 v, int3* total) {
-  __shared__ int3 warp_tot[kMcThreads / 32];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  int3 inc = v;
-  for (int o = 1; o < 32; o <<= 1) {
-    const int a = __shfl_up_sync(0xffffffffu, inc.x, o), b = __shfl_up_sync(0xffffffffu, inc.y, o),
-              c = __shfl_up_sync(0xffffffffu, inc.z, o);
-    if (lane >= o) inc.x += a, inc.y += b, inc.z += c;
-  }
-  if (lane == 31) warp_tot[wid] = inc;
-  __syncthreads();
-  int3 pre = make_int3(0, 0, 0), tot = make_int3(0, 0, 0);
-  for (int i = 0; i < nw; ++i) {
-    if (i < wid) pre.x += warp_tot[i].x, pre.y += warp_tot[i].y, pre.z += warp_tot[i].z;
-    tot.x += warp_tot[i].x, tot.y += warp_tot[i].y, tot.z += warp_tot[i].z;
-  }
-  __syncthreads();
-  *total = tot;
-  return make_int3(pre.x + inc.x - v.x, pre.y + inc.y - v.y, pre.z + inc.z - v.z);
-}
 
 // ---------------------------------------------------------------- row culling
 // Work unit = voxel row (y, z): its x-edges, the y-edges to row y+1, the
@@ -257,41 +214,105 @@ __global__ void __launch_bounds__(1024) mc_units_kernel(const uint32_t* __restri
   if (threadIdx.x == 1023) ctl->units = wsum[31], ctl->v_extra = 0;
 }
 
-__device__ __forceinline__ int3 block_reduce3(int3 v) {
-  __shared__ int3 wsum[32];
+// One warp per active unit (voxel row), 8 consecutive voxels per lane per
+// 256-voxel pass: the lane loads the 9 values x0..x0+8 of the 4 rows its
+// voxels touch (two float4 + one scalar per row) and classifies all 8 from
+// registers; no block-wide barrier anywhere.
+constexpr int kVpl = 8;
+
+struct RowVals {
+  float v[4][kVpl + 1];  // rows (y,z), (y+1,z), (y,z+1), (y+1,z+1); x0 .. x0+8
+};
+
+__device__ __forceinline__ void load_rows(const float* A, int nx, int ny, int nz, int y, int z, int x0, RowVals& r) {
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int yy = y + (q & 1), zz = z + (q >> 1);
+    const bool ok = yy < ny && zz < nz && x0 < nx;
+    const float* row = A + ((size_t)zz * ny + yy) * nx;
+    if (ok && nx >= kVpl) {
+      const float4 a = __ldg(reinterpret_cast<const float4*>(row + x0));
+      const float4 b = __ldg(reinterpret_cast<const float4*>(row + x0 + 4));
+      r.v[q][0] = a.x, r.v[q][1] = a.y, r.v[q][2] = a.z, r.v[q][3] = a.w;
+      r.v[q][4] = b.x, r.v[q][5] = b.y, r.v[q][6] = b.z, r.v[q][7] = b.w;
+      r.v[q][kVpl] = x0 + kVpl < nx ? __ldg(row + x0 + kVpl) : 0.f;
+    } else {
+#pragma unroll
+      for (int j = 0; j <= kVpl; ++j) r.v[q][j] = ok && x0 + j < nx ? __ldg(row + x0 + j) : 0.f;
+    }
+  }
+}
+
+// classify() on the lane's registers: voxel x0 + j
+__device__ __forceinline__ VoxelInfo classify_regs(const RowVals& r, int j, int x, int nx, bool hy, bool hz, float Lf) {
+  VoxelInfo o{0, -1};
+  if (x >= nx) return o;
+  const bool hx = x + 1 < nx;
+  const bool a0 = r.v[0][j] >= Lf;
+  const bool a1 = hx && r.v[0][j + 1] >= Lf;
+  const bool a2 = hy && r.v[1][j] >= Lf;
+  const bool a4 = hz && r.v[2][j] >= Lf;
+  if (hx && a1 != a0) o.mask |= 1;
+  if (hy && a2 != a0) o.mask |= 2;
+  if (hz && a4 != a0) o.mask |= 4;
+  if (hx && hy && hz) {
+    int cfg = (a0 ? 1 : 0) | (a1 ? 2 : 0) | (a2 ? 4 : 0) | (a4 ? 16 : 0);
+    cfg |= (r.v[1][j + 1] >= Lf) << 3;
+    cfg |= (r.v[2][j + 1] >= Lf) << 5;
+    cfg |= (r.v[3][j] >= Lf) << 6;
+    cfg |= (r.v[3][j + 1] >= Lf) << 7;
+    o.cfg = cfg;
+  }
+  return o;
+}
+
+__device__ __forceinline__ int3 warp_sum3(int3 v) {
   for (int o = 16; o > 0; o >>= 1)
     v.x += __shfl_xor_sync(0xffffffffu, v.x, o), v.y += __shfl_xor_sync(0xffffffffu, v.y, o),
         v.z += __shfl_xor_sync(0xffffffffu, v.z, o);
-  if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = v;
-  __syncthreads();
-  int3 t = make_int3(0, 0, 0);
-  for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t.x += wsum[i].x, t.y += wsum[i].y, t.z += wsum[i].z;
-  __syncthreads();
-  return t;
+  return v;
 }
 
-// per active unit: (owned cut edges, triangles, non-trivial cells)
+// per active unit: (owned cut edges, triangles, non-trivial cells) + the
+// per-voxel (mask, case) cache the emit pass reads
 __global__ void __launch_bounds__(256) mc_count_kernel(const float* __restrict__ A, DevCtl* ctl, int nx, int ny,
                                                        int nz, McSlab sl, const int32_t* __restrict__ units,
                                                        int3* unitcnt, MeshBufs mb) {
   if (ctl->status != 0) return;
   const int U = ctl->units;
   const float Lf = __double2float_ru(ctl->level);
-  for (int i = blockIdx.x; i < U; i += gridDim.x) {
+  const int lane = threadIdx.x & 31;
+  const int warps = gridDim.x * (blockDim.x >> 5);
+  for (int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i < U; i += warps) {
     const int u = units[i];
     const int y = u % ny, z = sl.z0 + u / ny;
     const bool own = z < sl.zend;
-    const size_t row0 = ((size_t)z * ny + y) * nx;
+    const bool hy = y + 1 < ny, hz = z + 1 < nz;
     int3 c = make_int3(0, 0, 0);
-    for (int x = threadIdx.x; x < nx; x += blockDim.x) {
-      const VoxelInfo vi = classify(A, nx, ny, nz, x, y, z, row0 + x, Lf);
-      const int nt = vi.cfg >= 0 && own ? c_mc_count[vi.cfg] : 0;
-      c.x += __popc(vi.mask), c.y += nt, c.z += nt > 0 ? 1 : 0;
-      // the emit pass reads this instead of classifying again
-      mb.vinfo[(size_t)i * nx + x] = (uint16_t)(vi.mask | (nt > 0 ? (vi.cfg << 3) | (1 << 11) : 0));
+    for (int p0 = 0; p0 < nx; p0 += 32 * kVpl) {
+      const int x0 = p0 + lane * kVpl;
+      RowVals r;
+      load_rows(A, nx, ny, nz, y, z, x0, r);
+      uint16_t info[kVpl];
+#pragma unroll
+      for (int j = 0; j < kVpl; ++j) {
+        const VoxelInfo vi = classify_regs(r, j, x0 + j, nx, hy, hz, Lf);
+        const int nt = vi.cfg >= 0 && own ? c_mc_count[vi.cfg] : 0;
+        c.x += __popc(vi.mask), c.y += nt, c.z += nt > 0 ? 1 : 0;
+        info[j] = (uint16_t)(vi.mask | (nt > 0 ? (vi.cfg << 3) | (1 << 11) : 0));
+      }
+      uint16_t* dst = mb.vinfo + (size_t)i * nx + x0;
+      if (x0 + kVpl <= nx) {
+        uint4 w;
+        w.x = info[0] | (uint32_t)info[1] << 16, w.y = info[2] | (uint32_t)info[3] << 16;
+        w.z = info[4] | (uint32_t)info[5] << 16, w.w = info[6] | (uint32_t)info[7] << 16;
+        *reinterpret_cast<uint4*>(dst) = w;
+      } else {
+        for (int j = 0; j < kVpl && x0 + j < nx; ++j) dst[j] = info[j];
+      }
     }
-    const int3 t = block_reduce3(c);
-    if (threadIdx.x == 0) {
+    const int3 t = warp_sum3(c);
+    if (lane == 0) {
       unitcnt[i] = t;
       if (!own) atomicAdd(&ctl->v_extra, t.x);
     }
@@ -375,57 +396,86 @@ __global__ void __launch_bounds__(1024) mc_scan_kernel(int3* blk, const DevCtl* 
   }
 }
 
-// per active unit, in order: vertex ids = rank of the cut edge in global edge
-// id order; fp64 positions (marching_cubes.cpp:153-155, volume.hpp:45)
+// per active unit (one warp, 8 voxels per lane per pass), in order: vertex
+// ids = rank of the cut edge in global edge id order (x ascending, then
+// axis); fp64 positions (marching_cubes.cpp:153-155, volume.hpp:45)
 __global__ void __launch_bounds__(256) mc_emit_kernel(const float* __restrict__ A, const DevCtl* ctl, int nx, int ny,
                                                       int nz, McSlab sl, const int32_t* __restrict__ units,
                                                       const int3* __restrict__ unitoff, MeshBufs mb) {
   if (ctl->status != 0 || ctl->overflow) return;
   const int U = ctl->units;
   const double L = ctl->level;
-  const float Lf = __double2float_ru(L);
   const DevGrid g = ctl->grid;
   const size_t step[3] = {1, (size_t)nx, (size_t)nx * ny};
-  for (int i = blockIdx.x; i < U; i += gridDim.x) {
+  const int lane = threadIdx.x & 31;
+  const int warps = gridDim.x * (blockDim.x >> 5);
+  for (int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i < U; i += warps) {
     const int u = units[i];
     const int y = u % ny, z = sl.z0 + u / ny;
     const bool own = z < sl.zend;  // else: only number the next rank's edges
     const size_t row0 = ((size_t)z * ny + y) * nx;
     int3 carry = unitoff[i];
-    for (int x0 = 0; x0 < nx; x0 += blockDim.x) {
-      const int x = x0 + threadIdx.x;
-      VoxelInfo vi{0, -1};
-      if (x < nx) {
-        const unsigned in = mb.vinfo[(size_t)i * nx + x];
-        vi.mask = (int)(in & 7u), vi.cfg = (in >> 11) & 1u ? (int)((in >> 3) & 255u) : -1;
+    for (int p0 = 0; p0 < nx; p0 += 32 * kVpl) {
+      const int x0 = p0 + lane * kVpl;
+      uint16_t info[kVpl];
+      const uint16_t* src = mb.vinfo + (size_t)i * nx + x0;
+      if (x0 + kVpl <= nx) {
+        const uint4 w = *reinterpret_cast<const uint4*>(src);
+        info[0] = w.x & 0xffff, info[1] = w.x >> 16, info[2] = w.y & 0xffff, info[3] = w.y >> 16;
+        info[4] = w.z & 0xffff, info[5] = w.z >> 16, info[6] = w.w & 0xffff, info[7] = w.w >> 16;
+      } else {
+#pragma unroll
+        for (int j = 0; j < kVpl; ++j) info[j] = x0 + j < nx ? src[j] : 0;
       }
-      const int nt = vi.cfg >= 0 ? c_mc_count[vi.cfg] : 0;
-      int3 tot;
-      const int3 ex = block_exclusive_scan3(make_int3(__popc(vi.mask), nt, nt > 0 ? 1 : 0), &tot);
-      const int vb = carry.x + ex.x, tb = carry.y + ex.y, cb = carry.z + ex.z;
-      const size_t v = row0 + x;
-      if (vi.mask) mb.vbase[v] = ((uint32_t)vb << 3) | (uint32_t)vi.mask;
-      if (vi.mask && own) {
-        const double v0 = (double)__ldg(A + v);
-        int id = vb;
-        for (int a = 0; a < 3; ++a) {
-          if (!(vi.mask & (1 << a))) continue;
-          const double v1 = (double)__ldg(A + v + step[a]);
-          double t = ddiv(dsub(L, v0), dsub(v1, v0));
-          t = t < 1e-6 ? 1e-6 : (t > 1.0 - 1e-6 ? 1.0 - 1e-6 : t);
-          double p[3] = {(double)x, (double)y, (double)z};
-          p[a] = dadd(p[a], t);
-          for (int c = 0; c < 3; ++c) mb.pos[3 * (size_t)id + c] = dadd(g.origin[c], dmul(g.edge, p[c]));
-          mb.edge_id[id] = (uint64_t)v * 3 + a;
-          ++id;
+      int3 cnt = make_int3(0, 0, 0);
+#pragma unroll
+      for (int j = 0; j < kVpl; ++j) {
+        const int nt = (info[j] >> 11) & 1 ? c_mc_count[(info[j] >> 3) & 255] : 0;
+        cnt.x += __popc(info[j] & 7), cnt.y += nt, cnt.z += nt > 0 ? 1 : 0;
+      }
+      int3 inc = cnt;  // warp inclusive scan
+      for (int o = 1; o < 32; o <<= 1) {
+        const int a = __shfl_up_sync(0xffffffffu, inc.x, o), b = __shfl_up_sync(0xffffffffu, inc.y, o),
+                  c = __shfl_up_sync(0xffffffffu, inc.z, o);
+        if (lane >= o) inc.x += a, inc.y += b, inc.z += c;
+      }
+      int vb = carry.x + inc.x - cnt.x, tb = carry.y + inc.y - cnt.y, cb = carry.z + inc.z - cnt.z;
+      carry.x += __shfl_sync(0xffffffffu, inc.x, 31), carry.y += __shfl_sync(0xffffffffu, inc.y, 31),
+          carry.z += __shfl_sync(0xffffffffu, inc.z, 31);
+      for (int j = 0; j < kVpl; ++j) {
+        const int mask = info[j] & 7;
+        const bool cell = (info[j] >> 11) & 1;
+        if (!mask && !cell) continue;
+        const int x = x0 + j;
+        const size_t v = row0 + x;
+        if (mask) {
+          mb.vbase[v] = ((uint32_t)vb << 3) | (uint32_t)mask;
+          if (own) {
+            const double v0 = (double)__ldg(A + v);
+            int id = vb;
+            for (int a = 0; a < 3; ++a) {
+              if (!(mask & (1 << a))) continue;
+              const double v1 = (double)__ldg(A + v + step[a]);
+              double t = ddiv(dsub(L, v0), dsub(v1, v0));
+              t = t < 1e-6 ? 1e-6 : (t > 1.0 - 1e-6 ? 1.0 - 1e-6 : t);
+              double p[3] = {(double)x, (double)y, (double)z};
+              p[a] = dadd(p[a], t);
+              for (int c = 0; c < 3; ++c) mb.pos[3 * (size_t)id + c] = dadd(g.origin[c], dmul(g.edge, p[c]));
+              mb.edge_id[id] = (uint64_t)v * 3 + a;
+              ++id;
+            }
+          }
+          vb += __popc(mask);
+        }
+        if (cell) {
+          const int cfg = (info[j] >> 3) & 255;
+          mb.cells[cb] = (int32_t)v;
+          mb.cell_tri[cb] = tb;
+          mb.cell_cfg[cb] = (uint8_t)cfg;
+          tb += c_mc_count[cfg];
+          ++cb;
         }
       }
-      if (nt > 0) {
-        mb.cells[cb] = (int32_t)v;
-        mb.cell_tri[cb] = tb;
-        mb.cell_cfg[cb] = (uint8_t)vi.cfg;
-      }
-      carry = make_int3(carry.x + tot.x, carry.y + tot.y, carry.z + tot.z);
     }
   }
 }
@@ -565,10 +615,6 @@ void launch_row_minmax(const float* A, int nx, int ny, int nz, float2* rowmm, cu
   row_minmax_kernel<<<(rows * 32 + 255) / 256, 256, 0, st>>>(A, nx, rows, rowmm);
 }
 
-namespace {
-int mc_threads(int nx) { return nx >= 256 ? 256 : (nx >= 128 ? 128 : (nx >= 64 ? 64 : 32)); }
-}  // namespace
-
 void launch_marching_cubes_count(const float* A, DevCtl* ctl, MeshBufs mb, int nx, int ny, int nz, McSlab sl,
                                  cudaStream_t st) {
   const int units = ny * sl.nzu;
@@ -577,14 +623,14 @@ void launch_marching_cubes_count(const float* A, DevCtl* ctl, MeshBufs mb, int n
   int3* ucnt = reinterpret_cast<int3*>(mb.unitcnt);
   mc_rows_kernel<<<nblk, kRowThreads, 0, st>>>(mb.rowmm, ctl, ny, nz, sl, rowmask);
   mc_units_kernel<<<1, 1024, 0, st>>>(rowmask, (units + 31) / 32, mb.units, ctl);
-  mc_count_kernel<<<148 * 8, mc_threads(nx), 0, st>>>(A, ctl, nx, ny, nz, sl, mb.units, ucnt, mb);
+  mc_count_kernel<<<148 * 8, 256, 0, st>>>(A, ctl, nx, ny, nz, sl, mb.units, ucnt, mb);
   mc_scan_kernel<<<1, 1024, kScanStage * sizeof(int3), st>>>(ucnt, ctl, ctl, mb.v_cap, mb.t_cap, mb.c_cap);
 }
 
 void launch_marching_cubes_emit(const float* A, DevCtl* ctl, MeshBufs mb, int nx, int ny, int nz, McSlab sl,
                                 cudaStream_t st) {
   int3* ucnt = reinterpret_cast<int3*>(mb.unitcnt);
-  mc_emit_kernel<<<148 * 8, mc_threads(nx), 0, st>>>(A, ctl, nx, ny, nz, sl, mb.units, ucnt, mb);
+  mc_emit_kernel<<<148 * 8, 256, 0, st>>>(A, ctl, nx, ny, nz, sl, mb.units, ucnt, mb);
   mc_normals_kernel<<<148 * 4, 256, 0, st>>>(A, ctl, nx, ny, nz, mb);
   mc_tris_kernel<<<148 * 4, 256, 0, st>>>(A, ctl, nx, ny, nz, mb);
 }
