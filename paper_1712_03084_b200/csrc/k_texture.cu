@@ -3,8 +3,8 @@
 // K11 — per-vertex texturing on sm_100a: vertex_visibility + assign_texture
 // (/root/reference/proj/core/src/appearance/texture.cpp:11-72) and the
 // visibility-weighted multi-view colour blend (rasterize.cpp:12-27
-// bilinear sample, rasterize.cpp:136-157 weighting) in one pass, one thread
-// per vertex, all K views unrolled.  fp64 with the reference's operation
+// bilinear sample, rasterize.cpp:136-157 weighting) in one pass, one lane per
+// (vertex, view).  fp64 with the reference's operation
 // order so lround pixel binning is bit-exact.
 #include "vc_device.cuh"
 
@@ -32,23 +32,38 @@ __device__ void sample_bilinear(const ViewPtrs& v, int W, int H, double uvx, dou
   }
 }
 
+// One lane per (vertex, view): a group of G = pow2 >= K adjacent lanes per
+// vertex runs the K views' dependent loads (mask -> depth, weight map, RGB)
+// side by side; the group's first lane then forms the blend in view order
+// with the same fp64 operations as the reference's sequential loop.  The
+// fp32 copy of the vertex positions (the output format) is written here too.
 __global__ void __launch_bounds__(128) texture_kernel(const __grid_constant__ SensorSet ss,
                                                       const float* __restrict__ weight_maps,
                                                       const double* __restrict__ vpos, const DevCtl* ctl,
                                                       double eps_vis, uint8_t* vis, float2* uv, float* wout,
-                                                      uint8_t* untex, uint8_t* rgb, int v_cap) {
+                                                      uint8_t* untex, uint8_t* rgb, float* posf, int v_cap,
+                                                      int lg) {
   if (ctl->status != 0 || ctl->overflow) return;
   const int V = ctl->V;
   if (V > v_cap) return;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < V; i += gridDim.x * blockDim.x) {
-    const d3 X = mk3(vpos[3 * i], vpos[3 * i + 1], vpos[3 * i + 2]);
-    bool any = false;
-    double r = 0, g = 0, b = 0, wsum = 0;
-    for (int k = 0; k < ss.k; ++k) {
+  const int G = 1 << lg, K = ss.k;
+  const int lane = threadIdx.x & 31, k = lane & (G - 1), lead = lane - k;
+  const int per_warp = 32 >> lg;
+  const int warps = gridDim.x * (blockDim.x >> 5);
+  for (int base = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * per_warp; base < V;
+       base += warps * per_warp) {
+    const int i = base + (lane >> lg);
+    const bool live = i < V && k < K;
+    uint8_t vk = 0;
+    float2 uvk = make_float2(0.f, 0.f);
+    float wk = 0.f;
+    bool contrib = false;
+    double tr = 0.0, tg = 0.0, tb = 0.0, twd = 0.0;
+    if (live) {
+      const d3 X = mk3(vpos[3 * i], vpos[3 * i + 1], vpos[3 * i + 2]);
       const DevSensor& s = ss.s[k];
       const ViewPtrs& v = ss.v[k];
       // texture.cpp:19-31 — world_to_cam = pose.inverse(); lround pixel
-      uint8_t vk = 0;
       const d3 local = add3(mat3(s.Ri, X), ld3(s.ti));
       double u, w;
       if (project_local(s.fx, s.fy, s.cx, s.cy, local, &u, &w)) {
@@ -60,10 +75,7 @@ __global__ void __launch_bounds__(128) texture_kernel(const __grid_constant__ Se
           }
         }
       }
-      float2 uvk = make_float2(0.f, 0.f);
-      float wk = 0.f;
       if (vk) {
-        any = true;
         // texture.cpp:54-63 — RGB camera UV (apply_inverse of pose.compose),
         // weight map at the lround depth-camera pixel (apply_inverse of pose)
         double ur, vr;
@@ -76,15 +88,13 @@ __global__ void __launch_bounds__(128) texture_kernel(const __grid_constant__ Se
             if (px >= 0 && px < s.w && py >= 0 && py < s.h)
               wk = __ldg(weight_maps + ss.pix_offset[k] + py * s.w + px);
           }
-          // rasterize.cpp:136-150 at the vertex: skip w <= 1e-9, sum w*s
+          // rasterize.cpp:136-150 at the vertex: skip w <= 1e-9, terms w*s
           const double wd = (double)wk;
           if (wd > 1e-9 && v.rgb) {
             double smp[3];
             sample_bilinear(v, s.rw, s.rh, uvx, uvy, smp);
-            r = dadd(r, dmul(wd, smp[0]));
-            g = dadd(g, dmul(wd, smp[1]));
-            b = dadd(b, dmul(wd, smp[2]));
-            wsum = dadd(wsum, wd);
+            contrib = true;
+            tr = dmul(wd, smp[0]), tg = dmul(wd, smp[1]), tb = dmul(wd, smp[2]), twd = wd;
           }
         }
       }
@@ -92,14 +102,29 @@ __global__ void __launch_bounds__(128) texture_kernel(const __grid_constant__ Se
       uv[(size_t)k * V + i] = uvk;
       wout[(size_t)k * V + i] = wk;
     }
-    untex[i] = any ? 0 : 1;
-    // rasterize.cpp:151-156: weighted mean (truncating cast) or light gray 200
-    uint8_t c[3] = {200, 200, 200};
-    if (wsum > 1e-9) {
-      const double m[3] = {ddiv(r, wsum), ddiv(g, wsum), ddiv(b, wsum)};
-      for (int ch = 0; ch < 3; ++ch) c[ch] = (uint8_t)(m[ch] < 0.0 ? 0.0 : (m[ch] > 255.0 ? 255.0 : m[ch]));
+    // the group's first lane sums the views in order (rasterize.cpp:136-157)
+    bool any = false;
+    double r = 0, g = 0, b = 0, wsum = 0;
+    for (int kk = 0; kk < K; ++kk) {
+      const int src = lead + kk;
+      const bool c = __shfl_sync(0xffffffffu, contrib, src);
+      any |= __shfl_sync(0xffffffffu, vk, src) != 0;
+      const double xr = __shfl_sync(0xffffffffu, tr, src), xg = __shfl_sync(0xffffffffu, tg, src),
+                   xb = __shfl_sync(0xffffffffu, tb, src), xw = __shfl_sync(0xffffffffu, twd, src);
+      if (c) r = dadd(r, xr), g = dadd(g, xg), b = dadd(b, xb), wsum = dadd(wsum, xw);
     }
-    rgb[3 * i + 0] = c[0], rgb[3 * i + 1] = c[1], rgb[3 * i + 2] = c[2];
+    if (k == 0 && i < V) {
+      untex[i] = any ? 0 : 1;
+      // rasterize.cpp:151-156: weighted mean (truncating cast) or light gray 200
+      uint8_t c[3] = {200, 200, 200};
+      if (wsum > 1e-9) {
+        const double m[3] = {ddiv(r, wsum), ddiv(g, wsum), ddiv(b, wsum)};
+        for (int ch = 0; ch < 3; ++ch) c[ch] = (uint8_t)(m[ch] < 0.0 ? 0.0 : (m[ch] > 255.0 ? 255.0 : m[ch]));
+      }
+      rgb[3 * i + 0] = c[0], rgb[3 * i + 1] = c[1], rgb[3 * i + 2] = c[2];
+      if (posf)
+        for (int c3 = 0; c3 < 3; ++c3) posf[3 * i + c3] = (float)vpos[3 * i + c3];
+    }
   }
 }
 
@@ -113,8 +138,11 @@ __global__ void mesh_f32_kernel(const double* pos, float* posf, const DevCtl* ct
 
 void launch_texture(const SensorSet& ss, const float* weight_maps, const double* vpos, const DevCtl* ctl,
                     double eps_vis, uint8_t* vis, float2* uv, float* w, uint8_t* untex, uint8_t* rgb, int v_cap,
-                    cudaStream_t st) {
-  texture_kernel<<<148 * 4, 128, 0, st>>>(ss, weight_maps, vpos, ctl, eps_vis, vis, uv, w, untex, rgb, v_cap);
+                    cudaStream_t st, float* posf) {
+  int lg = 0;
+  while ((1 << lg) < ss.k) ++lg;  // K <= 16 lanes per vertex
+  texture_kernel<<<148 * 8, 128, 0, st>>>(ss, weight_maps, vpos, ctl, eps_vis, vis, uv, w, untex, rgb, posf, v_cap,
+                                          lg);
 }
 
 void launch_mesh_to_f32(const double* pos, float* posf, const DevCtl* ctl, int v_cap, cudaStream_t st) {

@@ -456,8 +456,7 @@ vc_status run_dist_frame(vc_dist* d, const Geo& g, const vc_recon_config* c, boo
     mark(9);
     launch_texture(ctx->ss, P<float>(ctx->wmaps), P<double>(ctx->m_pos), ctx->ctl, c->eps_vis_mm,
                    P<uint8_t>(ctx->t_vis), P<float2>(ctx->t_uv), P<float>(ctx->t_w), P<uint8_t>(ctx->t_untex),
-                   P<uint8_t>(ctx->t_rgb), ctx->v_cap, ctx->st);
-    launch_mesh_to_f32(P<double>(ctx->m_pos), P<float>(ctx->m_posf), ctx->ctl, ctx->v_cap, ctx->st);
+                   P<uint8_t>(ctx->t_rgb), ctx->v_cap, ctx->st, P<float>(ctx->m_posf));
     return VC_OK;
   }));
   mark(10);

@@ -294,9 +294,8 @@ int enqueue_frame(vc_ctx* ctx, const FrameCfg& f) {
   record(ctx, 5);
   launch_texture(ctx->ss, P<float>(ctx->wmaps), P<double>(ctx->m_pos), ctx->ctl, f.eps_vis, P<uint8_t>(ctx->t_vis),
                  P<float2>(ctx->t_uv), P<float>(ctx->t_w), P<uint8_t>(ctx->t_untex), P<uint8_t>(ctx->t_rgb),
-                 ctx->v_cap, st);
-  launch_mesh_to_f32(P<double>(ctx->m_pos), P<float>(ctx->m_posf), ctx->ctl, ctx->v_cap, st);
-  n += 2;
+                 ctx->v_cap, st, P<float>(ctx->m_posf));
+  n += 1;
   record(ctx, 6);
   return n;
 }
@@ -579,8 +578,7 @@ vc_status vc_reconstruct_frame(vc_ctx* ctx, const vc_sensor* sensors, const vc_v
     launch_marching_cubes(P<float>(ctx->A), ctx->ctl, mesh_bufs(ctx), nx, ny, nz, ctx->st);
     launch_texture(ctx->ss, P<float>(ctx->wmaps), P<double>(ctx->m_pos), ctx->ctl, config->eps_vis_mm,
                    P<uint8_t>(ctx->t_vis), P<float2>(ctx->t_uv), P<float>(ctx->t_w), P<uint8_t>(ctx->t_untex),
-                   P<uint8_t>(ctx->t_rgb), ctx->v_cap, ctx->st);
-    launch_mesh_to_f32(P<double>(ctx->m_pos), P<float>(ctx->m_posf), ctx->ctl, ctx->v_cap, ctx->st);
+                   P<uint8_t>(ctx->t_rgb), ctx->v_cap, ctx->st, P<float>(ctx->m_posf));
     VC_CUDA(cudaGetLastError());
     VC_TRY(read_ctl(ctx));
     if (ctx->ctl_h->overflow) return fail(ctx, VC_ERR_CAPACITY, "marching cubes capacity");

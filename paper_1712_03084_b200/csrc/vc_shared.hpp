@@ -178,9 +178,10 @@ void launch_iso_final_samples(const double* samples, DevCtl* ctl, double* partia
 void launch_row_minmax(const float* A, int nx, int ny, int nz, float2* rowmm, cudaStream_t st);
 void upload_case_table_data(const int8_t* counts, const int8_t* tris, cudaStream_t st);
 // k_texture.cu
+// posf (nullable): fp32 copy of the vertex positions, written alongside
 void launch_texture(const SensorSet& ss, const float* weight_maps, const double* vpos, const DevCtl* ctl,
                     double eps_vis, uint8_t* vis, float2* uv, float* w, uint8_t* untex, uint8_t* rgb, int v_cap,
-                    cudaStream_t st);
+                    cudaStream_t st, float* posf = nullptr);
 void launch_mesh_to_f32(const double* pos, float* posf, const DevCtl* ctl, int v_cap, cudaStream_t st);
 // k_synth.cu
 void launch_render(const DevSensor& s, const double* joints, const double* radii, const uint8_t* colors,
