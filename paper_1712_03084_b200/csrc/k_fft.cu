@@ -544,7 +544,7 @@ __device__ __forceinline__ void z_body(float2* __restrict__ S0, const float2* __
     const float w2 = wxy + wz * wz;
     const float2 d = b0[kz * kCW + c];
     const float2 s = make_float2(d.x + wz * v[k1].x, d.y + wz * v[k1].y);
-    const float inv = (kx == 0 && ky == 0 && kz == 0) ? 0.f : __frcp_rn(w2);
+    const float inv = (kx == 0 && ky == 0 && kz == 0) ? 0.f : __fdividef(1.0f, w2);
     v[k1] = make_float2(s.y * inv, -s.x * inv);  // (-i/|w|^2) * s
   }
   __syncthreads();  // everyone has read its parked D before b0 becomes the exchange
@@ -561,7 +561,7 @@ __device__ __forceinline__ void z_body(float2* __restrict__ S0, const float2* __
 // Input: D, Z as [z][kyl][H] (kyl = ny on one GPU; a ky-slab starting at ky0
 // after the forward all-to-all).  The result overwrites S0 in place.
 template <int NZ>
-__global__ void __launch_bounds__(CCfg<NZ>::THREADS, NZ >= 1024 ? 1 : 3)
+__global__ void __launch_bounds__(CCfg<NZ>::THREADS, NZ >= 1024 ? 1 : 2)
     z_kernel(float2* __restrict__ S0, const float2* __restrict__ S1, int nx, int ny, int kyl, int ky0, int H, int nyq,
              float fx_step, float fy_step, const float2* __restrict__ tw, const uint32_t* __restrict__ planeflag) {
   if (blockIdx.x == nyq)
