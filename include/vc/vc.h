@@ -79,7 +79,8 @@ typedef struct vc_sensor {
 typedef enum vc_mem_kind { VC_MEM_HOST = 0, VC_MEM_DEVICE = 1 } vc_mem_kind;
 
 /* image.hpp:50-64 — one RgbdFrame.  depth: uint16 mm (0 = invalid),
- * mask: uint8 (nonzero = foreground), rgb: packed RGB8 of rgb_intr size.
+ * mask: uint8 (nonzero = foreground), or NULL: foreground := depth > 0, derived on the
+ * device (the dataset loader's rule, dataset.cpp:99-102); rgb: packed RGB8 of rgb_intr size.
  * Pitches are in bytes; 0 means tightly packed. */
 typedef struct vc_view {
   const uint16_t* depth;
@@ -263,6 +264,32 @@ vc_status vc_stage_marching_cubes(vc_ctx* ctx, const float* A, const vc_grid_spe
 vc_status vc_stage_texture(vc_ctx* ctx, const vc_sensor* sensors, const vc_view* views, const float* weight_maps,
                            int32_t k, const double* vertices, int32_t n_vertices, double eps_vis_mm,
                            uint8_t* visible, float* uv, float* weight, uint8_t* untextured, uint8_t* rgb);
+
+/* ---------------------------------------------- frame / mesh I/O (host)
+ * The formats either side of the path.  No context,
+ * no GPU; on error vc_io_last_error() holds "<what>: <path>" like the
+ * reference's std::runtime_error messages. */
+typedef struct vc_png_header {
+  int32_t width, height, bit_depth, color_type; /* PNG IHDR */
+} vc_png_header;
+const char* vc_io_last_error(void);
+vc_status vc_png_info(const char* path, vc_png_header* info);
+/* image_io.cpp:105-122: 16-bit grayscale only ("depth png must be 16-bit grayscale"). */
+vc_status vc_png_read_depth(const char* path, uint16_t* dst, int32_t width, int32_t height);
+/* image_io.cpp:84-103: any PNG colour type -> RGB8 (expand, strip 16, strip alpha, gray to RGB). */
+vc_status vc_png_read_color(const char* path, uint8_t* rgb, int32_t width, int32_t height);
+/* image_io.cpp:64-82: 16-bit gray / 8-bit RGB, non-interlaced. */
+vc_status vc_png_write_depth(const char* path, const uint16_t* src, int32_t width, int32_t height);
+vc_status vc_png_write_color(const char* path, const uint8_t* rgb, int32_t width, int32_t height);
+/* mesh_io.cpp:104-145 write_ply: binary little-endian, float xyz (+ normals
+ * when non-NULL) + float channels "<name>_<c>", uchar/int faces, channel directory comments. */
+vc_status vc_ply_write_mesh(const char* path, const float* xyz, const float* normals, int32_t n_vertices,
+                            const int32_t* triangles, int32_t n_triangles, const char* const* channel_names,
+                            const int32_t* channel_components, const float* const* channel_data,
+                            int32_t n_channels);
+/* write_ply(textured.with_channels()) of the reference CLI (volcap.cpp:312-316,
+ * texture.cpp:74-91) for a host-memory vc_textured_mesh. */
+vc_status vc_ply_write_textured(const char* path, const vc_textured_mesh* mesh);
 
 /* ------------------------------------------------------- synthetic capture
  * The reference's synthetic fixture (synth/capsule.cpp, scene.cpp,

@@ -82,6 +82,10 @@ class DistInfo(C.Structure):
                                          "triangle_offset", "triangle_total")]
 
 
+class PngHeader(C.Structure):
+    _fields_ = [(n, C.c_int32) for n in ("width", "height", "bit_depth", "color_type")]
+
+
 class Body(C.Structure):
     _fields_ = [("joints", C.c_double * 45), ("radii", C.c_double * 14), ("colors", C.c_uint8 * 42)]
 
@@ -105,6 +109,7 @@ def lib() -> C.CDLL:
         L.vc_status_string.restype = C.c_char_p
         L.vc_last_error.restype = C.c_char_p
         L.vc_last_error.argtypes = [P]
+        L.vc_io_last_error.restype = C.c_char_p
         L.vc_ctx_stream.restype = P
         L.vc_ctx_stream.argtypes = [P]
         L.vc_ctx_kernels_per_frame.argtypes = [P]

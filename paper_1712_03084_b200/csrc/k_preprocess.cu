@@ -413,7 +413,17 @@ Scratch carve(const SensorSet& ss, void* base) {
   return s;
 }
 
+// dataset.cpp:99-102: foreground := depth > 0 (views staged without a mask)
+__global__ void mask_from_depth_kernel(const uint16_t* __restrict__ depth, uint8_t* __restrict__ mask, int n) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) mask[i] = depth[i] > 0 ? 1 : 0;
+}
+
 }  // namespace
+
+void launch_mask_from_depth(const uint16_t* depth, uint8_t* mask, int n, cudaStream_t st) {
+  const int blocks = (n + 255) / 256 < 592 ? (n + 255) / 256 : 592;
+  mask_from_depth_kernel<<<blocks, 256, 0, st>>>(depth, mask, n);
+}
 
 void prepare_preprocess(const SensorSet&) {}  // no opt-in shared memory needed
 

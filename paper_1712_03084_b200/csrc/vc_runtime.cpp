@@ -121,12 +121,18 @@ vc_status stage_views(vc_ctx* ctx, const vc_sensor* sensors, const vc_view* view
     const int w = sensors[i].depth_intr.width, h = sensors[i].depth_intr.height;
     const int rw = sensors[i].rgb_intr.width, rh = sensors[i].rgb_intr.height;
     const vc_view& v = views[i];
-    if (!v.depth || !v.mask) return fail(ctx, VC_ERR_INVALID_ARGUMENT, "view depth/mask missing");
+    if (!v.depth) return fail(ctx, VC_ERR_INVALID_ARGUMENT, "view depth missing");
     const cudaMemcpyKind kind = v.mem_kind == VC_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
     VC_CUDA(cudaMemcpy2DAsync(base + off[3 * i], (size_t)w * 2, v.depth, v.depth_pitch ? v.depth_pitch : (size_t)w * 2,
                               (size_t)w * 2, h, kind, ctx->st));
-    VC_CUDA(cudaMemcpy2DAsync(base + off[3 * i + 1], (size_t)w, v.mask, v.mask_pitch ? v.mask_pitch : (size_t)w,
-                              (size_t)w, h, kind, ctx->st));
+    if (v.mask) {
+      VC_CUDA(cudaMemcpy2DAsync(base + off[3 * i + 1], (size_t)w, v.mask, v.mask_pitch ? v.mask_pitch : (size_t)w,
+                                (size_t)w, h, kind, ctx->st));
+    } else {  // the dataset loader's foreground := depth > 0 (dataset.cpp:99-102), on the device
+      launch_mask_from_depth(reinterpret_cast<const uint16_t*>(base + off[3 * i]), base + off[3 * i + 1], w * h,
+                             ctx->st);
+      VC_CUDA(cudaGetLastError());
+    }
     if (v.rgb && need_rgb)
       VC_CUDA(cudaMemcpy2DAsync(base + off[3 * i + 2], (size_t)rw * 3, v.rgb, v.rgb_pitch ? v.rgb_pitch : (size_t)rw * 3,
                                 (size_t)rw * 3, rh, kind, ctx->st));

@@ -100,6 +100,7 @@ void prepare_preprocess(const SensorSet& ss);  // smem opt-in; call outside grap
 void launch_preprocess(const SensorSet& ss, DevPoints pts, float* weight_maps, int32_t* scratch, DevCtl* ctl,
                        int dims_x, int dims_y, int dims_z, int padding, double disc_mm, int sil_r, cudaStream_t st,
                        int32_t* rowlist_reset = nullptr /*frame path: zero the touched-row count*/);
+void launch_mask_from_depth(const uint16_t* depth, uint8_t* mask, int n, cudaStream_t st);  // mask := depth > 0
 // k_splat.cu
 void launch_clear(float4* acc, size_t n, cudaStream_t st);
 // zoff/nzl: the z-slab [zoff, zoff+nzl) this rank accumulates (whole grid: 0, nz).

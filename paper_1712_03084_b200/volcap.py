@@ -104,7 +104,7 @@ class CameraRig:  # types.hpp:80-99
 class RgbdFrame:  # image.hpp:50-64
     depth: np.ndarray       # (h, w) uint16 mm, 0 = invalid
     color: np.ndarray       # (rh, rw, 3) uint8
-    foreground: np.ndarray  # (h, w) uint8
+    foreground: np.ndarray | None  # (h, w) uint8; None = depth > 0 (derived on the device)
 
 
 @dataclass
@@ -271,10 +271,12 @@ def _views(frames, k):
     for i in range(k):
         f = frames[i]
         d = np.ascontiguousarray(f.depth, np.uint16)
-        m = np.ascontiguousarray(f.foreground, np.uint8)
+        # no foreground: the library derives it on the device as depth > 0 (dataset.cpp:99-102)
+        m = None if f.foreground is None else np.ascontiguousarray(f.foreground, np.uint8)
         c = None if f.color is None else np.ascontiguousarray(f.color, np.uint8)
         keep += [d, m, c]
-        arr[i] = L.View(_ptr(d), _ptr(m), _ptr(c) if c is not None else None, 0, 0, 0, L.VC_MEM_HOST)
+        arr[i] = L.View(_ptr(d), _ptr(m) if m is not None else None, _ptr(c) if c is not None else None, 0, 0, 0,
+                        L.VC_MEM_HOST)
     return arr, keep
 
 

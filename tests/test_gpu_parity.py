@@ -389,3 +389,25 @@ def vc_topology_ok(mesh):
     e.sort(axis=1)
     _, counts = np.unique(e[:, 0] * (1 << 32) + e[:, 1], return_counts=True)
     return bool(np.all(counts == 2))
+
+
+def test_mask_derived_on_device_and_ply_export(scene, ctx, tmp_path):
+    """vc_view.mask = NULL: foreground := depth > 0 on the device (dataset.cpp:99-102)
+    gives the same frame as the host-side rule; the frame's PLY (mesh_io.cpp:104-145
+    of with_channels) is byte-identical to the restated writer on the same arrays."""
+    from oracle import oracle_io as OI
+    from paper_1712_03084_b200 import io as vio
+    rig, _, frames, _ = scene
+    host = [vc.RgbdFrame(f.depth, f.color, (f.depth > 0).astype(np.uint8)) for f in frames]
+    dev = [vc.RgbdFrame(f.depth, f.color, None) for f in frames]
+    cfg = vc.ReconConfig(dims=(128, 128, 128))
+    a = vc.reconstruct_frame(host, rig, cfg, ctx=ctx)
+    b = vc.reconstruct_frame(dev, rig, cfg, ctx=ctx)
+    assert np.array_equal(a.mesh.triangles, b.mesh.triangles)
+    assert np.array_equal(a.mesh.vertices, b.mesh.vertices)
+    assert np.array_equal(a.textured.visible, b.textured.visible)
+    p = str(tmp_path / "frame.ply")
+    vio.write_textured_ply(p, b.textured)
+    t = b.textured
+    assert open(p, "rb").read() == OI.write_ply(t.mesh.vertices, t.mesh.triangles, t.mesh.normals,
+                                                OI.with_channels(t.visible, t.uv, t.weight, t.untextured))
