@@ -291,6 +291,29 @@ vc_status vc_ply_write_mesh(const char* path, const float* xyz, const float* nor
  * texture.cpp:74-91) for a host-memory vc_textured_mesh. */
 vc_status vc_ply_write_textured(const char* path, const vc_textured_mesh* mesh);
 
+/* ---------------------------------------------- colour correction
+ * SURVEY §8(f) rank 2 (appearance/color_correction.cpp, hsv.cpp).  Errors of
+ * the context-free entry points: vc_io_last_error(). */
+/* ColorCorrection::apply(sensor, image) with that sensor's ValueMap: HSV value
+ * v := clamp(gain*v + offset, 0, 1), fp64, byte-exact; the identity map leaves
+ * the image unchanged.  rgb_in/out: n_pixels*3 bytes in mem_kind memory. */
+vc_status vc_color_apply(vc_ctx* ctx, const uint8_t* rgb_in, uint8_t* rgb_out, int64_t n_pixels, double gain,
+                         double offset, int32_t mem_kind);
+/* mutual_closest_pairs(a, b, max_dist) (color_correction.cpp:16-84) on the GPU:
+ * a, b: 3n doubles (host); pairs: 2*min(na, nb) int32 (i, j), ascending i. */
+vc_status vc_mutual_closest_pairs(vc_ctx* ctx, const double* a, int32_t na, const double* b, int32_t nb,
+                                  double max_dist_mm, int32_t* pairs, int32_t* n_pairs);
+/* fit_value_map (color_correction.cpp:97-138): pairs_rgb = n x (first RGB, second RGB). */
+vc_status vc_fit_value_map(const uint8_t* pairs_rgb, int32_t n, int32_t ransac_iterations, double inlier_threshold,
+                           uint64_t seed, double* gain, double* offset);
+/* chain_to_reference (color_correction.cpp:168-199): per-sensor maps toward the reference. */
+vc_status vc_chain_to_reference(const int32_t* from, const int32_t* to, const double* gain, const double* offset,
+                                int32_t n_edges, int32_t reference, int32_t sensor_count, double* out_gain,
+                                double* out_offset);
+/* Per-sensor maps applied to every RGB texel the frame's texture blend samples
+ * (the corrected images of sequence.cpp:71-73); k = 0 turns it off. */
+vc_status vc_ctx_set_color_correction(vc_ctx* ctx, const double* gain, const double* offset, int32_t k);
+
 /* ------------------------------------------------------- synthetic capture
  * The reference's synthetic fixture (synth/capsule.cpp, scene.cpp,
  * render.cpp), rendered on the GPU.  Body layout: 15 joints (xyz), 14 radii,

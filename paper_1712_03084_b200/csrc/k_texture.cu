@@ -6,13 +6,17 @@
 // bilinear sample, rasterize.cpp:136-157 weighting) in one pass, one lane per
 // (vertex, view).  fp64 with the reference's operation
 // order so lround pixel binning is bit-exact.
+#include "vc_color.cuh"
 #include "vc_device.cuh"
 
 namespace vc {
 namespace {
 
-// rasterize.cpp:12-27 sample_bilinear (uv -> pixel - 0.5, clamp, lround to uint8)
-__device__ void sample_bilinear(const ViewPtrs& v, int W, int H, double uvx, double uvy, double out[3]) {
+// rasterize.cpp:12-27 sample_bilinear (uv -> pixel - 0.5, clamp, lround to
+// uint8); with a colour correction the four texels are corrected first
+// (ColorCorrection::apply on the image, sequence.cpp:71-73)
+__device__ void sample_bilinear(const ViewPtrs& v, const DevSensor& s, int W, int H, double uvx, double uvy,
+                                double out[3]) {
   const double px = dsub(dmul(uvx, (double)W), 0.5), py = dsub(dmul(uvy, (double)H), 0.5);
   int x0 = (int)floor(px), y0 = (int)floor(py);
   x0 = x0 < 0 ? 0 : (x0 > W - 1 ? W - 1 : x0);
@@ -23,11 +27,21 @@ __device__ void sample_bilinear(const ViewPtrs& v, int W, int H, double uvx, dou
   ty = ty < 0.0 ? 0.0 : (ty > 1.0 ? 1.0 : ty);
   const uint8_t* r0 = v.rgb + (size_t)y0 * v.rpitch;
   const uint8_t* r1 = v.rgb + (size_t)y1 * v.rpitch;
+  uint8_t c00[3], c10[3], c01[3], c11[3];
+#pragma unroll
+  for (int ch = 0; ch < 3; ++ch) {
+    c00[ch] = __ldg(r0 + 3 * x0 + ch), c10[ch] = __ldg(r0 + 3 * x1 + ch);
+    c01[ch] = __ldg(r1 + 3 * x0 + ch), c11[ch] = __ldg(r1 + 3 * x1 + ch);
+  }
+  if (s.cc_on && !(s.cc_gain == 1.0 && s.cc_offset == 0.0)) {  // identity map: image unchanged (:151-153)
+    value_map_rgb(c00, s.cc_gain, s.cc_offset), value_map_rgb(c10, s.cc_gain, s.cc_offset);
+    value_map_rgb(c01, s.cc_gain, s.cc_offset), value_map_rgb(c11, s.cc_gain, s.cc_offset);
+  }
   const double ux = dsub(1.0, tx), uy = dsub(1.0, ty);
 #pragma unroll
   for (int ch = 0; ch < 3; ++ch) {
-    const double a = dadd(dmul((double)__ldg(r0 + 3 * x0 + ch), ux), dmul((double)__ldg(r0 + 3 * x1 + ch), tx));
-    const double b = dadd(dmul((double)__ldg(r1 + 3 * x0 + ch), ux), dmul((double)__ldg(r1 + 3 * x1 + ch), tx));
+    const double a = dadd(dmul((double)c00[ch], ux), dmul((double)c10[ch], tx));
+    const double b = dadd(dmul((double)c01[ch], ux), dmul((double)c11[ch], tx));
     out[ch] = (double)(uint8_t)lround_d(dadd(dmul(a, uy), dmul(b, ty)));
   }
 }
@@ -92,7 +106,7 @@ __global__ void __launch_bounds__(128) texture_kernel(const __grid_constant__ Se
           const double wd = (double)wk;
           if (wd > 1e-9 && v.rgb) {
             double smp[3];
-            sample_bilinear(v, s.rw, s.rh, uvx, uvy, smp);
+            sample_bilinear(v, s, s.rw, s.rh, uvx, uvy, smp);
             contrib = true;
             tr = dmul(wd, smp[0]), tg = dmul(wd, smp[1]), tb = dmul(wd, smp[2]), twd = wd;
           }

@@ -57,7 +57,8 @@ struct vc_ctx {
   int v_cap = 0, t_cap = 0, c_cap = 0;
   // host outputs (pinned)
   HostBuf h_posf, h_nrm, h_tri, h_vis, h_uv, h_w, h_untex, h_rgb, h_pos, h_eid;
-  // stage-API host scratch
+  // stage-API host scratch, device scratch of the colour-correction entry points
+  Buf scratch_dev;
   std::vector<uint8_t> scratch;
   // graph
   cudaGraphExec_t gexec = nullptr;
@@ -65,6 +66,7 @@ struct vc_ctx {
   cudaEvent_t ev[kEvents] = {};
   bool table_ready = false;
   int last_k = 0;
+  std::vector<double> cc_gain, cc_offset;  // per-sensor colour correction of the texture blend (empty: off)
   int kernels_per_frame = 0;
 };
 namespace vc::rt {

@@ -240,6 +240,13 @@ vc_status write_ply(const char* path, const float* xyz, const float* nrm, int nv
 
 }  // namespace
 
+namespace vc_io_detail {
+vc_status set_error(vc_status s, const std::string& msg) {  // context-free entry points' last error
+  g_io_err = msg;
+  return s;
+}
+}  // namespace vc_io_detail
+
 extern "C" {
 
 const char* vc_io_last_error(void) { return g_io_err.c_str(); }

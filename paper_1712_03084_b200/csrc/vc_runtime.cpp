@@ -152,6 +152,9 @@ vc_status setup_sensorset(vc_ctx* ctx, const vc_sensor* sensors, int k) {
   ss.row_offset[0] = 0;
   for (int i = 0; i < k; ++i) {
     fill_sensor(sensors[i], ss.s[i]);
+    const bool cc = i < (int)ctx->cc_gain.size();
+    ss.s[i].cc_on = cc ? 1 : 0;
+    ss.s[i].cc_gain = cc ? ctx->cc_gain[i] : 1.0, ss.s[i].cc_offset = cc ? ctx->cc_offset[i] : 0.0;
     ss.pix_offset[i + 1] = ss.pix_offset[i] + (int64_t)sensors[i].depth_intr.width * sensors[i].depth_intr.height;
     ss.row_offset[i + 1] = ss.row_offset[i] + sensors[i].depth_intr.height;
   }

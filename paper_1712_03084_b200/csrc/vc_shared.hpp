@@ -29,6 +29,10 @@ struct DevSensor {
   double rfx, rfy, rcx, rcy;
   int32_t rw, rh;
   double Rc[9], tc[3];  // RGB camera -> world
+  // ColorCorrection map of this sensor (color.hpp:50-57), applied to every
+  // RGB sample of the texture blend when cc_on (vc_ctx_set_color_correction)
+  double cc_gain, cc_offset;
+  int32_t cc_on;
 };
 
 struct ViewPtrs {
@@ -184,6 +188,12 @@ void launch_texture(const SensorSet& ss, const float* weight_maps, const double*
                     double eps_vis, uint8_t* vis, float2* uv, float* w, uint8_t* untex, uint8_t* rgb, int v_cap,
                     cudaStream_t st, float* posf = nullptr);
 void launch_mesh_to_f32(const double* pos, float* posf, const DevCtl* ctl, int v_cap, cudaStream_t st);
+// k_color.cu — colour correction
+void launch_color_apply(const uint8_t* in, uint8_t* out, int64_t n, double gain, double offset, cudaStream_t st);
+size_t grid_scratch_bytes(int n);
+void launch_mutual_pairs(const double* a, int na, const double* b, int nb, double max_dist, void* scratch_a,
+                         void* scratch_b, int32_t* partner, int32_t* pairs, int32_t* n_pairs, cudaStream_t st);
+
 // k_synth.cu
 void launch_render(const DevSensor& s, const double* joints, const double* radii, const uint8_t* colors,
                    double gain, uint16_t* depth, uint8_t* mask, uint8_t* rgb, cudaStream_t st);
