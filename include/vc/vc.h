@@ -314,6 +314,23 @@ vc_status vc_chain_to_reference(const int32_t* from, const int32_t* to, const do
  * (the corrected images of sequence.cpp:71-73); k = 0 turns it off. */
 vc_status vc_ctx_set_color_correction(vc_ctx* ctx, const double* gain, const double* offset, int32_t k);
 
+/* ---------------------------------------------- (A, L) consumers
+ * SURVEY §8(f) rank 3 (mocap/binary_volume.cpp, skeletonize.cpp). */
+/* binarize(A, L) (binary_volume.cpp:10-66) on the GPU: keep the side of L that
+ * holds max(A), then the largest 26-connected component (ties: first in raster
+ * order).  A: fp32 x-fastest in mem_kind memory, or NULL = this context's last
+ * frame volume.  keep_out (nullable): N bytes; voxels_out: 3*capacity int32
+ * (x, y, z) in raster order; *n_voxels = component size (may exceed capacity).
+ * Empty interior -> VC_ERR_EMPTY_SCENE ("binarize: empty interior"). */
+vc_status vc_binarize(vc_ctx* ctx, const float* A, int32_t mem_kind, const vc_grid_spec* grid, double level,
+                      uint8_t* keep_out, int32_t* voxels_out, int64_t capacity, int64_t* n_voxels);
+/* boundary_voxels (binary_volume.cpp:68-82): out_xyz 3*n doubles (world centres). */
+vc_status vc_boundary_voxels(vc_ctx* ctx, const uint8_t* keep, const vc_grid_spec* grid, const int32_t* voxels,
+                             int64_t n, double* out_xyz, int64_t* n_out);
+/* skeletonize (skeletonize.cpp:99-161), host: out 3*n int32. */
+vc_status vc_skeletonize(const uint8_t* grid, int32_t nx, int32_t ny, int32_t nz, const int32_t* voxels, int64_t n,
+                         int32_t* out, int64_t* n_out);
+
 /* ------------------------------------------------------- synthetic capture
  * The reference's synthetic fixture (synth/capsule.cpp, scene.cpp,
  * render.cpp), rendered on the GPU.  Body layout: 15 joints (xyz), 14 radii,

@@ -58,7 +58,7 @@ struct vc_ctx {
   // host outputs (pinned)
   HostBuf h_posf, h_nrm, h_tri, h_vis, h_uv, h_w, h_untex, h_rgb, h_pos, h_eid;
   // stage-API host scratch, device scratch of the colour-correction entry points
-  Buf scratch_dev;
+  Buf scratch_dev, scratch_dev2;
   std::vector<uint8_t> scratch;
   // graph
   cudaGraphExec_t gexec = nullptr;
