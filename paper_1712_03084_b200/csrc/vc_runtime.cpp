@@ -117,15 +117,38 @@ vc_status stage_views(vc_ctx* ctx, const vc_sensor* sensors, const vc_view* view
   }
   VC_TRY(ensure(ctx, ctx->views, bytes));
   uint8_t* base = P<uint8_t>(ctx->views);
+  // Views laid out exactly like the staging buffer (same order, tight rows,
+  // the segment offsets above, one memory kind): one copy for all of them.
+  bool contiguous = true;
+  const uint8_t* h0 = reinterpret_cast<const uint8_t*>(views[0].depth);
+  for (int i = 0; i < k && contiguous; ++i) {
+    const vc_view& v = views[i];
+    const int w = sensors[i].depth_intr.width, rw = sensors[i].rgb_intr.width;
+    contiguous = v.depth && v.mask && (v.rgb || !need_rgb) && v.mem_kind == views[0].mem_kind &&
+                 reinterpret_cast<const uint8_t*>(v.depth) == h0 + off[3 * i] && v.mask == h0 + off[3 * i + 1] &&
+                 (!need_rgb || v.rgb == h0 + off[3 * i + 2]) && (!v.depth_pitch || v.depth_pitch == w * 2) &&
+                 (!v.mask_pitch || v.mask_pitch == w) && (!v.rgb_pitch || v.rgb_pitch == rw * 3);
+  }
+  if (contiguous) {
+    const size_t last = need_rgb ? off[3 * k - 1] + (size_t)sensors[k - 1].rgb_intr.width *
+                                                         sensors[k - 1].rgb_intr.height * 3
+                                 : off[3 * k - 2] + (size_t)sensors[k - 1].depth_intr.width *
+                                                        sensors[k - 1].depth_intr.height;
+    VC_CUDA(cudaMemcpyAsync(base, h0, last,
+                            views[0].mem_kind == VC_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                            ctx->st));
+  }
   for (int i = 0; i < k; ++i) {
     const int w = sensors[i].depth_intr.width, h = sensors[i].depth_intr.height;
     const int rw = sensors[i].rgb_intr.width, rh = sensors[i].rgb_intr.height;
     const vc_view& v = views[i];
     if (!v.depth) return fail(ctx, VC_ERR_INVALID_ARGUMENT, "view depth missing");
     const cudaMemcpyKind kind = v.mem_kind == VC_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
-    VC_CUDA(cudaMemcpy2DAsync(base + off[3 * i], (size_t)w * 2, v.depth, v.depth_pitch ? v.depth_pitch : (size_t)w * 2,
-                              (size_t)w * 2, h, kind, ctx->st));
-    if (v.mask) {
+    if (!contiguous)
+      VC_CUDA(cudaMemcpy2DAsync(base + off[3 * i], (size_t)w * 2, v.depth,
+                                v.depth_pitch ? v.depth_pitch : (size_t)w * 2, (size_t)w * 2, h, kind, ctx->st));
+    if (contiguous) {
+    } else if (v.mask) {
       VC_CUDA(cudaMemcpy2DAsync(base + off[3 * i + 1], (size_t)w, v.mask, v.mask_pitch ? v.mask_pitch : (size_t)w,
                                 (size_t)w, h, kind, ctx->st));
     } else {  // the dataset loader's foreground := depth > 0 (dataset.cpp:99-102), on the device
@@ -133,7 +156,7 @@ vc_status stage_views(vc_ctx* ctx, const vc_sensor* sensors, const vc_view* view
                              ctx->st);
       VC_CUDA(cudaGetLastError());
     }
-    if (v.rgb && need_rgb)
+    if (v.rgb && need_rgb && !contiguous)
       VC_CUDA(cudaMemcpy2DAsync(base + off[3 * i + 2], (size_t)rw * 3, v.rgb, v.rgb_pitch ? v.rgb_pitch : (size_t)rw * 3,
                                 (size_t)rw * 3, rh, kind, ctx->st));
     ViewPtrs& vp = ctx->ss.v[i];
