@@ -331,6 +331,38 @@ vc_status vc_boundary_voxels(vc_ctx* ctx, const uint8_t* keep, const vc_grid_spe
 vc_status vc_skeletonize(const uint8_t* grid, int32_t nx, int32_t ny, int32_t nz, const int32_t* voxels, int64_t n,
                          int32_t* out, int64_t* n_out);
 
+/* ---------------------------------------------- evaluation renderer + metrics
+ * SURVEY §8(f) rank 4 (eval/rasterize.cpp, metrics.cpp, distance_transform.cpp,
+ * ssim.cpp).  Host arrays in and out. */
+typedef enum vc_render_mode { VC_RENDER_UV_BLEND = 0, VC_RENDER_COLOR_PER_VERTEX = 1 } vc_render_mode;
+/* rasterize(textured mesh, camera, view images, mode) (rasterize.cpp:35-161):
+ * vertices 3V doubles, triangles 3T, visible/uv/weight [k][V] as in
+ * vc_textured_mesh, camera = intr + camera-to-world pose, images[k] RGB8 of
+ * image_w[k] x image_h[k].  Outputs w*h: depth float (0 = empty), colour RGB8,
+ * silhouette.  The reference's order-dependent float z-buffer test is replayed
+ * per pixel in triangle order, so the outputs are exact. */
+vc_status vc_rasterize(vc_ctx* ctx, const double* vertices, int32_t n_vertices, const int32_t* triangles,
+                       int32_t n_triangles, int32_t k, const uint8_t* visible, const float* uv, const float* weight,
+                       const vc_intrinsics* intr, const vc_pose* pose, const uint8_t* const* images,
+                       const int32_t* image_w, const int32_t* image_h, int32_t mode, float* depth, uint8_t* color,
+                       uint8_t* silhouette);
+vc_status vc_vre(vc_ctx* ctx, const uint8_t* rendered, const uint8_t* ground, int32_t w, int32_t h, double* out);
+vc_status vc_distance_transform(vc_ctx* ctx, const uint8_t* mask, int32_t w, int32_t h, float* out);
+vc_status vc_hausdorff2d(vc_ctx* ctx, const uint8_t* rendered, const uint8_t* ground, int32_t w, int32_t h,
+                         double* out, int32_t* has_value);
+vc_status vc_cp_rmse(vc_ctx* ctx, const double* ground, int32_t n_ground, const double* recon, int32_t n_recon,
+                     double* out);
+typedef struct vc_wms3im_options { /* metrics.hpp:30-41 */
+  int32_t scales;
+  double alpha[3], beta[3], gamma[3];
+  double c1, c2, c3;
+  int32_t window;
+  double sigma;
+} vc_wms3im_options;
+/* opt NULL = the reference's defaults; *has_value = 0 for an empty silhouette. */
+vc_status vc_wms3im(vc_ctx* ctx, const uint8_t* rendered, const uint8_t* ground, const uint8_t* silhouette, int32_t w,
+                    int32_t h, const vc_wms3im_options* opt, double* out, int32_t* has_value);
+
 /* ------------------------------------------------------- synthetic capture
  * The reference's synthetic fixture (synth/capsule.cpp, scene.cpp,
  * render.cpp), rendered on the GPU.  Body layout: 15 joints (xyz), 14 radii,

@@ -86,6 +86,12 @@ class PngHeader(C.Structure):
     _fields_ = [(n, C.c_int32) for n in ("width", "height", "bit_depth", "color_type")]
 
 
+class Wms3imOptions(C.Structure):
+    _fields_ = [("scales", C.c_int32), ("alpha", C.c_double * 3), ("beta", C.c_double * 3), ("gamma", C.c_double * 3),
+                ("c1", C.c_double), ("c2", C.c_double), ("c3", C.c_double), ("window", C.c_int32),
+                ("sigma", C.c_double)]
+
+
 class Body(C.Structure):
     _fields_ = [("joints", C.c_double * 45), ("radii", C.c_double * 14), ("colors", C.c_uint8 * 42)]
 
