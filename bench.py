@@ -375,6 +375,15 @@ def run_gpu(args):
     run_steps(host_views, max(args.warmup, S))
     e2e_ms, _, d2h_per = timed(host_views, args.steps)
     e2e_value = total_frames / (e2e_ms / 1000.0)
+    split = None
+    if os.environ.get("VC_E2E_SPLIT"):  # diagnostics: H2D only / D2H only
+        for c in ctxs:
+            lib.vc_ctx_set_output(c.handle, L.VC_MEM_DEVICE)
+        h2d_ms, _, _ = timed(host_views, args.steps)
+        for c in ctxs:
+            lib.vc_ctx_set_output(c.handle, L.VC_MEM_HOST)
+        d2h_ms, _, _ = timed(dev_views, args.steps)
+        split = {"h2d_only_fps": total_frames / (h2d_ms / 1000.0), "d2h_only_fps": total_frames / (d2h_ms / 1000.0)}
 
     if rank == 0:
         cpu = cpu_baseline_sample() if (world == 1 and not args.no_cpu_baseline) else None
@@ -402,6 +411,8 @@ def run_gpu(args):
             "clocks": clk.summary(),
             "wall_s": wall,
         }
+        if split:
+            line["e2e_split"] = split
         if cpu:
             line["cpu_baseline"] = cpu
         print(json.dumps(line), flush=True)

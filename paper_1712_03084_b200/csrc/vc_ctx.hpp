@@ -55,6 +55,7 @@ struct vc_ctx {
   // mesh + texture
   Buf m_pos, m_nrm, m_tri, m_eid, m_cells, m_celltri, m_cellcfg, m_posf, t_vis, t_uv, t_w, t_untex, t_rgb;
   int v_cap = 0, t_cap = 0, c_cap = 0;
+  int spec_v = 0, spec_t = 0;  // host output: sizes copied speculatively behind the next frame
   // host outputs (pinned)
   HostBuf h_posf, h_nrm, h_tri, h_vis, h_uv, h_w, h_untex, h_rgb, h_pos, h_eid;
   // stage-API host scratch, device scratch of the colour-correction entry points

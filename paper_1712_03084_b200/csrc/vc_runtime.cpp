@@ -432,6 +432,7 @@ vc_status copy_out(vc_ctx* ctx, int V, int T, int k, vc_textured_mesh* out) {
     VC_CUDA(d2h(ctx->h_untex, ctx->t_untex, (size_t)V));
     VC_CUDA(d2h(ctx->h_rgb, ctx->t_rgb, (size_t)V * 3));
     VC_CUDA(d2h(ctx->h_pos, ctx->m_pos, (size_t)V * 24));
+    if (!out) return VC_OK;  // speculative copies (pointers set later)
     out->positions = (const float*)ctx->h_posf.p, out->normals = (const float*)ctx->h_nrm.p;
     out->triangles = (const int32_t*)ctx->h_tri.p, out->visible = (const uint8_t*)ctx->h_vis.p;
     out->uv = (const float*)ctx->h_uv.p, out->weight = (const float*)ctx->h_w.p;
@@ -600,7 +601,19 @@ vc_status vc_reconstruct_frame(vc_ctx* ctx, const vc_sensor* sensors, const vc_v
   vc_status s = run_frame(ctx, f);
   ctx->profiling = prof_saved;
   if (s != VC_OK) return s;
-  VC_TRY(read_ctl(ctx));
+  // Host output: copy the outputs at the previous frame's sizes (+12%) right
+  // behind the frame, with the control block, and synchronise once; only a
+  // larger mesh needs a second round (the per-sensor arrays are laid out by
+  // the actual V, so a longer copy covers them).
+  int spec_v = 0, spec_t = 0;
+  if (ctx->out_kind == VC_MEM_HOST && ctx->spec_v > 0 && !prof) {
+    spec_v = std::min(ctx->spec_v, ctx->v_cap), spec_t = std::min(ctx->spec_t, ctx->t_cap);
+    VC_CUDA(cudaMemcpyAsync(ctx->ctl_h, ctx->ctl, sizeof(DevCtl), cudaMemcpyDeviceToHost, ctx->st));
+    VC_TRY(copy_out(ctx, spec_v, spec_t, k, nullptr));
+    VC_CUDA(cudaStreamSynchronize(ctx->st));
+  } else {
+    VC_TRY(read_ctl(ctx));
+  }
   const DevCtl& c = *ctx->ctl_h;
   if (c.status == 2) return fail(ctx, VC_ERR_EMPTY_SCENE, "reconstruct_frame: empty foreground in all views");
   if (c.status != 0) return fail(ctx, VC_ERR_CUDA, "preprocess failed");
@@ -614,6 +627,7 @@ vc_status vc_reconstruct_frame(vc_ctx* ctx, const vc_sensor* sensors, const vc_v
     VC_CUDA(cudaGetLastError());
     VC_TRY(read_ctl(ctx));
     if (ctx->ctl_h->overflow) return fail(ctx, VC_ERR_CAPACITY, "marching cubes capacity");
+    spec_v = spec_t = 0;
   }
   const int V = ctx->ctl_h->V, T = ctx->ctl_h->T;
   std::memset(out, 0, sizeof(*out));
@@ -624,9 +638,14 @@ vc_status vc_reconstruct_frame(vc_ctx* ctx, const vc_sensor* sensors, const vc_v
   out->grid.edge_mm = ctx->ctl_h->grid.edge;
   out->mem_kind = ctx->out_kind;
   if (prof) record_event(ctx->ev[10], ctx->st);
-  VC_TRY(copy_out(ctx, V, T, k, out));
+  if (spec_v >= V && spec_t >= T && V > 0) {
+    VC_TRY(copy_out(ctx, 0, 0, k, out));  // already copied: pointers only
+  } else {
+    VC_TRY(copy_out(ctx, V, T, k, out));
+  }
   if (prof) record_event(ctx->ev[11], ctx->st);
   VC_CUDA(cudaStreamSynchronize(ctx->st));
+  if (ctx->out_kind == VC_MEM_HOST) ctx->spec_v = V + V / 8 + 1024, ctx->spec_t = T + T / 8 + 2048;
   if (timings) {
     std::memset(timings, 0, sizeof(*timings));
     timings->h2d_ms = ev_ms(ctx, 8, 9);
