@@ -412,3 +412,52 @@ def test_mask_derived_on_device_and_ply_export(scene, ctx, tmp_path):
     t = b.textured
     assert open(p, "rb").read() == OI.write_ply(t.mesh.vertices, t.mesh.triangles, t.mesh.normals,
                                                 OI.with_channels(t.visible, t.uv, t.weight, t.untextured))
+
+
+def test_r_mode_grid_matches_oracle(O, scene, ctx):
+    """ReconConfig.r (reconstruct.hpp:12-18: 2^r x 2^(r+1) x 2^r) end to end."""
+    rig, _, frames, orig = scene
+    rec = vc.reconstruct_frame(frames, rig, vc.ReconConfig(r=6), ctx=ctx, want_volume=True)
+    assert rec.volume.values.shape == (64, 128, 64)
+    ref = oracle_frame(O, orig, frames, dims=(64, 128, 64))
+    assert rel_l2(rec.volume.values, ref.volume) < REL_L2_A
+    d1, _ = cKDTree(ref.mesh.vertices).query(rec.mesh.vertices)
+    assert d1.max() <= HAUSDORFF_VOX * ref.grid.edge
+
+
+def test_mc_capacity_overflow_retry(O, ctx):
+    """A noise field with far more cut edges than the initial capacity (N/16):
+    the GPU grows its buffers and reruns, topology still bit-exact."""
+    rng = np.random.default_rng(77)
+    A = rng.uniform(-1, 1, (40, 40, 40)).astype(np.float32)
+    m = _mc_compare(O, ctx, A, 0.0)
+    assert len(m.vertices) > 40 ** 3 // 16
+
+
+def test_concurrent_contexts_threads(scene):
+    """One context per host thread, frames in flight together (the bench's mode):
+    each thread's results equal a sequential run's."""
+    import threading
+    rig, _, frames, _ = scene
+    kick = [[vc.render_frame(rig, vc.kick_body(300, f), k) for k in range(4)] for f in (0, 90, 180, 270)]
+    cfg = vc.ReconConfig(dims=(128, 128, 128))
+    seq_ctx = vc.Context(0)
+    ref = [vc.reconstruct_frame(fr, rig, cfg, ctx=seq_ctx) for fr in kick]
+    seq_ctx.close()
+    ctxs = [vc.Context(0) for _ in kick]
+    out = [None] * len(kick)
+
+    def work(i):
+        for _ in range(3):
+            out[i] = vc.reconstruct_frame(kick[i], rig, cfg, ctx=ctxs[i])
+
+    ts = [threading.Thread(target=work, args=(i,)) for i in range(len(kick))]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    for a, b in zip(out, ref):
+        assert np.array_equal(a.mesh.triangles, b.mesh.triangles) or abs(len(a.mesh.vertices) - len(b.mesh.vertices)) <= 2
+        assert abs(len(a.mesh.vertices) - len(b.mesh.vertices)) <= 0.002 * len(b.mesh.vertices)
+    for c in ctxs:
+        c.close()
