@@ -848,14 +848,11 @@ size_t spectrum_elems(int nx, int ny, int nz) { return (size_t)hpitch(nx) * ny *
 size_t twiddle_elems(int nx, int ny, int nz) { return (size_t)nx + ny + nz; }
 
 void upload_twiddles(float2* dev, int nx, int ny, int nz, cudaStream_t st) {
-  static bool w32_done = false;
-  if (!w32_done) {
-    float2 w[32];
-    for (int k = 0; k < 32; ++k)
-      w[k] = make_float2((float)std::cos(-2.0 * M_PI * k / 32.0), (float)std::sin(-2.0 * M_PI * k / 32.0));
-    cudaMemcpyToSymbol(c_w32, w, sizeof(w));
-    w32_done = true;
-  }
+  // __constant__ data is per device: upload with every table (cheap, on the caller's device)
+  float2 w[32];
+  for (int k = 0; k < 32; ++k)
+    w[k] = make_float2((float)std::cos(-2.0 * M_PI * k / 32.0), (float)std::sin(-2.0 * M_PI * k / 32.0));
+  cudaMemcpyToSymbolAsync(c_w32, w, sizeof(w), 0, cudaMemcpyHostToDevice, st);
   std::vector<float2> h;
   for (int n : {nx, ny, nz})
     for (int m = 0; m < n; ++m)

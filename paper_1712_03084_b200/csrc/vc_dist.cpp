@@ -33,6 +33,7 @@
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <type_traits>
 #include <vector>
@@ -68,10 +69,9 @@ struct Nccl {
 
 const Nccl* nccl_lib(std::string* why) {
   static Nccl lib;
-  static bool tried = false;
   static std::string err;
-  if (!tried) {
-    tried = true;
+  static std::once_flag once;
+  std::call_once(once, [] {
     const char* env = std::getenv("VC_NCCL_LIB");
     const char* names[] = {env, "libnccl.so.2", "libnccl.so"};
     for (const char* n : names) {
@@ -97,7 +97,7 @@ const Nccl* nccl_lib(std::string* why) {
       sym(lib.AllGather, "ncclAllGather");
       sym(lib.GetErrorString, "ncclGetErrorString");
     }
-  }
+  });
   if (!err.empty()) {
     if (why) *why = err;
     return nullptr;
