@@ -461,3 +461,16 @@ def test_concurrent_contexts_threads(scene):
         assert abs(len(a.mesh.vertices) - len(b.mesh.vertices)) <= 0.002 * len(b.mesh.vertices)
     for c in ctxs:
         c.close()
+
+
+def test_sixteen_views(O, ctx):
+    """The maximum sensor count (kMaxViews = 16): field and mesh vs the oracle."""
+    rig = vc.make_circle_rig(16, 0, 2500, 256, 212, 182)
+    orig = O.make_circle_rig(16, 0, 2500, 1000, 256, 212, 182)
+    body = vc.kick_body(300, 150)
+    frames = [vc.render_frame(rig, body, k) for k in range(16)]
+    rec = vc.reconstruct_frame(frames, rig, vc.ReconConfig(dims=(64, 64, 64)), ctx=ctx, want_volume=True)
+    ref = oracle_frame(O, orig, frames, dims=(64, 64, 64))
+    assert rel_l2(rec.volume.values, ref.volume) < REL_L2_A
+    assert rec.textured.visible.shape == (16, len(rec.mesh.vertices))
+    assert rec.textured.visible.any(0).mean() > 0.9
