@@ -628,17 +628,26 @@ void launch_marching_cubes_count(const float* A, DevCtl* ctl, MeshBufs mb, int n
 }
 
 void launch_marching_cubes_emit(const float* A, DevCtl* ctl, MeshBufs mb, int nx, int ny, int nz, McSlab sl,
-                                cudaStream_t st) {
+                                cudaStream_t st, cudaStream_t aux, cudaEvent_t fork, cudaEvent_t join) {
   int3* ucnt = reinterpret_cast<int3*>(mb.unitcnt);
   mc_emit_kernel<<<148 * 8, 256, 0, st>>>(A, ctl, nx, ny, nz, sl, mb.units, ucnt, mb);
-  mc_normals_kernel<<<148 * 4, 256, 0, st>>>(A, ctl, nx, ny, nz, mb);
-  mc_tris_kernel<<<148 * 4, 256, 0, st>>>(A, ctl, nx, ny, nz, mb);
+  if (aux) {  // normals and triangles are independent: normals on the side stream
+    cudaEventRecord(fork, st);
+    cudaStreamWaitEvent(aux, fork, 0);
+    mc_normals_kernel<<<148 * 4, 256, 0, aux>>>(A, ctl, nx, ny, nz, mb);
+    cudaEventRecord(join, aux);
+    mc_tris_kernel<<<148 * 4, 256, 0, st>>>(A, ctl, nx, ny, nz, mb);
+  } else {
+    mc_normals_kernel<<<148 * 4, 256, 0, st>>>(A, ctl, nx, ny, nz, mb);
+    mc_tris_kernel<<<148 * 4, 256, 0, st>>>(A, ctl, nx, ny, nz, mb);
+  }
 }
 
-void launch_marching_cubes(const float* A, DevCtl* ctl, MeshBufs mb, int nx, int ny, int nz, cudaStream_t st) {
+void launch_marching_cubes(const float* A, DevCtl* ctl, MeshBufs mb, int nx, int ny, int nz, cudaStream_t st,
+                           cudaStream_t aux, cudaEvent_t fork, cudaEvent_t join) {
   const McSlab whole{0, nz, nz};
   launch_marching_cubes_count(A, ctl, mb, nx, ny, nz, whole, st);
-  launch_marching_cubes_emit(A, ctl, mb, nx, ny, nz, whole, st);
+  launch_marching_cubes_emit(A, ctl, mb, nx, ny, nz, whole, st, aux, fork, join);
 }
 
 void launch_iso_samples(const DevPoints& pts, const float* A, const DevCtl* ctl, int zoff, int nzl, double* samples,

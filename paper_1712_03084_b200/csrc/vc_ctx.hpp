@@ -35,6 +35,8 @@ struct vc_ctx {
   static constexpr int kEvents = vc::rt::kEvents;
   int device = 0;
   cudaStream_t st = nullptr;
+  cudaStream_t aux = nullptr;        // side stream: branches of the frame graph
+  cudaEvent_t fork[2] = {}, join[2] = {};
   std::string err;
   int out_kind = VC_MEM_HOST;
   bool profiling = false;

@@ -301,14 +301,30 @@ int enqueue_frame(vc_ctx* ctx, const FrameCfg& f) {
   int n = 0;
   // the clear walks the previous frame's touched-row list: before the
   // preprocess, whose scan resets the list for this frame's splat
+  // Graph branches (not in profiled frames, which time each kernel on one
+  // stream): the clear runs beside the preprocess, the MC normals beside the
+  // triangles and texturing.
+  const bool branch = !ctx->profiling && ctx->aux;
   record(ctx, 12);
-  launch_sparse_clear(P<float4>(ctx->acc), P<uint32_t>(ctx->rowbits), P<int32_t>(ctx->rowlist), f.nx, st);
+  if (branch) {
+    cudaEventRecord(ctx->fork[0], st);
+    cudaStreamWaitEvent(ctx->aux, ctx->fork[0], 0);
+  }
+  launch_sparse_clear(P<float4>(ctx->acc), P<uint32_t>(ctx->rowbits), P<int32_t>(ctx->rowlist), f.nx,
+                      branch ? ctx->aux : st);
+  if (branch) cudaEventRecord(ctx->join[0], ctx->aux);
   record(ctx, 13);
   record(ctx, 0);
+  // (the clear reads the previous touched-row list; the list is reset once
+  // the clear has joined, just before this frame's splat appends to it)
   launch_preprocess(ctx->ss, points(ctx), P<float>(ctx->wmaps), P<int32_t>(ctx->pre_scratch), ctx->ctl, f.nx, f.ny,
-                    f.nz, f.pad, f.disc, f.sil_r, st, P<int32_t>(ctx->rowlist));
+                    f.nz, f.pad, f.disc, f.sil_r, st, branch ? nullptr : P<int32_t>(ctx->rowlist));
   n += 6;
   record(ctx, 1);
+  if (branch) {
+    cudaStreamWaitEvent(st, ctx->join[0], 0);
+    cudaMemsetAsync(ctx->rowlist.p, 0, sizeof(int32_t), st);
+  }
   launch_splat(points(ctx), ctx->ctl, P<float4>(ctx->acc), P<uint32_t>(ctx->rowbits), P<int32_t>(ctx->rowlist),
                f.mode, st, 0, f.nz);
   n += 2;
@@ -321,13 +337,15 @@ int enqueue_frame(vc_ctx* ctx, const FrameCfg& f) {
   launch_iso_level(points(ctx), P<float>(ctx->A), ctx->ctl, P<double>(ctx->iso_partial), 1024, st);
   n += 2;
   record(ctx, 4);
-  launch_marching_cubes(P<float>(ctx->A), ctx->ctl, mesh_bufs(ctx), f.nx, f.ny, f.nz, st);
+  launch_marching_cubes(P<float>(ctx->A), ctx->ctl, mesh_bufs(ctx), f.nx, f.ny, f.nz, st, branch ? ctx->aux : nullptr,
+                        ctx->fork[1], ctx->join[1]);
   n += 7;
   record(ctx, 5);
   launch_texture(ctx->ss, P<float>(ctx->wmaps), P<double>(ctx->m_pos), ctx->ctl, f.eps_vis, P<uint8_t>(ctx->t_vis),
                  P<float2>(ctx->t_uv), P<float>(ctx->t_w), P<uint8_t>(ctx->t_untex), P<uint8_t>(ctx->t_rgb),
                  ctx->v_cap, st, P<float>(ctx->m_posf));
   n += 1;
+  if (branch) cudaStreamWaitEvent(st, ctx->join[1], 0);  // the normals branch rejoins
   record(ctx, 6);
   return n;
 }
@@ -478,6 +496,11 @@ vc_status vc_ctx_create(int device, vc_ctx** out) {
   };
   if (cudaSetDevice(device) != cudaSuccess) return cleanup(VC_ERR_CUDA);
   if (cudaStreamCreateWithFlags(&ctx->st, cudaStreamNonBlocking) != cudaSuccess) return cleanup(VC_ERR_CUDA);
+  if (cudaStreamCreateWithFlags(&ctx->aux, cudaStreamNonBlocking) != cudaSuccess) return cleanup(VC_ERR_CUDA);
+  for (int i = 0; i < 2; ++i)
+    if (cudaEventCreateWithFlags(&ctx->fork[i], cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ctx->join[i], cudaEventDisableTiming) != cudaSuccess)
+      return cleanup(VC_ERR_CUDA);
   if (cudaMalloc(&ctx->ctl, sizeof(DevCtl)) != cudaSuccess) return cleanup(VC_ERR_OOM);
   if (cudaMemset(ctx->ctl, 0, sizeof(DevCtl)) != cudaSuccess) return cleanup(VC_ERR_CUDA);
   if (cudaHostAlloc(&ctx->ctl_h, sizeof(DevCtl), cudaHostAllocDefault) != cudaSuccess) return cleanup(VC_ERR_OOM);
@@ -501,6 +524,11 @@ vc_status vc_ctx_destroy(vc_ctx* ctx) {
   for (HostBuf* b : {&ctx->h_posf, &ctx->h_nrm, &ctx->h_tri, &ctx->h_vis, &ctx->h_uv, &ctx->h_w, &ctx->h_untex,
                      &ctx->h_rgb, &ctx->h_pos, &ctx->h_eid})
     if (b->p) cudaFreeHost(b->p);
+  if (ctx->aux) cudaStreamSynchronize(ctx->aux), cudaStreamDestroy(ctx->aux);
+  for (int i = 0; i < 2; ++i) {
+    if (ctx->fork[i]) cudaEventDestroy(ctx->fork[i]);
+    if (ctx->join[i]) cudaEventDestroy(ctx->join[i]);
+  }
   if (ctx->ctl) cudaFree(ctx->ctl);
   if (ctx->ctl_h) cudaFreeHost(ctx->ctl_h);
   for (auto& e : ctx->ev)

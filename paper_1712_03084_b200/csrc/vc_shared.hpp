@@ -159,7 +159,10 @@ int iso_blocks();
 void launch_iso_level(const DevPoints& pts, const float* A, DevCtl* ctl, double* partial, int nblk_max,
                       cudaStream_t st);
 int mc_blocks(int nx, int ny, int nz);
-void launch_marching_cubes(const float* A, DevCtl* ctl, MeshBufs mb, int nx, int ny, int nz, cudaStream_t st);
+// aux/fork/join (nullable): run the normals on `aux` beside the triangles; the
+// caller waits on `join` before the frame ends
+void launch_marching_cubes(const float* A, DevCtl* ctl, MeshBufs mb, int nx, int ny, int nz, cudaStream_t st,
+                           cudaStream_t aux = nullptr, cudaEvent_t fork = nullptr, cudaEvent_t join = nullptr);
 // Slab variant: units (voxel rows) of planes [z0, z0+nzu); planes >= zend
 // belong to the next rank: their cut edges are numbered (vbase) but neither
 // emitted nor meshed.  A, vbase are indexed with GLOBAL voxel ids (callers
@@ -172,7 +175,8 @@ struct McSlab {
 void launch_marching_cubes_count(const float* A, DevCtl* ctl, MeshBufs mb, int nx, int ny, int nz, McSlab sl,
                                  cudaStream_t st);
 void launch_marching_cubes_emit(const float* A, DevCtl* ctl, MeshBufs mb, int nx, int ny, int nz, McSlab sl,
-                                cudaStream_t st);
+                                cudaStream_t st, cudaStream_t aux = nullptr, cudaEvent_t fork = nullptr,
+                                cudaEvent_t join = nullptr);
 // Slab iso level: samples[p] = trilinear(A, point p) if this rank owns the
 // point's lower z plane, else 0 (summed over ranks, then launch_iso_final_samples)
 void launch_iso_samples(const DevPoints& pts, const float* A, const DevCtl* ctl, int zoff, int nzl, double* samples,
