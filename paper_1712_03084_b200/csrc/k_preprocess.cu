@@ -17,10 +17,11 @@
 //   pre_points  one thread per pixel: the six incident triangles in the
 //               reference's accumulation order (cloud.cpp:53-71), world
 //               position/normal (:73-74), W = W1*W2 (:108-114) -> per-pixel
-//               staging slot + flag, weight map, per-segment count and bbox
-//   pre_scan    exclusive scan of the segment counts (single CTA) -> P
+//               staging slot + flag, weight map, per-segment count; the
+//               bbox is folded in with atomic min/max on order-preserving keys
+//   pre_scan    exclusive scan of the segment counts (single CTA) -> P,
+//               empty-scene status, fit_grid from the bbox
 //   pre_gather  one thread per pixel: staged points -> final SoA in order
-//   pre_fit     bbox reduction + fit_grid + empty-scene status
 // fp64 with the reference's operation order and no FMA (vc_device.cuh), so
 // positions — hence every downstream binning decision — are bit-exact.
 #include <cfloat>
@@ -31,6 +32,16 @@ namespace vc {
 namespace {
 
 constexpr int kSeg = 128;  // pixels per segment (= threads per CTA)
+
+// Order-preserving map double -> u64 (for finite values and +-inf), so the
+// bounding box is an exact atomic min/max whatever the order of updates.
+__device__ __forceinline__ unsigned long long dkey(double d) {
+  const unsigned long long b = (unsigned long long)__double_as_longlong(d);
+  return (b >> 63) ? ~b : b ^ 0x8000000000000000ull;
+}
+__device__ __forceinline__ double dunkey(unsigned long long k) {
+  return __longlong_as_double((long long)((k >> 63) ? k ^ 0x8000000000000000ull : ~k));
+}
 
 __device__ __forceinline__ void row_of(const SensorSet& ss, int r, int* k, int* y) {
   int kk = 0;
@@ -53,7 +64,8 @@ __device__ __forceinline__ d3 local_px(const DevSensor& s, const ViewPtrs& v, in
 
 // inclusive prefix of (mask != 0) along each row (lane = 16 consecutive pixels)
 __global__ void __launch_bounds__(256) pre_prefix_kernel(const __grid_constant__ SensorSet ss, int rows,
-                                                         uint16_t* __restrict__ pref, int pitch) {
+                                                         uint16_t* __restrict__ pref, int pitch, DevCtl* ctl) {
+  if (blockIdx.x == 0 && threadIdx.x < 6) ctl->bbox_key[threadIdx.x] = threadIdx.x < 3 ? ~0ull : 0ull;
   const int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (r >= rows) return;
   int k, y;
@@ -141,8 +153,7 @@ __global__ void __launch_bounds__(kSeg) pre_points_kernel(const __grid_constant_
                                                           const double* __restrict__ tri,
                                                           const uint16_t* __restrict__ pref, int ppitch,
                                                           Staged* __restrict__ stage, uint8_t* __restrict__ flags,
-                                                          int32_t* __restrict__ seg_counts,
-                                                          double* __restrict__ seg_bbox,
+                                                          int32_t* __restrict__ seg_counts, DevCtl* ctl,
                                                           float* __restrict__ weight_maps) {
   __shared__ int wc[kSeg / 32];
   __shared__ double bb[kSeg / 32][6];
@@ -228,12 +239,14 @@ __global__ void __launch_bounds__(kSeg) pre_points_kernel(const __grid_constant_
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const unsigned ball = __ballot_sync(0xffffffffu, is_pt);
   double lo[3] = {p.x, p.y, p.z}, hi[3] = {is_pt ? p.x : -inf, is_pt ? p.y : -inf, is_pt ? p.z : -inf};
+  if (ball != 0u) {  // warp-uniform: most warps of a frame hold no point
 #pragma unroll
-  for (int a = 0; a < 3; ++a)
-    for (int o = 16; o > 0; o >>= 1) {
-      lo[a] = fmin(lo[a], __shfl_xor_sync(0xffffffffu, lo[a], o));
-      hi[a] = fmax(hi[a], __shfl_xor_sync(0xffffffffu, hi[a], o));
-    }
+    for (int a = 0; a < 3; ++a)
+      for (int o = 16; o > 0; o >>= 1) {
+        lo[a] = fmin(lo[a], __shfl_xor_sync(0xffffffffu, lo[a], o));
+        hi[a] = fmax(hi[a], __shfl_xor_sync(0xffffffffu, hi[a], o));
+      }
+  }
   if (lane == 0) {
     wc[wid] = __popc(ball);
     for (int a = 0; a < 3; ++a) bb[wid][a] = lo[a], bb[wid][3 + a] = hi[a];
@@ -247,13 +260,21 @@ __global__ void __launch_bounds__(kSeg) pre_points_kernel(const __grid_constant_
   if (threadIdx.x < 6) {
     double r = bb[0][threadIdx.x];
     for (int i = 1; i < kSeg / 32; ++i) r = threadIdx.x < 3 ? fmin(r, bb[i][threadIdx.x]) : fmax(r, bb[i][threadIdx.x]);
-    seg_bbox[(size_t)seg * 6 + threadIdx.x] = r;
+    if (r != inf && r != -inf) {  // this segment holds points
+      if (threadIdx.x < 3)
+        atomicMin(&ctl->bbox_key[threadIdx.x], dkey(r));
+      else
+        atomicMax(&ctl->bbox_key[threadIdx.x], dkey(r));
+    }
   }
 }
 
 // single CTA: exclusive scan of the segment counts (contiguous runs per thread)
+__device__ void fit_grid_dev(DevCtl* ctl, int nx, int ny, int nz, int pad);
+
 __global__ void __launch_bounds__(1024) pre_scan_kernel(const int32_t* counts, int32_t* offsets, int n, int cap,
-                                                        DevCtl* ctl, int32_t* rowlist_reset) {
+                                                        DevCtl* ctl, int32_t* rowlist_reset, int nx, int ny, int nz,
+                                                        int pad) {
   __shared__ int wsum[32];
   const int per = (n + 1023) / 1024;
   const int b0 = min(n, (int)threadIdx.x * per), b1 = min(n, b0 + per);
@@ -293,6 +314,7 @@ __global__ void __launch_bounds__(1024) pre_scan_kernel(const int32_t* counts, i
     ctl->status = P == 0 ? 2 : (P > cap ? 3 : 0);
     ctl->voff = 0;
     if (rowlist_reset) *rowlist_reset = 0;  // the frame's clear (launched before) has read the previous list
+    fit_grid_dev(ctl, nx, ny, nz, pad);
   }
 }
 
@@ -323,35 +345,11 @@ __global__ void __launch_bounds__(kSeg) pre_gather_kernel(const __grid_constant_
   pts.pix[3 * idx + 0] = x, pts.pix[3 * idx + 1] = y, pts.pix[3 * idx + 2] = k;
 }
 
-// reconstruct.cpp:56-68 (bbox) + fit_grid (reconstruct.cpp:16-35, dims given)
-__global__ void __launch_bounds__(1024) pre_fit_kernel(const double* seg_bbox, int nseg, int nx, int ny, int nz,
-                                                       int pad, DevCtl* ctl) {
-  __shared__ double sh[6][32];
-  const double inf = DBL_MAX * 2.0;
-  double r[6] = {inf, inf, inf, -inf, -inf, -inf};
-  for (int i = threadIdx.x; i < nseg; i += 1024) {
-#pragma unroll
-    for (int a = 0; a < 3; ++a) {
-      r[a] = fmin(r[a], seg_bbox[(size_t)i * 6 + a]);
-      r[3 + a] = fmax(r[3 + a], seg_bbox[(size_t)i * 6 + 3 + a]);
-    }
-  }
-#pragma unroll
-  for (int a = 0; a < 6; ++a)
-    for (int o = 16; o > 0; o >>= 1) {
-      const double t = __shfl_xor_sync(0xffffffffu, r[a], o);
-      r[a] = a < 3 ? fmin(r[a], t) : fmax(r[a], t);
-    }
-  if ((threadIdx.x & 31) == 0)
-    for (int a = 0; a < 6; ++a) sh[a][threadIdx.x >> 5] = r[a];
-  __syncthreads();
-  if (threadIdx.x != 0) return;
-  for (int a = 0; a < 6; ++a) {
-    double t = sh[a][0];
-    for (int i = 1; i < 32; ++i) t = a < 3 ? fmin(t, sh[a][i]) : fmax(t, sh[a][i]);
-    r[a] = t;
-    ctl->bbox[a] = t;
-  }
+// reconstruct.cpp:56-68 (bbox) + fit_grid (reconstruct.cpp:16-35, dims given);
+// one thread, after the scan has set the status
+__device__ void fit_grid_dev(DevCtl* ctl, int nx, int ny, int nz, int pad) {
+  double r[6];
+  for (int a = 0; a < 6; ++a) r[a] = ctl->bbox[a] = dunkey(ctl->bbox_key[a]);
   DevGrid g;
   g.nx = nx, g.ny = ny, g.nz = nz;
   if (ctl->status != 0) {
@@ -382,7 +380,6 @@ struct Scratch {
   uint16_t* pref;     // rows x ppitch
   int32_t* counts;    // per segment
   int32_t* offsets;   // per segment
-  double* bbox;       // 6 per segment
   int ppitch, spr, nseg;
 };
 
@@ -408,8 +405,6 @@ Scratch carve(const SensorSet& ss, void* base) {
   s.counts = reinterpret_cast<int32_t*>(p);
   p = up(p + (size_t)s.nseg * sizeof(int32_t));
   s.offsets = reinterpret_cast<int32_t*>(p);
-  p = up(p + (size_t)s.nseg * sizeof(int32_t));
-  s.bbox = reinterpret_cast<double*>(p);
   return s;
 }
 
@@ -429,7 +424,7 @@ void prepare_preprocess(const SensorSet&) {}  // no opt-in shared memory needed
 
 size_t preprocess_scratch_bytes(const SensorSet& ss) {
   const Scratch s = carve(ss, nullptr);
-  return reinterpret_cast<uintptr_t>(s.bbox) + (size_t)s.nseg * 6 * sizeof(double) + 512;
+  return reinterpret_cast<uintptr_t>(s.offsets) + (size_t)s.nseg * sizeof(int32_t) + 512;
 }
 
 void launch_preprocess(const SensorSet& ss, DevPoints pts, float* weight_maps, int32_t* scratch, DevCtl* ctl,
@@ -438,13 +433,12 @@ void launch_preprocess(const SensorSet& ss, DevPoints pts, float* weight_maps, i
   const int rows = ss.row_offset[ss.k];
   const Scratch s = carve(ss, scratch);
   const dim3 grid(s.spr, rows);
-  pre_prefix_kernel<<<(rows * 32 + 255) / 256, 256, 0, st>>>(ss, rows, s.pref, s.ppitch);
+  pre_prefix_kernel<<<(rows * 32 + 255) / 256, 256, 0, st>>>(ss, rows, s.pref, s.ppitch, ctl);
   pre_tri_kernel<<<grid, kSeg, 0, st>>>(ss, disc_mm, s.tri);
-  pre_points_kernel<<<grid, kSeg, 0, st>>>(ss, sil_r, s.tri, s.pref, s.ppitch, s.stage, s.flags, s.counts, s.bbox,
+  pre_points_kernel<<<grid, kSeg, 0, st>>>(ss, sil_r, s.tri, s.pref, s.ppitch, s.stage, s.flags, s.counts, ctl,
                                            weight_maps);
-  pre_scan_kernel<<<1, 1024, 0, st>>>(s.counts, s.offsets, s.nseg, pts.cap, ctl, rowlist_reset);
+  pre_scan_kernel<<<1, 1024, 0, st>>>(s.counts, s.offsets, s.nseg, pts.cap, ctl, rowlist_reset, nx, ny, nz, padding);
   pre_gather_kernel<<<grid, kSeg, 0, st>>>(ss, s.stage, s.flags, s.offsets, pts);
-  pre_fit_kernel<<<1, 1024, 0, st>>>(s.bbox, s.nseg, nx, ny, nz, padding, ctl);
 }
 
 }  // namespace vc

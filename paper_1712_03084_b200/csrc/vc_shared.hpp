@@ -62,6 +62,7 @@ struct DevCtl {
   int32_t voff;       // MC slab: global id of this rank's first vertex
   int32_t pad;
   double bbox[6];
+  unsigned long long bbox_key[6];  // bbox as order-preserving keys (atomic min/max while preprocessing)
   DevGrid grid;
   double level;
 };
