@@ -198,6 +198,17 @@ def alg_bytes(nx, ny, nz, P, V, T, k, chunks, nzrows, nzplanes):
             "mc": 8 * rows, "preprocess": k * W * H * 7 + P * 60, "iso": P * 32, "texture": V * (24 + 13 * k)}
 
 
+def survey_bytes(nx, ny, nz, P, V, T, k):
+    """SURVEY.md §8(d) algorithmic bytes per launch (fp32 device layout, each
+    tensor read once and written once, dense), with the divergence epilogue
+    of Appendix A.4(iv): y-C2C 3 in / 2 out, z-fused 2 in / 1 out."""
+    N = nx * ny * nz
+    Nh = nz * ny * (nx // 2 + 1)
+    return {"preprocess": k * W * H * 7 + P * 32, "splat": 16 * N + 16 * 64 * P, "fft_x": 16 * N + 3 * 8 * Nh,
+            "fft_y": 3 * 8 * Nh + 2 * 8 * Nh, "fft_z": 2 * 8 * Nh + 8 * Nh, "ifft_y": 2 * 8 * Nh,
+            "ifft_x": 8 * Nh + 4 * N, "iso": P * 44, "mc": 4 * N + V * 24 + T * 12, "texture": V * (15 + 13 * k)}
+
+
 def profile_kernels(lib, h, sensors, views_list, cfg, dims, out):
     """Per-stage and per-kernel-group CUDA-event times (profiling replay on
     context h, outside the timed loop) + the roofline of the dominant kernel."""
@@ -236,9 +247,14 @@ def profile_kernels(lib, h, sensors, views_list, cfg, dims, out):
             traffic = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))[dom]["dram_bytes_per_launch"]
         except Exception:
             traffic = None
-    roofline = {"bound": "hbm", "kernel": dom, "achieved": bw[dom], "peak": hbm, "unit": "GB/s",
-                "frac": bw[dom] / hbm, "traffic": traffic,
-                "algorithmic_bytes": ab[dom], "avg_launch_ms": kernel_ms[dom],
+    sb = survey_bytes(*dims, P, V, T, K_VIEWS)
+    alg = sb.get(dom, ab[dom])
+    achieved = alg / (kernel_ms[dom] * 1e-3) / 1e9
+    roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                "frac": achieved / hbm, "traffic": traffic,
+                "algorithmic_bytes": alg, "bytes_source": "SURVEY.md §8(d) (divergence epilogue, dense)",
+                "compulsory_bytes": ab[dom], "frac_compulsory": bw[dom] / hbm,
+                "avg_launch_ms": kernel_ms[dom],
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)" if "_fallback" not in pk else "fallback"}
     return {"stages": acc, "kernel_ms": kernel_ms, "bw": bw, "ab": ab, "roofline": roofline, "P": P, "V": V, "T": T,
             "sparse": sp}

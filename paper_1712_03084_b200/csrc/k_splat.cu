@@ -68,7 +68,11 @@ __device__ __forceinline__ void red_add_v4(float4* addr, float4 v) {
 }
 
 // splat.cpp:58-87 weighted mode: 64 threads (two warps) per point, one per support voxel
-// floor(c)-1 .. floor(c)+2 per axis (support_around, splat.cpp:19-29).
+// floor(c)-1 .. floor(c)+2 per axis (support_around, splat.cpp:19-29).  Each
+// 64-thread group walks a contiguous run of points (neighbouring pixels, so
+// mostly the same voxel rows): a row's chunk bits are or-ed in only when they
+// add to what this lane marked for the previous point, which removes most of
+// the row-mask atomics; the reduction is issued before the marking.
 __global__ void __launch_bounds__(kSplatThreads) splat_weighted_kernel(const double* __restrict__ pos,
                                                                        const double* __restrict__ nrm,
                                                                        const double* __restrict__ wgt,
@@ -84,32 +88,58 @@ __global__ void __launch_bounds__(kSplatThreads) splat_weighted_kernel(const dou
   const int ox = sub & 3, oy = (sub >> 2) & 3, oz = sub >> 4;
   // exp(-s/0.75) = exp2(s * k1), exp(-s/1.125) = exp2(s * k2)
   const float k1 = -1.4426950408889634f / 0.75f, k2 = -1.4426950408889634f / 1.125f;
-  for (int p = blockIdx.x * (kSplatThreads / 64) + (threadIdx.x >> 6); p < P; p += gridDim.x * (kSplatThreads / 64)) {
+  const int groups = gridDim.x * (kSplatThreads / 64);
+  const int run = (P + groups - 1) / groups;
+  const int p0 = (blockIdx.x * (kSplatThreads / 64) + (threadIdx.x >> 6)) * run;
+  const int p1 = min(P, p0 + run);
+  int last_row = -1, pend_row = -1;
+  uint32_t last_m = 0u, pend_old = 1u;
+  const int lane = threadIdx.x & 31;
+  const double o = lane == 0 ? g.origin[0] : (lane == 1 ? g.origin[1] : g.origin[2]);
+  // the next point's inputs are loaded while the current one is scattered
+  auto load = [&](int q, double& pc, float4& nw) {
+    pc = lane < 3 ? __ldg(pos + 3 * q + lane) : 0.0;
+    nw = make_float4((float)__ldg(nrm + 3 * q + 0), (float)__ldg(nrm + 3 * q + 1), (float)__ldg(nrm + 3 * q + 2),
+                     (float)__ldg(wgt + q));
+  };
+  double pc_n = 0.0;
+  float4 nw_n = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (p0 < p1) load(p0, pc_n, nw_n);
+  for (int p = p0; p < p1; ++p) {
+    const double pc = pc_n;
+    const float4 nw = nw_n;
+    if (p + 1 < p1) load(p + 1, pc_n, nw_n);
     // to_voxel (volume.hpp:44) once per warp: lanes 0-2 divide one coordinate
     // each (IEEE fp64, bit-exact), the warp shares them by shuffle
-    const int lane = threadIdx.x & 31;
-    double c = 0.0;
-    if (lane < 3) {
-      const double o = lane == 0 ? g.origin[0] : (lane == 1 ? g.origin[1] : g.origin[2]);
-      c = ddiv(dsub(__ldg(pos + 3 * p + lane), o), g.edge);
-    }
+    const double c = lane < 3 ? ddiv(dsub(pc, o), g.edge) : 0.0;
     const double cx = __shfl_sync(0xffffffffu, c, 0), cy = __shfl_sync(0xffffffffu, c, 1),
                  cz = __shfl_sync(0xffffffffu, c, 2);
     const int fx = (int)floor(cx);
     const int x = fx - 1 + ox, y = (int)floor(cy) - 1 + oy, z = (int)floor(cz) - 1 + oz;
     // z-slab [zoff, zoff+nzl) of this rank (the reference's own slab split, splat.cpp:61-77)
     const int zl = z - zoff;
-    if (ox == 0 && y >= 0 && zl >= 0 && y < g.ny && zl < nzl && z < g.nz && fx + 2 >= 0 && fx - 1 < g.nx)
-      mark_chunks(rowbits, rowlist, zl * g.ny + y, max(fx - 1, 0), min(fx + 2, g.nx - 1));
-    if (x < 0 || y < 0 || zl < 0 || x >= g.nx || y >= g.ny || zl >= nzl || z >= g.nz) continue;
-    const float dx = (float)(cx - (double)x), dy = (float)(cy - (double)y), dz = (float)(cz - (double)z);
-    const float s = dx * dx + dy * dy + dz * dz;
-    const float w = (float)__ldg(wgt + p);
-    const float g1w = exp2f(s * k1) * w, g2w = exp2f(s * k2) * w;
-    const float4 v = make_float4(g1w * (float)__ldg(nrm + 3 * p + 0), g1w * (float)__ldg(nrm + 3 * p + 1),
-                                 g1w * (float)__ldg(nrm + 3 * p + 2), g2w);
-    red_add_v4(acc + ((size_t)zl * g.ny + y) * g.nx + x, v);
+    if (x >= 0 && y >= 0 && zl >= 0 && x < g.nx && y < g.ny && zl < nzl && z < g.nz) {
+      const float dx = (float)(cx - (double)x), dy = (float)(cy - (double)y), dz = (float)(cz - (double)z);
+      const float s = dx * dx + dy * dy + dz * dz;
+      const float g1w = exp2f(s * k1) * nw.w, g2w = exp2f(s * k2) * nw.w;
+      red_add_v4(acc + ((size_t)zl * g.ny + y) * g.nx + x, make_float4(g1w * nw.x, g1w * nw.y, g1w * nw.z, g2w));
+    }
+    if (ox == 0 && y >= 0 && zl >= 0 && y < g.ny && zl < nzl && z < g.nz && fx + 2 >= 0 && fx - 1 < g.nx) {
+      const int row = zl * g.ny + y;
+      const int xa = max(fx - 1, 0), xb = min(fx + 2, g.nx - 1);
+      const uint32_t m = (0xffffffffu >> (31 - (xb >> 5))) & (0xffffffffu << (xa >> 5));
+      if (row != last_row || (m & ~last_m) != 0u) {
+        // the previous mark's result is consumed here, one point later, so
+        // the atomic's round trip overlaps this point's scatter
+        const uint32_t old = atomicOr(rowbits + row, m);
+        if (pend_row >= 0 && pend_old == 0u) rowlist[1 + atomicAdd(rowlist, 1)] = pend_row;  // first touch
+        pend_row = row, pend_old = old;
+        last_m = row == last_row ? (last_m | m) : m;
+        last_row = row;
+      }
+    }
   }
+  if (pend_row >= 0 && pend_old == 0u) rowlist[1 + atomicAdd(rowlist, 1)] = pend_row;
 }
 
 // splat.cpp:40-56 simple mode: lround nearest voxel, (sum N, count)
