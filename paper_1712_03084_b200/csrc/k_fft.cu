@@ -372,9 +372,34 @@ struct RowMap {
     return (size_t)(j >> lp) * blkstride + (size_t)(j & ((1 << lp) - 1)) * stride;
   }
 };
+// Uniform row stride: one base address per thread, stepped by RSTEP rows (rows
+// past the pitch or flagged empty are zero-filled, their address is not read).
+template <int N, int CW, int THREADS>
+__device__ __forceinline__ void stage_tile_u(float2* tile, const float2* src, size_t stride, int kx0, int H,
+                                             uint32_t rowmask) {
+  constexpr int CPR = CW / 2, RSTEP = THREADS / CPR, NR = N / RSTEP;
+  const int j0 = threadIdx.x / CPR, c2 = threadIdx.x % CPR;
+  const int kx = kx0 + 2 * c2;
+  const bool colok = kx < H;
+  const float2* p = src + (colok ? (size_t)j0 * stride + kx : (size_t)0);
+  const size_t step = (size_t)RSTEP * stride;
+  float2* t = tile + j0 * CW + 2 * c2;
+#pragma unroll
+  for (int k = 0; k < NR; ++k, p += step) cp_async16(t + k * RSTEP * CW, p, colok && ((rowmask >> k) & 1u));
+}
+
+template <int N, int CW, int THREADS>
+__device__ __forceinline__ void stage_tile(float2* tile, const float2* src, size_t stride, int kx0, int H,
+                                           uint32_t rowmask) {
+  stage_tile_u<N, CW, THREADS>(tile, src, stride, kx0, H, rowmask);
+}
 template <int N, int CW, int THREADS>
 __device__ __forceinline__ void stage_tile(float2* tile, const float2* src, RowMap rm, int kx0, int H,
                                            uint32_t rowmask) {
+  if (rm.lp >= 30 || (N >> rm.lp) <= 1) {  // all N rows in one block: uniform stride (one GPU)
+    stage_tile_u<N, CW, THREADS>(tile, src, rm.stride, kx0, H, rowmask);
+    return;
+  }
   constexpr int CPR = CW / 2, RSTEP = THREADS / CPR, NR = N / RSTEP;
   const int j0 = threadIdx.x / CPR, c2 = threadIdx.x % CPR;
   const int kx = kx0 + 2 * c2;
@@ -384,11 +409,6 @@ __device__ __forceinline__ void stage_tile(float2* tile, const float2* src, RowM
     const bool ok = kx < H && ((rowmask >> k) & 1u);
     cp_async16(tile + j * CW + 2 * c2, ok ? (const void*)(src + rm.off(j) + kx) : (const void*)src, ok);
   }
-}
-template <int N, int CW, int THREADS>
-__device__ __forceinline__ void stage_tile(float2* tile, const float2* src, size_t stride, int kx0, int H,
-                                           uint32_t rowmask) {
-  stage_tile<N, CW, THREADS>(tile, src, RowMap{stride, 0, 31}, kx0, H, rowmask);
 }
 
 // Nyquist tile: column c is the kx = nx/2 column of line group c (another
