@@ -4,7 +4,7 @@
 // (/root/reference/proj/core/src/recon/cloud.cpp:19-117), the foreground
 // bounding box and fit_grid (reconstruct.cpp:16-35, 56-68).
 //
-// Pixel-parallel, with one ordered compaction at the end.  A "segment" is 128
+// Pixel-parallel, with one ordered compaction at the end.  A "segment" is 32
 // consecutive pixels of one depth row; segments are numbered row-major over
 // the rows of all views concatenated, which is the reference's point order
 // (views in sensor order, pixels row-major).
@@ -31,7 +31,10 @@
 namespace vc {
 namespace {
 
-constexpr int kSeg = 128;  // pixels per segment (= threads per CTA)
+constexpr int kSeg = 128;  // pixels (quads) per CTA of pre_tri
+constexpr int kSegPx = 32;  // pixels per segment: one warp, one CTA of pre_points (a CTA
+                            // retires with its slowest warp, so one-warp CTAs let the
+                            // empty segments' slots recycle while point warps compute)
 
 // Order-preserving map double -> u64 (for finite values and +-inf), so the
 // bounding box is an exact atomic min/max whatever the order of updates.
@@ -149,20 +152,18 @@ struct Staged {  // one point (per-pixel staging slot)
   int32_t pad;
 };
 
-__global__ void __launch_bounds__(kSeg) pre_points_kernel(const __grid_constant__ SensorSet ss, int sil_r,
-                                                          const double* __restrict__ tri,
-                                                          const uint16_t* __restrict__ pref, int ppitch,
-                                                          Staged* __restrict__ stage, uint8_t* __restrict__ flags,
-                                                          int32_t* __restrict__ seg_counts, DevCtl* ctl,
-                                                          float* __restrict__ weight_maps) {
-  __shared__ int wc[kSeg / 32];
-  __shared__ double bb[kSeg / 32][6];
+__global__ void __launch_bounds__(kSegPx) pre_points_kernel(const __grid_constant__ SensorSet ss, int sil_r,
+                                                            const double* __restrict__ tri,
+                                                            const uint16_t* __restrict__ pref, int ppitch,
+                                                            Staged* __restrict__ stage, uint8_t* __restrict__ flags,
+                                                            int32_t* __restrict__ seg_counts, DevCtl* ctl,
+                                                            float* __restrict__ weight_maps) {
   int k, y;
   row_of(ss, blockIdx.y, &k, &y);
   const DevSensor& s = ss.s[k];
   const ViewPtrs& v = ss.v[k];
   const int w = s.w, h = s.h;
-  const int x = blockIdx.x * kSeg + threadIdx.x;
+  const int x = blockIdx.x * kSegPx + threadIdx.x;
   const int64_t pix = ss.pix_offset[k] + (int64_t)y * w + x;
   const int seg = blockIdx.y * gridDim.x + blockIdx.x;
   const double inf = DBL_MAX * 2.0;
@@ -208,7 +209,7 @@ __global__ void __launch_bounds__(kSeg) pre_points_kernel(const __grid_constant_
         // cloud.cpp:99-106 W2: (2r+1)^2 window clipped to the image, fixed divisor
         const int xa = max(0, x - sil_r), xb = min(w - 1, x + sil_r);
         const int wy0 = max(0, y - sil_r), wy1 = min(h - 1, y + sil_r);
-        const uint16_t* pr = pref + (size_t)(blockIdx.y - y + wy0) * ppitch;
+        const uint16_t* pr = pref + (size_t)(blockIdx.y - y + wy0) * ppitch;  // blockIdx.y = global row
         uint32_t c2 = 0;
         const int nrow = wy1 - wy0 + 1;
         for (int r0 = 0; r0 < nrow; r0 += 16) {
@@ -235,81 +236,80 @@ __global__ void __launch_bounds__(kSeg) pre_points_kernel(const __grid_constant_
     flags[pix] = is_pt ? 1 : 0;
     weight_maps[pix] = is_pt ? (float)wt : 0.f;  // cloud.cpp:63,80,115
   }
-  // segment count + bbox
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  // segment count + bbox (one warp = one segment: no barrier)
+  const int lane = threadIdx.x & 31;
   const unsigned ball = __ballot_sync(0xffffffffu, is_pt);
+  if (lane == 0) seg_counts[seg] = __popc(ball);
+  if (ball == 0u) return;  // warp-uniform: most segments of a frame hold no point
   double lo[3] = {p.x, p.y, p.z}, hi[3] = {is_pt ? p.x : -inf, is_pt ? p.y : -inf, is_pt ? p.z : -inf};
-  if (ball != 0u) {  // warp-uniform: most warps of a frame hold no point
 #pragma unroll
-    for (int a = 0; a < 3; ++a)
-      for (int o = 16; o > 0; o >>= 1) {
-        lo[a] = fmin(lo[a], __shfl_xor_sync(0xffffffffu, lo[a], o));
-        hi[a] = fmax(hi[a], __shfl_xor_sync(0xffffffffu, hi[a], o));
-      }
-  }
-  if (lane == 0) {
-    wc[wid] = __popc(ball);
-    for (int a = 0; a < 3; ++a) bb[wid][a] = lo[a], bb[wid][3 + a] = hi[a];
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    int t = 0;
-    for (int i = 0; i < kSeg / 32; ++i) t += wc[i];
-    seg_counts[seg] = t;
-  }
-  if (threadIdx.x < 6) {
-    double r = bb[0][threadIdx.x];
-    for (int i = 1; i < kSeg / 32; ++i) r = threadIdx.x < 3 ? fmin(r, bb[i][threadIdx.x]) : fmax(r, bb[i][threadIdx.x]);
-    if (r != inf && r != -inf) {  // this segment holds points
-      if (threadIdx.x < 3)
-        atomicMin(&ctl->bbox_key[threadIdx.x], dkey(r));
-      else
-        atomicMax(&ctl->bbox_key[threadIdx.x], dkey(r));
+  for (int a = 0; a < 3; ++a)
+    for (int o = 16; o > 0; o >>= 1) {
+      lo[a] = fmin(lo[a], __shfl_xor_sync(0xffffffffu, lo[a], o));
+      hi[a] = fmax(hi[a], __shfl_xor_sync(0xffffffffu, hi[a], o));
     }
-  }
+  if (lane < 3) atomicMin(&ctl->bbox_key[lane], dkey(lane == 0 ? lo[0] : (lane == 1 ? lo[1] : lo[2])));
+  else if (lane < 6) atomicMax(&ctl->bbox_key[lane], dkey(lane == 3 ? hi[0] : (lane == 4 ? hi[1] : hi[2])));
 }
 
-// single CTA: exclusive scan of the segment counts (contiguous runs per thread)
+// single CTA: exclusive scan of the segment counts, in chunks of 8192 (each
+// thread 8 consecutive counts as two 16 B loads: coalesced)
 __device__ void fit_grid_dev(DevCtl* ctl, int nx, int ny, int nz, int pad);
 
 __global__ void __launch_bounds__(1024) pre_scan_kernel(const int32_t* counts, int32_t* offsets, int n, int cap,
                                                         DevCtl* ctl, int32_t* rowlist_reset, int nx, int ny, int nz,
                                                         int pad) {
   __shared__ int wsum[32];
-  const int per = (n + 1023) / 1024;
-  const int b0 = min(n, (int)threadIdx.x * per), b1 = min(n, b0 + per);
-  int vals[16];
-  int tot = 0;
-#pragma unroll
-  for (int i = 0; i < 16; ++i) {
-    vals[i] = b0 + i < b1 ? counts[b0 + i] : 0;
-    tot += vals[i];
-  }
-  for (int i = b0 + 16; i < b1; ++i) tot += counts[i];
+  __shared__ int carry_s;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  int inc = tot;
-  for (int o = 1; o < 32; o <<= 1) {
-    const int t = __shfl_up_sync(0xffffffffu, inc, o);
-    if (lane >= o) inc += t;
-  }
-  if (lane == 31) wsum[wid] = inc;
-  __syncthreads();
-  if (wid == 0) {
-    int s = wsum[lane];
-    for (int o = 1; o < 32; o <<= 1) {
-      const int t = __shfl_up_sync(0xffffffffu, s, o);
-      if (lane >= o) s += t;
-    }
-    wsum[lane] = s;
-  }
-  __syncthreads();
-  int run = (wid ? wsum[wid - 1] : 0) + inc - tot;
+  int carry = 0;
+  for (int base = 0; base < n; base += 8192) {
+    const int i0 = base + (int)threadIdx.x * 8;
+    int v[8];
+    if (i0 + 8 <= n) {  // counts/offsets are 256 B aligned, i0 a multiple of 8
+      const int4 a = reinterpret_cast<const int4*>(counts + i0)[0], b = reinterpret_cast<const int4*>(counts + i0)[1];
+      v[0] = a.x, v[1] = a.y, v[2] = a.z, v[3] = a.w, v[4] = b.x, v[5] = b.y, v[6] = b.z, v[7] = b.w;
+    } else {
 #pragma unroll
-  for (int i = 0; i < 16; ++i)
-    if (b0 + i < b1) offsets[b0 + i] = run, run += vals[i];
-  for (int i = b0 + 16; i < b1; ++i) offsets[i] = run, run += counts[i];
-  if (threadIdx.x == 1023) {
-    const int P = wsum[31];
+      for (int i = 0; i < 8; ++i) v[i] = i0 + i < n ? counts[i0 + i] : 0;
+    }
+    int tot = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) tot += v[i];
+    int inc = tot;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += t;
+    }
+    if (lane == 31) wsum[wid] = inc;
+    __syncthreads();
+    if (wid == 0) {
+      int s = wsum[lane];
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, s, o);
+        if (lane >= o) s += t;
+      }
+      wsum[lane] = s;
+      if (lane == 31) carry_s = carry + s;
+    }
+    __syncthreads();
+    int run = carry + (wid ? wsum[wid - 1] : 0) + inc - tot;
+    int o8[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) o8[i] = run, run += v[i];
+    if (i0 + 8 <= n) {
+      reinterpret_cast<int4*>(offsets + i0)[0] = make_int4(o8[0], o8[1], o8[2], o8[3]);
+      reinterpret_cast<int4*>(offsets + i0)[1] = make_int4(o8[4], o8[5], o8[6], o8[7]);
+    } else {
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        if (i0 + i < n) offsets[i0 + i] = o8[i];
+    }
+    carry = carry_s;
+    __syncthreads();  // wsum / carry_s are rewritten by the next chunk
+  }
+  if (threadIdx.x == 0) {
+    const int P = carry;
     ctl->P = P;
     ctl->status = P == 0 ? 2 : (P > cap ? 3 : 0);
     ctl->voff = 0;
@@ -318,26 +318,23 @@ __global__ void __launch_bounds__(1024) pre_scan_kernel(const int32_t* counts, i
   }
 }
 
-// one thread per pixel: staged point -> its rank in segment order
-__global__ void __launch_bounds__(kSeg) pre_gather_kernel(const __grid_constant__ SensorSet ss,
-                                                          const Staged* __restrict__ stage,
-                                                          const uint8_t* __restrict__ flags,
-                                                          const int32_t* __restrict__ seg_offsets, DevPoints pts) {
-  __shared__ int wc[kSeg / 32];
+// one warp per segment: staged point -> its rank in segment order
+__global__ void __launch_bounds__(128) pre_gather_kernel(const __grid_constant__ SensorSet ss,
+                                                         const Staged* __restrict__ stage,
+                                                         const uint8_t* __restrict__ flags,
+                                                         const int32_t* __restrict__ seg_offsets, DevPoints pts,
+                                                         int spr) {
+  const int sx = blockIdx.x * 4 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (sx >= spr) return;
   int k, y;
   row_of(ss, blockIdx.y, &k, &y);
   const int w = ss.s[k].w;
-  const int x = blockIdx.x * kSeg + threadIdx.x;
+  const int x = sx * kSegPx + lane;
   const int64_t pix = ss.pix_offset[k] + (int64_t)y * w + x;
   const bool is_pt = x < w && flags[pix];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const unsigned ball = __ballot_sync(0xffffffffu, is_pt);
-  if (lane == 0) wc[wid] = __popc(ball);
-  __syncthreads();
   if (!is_pt) return;
-  int pre = 0;
-  for (int i = 0; i < wid; ++i) pre += wc[i];
-  const int idx = seg_offsets[blockIdx.y * gridDim.x + blockIdx.x] + pre + __popc(ball & ((1u << lane) - 1u));
+  const int idx = seg_offsets[blockIdx.y * spr + sx] + __popc(ball & ((1u << lane) - 1u));
   const Staged s = stage[pix];
   pts.pos[3 * idx + 0] = s.pos[0], pts.pos[3 * idx + 1] = s.pos[1], pts.pos[3 * idx + 2] = s.pos[2];
   pts.nrm[3 * idx + 0] = s.nrm[0], pts.nrm[3 * idx + 1] = s.nrm[1], pts.nrm[3 * idx + 2] = s.nrm[2];
@@ -390,7 +387,7 @@ Scratch carve(const SensorSet& ss, void* base) {
   for (int k = 0; k < ss.k; ++k) maxw = maxw > ss.s[k].w ? maxw : ss.s[k].w;
   auto up = [](uintptr_t p) { return (p + 255) & ~uintptr_t(255); };
   Scratch s;
-  s.spr = (maxw + kSeg - 1) / kSeg;
+  s.spr = (maxw + kSegPx - 1) / kSegPx;
   s.nseg = rows * s.spr;
   s.ppitch = (maxw + 127) & ~127;
   uintptr_t p = up(reinterpret_cast<uintptr_t>(base));
@@ -434,11 +431,11 @@ void launch_preprocess(const SensorSet& ss, DevPoints pts, float* weight_maps, i
   const Scratch s = carve(ss, scratch);
   const dim3 grid(s.spr, rows);
   pre_prefix_kernel<<<(rows * 32 + 255) / 256, 256, 0, st>>>(ss, rows, s.pref, s.ppitch, ctl);
-  pre_tri_kernel<<<grid, kSeg, 0, st>>>(ss, disc_mm, s.tri);
-  pre_points_kernel<<<grid, kSeg, 0, st>>>(ss, sil_r, s.tri, s.pref, s.ppitch, s.stage, s.flags, s.counts, ctl,
-                                           weight_maps);
+  pre_tri_kernel<<<dim3((s.spr * kSegPx + kSeg - 1) / kSeg, rows), kSeg, 0, st>>>(ss, disc_mm, s.tri);
+  pre_points_kernel<<<grid, kSegPx, 0, st>>>(ss, sil_r, s.tri, s.pref, s.ppitch, s.stage, s.flags, s.counts, ctl,
+                                             weight_maps);
   pre_scan_kernel<<<1, 1024, 0, st>>>(s.counts, s.offsets, s.nseg, pts.cap, ctl, rowlist_reset, nx, ny, nz, padding);
-  pre_gather_kernel<<<grid, kSeg, 0, st>>>(ss, s.stage, s.flags, s.offsets, pts);
+  pre_gather_kernel<<<dim3((s.spr + 3) / 4, rows), 128, 0, st>>>(ss, s.stage, s.flags, s.offsets, pts, s.spr);
 }
 
 }  // namespace vc
