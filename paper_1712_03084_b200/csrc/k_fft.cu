@@ -694,10 +694,9 @@ __global__ void __launch_bounds__(IXCfg<NX>::THREADS, 2) ix_kernel(const float2*
   const int chunks = (H * 8) / 16;  // 16 B per cp.async; H is a multiple of 4
   auto stage = [&](int pr, float2* b) {
     const float2* src = S0 + (size_t)(2 * pr) * H;
-    for (int i = t; i < 2 * chunks; i += T) {
-      const int l = i / chunks, c = i - l * chunks;
-      cp_async16(b + l * CF::LINE + 2 * c, src + (size_t)l * H + 2 * c, true);
-    }
+#pragma unroll
+    for (int l = 0; l < 2; ++l)
+      for (int c = t; c < chunks; c += T) cp_async16(b + l * CF::LINE + 2 * c, src + (size_t)l * H + 2 * c, true);
   };
   int pr = blockIdx.x * CF::TEAMS + team;
   if (pr < pairs) stage(pr, bufs);
