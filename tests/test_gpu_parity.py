@@ -73,6 +73,51 @@ def test_preprocess_bit_exact(O, scene, ctx):
     assert grid.edge_mm == ref.grid.edge and list(grid.origin) == list(ref.grid.origin[:])
 
 
+@pytest.mark.parametrize("w,h,f", [(333, 247, 160.0), (97, 61, 48.0)])
+def test_preprocess_bit_exact_ragged_size(O, ctx, w, h, f):
+    """Image widths that are not a multiple of the 32-pixel segment (ragged
+    last segment per row) and odd heights: points, weights and grid stay
+    bit-exact."""
+    rig = vc.make_circle_rig(4, 0, 2500, w, h, f)
+    orig = O.make_circle_rig(4, 0, 2500, 1000, w, h, f)
+    body = vc.kick_body(300, 77)
+    frames = [vc.render_frame(rig, body, k) for k in range(4)]
+    clouds, grid = vc.preprocess(frames, rig, vc.ReconConfig(dims=(64, 64, 64)), ctx=ctx)
+    ref = oracle_frame(O, orig, frames, dims=(64, 64, 64), want_volume=False)
+    p = ref.points
+    assert len(clouds.position) == len(p["position"]) > 100
+    assert np.array_equal(clouds.position, p["position"])
+    assert np.array_equal(clouds.normal, p["normal"])
+    assert np.array_equal(clouds.weight, p["weight"])
+    assert np.array_equal(clouds.px, p["px"]) and np.array_equal(clouds.py, p["py"])
+    for k in range(4):
+        assert np.array_equal(clouds.weight_maps[k], ref.weight_maps[k])
+    assert grid.edge_mm == ref.grid.edge and list(grid.origin) == list(ref.grid.origin[:])
+
+
+def test_preprocess_bit_exact_mixed_resolutions(O, ctx):
+    """Views of different sizes in one rig (segments past a narrower view's
+    width): points, weight maps and grid bit-exact."""
+    a = vc.make_circle_rig(4, 0, 2500, 333, 247, 160.0)
+    b = vc.make_circle_rig(4, 0, 2500, 512, 424, 365.0)
+    rig = vc.CameraRig([a.sensors[0], b.sensors[1], a.sensors[2], b.sensors[3]], 4)
+    oa = O.make_circle_rig(4, 0, 2500, 1000, 333, 247, 160.0)
+    ob = O.make_circle_rig(4, 0, 2500, 1000, 512, 424, 365.0)
+    orig = (O.Sensor * 4)()
+    orig[0], orig[1], orig[2], orig[3] = oa[0], ob[1], oa[2], ob[3]
+    body = vc.kick_body(300, 200)
+    frames = [vc.render_frame(rig, body, k) for k in range(4)]
+    clouds, grid = vc.preprocess(frames, rig, vc.ReconConfig(dims=(64, 64, 64)), ctx=ctx)
+    ref = oracle_frame(O, orig, frames, dims=(64, 64, 64), want_volume=False)
+    assert len(clouds.position) == len(ref.points["position"]) > 1000
+    assert np.array_equal(clouds.position, ref.points["position"])
+    assert np.array_equal(clouds.weight, ref.points["weight"])
+    assert np.array_equal(clouds.sensor, ref.points["sensor"])
+    for k in range(4):
+        assert np.array_equal(clouds.weight_maps[k], ref.weight_maps[k])
+    assert grid.edge_mm == ref.grid.edge and list(grid.origin) == list(ref.grid.origin[:])
+
+
 def test_preprocess_noisy_and_discontinuity(O, scene, ctx):
     rig, body, _, orig = scene
     frames = [vc.render_frame(rig, body, k, 0, sigma_mm_at_2m=2.0, seed=7) for k in range(4)]
