@@ -225,6 +225,15 @@ struct ICfg {
   static constexpr int SMEM = N * CW * 8;
 };
 
+// F-y: narrower tiles from 256 points up (only the non-empty planes work, so
+// more, smaller CTAs spread them over the SMs)
+template <int N>
+struct FCfg {
+  static constexpr int CW = N >= 256 ? 8 : 16;
+  static constexpr int THREADS = CW * Shape<N>::R2;
+  static constexpr int SMEM = N * CW * 8;
+};
+
 // ------------------------------------------------------------------ F-x
 template <int NX>
 __global__ void __launch_bounds__(XCfg<NX>::THREADS, 2) fx_kernel(const float4* __restrict__ acc, float2* __restrict__ S0,
@@ -462,14 +471,14 @@ __device__ __forceinline__ void tile_to_regs(const float2* tile, int c, int t, f
 // for the slab transform that is the send layout of the forward all-to-all
 // (block s = the ky-slab of rank s); with kyl = ny it is the plain layout.
 template <int NY>
-__global__ void __launch_bounds__(CCfg<NY>::THREADS, NY >= 1024 ? 1 : 2) fy_kernel(const float2* S0, const float2* S1,
+__global__ void __launch_bounds__(FCfg<NY>::THREADS, NY >= 1024 ? 1 : (NY >= 256 ? 4 : 2)) fy_kernel(const float2* S0, const float2* S1,
                                                                  const float2* __restrict__ S2, float2* O0, float2* O1,
                                                                  int nxh, int H, int lk,
                                                                  const float2* __restrict__ tw,
                                                                  const uint32_t* __restrict__ rowbits,
                                                                  uint32_t* __restrict__ planeflag) {
   using S = Shape<NY>;
-  constexpr int T = S::R2, R1 = S::R1, kCW = CCfg<NY>::CW, TH = CCfg<NY>::THREADS;
+  constexpr int T = S::R2, R1 = S::R1, kCW = FCfg<NY>::CW, TH = FCfg<NY>::THREADS;
   extern __shared__ float2 sh[];  // 3 tiles of NY x kCW
   float2* b0 = sh;
   float2* b1 = sh + NY * kCW;
@@ -788,7 +797,7 @@ struct Prep {
       allow_smem(fx_kernel<N>, XCfg<N>::SMEM);
       allow_smem(ix_kernel<N>, IXCfg<N>::SMEM);
     } else if (axis == 1) {
-      allow_smem(fy_kernel<N>, 3 * CCfg<N>::SMEM);
+      allow_smem(fy_kernel<N>, 3 * FCfg<N>::SMEM);
       allow_smem(iy_kernel<N>, ICfg<N>::SMEM);
     } else {
       allow_smem(z_kernel<N>, 2 * CCfg<N>::SMEM);
@@ -827,7 +836,7 @@ inline void col_grid(int nx, int cw, int* tiles, int* nyq, int bit) {
 template <int N>
 struct RunFy {
   static void run(const SlabFft& a) {
-    using C = CCfg<N>;
+    using C = FCfg<N>;
     // (no Nyquist packing here: F-y's per-row empty flags make the packed
     // gather slower than the one wasted tile, measured)
     dim3 grid((a.nx / 2 + 1 + C::CW - 1) / C::CW, a.nzl);
