@@ -234,6 +234,14 @@ struct FCfg {
   static constexpr int SMEM = N * CW * 8;
 };
 
+// Z: 8-column tiles from 256 points up (4 CTAs/SM at 256)
+template <int N>
+struct ZCfg {
+  static constexpr int CW = N >= 256 ? 8 : 16;
+  static constexpr int THREADS = CW * Shape<N>::R2;
+  static constexpr int SMEM = N * CW * 8;
+};
+
 // ------------------------------------------------------------------ F-x
 template <int NX>
 __global__ void __launch_bounds__(XCfg<NX>::THREADS, 2) fx_kernel(const float4* __restrict__ acc, float2* __restrict__ S0,
@@ -543,7 +551,7 @@ __device__ __forceinline__ void z_body(float2* __restrict__ S0, const float2* __
                                        int ky0, int H, float fx_step, float fy_step, const float2* __restrict__ tw,
                                        const uint32_t* __restrict__ planeflag) {
   using S = Shape<NZ>;
-  constexpr int T = S::R2, R1 = S::R1, kCW = CCfg<NZ>::CW, TH = CCfg<NZ>::THREADS;
+  constexpr int T = S::R2, R1 = S::R1, kCW = ZCfg<NZ>::CW, TH = ZCfg<NZ>::THREADS;
   extern __shared__ float2 sh[];  // 2 tiles of NZ x kCW
   float2* b0 = sh;
   float2* b1 = sh + NZ * kCW;
@@ -613,7 +621,7 @@ __device__ __forceinline__ void z_body(float2* __restrict__ S0, const float2* __
 // Input: D, Z as [z][kyl][H] (kyl = ny on one GPU; a ky-slab starting at ky0
 // after the forward all-to-all).  The result overwrites S0 in place.
 template <int NZ>
-__global__ void __launch_bounds__(CCfg<NZ>::THREADS, NZ >= 1024 ? 1 : 2)
+__global__ void __launch_bounds__(ZCfg<NZ>::THREADS, NZ >= 1024 ? 1 : (NZ == 256 ? 4 : 2))
     z_kernel(float2* __restrict__ S0, const float2* __restrict__ S1, int nx, int ny, int kyl, int ky0, int H, int nyq,
              float fx_step, float fy_step, const float2* __restrict__ tw, const uint32_t* __restrict__ planeflag) {
   if (blockIdx.x == nyq)
@@ -800,7 +808,7 @@ struct Prep {
       allow_smem(fy_kernel<N>, 3 * FCfg<N>::SMEM);
       allow_smem(iy_kernel<N>, ICfg<N>::SMEM);
     } else {
-      allow_smem(z_kernel<N>, 2 * CCfg<N>::SMEM);
+      allow_smem(z_kernel<N>, 2 * ZCfg<N>::SMEM);
     }
   }
 };
@@ -847,7 +855,7 @@ struct RunFy {
 template <int N>
 struct RunZ {
   static void run(const SlabFft& a) {
-    using C = CCfg<N>;
+    using C = ZCfg<N>;
     int tiles, nyq;
     col_grid(a.nx, C::CW, &tiles, &nyq, 1);
     dim3 grid(tiles, a.kyl);
