@@ -56,9 +56,31 @@ __global__ void __launch_bounds__(256) sparse_clear_kernel(float4* acc, uint32_t
   }
 }
 
-__device__ __forceinline__ void mark_chunks(uint32_t* rowbits, int32_t* rowlist, int row, int x0, int x1) {
+// chunk bits x0/32 .. x1/32 of a row (a reduction: nothing waits for it; the
+// touched-row list is built from the bits after the splat)
+__device__ __forceinline__ void mark_chunks(uint32_t* rowbits, int row, int x0, int x1) {
   const uint32_t m = (0xffffffffu >> (31 - (x1 >> 5))) & (0xffffffffu << (x0 >> 5));
-  if (atomicOr(rowbits + row, m) == 0u) rowlist[1 + atomicAdd(rowlist, 1)] = row;  // first touch of the row
+  atomicOr(rowbits + row, m);
+}
+
+// Touched-row list [count, rows...] from the chunk bits (warp-aggregated appends; any order)
+__global__ void __launch_bounds__(256) rowlist_build_kernel(const uint32_t* __restrict__ rowbits,
+                                                            const DevCtl* __restrict__ ctl, int nzl,
+                                                            int32_t* __restrict__ rowlist) {
+  if (ctl->status != 0) return;
+  const int rows = ctl->grid.ny * nzl;
+  const int lane = threadIdx.x & 31;
+  const int wstride = gridDim.x * blockDim.x;
+  for (int r0 = (blockIdx.x * blockDim.x + threadIdx.x) & ~31; r0 < rows; r0 += wstride) {
+    const int r = r0 + lane;
+    const bool touched = r < rows && __ldg(rowbits + r) != 0u;
+    const unsigned ball = __ballot_sync(0xffffffffu, touched);
+    if (!ball) continue;
+    int base = 0;
+    if (lane == 0) base = atomicAdd(rowlist, __popc(ball));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (touched) rowlist[1 + base + __popc(ball & ((1u << lane) - 1u))] = r;
+  }
 }
 
 __device__ __forceinline__ void red_add_v4(float4* addr, float4 v) {
@@ -92,8 +114,8 @@ __global__ void __launch_bounds__(kSplatThreads) splat_weighted_kernel(const dou
   const int run = (P + groups - 1) / groups;
   const int p0 = (blockIdx.x * (kSplatThreads / 64) + (threadIdx.x >> 6)) * run;
   const int p1 = min(P, p0 + run);
-  int last_row = -1, pend_row = -1;
-  uint32_t last_m = 0u, pend_old = 1u;
+  int last_row = -1;
+  uint32_t last_m = 0u;
   const int lane = threadIdx.x & 31;
   const double o = lane == 0 ? g.origin[0] : (lane == 1 ? g.origin[1] : g.origin[2]);
   // the next point's inputs are loaded while the current one is scattered
@@ -129,17 +151,12 @@ __global__ void __launch_bounds__(kSplatThreads) splat_weighted_kernel(const dou
       const int xa = max(fx - 1, 0), xb = min(fx + 2, g.nx - 1);
       const uint32_t m = (0xffffffffu >> (31 - (xb >> 5))) & (0xffffffffu << (xa >> 5));
       if (row != last_row || (m & ~last_m) != 0u) {
-        // the previous mark's result is consumed here, one point later, so
-        // the atomic's round trip overlaps this point's scatter
-        const uint32_t old = atomicOr(rowbits + row, m);
-        if (pend_row >= 0 && pend_old == 0u) rowlist[1 + atomicAdd(rowlist, 1)] = pend_row;  // first touch
-        pend_row = row, pend_old = old;
+        atomicOr(rowbits + row, m);
         last_m = row == last_row ? (last_m | m) : m;
         last_row = row;
       }
     }
   }
-  if (pend_row >= 0 && pend_old == 0u) rowlist[1 + atomicAdd(rowlist, 1)] = pend_row;
 }
 
 // splat.cpp:40-56 simple mode: lround nearest voxel, (sum N, count)
@@ -159,7 +176,7 @@ __global__ void __launch_bounds__(256) splat_simple_kernel(const double* __restr
     if (!(x >= 0 && x < g.nx && y >= 0 && y < g.ny && z >= 0 && z < g.nz)) continue;
     const long long zl = z - zoff;
     if (zl < 0 || zl >= nzl) continue;
-    mark_chunks(rowbits, rowlist, (int)(zl * g.ny + y), (int)x, (int)x);
+    mark_chunks(rowbits, (int)(zl * g.ny + y), (int)x, (int)x);
     red_add_v4(acc + ((size_t)zl * g.ny + y) * g.nx + x,
                make_float4((float)nrm[3 * p + 0], (float)nrm[3 * p + 1], (float)nrm[3 * p + 2], 1.f));
   }
@@ -203,6 +220,7 @@ void launch_splat(const DevPoints& pts, DevCtl* ctl, float4* acc, uint32_t* rowb
                                                              rowlist, zoff, nzl);
   else
     splat_simple_kernel<<<148 * 4, 256, 0, st>>>(pts.pos, pts.nrm, ctl, acc, rowbits, rowlist, zoff, nzl);
+  rowlist_build_kernel<<<148 * 4, 256, 0, st>>>(rowbits, ctl, nzl, rowlist);
 }
 
 void launch_splat_finalize(const float4* acc, size_t n, int mode, int negate, double sigma2, float* field,

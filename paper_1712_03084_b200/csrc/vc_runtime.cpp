@@ -327,7 +327,7 @@ int enqueue_frame(vc_ctx* ctx, const FrameCfg& f) {
   }
   launch_splat(points(ctx), ctx->ctl, P<float4>(ctx->acc), P<uint32_t>(ctx->rowbits), P<int32_t>(ctx->rowlist),
                f.mode, st, 0, f.nz);
-  n += 2;
+  n += 3;  // clear, splat, row-list build
   record(ctx, 2);
   launch_integrate(P<float4>(ctx->acc), P<float2>(ctx->spec), P<float>(ctx->A), f.nx, f.ny, f.nz, f.mode,
                    P<float2>(ctx->tw), st, ctx->profiling ? &ctx->ev[14] : nullptr, P<float2>(ctx->rowmm),
