@@ -9,11 +9,11 @@
 // the rows of all views concatenated, which is the reference's point order
 // (views in sensor order, pixels row-major).
 //
-//   pre_prefix  one warp per depth row: inclusive prefix count of the mask
-//               along x, so the 21x21 silhouette box count of cloud.cpp:89-106
-//               costs 2 loads per window row
-//   pre_tri     one thread per 2x2 quad with a valid corner: the T1/T2
-//               triangle normals of cloud.cpp:38-59, computed once each
+//   pre_prefix_tri  one warp per depth row: inclusive prefix count of the
+//               mask along x (so the 21x21 silhouette box count of
+//               cloud.cpp:89-106 costs 2 loads per window row), and the T1/T2
+//               triangle normals of the row's quads with a valid corner
+//               (cloud.cpp:38-59), compacted across the warp, computed once each
 //   pre_points  one thread per pixel: the six incident triangles in the
 //               reference's accumulation order (cloud.cpp:53-71), world
 //               position/normal (:73-74), W = W1*W2 (:108-114) -> per-pixel
@@ -31,7 +31,6 @@
 namespace vc {
 namespace {
 
-constexpr int kSeg = 128;  // pixels (quads) per CTA of pre_tri
 constexpr int kSegPx = 32;  // pixels per segment: one warp, one CTA of pre_points (a CTA
                             // retires with its slowest warp, so one-warp CTAs let the
                             // empty segments' slots recycle while point warps compute)
@@ -65,16 +64,53 @@ __device__ __forceinline__ d3 local_px(const DevSensor& s, const ViewPtrs& v, in
   return {ddiv(dmul(dsub((double)x, s.cx), z), s.fx), ddiv(dmul(dsub((double)y, s.cy), z), s.fy), z};
 }
 
-// inclusive prefix of (mask != 0) along each row (lane = 16 consecutive pixels)
-__global__ void __launch_bounds__(256) pre_prefix_kernel(const __grid_constant__ SensorSet ss, int rows,
-                                                         uint16_t* __restrict__ pref, int pitch, DevCtl* ctl) {
+// cloud.cpp:38-51 add_triangle(ia, ib, ic): the normalised normal, or NaN
+// when the triangle is rejected (invalid vertex, depth step > disc, len < 1e-12)
+__device__ d3 triangle_normal(bool ok, d3 a, d3 b, d3 c, double disc) {
+  const d3 bad{__longlong_as_double(0x7ff8000000000000ll), 0.0, 0.0};
+  if (!ok) return bad;
+  const double lo = fmin(fmin(a.z, b.z), c.z), hi = fmax(fmax(a.z, b.z), c.z);
+  if (dsub(hi, lo) > disc) return bad;
+  const d3 n = cross3(sub3(c, a), sub3(b, a));
+  const double len = norm3(n);
+  if (len < 1e-12) return bad;
+  return div3(n, len);
+}
+
+// quad (qx, qy) = pixel index of its i00 corner; T1 = (i00, i10, i01),
+// T2 = (i10, i11, i01) (cloud.cpp:53-59), stored at the quad's pixel index
+__device__ __forceinline__ void quad_triangles(const SensorSet& ss, int k, int qx, int qy, double disc,
+                                               double* __restrict__ tri) {
+  const DevSensor& s = ss.s[k];
+  const ViewPtrs& v = ss.v[k];
+  const bool v00 = valid_px(v, s.w, s.h, qx, qy), v10 = valid_px(v, s.w, s.h, qx + 1, qy);
+  const bool v01 = valid_px(v, s.w, s.h, qx, qy + 1), v11 = valid_px(v, s.w, s.h, qx + 1, qy + 1);
+  const d3 z{0, 0, 0};
+  const d3 p00 = v00 ? local_px(s, v, qx, qy) : z, p10 = v10 ? local_px(s, v, qx + 1, qy) : z;
+  const d3 p01 = v01 ? local_px(s, v, qx, qy + 1) : z, p11 = v11 ? local_px(s, v, qx + 1, qy + 1) : z;
+  const d3 t1 = triangle_normal(v00 && v10 && v01, p00, p10, p01, disc);
+  const d3 t2 = triangle_normal(v10 && v11 && v01, p10, p11, p01, disc);
+  double* o = tri + 6 * (ss.pix_offset[k] + (int64_t)qy * s.w + qx);
+  o[0] = t1.x, o[1] = t1.y, o[2] = t1.z, o[3] = t2.x, o[4] = t2.y, o[5] = t2.z;
+}
+
+// One warp per depth row (lane = 16 consecutive pixels):
+//  (1) inclusive prefix of (mask != 0) along the row, so the 21x21 silhouette
+//      box count of cloud.cpp:89-106 costs 2 loads per window row;
+//  (2) the row's quads with a valid corner, compacted across the warp in x
+//      order, then their two triangle normals with the lanes taking turns
+//      (most quads of a frame are empty; the rest cluster on the silhouette).
+__global__ void __launch_bounds__(256) pre_prefix_tri_kernel(const __grid_constant__ SensorSet ss, int rows,
+                                                             uint16_t* __restrict__ pref, int pitch, DevCtl* ctl,
+                                                             double disc, double* __restrict__ tri) {
+  __shared__ uint16_t qlist[8][512];
   if (blockIdx.x == 0 && threadIdx.x < 6) ctl->bbox_key[threadIdx.x] = threadIdx.x < 3 ? ~0ull : 0ull;
-  const int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-  if (r >= rows) return;
+  const int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31, wid = (threadIdx.x >> 5) & 7;
+  if (r >= rows) return;  // whole warps
   int k, y;
   row_of(ss, r, &k, &y);
   const ViewPtrs& v = ss.v[k];
-  const int w = ss.s[k].w;
+  const int w = ss.s[k].w, h = ss.s[k].h;
   const uint8_t* m = v.mask + (size_t)y * v.mpitch;
   uint16_t* o = pref + (size_t)r * pitch;
   int carry = 0;
@@ -98,42 +134,34 @@ __global__ void __launch_bounds__(256) pre_prefix_kernel(const __grid_constant__
       if (xb + i < w) o[xb + i] = (uint16_t)acc;
     }
     carry += __shfl_sync(0xffffffffu, inc, 31);
+    if (y + 1 >= h) continue;  // no quads below the last row
+    // pixels xb .. xb+16 valid in rows y, y+1 -> quads xb+i (i < 16) with a valid corner
+    uint32_t any = 0;
+#pragma unroll
+    for (int i = 0; i <= 16; ++i) {
+      const int x = xb + i;
+      if (x < w) {
+        const bool a0 = (i < 16 ? b[i] : __ldg(m + x)) != 0 && __ldg(v.depth + (size_t)y * v.dpitch + x) != 0;
+        const bool a1 = valid_px(v, w, h, x, y + 1);
+        any |= (a0 || a1 ? 1u : 0u) << i;
+      }
+    }
+    uint32_t am = (any | (any >> 1)) & 0xffffu;
+    const int lim = w - 1 - xb;  // quads xb+i need xb+i+1 < w
+    am &= lim >= 16 ? 0xffffu : (lim <= 0 ? 0u : (1u << lim) - 1u);
+    const int cnt = __popc(am);
+    int pos = cnt;
+    for (int d = 1; d < 32; d <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, pos, d);
+      if (lane >= d) pos += t;
+    }
+    const int total = __shfl_sync(0xffffffffu, pos, 31);
+    pos -= cnt;
+    for (uint32_t mm = am; mm; mm &= mm - 1) qlist[wid][pos++] = (uint16_t)(xb + __ffs(mm) - 1);
+    __syncwarp();
+    for (int i = lane; i < total; i += 32) quad_triangles(ss, k, qlist[wid][i], y, disc, tri);
+    __syncwarp();  // the list is rebuilt by the next chunk
   }
-}
-
-// cloud.cpp:38-51 add_triangle(ia, ib, ic): the normalised normal, or NaN
-// when the triangle is rejected (invalid vertex, depth step > disc, len < 1e-12)
-__device__ d3 triangle_normal(bool ok, d3 a, d3 b, d3 c, double disc) {
-  const d3 bad{__longlong_as_double(0x7ff8000000000000ll), 0.0, 0.0};
-  if (!ok) return bad;
-  const double lo = fmin(fmin(a.z, b.z), c.z), hi = fmax(fmax(a.z, b.z), c.z);
-  if (dsub(hi, lo) > disc) return bad;
-  const d3 n = cross3(sub3(c, a), sub3(b, a));
-  const double len = norm3(n);
-  if (len < 1e-12) return bad;
-  return div3(n, len);
-}
-
-// quad (qx, qy) = pixel index of its i00 corner; T1 = (i00, i10, i01),
-// T2 = (i10, i11, i01) (cloud.cpp:53-59)
-__global__ void __launch_bounds__(kSeg) pre_tri_kernel(const __grid_constant__ SensorSet ss, double disc,
-                                                       double* __restrict__ tri) {
-  int k, qy;
-  row_of(ss, blockIdx.y, &k, &qy);
-  const DevSensor& s = ss.s[k];
-  const ViewPtrs& v = ss.v[k];
-  const int qx = blockIdx.x * kSeg + threadIdx.x;
-  if (qx + 1 >= s.w || qy + 1 >= s.h) return;
-  const bool v00 = valid_px(v, s.w, s.h, qx, qy), v10 = valid_px(v, s.w, s.h, qx + 1, qy);
-  const bool v01 = valid_px(v, s.w, s.h, qx, qy + 1), v11 = valid_px(v, s.w, s.h, qx + 1, qy + 1);
-  if (!(v00 || v10 || v01 || v11)) return;
-  const d3 z{0, 0, 0};
-  const d3 p00 = v00 ? local_px(s, v, qx, qy) : z, p10 = v10 ? local_px(s, v, qx + 1, qy) : z;
-  const d3 p01 = v01 ? local_px(s, v, qx, qy + 1) : z, p11 = v11 ? local_px(s, v, qx + 1, qy + 1) : z;
-  const d3 t1 = triangle_normal(v00 && v10 && v01, p00, p10, p01, disc);
-  const d3 t2 = triangle_normal(v10 && v11 && v01, p10, p11, p01, disc);
-  double* o = tri + 6 * (ss.pix_offset[k] + (int64_t)qy * s.w + qx);
-  o[0] = t1.x, o[1] = t1.y, o[2] = t1.z, o[3] = t2.x, o[4] = t2.y, o[5] = t2.z;
 }
 
 __device__ __forceinline__ void add_tri(const d3& n, d3& sum, int& cnt) {
@@ -430,8 +458,7 @@ void launch_preprocess(const SensorSet& ss, DevPoints pts, float* weight_maps, i
   const int rows = ss.row_offset[ss.k];
   const Scratch s = carve(ss, scratch);
   const dim3 grid(s.spr, rows);
-  pre_prefix_kernel<<<(rows * 32 + 255) / 256, 256, 0, st>>>(ss, rows, s.pref, s.ppitch, ctl);
-  pre_tri_kernel<<<dim3((s.spr * kSegPx + kSeg - 1) / kSeg, rows), kSeg, 0, st>>>(ss, disc_mm, s.tri);
+  pre_prefix_tri_kernel<<<(rows * 32 + 255) / 256, 256, 0, st>>>(ss, rows, s.pref, s.ppitch, ctl, disc_mm, s.tri);
   pre_points_kernel<<<grid, kSegPx, 0, st>>>(ss, sil_r, s.tri, s.pref, s.ppitch, s.stage, s.flags, s.counts, ctl,
                                              weight_maps);
   pre_scan_kernel<<<1, 1024, 0, st>>>(s.counts, s.offsets, s.nseg, pts.cap, ctl, rowlist_reset, nx, ny, nz, padding);
