@@ -60,8 +60,12 @@ __device__ double trilinear(const float* A, const DevGrid& g, double vx, double 
 
 constexpr int kIsoBlocks = 296;
 
+__device__ void iso_final_tree(const double* partial, int n, DevCtl* ctl, double* sh);
+
+// The CTA that finishes last also forms the level (the same fixed tree over
+// the per-CTA partials as iso_final_kernel, so the result is deterministic).
 __global__ void __launch_bounds__(256) iso_partial_kernel(const double* __restrict__ pos, const float* __restrict__ A,
-                                                          const DevCtl* __restrict__ ctl, double* partial) {
+                                                          DevCtl* __restrict__ ctl, double* partial) {
   __shared__ double sh[256];
   double sum = 0.0;
   if (ctl->status == 0) {
@@ -80,7 +84,30 @@ __global__ void __launch_bounds__(256) iso_partial_kernel(const double* __restri
     if (threadIdx.x < o) sh[threadIdx.x] = dadd(sh[threadIdx.x], sh[threadIdx.x + o]);
     __syncthreads();
   }
-  if (threadIdx.x == 0) partial[blockIdx.x] = sh[0];
+  __shared__ bool last;
+  if (threadIdx.x == 0) {
+    partial[blockIdx.x] = sh[0];
+    __threadfence();
+    last = atomicAdd(&ctl->iso_ticket, 1) == (int)gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  iso_final_tree(partial, gridDim.x, ctl, sh);
+  if (threadIdx.x == 0) ctl->iso_ticket = 0;
+}
+// 512-slot tree over the partials (slot i >= n holds 0) with 256 threads: the
+// first level adds slots t and t+256, then halves, as iso_final_kernel does
+__device__ void iso_final_tree(const double* partial, int n, DevCtl* ctl, double* sh) {
+  const int t = threadIdx.x;
+  const volatile double* vp = partial;
+  sh[t] = dadd(t < n ? vp[t] : 0.0, t + 256 < n ? vp[t + 256] : 0.0);
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if (t < o) sh[t] = dadd(sh[t], sh[t + o]);
+    __syncthreads();
+  }
+  if (t == 0 && ctl->status == 0) ctl->level = ddiv(sh[0], (double)ctl->P);
 }
 
 // trilinear()'s lower z plane of the point, owned by exactly one slab
@@ -602,7 +629,6 @@ int iso_blocks() { return kIsoBlocks; }
 
 void launch_iso_level(const DevPoints& pts, const float* A, DevCtl* ctl, double* partial, int, cudaStream_t st) {
   iso_partial_kernel<<<kIsoBlocks, 256, 0, st>>>(pts.pos, A, ctl, partial);
-  iso_final_kernel<<<1, 512, 0, st>>>(partial, kIsoBlocks, ctl);
 }
 
 int mc_blocks(int nx, int ny, int nz) {  // per-unit / per-block scratch entries

@@ -335,7 +335,7 @@ int enqueue_frame(vc_ctx* ctx, const FrameCfg& f) {
   n += 5;
   record(ctx, 3);
   launch_iso_level(points(ctx), P<float>(ctx->A), ctx->ctl, P<double>(ctx->iso_partial), 1024, st);
-  n += 2;
+  n += 1;
   record(ctx, 4);
   launch_marching_cubes(P<float>(ctx->A), ctx->ctl, mesh_bufs(ctx), f.nx, f.ny, f.nz, st, branch ? ctx->aux : nullptr,
                         ctx->fork[1], ctx->join[1]);

@@ -60,7 +60,7 @@ struct DevCtl {
   int32_t units;      // MC: active voxel-row units
   int32_t v_extra;    // MC slab: cut edges counted on the next rank's first plane
   int32_t voff;       // MC slab: global id of this rank's first vertex
-  int32_t pad;
+  int32_t iso_ticket; // iso level: CTAs done (the last one reduces; reset by it)
   double bbox[6];
   unsigned long long bbox_key[6];  // bbox as order-preserving keys (atomic min/max while preprocessing)
   DevGrid grid;
