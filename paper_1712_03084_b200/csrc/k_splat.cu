@@ -17,8 +17,8 @@
 //
 // Sparsity: the splat touches only a thin shell of the grid (~5% of 256^3).
 // Every scatter also sets the bit of its 32-voxel x-chunk in a per-row mask
-// (rowbits[(z*ny+y)], bit = x/32); the first marking of a row appends it to
-// a compact row list.  The next frame's clear zeroes only the chunks of the
+// (rowbits[(z*ny+y)], bit = x/32) with fire-and-forget reductions; a pass
+// after the splat lists the touched rows compactly.  The next frame's clear zeroes only the chunks of the
 // listed rows, and the FFT's first pass works through the list, loading only
 // the marked chunks.
 #include "vc_device.cuh"
@@ -100,8 +100,7 @@ __global__ void __launch_bounds__(kSplatThreads) splat_weighted_kernel(const dou
                                                                        const double* __restrict__ wgt,
                                                                        const DevCtl* __restrict__ ctl,
                                                                        float4* __restrict__ acc,
-                                                                       uint32_t* __restrict__ rowbits,
-                                                                       int32_t* __restrict__ rowlist, int zoff,
+                                                                       uint32_t* __restrict__ rowbits, int zoff,
                                                                        int nzl) {
   const int P = ctl->P;
   if (ctl->status != 0) return;
@@ -163,8 +162,7 @@ __global__ void __launch_bounds__(kSplatThreads) splat_weighted_kernel(const dou
 __global__ void __launch_bounds__(256) splat_simple_kernel(const double* __restrict__ pos,
                                                            const double* __restrict__ nrm,
                                                            const DevCtl* __restrict__ ctl, float4* __restrict__ acc,
-                                                           uint32_t* __restrict__ rowbits,
-                                                           int32_t* __restrict__ rowlist, int zoff, int nzl) {
+                                                           uint32_t* __restrict__ rowbits, int zoff, int nzl) {
   const int P = ctl->P;
   if (ctl->status != 0) return;
   const DevGrid g = ctl->grid;
@@ -216,10 +214,10 @@ void launch_sparse_clear(float4* acc, uint32_t* rowbits, const int32_t* rowlist,
 void launch_splat(const DevPoints& pts, DevCtl* ctl, float4* acc, uint32_t* rowbits, int32_t* rowlist, int mode,
                   cudaStream_t st, int zoff, int nzl) {
   if (mode == 0)
-    splat_weighted_kernel<<<148 * 8, kSplatThreads, 0, st>>>(pts.pos, pts.nrm, pts.weight, ctl, acc, rowbits,
-                                                             rowlist, zoff, nzl);
+    splat_weighted_kernel<<<148 * 8, kSplatThreads, 0, st>>>(pts.pos, pts.nrm, pts.weight, ctl, acc, rowbits, zoff,
+                                                             nzl);
   else
-    splat_simple_kernel<<<148 * 4, 256, 0, st>>>(pts.pos, pts.nrm, ctl, acc, rowbits, rowlist, zoff, nzl);
+    splat_simple_kernel<<<148 * 4, 256, 0, st>>>(pts.pos, pts.nrm, ctl, acc, rowbits, zoff, nzl);
   rowlist_build_kernel<<<148 * 4, 256, 0, st>>>(rowbits, ctl, nzl, rowlist);
 }
 

@@ -109,9 +109,9 @@ void launch_mask_from_depth(const uint16_t* depth, uint8_t* mask, int n, cudaStr
 // k_splat.cu
 void launch_clear(float4* acc, size_t n, cudaStream_t st);
 // zoff/nzl: the z-slab [zoff, zoff+nzl) this rank accumulates (whole grid: 0, nz).
-// Every voxel row the splat touches is appended once to the touched-row list
-// rowlist = [count, rows...] (the first marking of the row's chunk mask
-// appends it).  The list lives outside DevCtl: only the frame path's clear,
+// Every voxel row the splat touches is listed once in the touched-row list
+// rowlist = [count, rows...] (built from the chunk masks right after the
+// splat).  The list lives outside DevCtl: only the frame path's clear,
 // preprocess (reset) and splat touch it, so stage calls cannot desynchronise
 // it from the accumulator.
 void launch_splat(const DevPoints& pts, DevCtl* ctl, float4* acc, uint32_t* rowbits, int32_t* rowlist, int mode,
