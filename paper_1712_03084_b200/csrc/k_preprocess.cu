@@ -102,7 +102,11 @@ __device__ __forceinline__ void quad_triangles(const SensorSet& ss, int k, int q
 //      (most quads of a frame are empty; the rest cluster on the silhouette).
 __global__ void __launch_bounds__(256) pre_prefix_tri_kernel(const __grid_constant__ SensorSet ss, int rows,
                                                              uint16_t* __restrict__ pref, int pitch, DevCtl* ctl,
-                                                             double disc, double* __restrict__ tri) {
+                                                             double disc, double* __restrict__ tri, int spr,
+                                                             int32_t* __restrict__ seg_counts,
+                                                             uint8_t* __restrict__ flags,
+                                                             float* __restrict__ weight_maps,
+                                                             int32_t* __restrict__ act) {
   __shared__ uint16_t qlist[8][512];
   if (blockIdx.x == 0 && threadIdx.x < 6) ctl->bbox_key[threadIdx.x] = threadIdx.x < 3 ? ~0ull : 0ull;
   const int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31, wid = (threadIdx.x >> 5) & 7;
@@ -134,6 +138,33 @@ __global__ void __launch_bounds__(256) pre_prefix_tri_kernel(const __grid_consta
       if (xb + i < w) o[xb + i] = (uint16_t)acc;
     }
     carry += __shfl_sync(0xffffffffu, inc, 31);
+    {  // 32-pixel segments (lane pairs): no foreground -> no point: zero its
+       // outputs here; the others go to the active list pre_points walks
+      const int fg = run + __shfl_xor_sync(0xffffffffu, run, 1);
+      const int sx = (x0 >> 5) + (lane >> 1);
+      const bool seg_ok = xb < w && sx < spr;
+      const int64_t pix0 = ss.pix_offset[k] + (int64_t)y * w;
+      if (seg_ok && fg == 0) {
+        const int64_t q = pix0 + xb;
+        if (xb + 16 <= w && (q & 15) == 0) {  // 16 flags + 16 weights as vector stores
+          *reinterpret_cast<uint4*>(flags + q) = make_uint4(0u, 0u, 0u, 0u);
+          float4* wm4 = reinterpret_cast<float4*>(weight_maps + q);
+          const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+          wm4[0] = z4, wm4[1] = z4, wm4[2] = z4, wm4[3] = z4;
+        } else {
+#pragma unroll
+          for (int i = 0; i < 16; ++i)
+            if (xb + i < w) flags[q + i] = 0, weight_maps[q + i] = 0.f;
+        }
+      }
+      const bool lead = seg_ok && (lane & 1) == 0;
+      if (lead && fg == 0) seg_counts[r * spr + sx] = 0;
+      const unsigned ball = __ballot_sync(0xffffffffu, lead && fg != 0);
+      int base = 0;
+      if (lane == 0 && ball) base = atomicAdd(act, __popc(ball));
+      base = __shfl_sync(0xffffffffu, base, 0);
+      if (lead && fg != 0) act[1 + base + __popc(ball & ((1u << lane) - 1u))] = r * spr + sx;
+    }
     if (y + 1 >= h) continue;  // no quads below the last row
     // pixels xb .. xb+16 valid in rows y, y+1 -> quads xb+i (i < 16) with a valid corner
     uint32_t any = 0;
@@ -162,6 +193,7 @@ __global__ void __launch_bounds__(256) pre_prefix_tri_kernel(const __grid_consta
     for (int i = lane; i < total; i += 32) quad_triangles(ss, k, qlist[wid][i], y, disc, tri);
     __syncwarp();  // the list is rebuilt by the next chunk
   }
+  for (int sx = (w + 31) / 32 + lane; sx < spr; sx += 32) seg_counts[r * spr + sx] = 0;  // past this view's width
 }
 
 __device__ __forceinline__ void add_tri(const d3& n, d3& sum, int& cnt) {
@@ -180,20 +212,19 @@ struct Staged {  // one point (per-pixel staging slot)
   int32_t pad;
 };
 
-__global__ void __launch_bounds__(kSegPx) pre_points_kernel(const __grid_constant__ SensorSet ss, int sil_r,
-                                                            const double* __restrict__ tri,
-                                                            const uint16_t* __restrict__ pref, int ppitch,
-                                                            Staged* __restrict__ stage, uint8_t* __restrict__ flags,
-                                                            int32_t* __restrict__ seg_counts, DevCtl* ctl,
-                                                            float* __restrict__ weight_maps) {
+__device__ __forceinline__ void points_segment(const SensorSet& ss, int sil_r, const double* __restrict__ tri,
+                                               const uint16_t* __restrict__ pref, int ppitch,
+                                               Staged* __restrict__ stage, uint8_t* __restrict__ flags,
+                                               int32_t* __restrict__ seg_counts, DevCtl* ctl,
+                                               float* __restrict__ weight_maps, int seg, int spr) {
+  const int row = seg / spr, sx = seg - row * spr;
   int k, y;
-  row_of(ss, blockIdx.y, &k, &y);
+  row_of(ss, row, &k, &y);
   const DevSensor& s = ss.s[k];
   const ViewPtrs& v = ss.v[k];
   const int w = s.w, h = s.h;
-  const int x = blockIdx.x * kSegPx + threadIdx.x;
+  const int x = sx * kSegPx + threadIdx.x;
   const int64_t pix = ss.pix_offset[k] + (int64_t)y * w + x;
-  const int seg = blockIdx.y * gridDim.x + blockIdx.x;
   const double inf = DBL_MAX * 2.0;
   d3 p{inf, inf, inf}, nw{0, 0, 0};
   bool is_pt = false;
@@ -237,7 +268,7 @@ __global__ void __launch_bounds__(kSegPx) pre_points_kernel(const __grid_constan
         // cloud.cpp:99-106 W2: (2r+1)^2 window clipped to the image, fixed divisor
         const int xa = max(0, x - sil_r), xb = min(w - 1, x + sil_r);
         const int wy0 = max(0, y - sil_r), wy1 = min(h - 1, y + sil_r);
-        const uint16_t* pr = pref + (size_t)(blockIdx.y - y + wy0) * ppitch;  // blockIdx.y = global row
+        const uint16_t* pr = pref + (size_t)(row - y + wy0) * ppitch;
         uint32_t c2 = 0;
         const int nrow = wy1 - wy0 + 1;
         for (int r0 = 0; r0 < nrow; r0 += 16) {
@@ -278,6 +309,21 @@ __global__ void __launch_bounds__(kSegPx) pre_points_kernel(const __grid_constan
     }
   if (lane < 3) atomicMin(&ctl->bbox_key[lane], dkey(lane == 0 ? lo[0] : (lane == 1 ? lo[1] : lo[2])));
   else if (lane < 6) atomicMax(&ctl->bbox_key[lane], dkey(lane == 3 ? hi[0] : (lane == 4 ? hi[1] : hi[2])));
+}
+
+// persistent one-warp CTAs over the active segments (pre_prefix_tri zeroed
+// the outputs of the others); any order: outputs are per pixel / segment and
+// the bbox an exact min/max
+__global__ void __launch_bounds__(kSegPx) pre_points_kernel(const __grid_constant__ SensorSet ss, int sil_r,
+                                                            const double* __restrict__ tri,
+                                                            const uint16_t* __restrict__ pref, int ppitch,
+                                                            Staged* __restrict__ stage, uint8_t* __restrict__ flags,
+                                                            int32_t* __restrict__ seg_counts, DevCtl* ctl,
+                                                            float* __restrict__ weight_maps,
+                                                            const int32_t* __restrict__ act, int spr) {
+  const int n = act[0];
+  for (int i = blockIdx.x; i < n; i += gridDim.x)
+    points_segment(ss, sil_r, tri, pref, ppitch, stage, flags, seg_counts, ctl, weight_maps, act[1 + i], spr);
 }
 
 // single CTA: exclusive scan of the segment counts, in chunks of 8192 (each
@@ -405,6 +451,7 @@ struct Scratch {
   uint16_t* pref;     // rows x ppitch
   int32_t* counts;    // per segment
   int32_t* offsets;   // per segment
+  int32_t* act;       // [count, active segment ids...]
   int ppitch, spr, nseg;
 };
 
@@ -430,6 +477,8 @@ Scratch carve(const SensorSet& ss, void* base) {
   s.counts = reinterpret_cast<int32_t*>(p);
   p = up(p + (size_t)s.nseg * sizeof(int32_t));
   s.offsets = reinterpret_cast<int32_t*>(p);
+  p = up(p + (size_t)s.nseg * sizeof(int32_t));
+  s.act = reinterpret_cast<int32_t*>(p);
   return s;
 }
 
@@ -449,7 +498,7 @@ void prepare_preprocess(const SensorSet&) {}  // no opt-in shared memory needed
 
 size_t preprocess_scratch_bytes(const SensorSet& ss) {
   const Scratch s = carve(ss, nullptr);
-  return reinterpret_cast<uintptr_t>(s.offsets) + (size_t)s.nseg * sizeof(int32_t) + 512;
+  return reinterpret_cast<uintptr_t>(s.act) + (size_t)(s.nseg + 1) * sizeof(int32_t) + 512;
 }
 
 void launch_preprocess(const SensorSet& ss, DevPoints pts, float* weight_maps, int32_t* scratch, DevCtl* ctl,
@@ -457,10 +506,12 @@ void launch_preprocess(const SensorSet& ss, DevPoints pts, float* weight_maps, i
                        int32_t* rowlist_reset) {
   const int rows = ss.row_offset[ss.k];
   const Scratch s = carve(ss, scratch);
-  const dim3 grid(s.spr, rows);
-  pre_prefix_tri_kernel<<<(rows * 32 + 255) / 256, 256, 0, st>>>(ss, rows, s.pref, s.ppitch, ctl, disc_mm, s.tri);
-  pre_points_kernel<<<grid, kSegPx, 0, st>>>(ss, sil_r, s.tri, s.pref, s.ppitch, s.stage, s.flags, s.counts, ctl,
-                                             weight_maps);
+  cudaMemsetAsync(s.act, 0, sizeof(int32_t), st);
+  pre_prefix_tri_kernel<<<(rows * 32 + 255) / 256, 256, 0, st>>>(ss, rows, s.pref, s.ppitch, ctl, disc_mm, s.tri,
+                                                                  s.spr, s.counts, s.flags, weight_maps, s.act);
+  const int pgrid = s.nseg < 148 * 16 ? s.nseg : 148 * 16;  // resident one-warp CTAs (registers: 16 warps/SM)
+  pre_points_kernel<<<pgrid, kSegPx, 0, st>>>(ss, sil_r, s.tri, s.pref, s.ppitch, s.stage, s.flags, s.counts, ctl,
+                                              weight_maps, s.act, s.spr);
   pre_scan_kernel<<<1, 1024, 0, st>>>(s.counts, s.offsets, s.nseg, pts.cap, ctl, rowlist_reset, nx, ny, nz, padding);
   pre_gather_kernel<<<dim3((s.spr + 3) / 4, rows), 128, 0, st>>>(ss, s.stage, s.flags, s.offsets, pts, s.spr);
 }
