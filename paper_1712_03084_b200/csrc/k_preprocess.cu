@@ -392,28 +392,33 @@ __global__ void __launch_bounds__(1024) pre_scan_kernel(const int32_t* counts, i
   }
 }
 
-// one warp per segment: staged point -> its rank in segment order
+// one warp per active segment (the others hold no point): staged point -> its
+// rank in segment order
 __global__ void __launch_bounds__(128) pre_gather_kernel(const __grid_constant__ SensorSet ss,
                                                          const Staged* __restrict__ stage,
                                                          const uint8_t* __restrict__ flags,
                                                          const int32_t* __restrict__ seg_offsets, DevPoints pts,
-                                                         int spr) {
-  const int sx = blockIdx.x * 4 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
-  if (sx >= spr) return;
-  int k, y;
-  row_of(ss, blockIdx.y, &k, &y);
-  const int w = ss.s[k].w;
-  const int x = sx * kSegPx + lane;
-  const int64_t pix = ss.pix_offset[k] + (int64_t)y * w + x;
-  const bool is_pt = x < w && flags[pix];
-  const unsigned ball = __ballot_sync(0xffffffffu, is_pt);
-  if (!is_pt) return;
-  const int idx = seg_offsets[blockIdx.y * spr + sx] + __popc(ball & ((1u << lane) - 1u));
-  const Staged s = stage[pix];
-  pts.pos[3 * idx + 0] = s.pos[0], pts.pos[3 * idx + 1] = s.pos[1], pts.pos[3 * idx + 2] = s.pos[2];
-  pts.nrm[3 * idx + 0] = s.nrm[0], pts.nrm[3 * idx + 1] = s.nrm[1], pts.nrm[3 * idx + 2] = s.nrm[2];
-  pts.weight[idx] = s.w;
-  pts.pix[3 * idx + 0] = x, pts.pix[3 * idx + 1] = y, pts.pix[3 * idx + 2] = k;
+                                                         int spr, const int32_t* __restrict__ act) {
+  const int lane = threadIdx.x & 31;
+  const int n = act[0];
+  for (int i = blockIdx.x * 4 + (threadIdx.x >> 5); i < n; i += gridDim.x * 4) {
+    const int seg = act[1 + i];
+    const int row = seg / spr, sx = seg - row * spr;
+    int k, y;
+    row_of(ss, row, &k, &y);
+    const int w = ss.s[k].w;
+    const int x = sx * kSegPx + lane;
+    const int64_t pix = ss.pix_offset[k] + (int64_t)y * w + x;
+    const bool is_pt = x < w && flags[pix];
+    const unsigned ball = __ballot_sync(0xffffffffu, is_pt);
+    if (!is_pt) continue;
+    const int idx = seg_offsets[seg] + __popc(ball & ((1u << lane) - 1u));
+    const Staged s = stage[pix];
+    pts.pos[3 * idx + 0] = s.pos[0], pts.pos[3 * idx + 1] = s.pos[1], pts.pos[3 * idx + 2] = s.pos[2];
+    pts.nrm[3 * idx + 0] = s.nrm[0], pts.nrm[3 * idx + 1] = s.nrm[1], pts.nrm[3 * idx + 2] = s.nrm[2];
+    pts.weight[idx] = s.w;
+    pts.pix[3 * idx + 0] = x, pts.pix[3 * idx + 1] = y, pts.pix[3 * idx + 2] = k;
+  }
 }
 
 // reconstruct.cpp:56-68 (bbox) + fit_grid (reconstruct.cpp:16-35, dims given);
@@ -513,7 +518,7 @@ void launch_preprocess(const SensorSet& ss, DevPoints pts, float* weight_maps, i
   pre_points_kernel<<<pgrid, kSegPx, 0, st>>>(ss, sil_r, s.tri, s.pref, s.ppitch, s.stage, s.flags, s.counts, ctl,
                                               weight_maps, s.act, s.spr);
   pre_scan_kernel<<<1, 1024, 0, st>>>(s.counts, s.offsets, s.nseg, pts.cap, ctl, rowlist_reset, nx, ny, nz, padding);
-  pre_gather_kernel<<<dim3((s.spr + 3) / 4, rows), 128, 0, st>>>(ss, s.stage, s.flags, s.offsets, pts, s.spr);
+  pre_gather_kernel<<<148 * 8, 128, 0, st>>>(ss, s.stage, s.flags, s.offsets, pts, s.spr, s.act);
 }
 
 }  // namespace vc
