@@ -54,7 +54,7 @@ def test_gpu_arm_line():
     assert d["warmup"] >= 3 and d["steps"] == 40 and d["scaling"] == "weak"
     assert d["e2e"]["h2d_bytes_per_step"] > 5_000_000 and d["e2e"]["d2h_bytes_per_step"] > 0
     # kernels launched inside the timed region: the frame graph's kernels x steps
-    assert d["gpu_launches"] >= 20 * d["steps"]
+    assert d["gpu_launches"] >= 15 * d["steps"]
     r = d["roofline"]
     for key in ("bound", "achieved", "peak", "unit", "frac", "traffic"):
         assert key in r, key
