@@ -106,11 +106,13 @@ __global__ void __launch_bounds__(256) pre_prefix_tri_kernel(const __grid_consta
                                                              int32_t* __restrict__ seg_counts,
                                                              uint8_t* __restrict__ flags,
                                                              float* __restrict__ weight_maps,
-                                                             int32_t* __restrict__ act) {
+                                                             int32_t* __restrict__ act,
+                                                             int32_t* __restrict__ rowcnt) {
   __shared__ uint16_t qlist[8][512];
   if (blockIdx.x == 0 && threadIdx.x < 6) ctl->bbox_key[threadIdx.x] = threadIdx.x < 3 ? ~0ull : 0ull;
   const int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31, wid = (threadIdx.x >> 5) & 7;
   if (r >= rows) return;  // whole warps
+  if (lane == 0) rowcnt[r] = 0;  // the row's point count (pre_points adds, pre_scan scans)
   int k, y;
   row_of(ss, r, &k, &y);
   const ViewPtrs& v = ss.v[k];
@@ -216,7 +218,8 @@ __device__ __forceinline__ void points_segment(const SensorSet& ss, int sil_r, c
                                                const uint16_t* __restrict__ pref, int ppitch,
                                                Staged* __restrict__ stage, uint8_t* __restrict__ flags,
                                                int32_t* __restrict__ seg_counts, DevCtl* ctl,
-                                               float* __restrict__ weight_maps, int seg, int spr) {
+                                               float* __restrict__ weight_maps, int seg, int spr,
+                                               int32_t* __restrict__ rowcnt) {
   const int row = seg / spr, sx = seg - row * spr;
   int k, y;
   row_of(ss, row, &k, &y);
@@ -300,6 +303,7 @@ __device__ __forceinline__ void points_segment(const SensorSet& ss, int sil_r, c
   const unsigned ball = __ballot_sync(0xffffffffu, is_pt);
   if (lane == 0) seg_counts[seg] = __popc(ball);
   if (ball == 0u) return;  // warp-uniform: most segments of a frame hold no point
+  if (lane == 0) atomicAdd(rowcnt + row, __popc(ball));
   double lo[3] = {p.x, p.y, p.z}, hi[3] = {is_pt ? p.x : -inf, is_pt ? p.y : -inf, is_pt ? p.z : -inf};
 #pragma unroll
   for (int a = 0; a < 3; ++a)
@@ -320,10 +324,12 @@ __global__ void __launch_bounds__(kSegPx) pre_points_kernel(const __grid_constan
                                                             Staged* __restrict__ stage, uint8_t* __restrict__ flags,
                                                             int32_t* __restrict__ seg_counts, DevCtl* ctl,
                                                             float* __restrict__ weight_maps,
-                                                            const int32_t* __restrict__ act, int spr) {
+                                                            const int32_t* __restrict__ act, int spr,
+                                                            int32_t* __restrict__ rowcnt) {
   const int n = act[0];
   for (int i = blockIdx.x; i < n; i += gridDim.x)
-    points_segment(ss, sil_r, tri, pref, ppitch, stage, flags, seg_counts, ctl, weight_maps, act[1 + i], spr);
+    points_segment(ss, sil_r, tri, pref, ppitch, stage, flags, seg_counts, ctl, weight_maps, act[1 + i], spr,
+                   rowcnt);
 }
 
 // single CTA: exclusive scan of the segment counts, in chunks of 8192 (each
@@ -397,7 +403,8 @@ __global__ void __launch_bounds__(1024) pre_scan_kernel(const int32_t* counts, i
 __global__ void __launch_bounds__(128) pre_gather_kernel(const __grid_constant__ SensorSet ss,
                                                          const Staged* __restrict__ stage,
                                                          const uint8_t* __restrict__ flags,
-                                                         const int32_t* __restrict__ seg_offsets, DevPoints pts,
+                                                         const int32_t* __restrict__ row_offsets,
+                                                         const int32_t* __restrict__ seg_counts, DevPoints pts,
                                                          int spr, const int32_t* __restrict__ act) {
   const int lane = threadIdx.x & 31;
   const int n = act[0];
@@ -411,8 +418,12 @@ __global__ void __launch_bounds__(128) pre_gather_kernel(const __grid_constant__
     const int64_t pix = ss.pix_offset[k] + (int64_t)y * w + x;
     const bool is_pt = x < w && flags[pix];
     const unsigned ball = __ballot_sync(0xffffffffu, is_pt);
+    // the segment's rank: its row's offset + the points of the row's earlier segments
+    int before = 0;
+    for (int b = 0; b < sx; b += 32) before += b + lane < sx ? seg_counts[row * spr + b + lane] : 0;
+    for (int o = 16; o > 0; o >>= 1) before += __shfl_xor_sync(0xffffffffu, before, o);
     if (!is_pt) continue;
-    const int idx = seg_offsets[seg] + __popc(ball & ((1u << lane) - 1u));
+    const int idx = row_offsets[row] + before + __popc(ball & ((1u << lane) - 1u));
     const Staged s = stage[pix];
     pts.pos[3 * idx + 0] = s.pos[0], pts.pos[3 * idx + 1] = s.pos[1], pts.pos[3 * idx + 2] = s.pos[2];
     pts.nrm[3 * idx + 0] = s.nrm[0], pts.nrm[3 * idx + 1] = s.nrm[1], pts.nrm[3 * idx + 2] = s.nrm[2];
@@ -457,6 +468,7 @@ struct Scratch {
   int32_t* counts;    // per segment
   int32_t* offsets;   // per segment
   int32_t* act;       // [count, active segment ids...]
+  int32_t* rowcnt;    // per depth row: points
   int ppitch, spr, nseg;
 };
 
@@ -484,6 +496,8 @@ Scratch carve(const SensorSet& ss, void* base) {
   s.offsets = reinterpret_cast<int32_t*>(p);
   p = up(p + (size_t)s.nseg * sizeof(int32_t));
   s.act = reinterpret_cast<int32_t*>(p);
+  p = up(p + (size_t)(s.nseg + 1) * sizeof(int32_t));
+  s.rowcnt = reinterpret_cast<int32_t*>(p);
   return s;
 }
 
@@ -503,7 +517,7 @@ void prepare_preprocess(const SensorSet&) {}  // no opt-in shared memory needed
 
 size_t preprocess_scratch_bytes(const SensorSet& ss) {
   const Scratch s = carve(ss, nullptr);
-  return reinterpret_cast<uintptr_t>(s.act) + (size_t)(s.nseg + 1) * sizeof(int32_t) + 512;
+  return reinterpret_cast<uintptr_t>(s.rowcnt) + (size_t)ss.row_offset[ss.k] * sizeof(int32_t) + 512;
 }
 
 void launch_preprocess(const SensorSet& ss, DevPoints pts, float* weight_maps, int32_t* scratch, DevCtl* ctl,
@@ -513,12 +527,15 @@ void launch_preprocess(const SensorSet& ss, DevPoints pts, float* weight_maps, i
   const Scratch s = carve(ss, scratch);
   cudaMemsetAsync(s.act, 0, sizeof(int32_t), st);
   pre_prefix_tri_kernel<<<(rows * 32 + 255) / 256, 256, 0, st>>>(ss, rows, s.pref, s.ppitch, ctl, disc_mm, s.tri,
-                                                                  s.spr, s.counts, s.flags, weight_maps, s.act);
+                                                                  s.spr, s.counts, s.flags, weight_maps, s.act,
+                                                                  s.rowcnt);
   const int pgrid = s.nseg < 148 * 16 ? s.nseg : 148 * 16;  // resident one-warp CTAs (registers: 16 warps/SM)
   pre_points_kernel<<<pgrid, kSegPx, 0, st>>>(ss, sil_r, s.tri, s.pref, s.ppitch, s.stage, s.flags, s.counts, ctl,
-                                              weight_maps, s.act, s.spr);
-  pre_scan_kernel<<<1, 1024, 0, st>>>(s.counts, s.offsets, s.nseg, pts.cap, ctl, rowlist_reset, nx, ny, nz, padding);
-  pre_gather_kernel<<<148 * 8, 128, 0, st>>>(ss, s.stage, s.flags, s.offsets, pts, s.spr, s.act);
+                                              weight_maps, s.act, s.spr, s.rowcnt);
+  // exclusive scan of the per-row point counts (segment order within a row is
+  // resolved by pre_gather from the segment counts)
+  pre_scan_kernel<<<1, 1024, 0, st>>>(s.rowcnt, s.offsets, rows, pts.cap, ctl, rowlist_reset, nx, ny, nz, padding);
+  pre_gather_kernel<<<148 * 8, 128, 0, st>>>(ss, s.stage, s.flags, s.offsets, s.counts, pts, s.spr, s.act);
 }
 
 }  // namespace vc
