@@ -592,7 +592,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--workload", default="c2", choices=["c2", "c5"],
                     help="c2: the BASELINE metric (256^3 stream, frame-parallel); c5: 1024^3 frames (z-slabs on N>1)")
-    ap.add_argument("--streams", type=int, default=5,
+    ap.add_argument("--streams", type=int, default=4,
                     help="concurrent frames per GPU (one context + host thread each)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl != "reference":
