@@ -346,80 +346,70 @@ __global__ void __launch_bounds__(256) mc_count_kernel(const float* __restrict__
   }
 }
 
-// Single CTA: exclusive scan of the per-unit (V, T, C) counts, contiguous
-// runs per thread; when they fit, the runs are staged through shared memory
-// so the global loads/stores are coalesced (a single SM otherwise issues one
-// L2 transaction per thread per element).
-constexpr int kScanStage = 12288;  // int3 entries staged (144 KB, opt-in)
-
+// Single CTA: exclusive scan of the per-unit (V, T, C) counts in chunks of
+// 4096 units (each thread 4 consecutive int3 = three 16 B loads: coalesced).
 __global__ void __launch_bounds__(1024) mc_scan_kernel(int3* blk, const DevCtl* ctl_in, DevCtl* ctl, int v_cap,
                                                        int t_cap, int c_cap) {
   __shared__ int3 wsum[32];
-  extern __shared__ int3 sstage[];
   const int n = ctl_in->status == 0 ? ctl_in->units : 0;
-  const bool staged = n <= kScanStage;
-  if (staged) {
-    int* si = reinterpret_cast<int*>(sstage);
-    const int* gi = reinterpret_cast<const int*>(blk);
-    for (int i = threadIdx.x; i < 3 * n; i += 1024) si[i] = gi[i];
-    __syncthreads();
-  }
-  int3* buf = staged ? sstage : blk;
-  const int per = (n + 1023) / 1024;
-  const int b0 = min(n, (int)threadIdx.x * per), b1 = min(n, b0 + per);
-  int3 vals[16];
-  int3 tot = make_int3(0, 0, 0);
-#pragma unroll
-  for (int i = 0; i < 16; ++i) {
-    vals[i] = b0 + i < b1 ? buf[b0 + i] : make_int3(0, 0, 0);
-    tot.x += vals[i].x, tot.y += vals[i].y, tot.z += vals[i].z;
-  }
-  for (int i = b0 + 16; i < b1; ++i) {
-    const int3 v = buf[i];
-    tot.x += v.x, tot.y += v.y, tot.z += v.z;
-  }
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  int3 inc = tot;
-  for (int o = 1; o < 32; o <<= 1) {
-    const int a = __shfl_up_sync(0xffffffffu, inc.x, o), b = __shfl_up_sync(0xffffffffu, inc.y, o),
-              c = __shfl_up_sync(0xffffffffu, inc.z, o);
-    if (lane >= o) inc.x += a, inc.y += b, inc.z += c;
-  }
-  if (lane == 31) wsum[wid] = inc;
-  __syncthreads();
-  if (wid == 0) {
-    int3 w = wsum[lane];
-    for (int o = 1; o < 32; o <<= 1) {
-      const int a = __shfl_up_sync(0xffffffffu, w.x, o), b = __shfl_up_sync(0xffffffffu, w.y, o),
-                c = __shfl_up_sync(0xffffffffu, w.z, o);
-      if (lane >= o) w.x += a, w.y += b, w.z += c;
-    }
-    wsum[lane] = w;
-  }
-  __syncthreads();
-  const int3 wp = wid ? wsum[wid - 1] : make_int3(0, 0, 0);
-  int3 run = make_int3(wp.x + inc.x - tot.x, wp.y + inc.y - tot.y, wp.z + inc.z - tot.z);
+  int3 carry = make_int3(0, 0, 0);
+  for (int base = 0; base < n; base += 4096) {
+    const int i0 = base + (int)threadIdx.x * 4;
+    int3 v[4];
+    if (i0 + 4 <= n) {  // blk is 256 B aligned and i0 a multiple of 4: 48 B = three int4
+      const int4* q = reinterpret_cast<const int4*>(blk + i0);
+      const int4 a = q[0], b = q[1], c = q[2];
+      v[0] = make_int3(a.x, a.y, a.z), v[1] = make_int3(a.w, b.x, b.y);
+      v[2] = make_int3(b.z, b.w, c.x), v[3] = make_int3(c.y, c.z, c.w);
+    } else {
 #pragma unroll
-  for (int i = 0; i < 16; ++i)
-    if (b0 + i < b1) {
-      buf[b0 + i] = run;
-      run.x += vals[i].x, run.y += vals[i].y, run.z += vals[i].z;
+      for (int i = 0; i < 4; ++i) v[i] = i0 + i < n ? blk[i0 + i] : make_int3(0, 0, 0);
     }
-  for (int i = b0 + 16; i < b1; ++i) {
-    const int3 v = buf[i];
-    buf[i] = run;
-    run.x += v.x, run.y += v.y, run.z += v.z;
-  }
-  if (staged) {
+    int3 tot = make_int3(0, 0, 0);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) tot.x += v[i].x, tot.y += v[i].y, tot.z += v[i].z;
+    int3 inc = tot;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int a = __shfl_up_sync(0xffffffffu, inc.x, o), b = __shfl_up_sync(0xffffffffu, inc.y, o),
+                c = __shfl_up_sync(0xffffffffu, inc.z, o);
+      if (lane >= o) inc.x += a, inc.y += b, inc.z += c;
+    }
+    if (lane == 31) wsum[wid] = inc;
     __syncthreads();
-    int* gi = reinterpret_cast<int*>(blk);
-    const int* si = reinterpret_cast<const int*>(sstage);
-    for (int i = threadIdx.x; i < 3 * n; i += 1024) gi[i] = si[i];
+    if (wid == 0) {
+      int3 w = wsum[lane];
+      for (int o = 1; o < 32; o <<= 1) {
+        const int a = __shfl_up_sync(0xffffffffu, w.x, o), b = __shfl_up_sync(0xffffffffu, w.y, o),
+                  c = __shfl_up_sync(0xffffffffu, w.z, o);
+        if (lane >= o) w.x += a, w.y += b, w.z += c;
+      }
+      wsum[lane] = w;
+    }
+    __syncthreads();
+    const int3 wp = wid ? wsum[wid - 1] : make_int3(0, 0, 0);
+    int3 run = make_int3(carry.x + wp.x + inc.x - tot.x, carry.y + wp.y + inc.y - tot.y,
+                         carry.z + wp.z + inc.z - tot.z);
+    int3 o[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) o[i] = run, run.x += v[i].x, run.y += v[i].y, run.z += v[i].z;
+    if (i0 + 4 <= n) {
+      int4* q = reinterpret_cast<int4*>(blk + i0);
+      q[0] = make_int4(o[0].x, o[0].y, o[0].z, o[1].x);
+      q[1] = make_int4(o[1].y, o[1].z, o[2].x, o[2].y);
+      q[2] = make_int4(o[2].z, o[3].x, o[3].y, o[3].z);
+    } else {
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        if (i0 + i < n) blk[i0 + i] = o[i];
+    }
+    const int3 ct = wsum[31];
+    carry.x += ct.x, carry.y += ct.y, carry.z += ct.z;
+    __syncthreads();  // wsum is rewritten by the next chunk
   }
-  if (threadIdx.x == 1023) {
-    const int3 t = wsum[31];
-    ctl->V = t.x - ctl->v_extra, ctl->T = t.y, ctl->C = t.z;
-    ctl->overflow = (t.x > v_cap || t.y > t_cap || t.z > c_cap) ? 1 : 0;
+  if (threadIdx.x == 0) {
+    ctl->V = carry.x - ctl->v_extra, ctl->T = carry.y, ctl->C = carry.z;
+    ctl->overflow = (carry.x > v_cap || carry.y > t_cap || carry.z > c_cap) ? 1 : 0;
   }
 }
 
@@ -615,7 +605,6 @@ void launch_mc_set_voff(const int32_t* counts, int rank, DevCtl* ctl, cudaStream
 }
 
 void upload_case_table_data(const int8_t* counts, const int8_t* tris, cudaStream_t st) {
-  cudaFuncSetAttribute(mc_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kScanStage * sizeof(int3)));
   cudaMemcpyToSymbolAsync(c_mc_count, counts, 256, 0, cudaMemcpyHostToDevice, st);
   cudaMemcpyToSymbolAsync(c_mc_tris, tris, 256 * 15, 0, cudaMemcpyHostToDevice, st);
   const int8_t c0[12] = {0, 2, 4, 6, 0, 1, 4, 5, 0, 1, 2, 3};  // marching_cubes.cpp:15-19
@@ -650,7 +639,7 @@ void launch_marching_cubes_count(const float* A, DevCtl* ctl, MeshBufs mb, int n
   mc_rows_kernel<<<nblk, kRowThreads, 0, st>>>(mb.rowmm, ctl, ny, nz, sl, rowmask);
   mc_units_kernel<<<1, 1024, 0, st>>>(rowmask, (units + 31) / 32, mb.units, ctl);
   mc_count_kernel<<<148 * 8, 256, 0, st>>>(A, ctl, nx, ny, nz, sl, mb.units, ucnt, mb);
-  mc_scan_kernel<<<1, 1024, kScanStage * sizeof(int3), st>>>(ucnt, ctl, ctl, mb.v_cap, mb.t_cap, mb.c_cap);
+  mc_scan_kernel<<<1, 1024, 0, st>>>(ucnt, ctl, ctl, mb.v_cap, mb.t_cap, mb.c_cap);
 }
 
 void launch_marching_cubes_emit(const float* A, DevCtl* ctl, MeshBufs mb, int nx, int ny, int nz, McSlab sl,
