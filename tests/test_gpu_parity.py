@@ -73,7 +73,7 @@ def test_preprocess_bit_exact(O, scene, ctx):
     assert grid.edge_mm == ref.grid.edge and list(grid.origin) == list(ref.grid.origin[:])
 
 
-@pytest.mark.parametrize("w,h,f", [(333, 247, 160.0), (97, 61, 48.0)])
+@pytest.mark.parametrize("w,h,f", [(333, 247, 160.0), (97, 61, 48.0), (1100, 300, 500.0)])
 def test_preprocess_bit_exact_ragged_size(O, ctx, w, h, f):
     """Image widths that are not a multiple of the 32-pixel segment (ragged
     last segment per row) and odd heights: points, weights and grid stay
