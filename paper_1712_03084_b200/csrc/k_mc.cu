@@ -416,7 +416,7 @@ __global__ void __launch_bounds__(1024) mc_scan_kernel(int3* blk, const DevCtl* 
 // per active unit (one warp, 8 voxels per lane per pass), in order: vertex
 // ids = rank of the cut edge in global edge id order (x ascending, then
 // axis); fp64 positions (marching_cubes.cpp:153-155, volume.hpp:45)
-__global__ void __launch_bounds__(256) mc_emit_kernel(const float* __restrict__ A, const DevCtl* ctl, int nx, int ny,
+__global__ void __launch_bounds__(256, 4) mc_emit_kernel(const float* __restrict__ A, const DevCtl* ctl, int nx, int ny,
                                                       int nz, McSlab sl, const int32_t* __restrict__ units,
                                                       const int3* __restrict__ unitoff, MeshBufs mb) {
   if (ctl->status != 0 || ctl->overflow) return;
