@@ -51,7 +51,7 @@ __device__ void sample_bilinear(const ViewPtrs& v, const DevSensor& s, int W, in
 // side by side; the group's first lane then forms the blend in view order
 // with the same fp64 operations as the reference's sequential loop.  The
 // fp32 copy of the vertex positions (the output format) is written here too.
-__global__ void __launch_bounds__(128) texture_kernel(const __grid_constant__ SensorSet ss,
+__global__ void __launch_bounds__(128, 8) texture_kernel(const __grid_constant__ SensorSet ss,
                                                       const float* __restrict__ weight_maps,
                                                       const double* __restrict__ vpos, const DevCtl* ctl,
                                                       double eps_vis, uint8_t* vis, float2* uv, float* wout,
