@@ -31,10 +31,45 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "reconstructed frames/sec at 256^3 grid, 4x512x424 RGB-D views; per-stage ms/frame"
-STREAM = 300
-DIMS = (256, 256, 256)
-K_VIEWS, W, H, F = 4, 512, 424, 365.0
-WORKLOAD = "C2: 300-frame synthetic kick stream, 4 views 512x424 depth+RGB (f=365, 2500 mm circle rig), 256^3 grid"
+STREAM = 300            # frames of the synthetic kick stream (make_kick_sequence(300), capsule.cpp:197-219)
+W, H, F = 512, 424, 365.0
+
+
+class Workload:
+    """One BASELINE.json config as a bench workload.  `frames` views are kept
+    resident (device + pinned host); resident frame j is kick-stream frame
+    j * STREAM // frames; global step g reconstructs resident frame
+    stream_frame(g, frames) (stride 97, coprime with 300 and 60: any `frames`
+    consecutive global steps visit every resident frame once)."""
+
+    def __init__(self, key, metric, dims, k, hd, frames, text):
+        self.key, self.metric, self.dims, self.k, self.hd, self.frames, self.text = key, metric, dims, k, hd, frames, text
+        self.rgb_w, self.rgb_h = (1920, 1080) if hd else (W, H)
+
+    def kick_frame(self, j):
+        return j * STREAM // self.frames
+
+    @property
+    def view_bytes(self):
+        return W * H * 3 + self.rgb_w * self.rgb_h * 3  # depth u16 + mask u8 + RGB8
+
+    @property
+    def frame_bytes(self):
+        return self.k * self.view_bytes
+
+
+WORKLOADS = {
+    "c2": Workload("c2", METRIC, (256, 256, 256), 4, False, STREAM,
+                   "C2: 300-frame synthetic kick stream, 4 views 512x424 depth+RGB (f=365, 2500 mm circle rig), "
+                   "256^3 grid"),
+    "c3": Workload("c3", "reconstructed frames/sec at 512^3 grid, 6x512x424 depth + 1920x1080 colour views",
+                   (512, 512, 512), 6, True, 60,
+                   "C3: 60 frames of the kick stream (every 5th of 300), 6 views 512x424 depth (f=365) + 1920x1080 "
+                   "colour (f=1060, 52 mm offset), 512^3 grid"),
+}
+WORKLOAD = WORKLOADS["c2"].text
+DIMS = WORKLOADS["c2"].dims
+K_VIEWS = 4
 
 
 def peaks():
@@ -93,72 +128,90 @@ class Clocks:
 
 
 # ------------------------------------------------------------------ reference arm
+def oracle_rig(O, wl):
+    rig = O.make_circle_rig(wl.k, 0, 2500, 1000, W, H, F)
+    if wl.hd:  # C3 colour camera; Sensor::rgb_relative, types.hpp:68-76
+        for i in range(wl.k):
+            rig[i].rgb_intr = O.Intrinsics(1060.0, 1060.0, 959.5, 539.5, 1920, 1080)
+            rig[i].rgb_relative.t[0] = 52.0
+    return rig
+
+
+def oracle_inputs(O, rig, wl, j):
+    """Views of resident frame j (kick frame wl.kick_frame(j)), rendered by the oracle."""
+    f = wl.kick_frame(j)
+    body = O.kick_body(STREAM, f)
+    views = [O.render_frame(rig[k], body, k, f) for k in range(wl.k)]
+    return [v.depth for v in views], [v.mask for v in views], [v.rgb for v in views]
+
+
 def run_reference(args):
+    """The reference's CPU path (the oracle restatement of proj/core on the host
+    cores) on the same workload, frames and metric as the GPU arm."""
+    from paper_1712_03084_b200.frame_parallel import stream_frame
     rank, world, _ = dist_env()
     if rank != 0:
         return
     from oracle import oracle as O
-    rig = O.make_circle_rig(K_VIEWS, 0, 2500, 1000, W, H, F)
+    wl = WORKLOADS[args.workload]
+    rig = oracle_rig(O, wl)
     threads = O.lib().orc_hardware_threads()
-
-    def frame_inputs(f):
-        body = O.kick_body(STREAM, f)
-        views = [O.render_frame(rig[k], body, k, f) for k in range(K_VIEWS)]
-        return [v.depth for v in views], [v.mask for v in views], [v.rgb for v in views]
-
     t0 = time.perf_counter()
-    inp = frame_inputs(0)
-    O.reconstruct_frame(rig, *inp, dims=DIMS, want_volume=False)
+    O.reconstruct_frame(rig, *oracle_inputs(O, rig, wl, stream_frame(0, wl.frames)), dims=wl.dims, want_volume=False)
     t_frame = time.perf_counter() - t0
     # bounded sample: at most ~150 s of CPU work for the timed steps
     steps = max(1, min(args.steps, int(150.0 / max(t_frame, 1e-3))))
     warm = min(args.warmup, 1)
     for i in range(warm):
-        O.reconstruct_frame(rig, *frame_inputs(1 + i), dims=DIMS, want_volume=False)
+        O.reconstruct_frame(rig, *oracle_inputs(O, rig, wl, stream_frame(1 + i, wl.frames)), dims=wl.dims,
+                            want_volume=False)
     stage = {"raw_ms": [], "weights_ms": [], "volumetric_ms": [], "other_ms": [], "blend_ms": [],
              "splat_ms": [], "integrate_ms": [], "iso_ms": [], "mc_ms": []}
     total = 0.0
+    used = []
     for i in range(steps):
-        f = (7 * i + 3) % STREAM
-        inp = frame_inputs(f)
+        j = stream_frame(i, wl.frames)  # the GPU arm's global-step order
+        used.append(wl.kick_frame(j))
+        inp = oracle_inputs(O, rig, wl, j)
         t0 = time.perf_counter()
-        r = O.reconstruct_frame(rig, *inp, dims=DIMS, want_volume=False)
+        r = O.reconstruct_frame(rig, *inp, dims=wl.dims, want_volume=False)
         total += time.perf_counter() - t0
         assert r.status == 0
         for k in stage:
             stage[k].append(r.timings[k])
     fps = steps / total
-    sample = (f"{steps} frame(s) of the C2 stream (of {args.steps} requested steps; bounded to ~150 s), "
-              f"CPU oracle restated from proj/core (splat on {threads} threads over z-slabs as splat.cpp:59-78, "
-              f"other stages single-threaded as the reference; own fp64 radix-2 FFT instead of FFTW)")
-    line = {"metric": METRIC, "value": fps, "unit": "frames/s", "n_gpus": world, "steps": steps, "warmup": warm,
+    sample = (f"{steps} frame(s) of the {wl.key.upper()} stream (kick frames {used[:6]}{'...' if steps > 6 else ''}, "
+              f"the GPU arm's first global steps; of {args.steps} requested steps; bounded to ~150 s), CPU oracle "
+              f"restated from proj/core (splat on {threads} threads over z-slabs as splat.cpp:59-78, other stages "
+              f"single-threaded as the reference; own fp64 radix-2 FFT instead of FFTW)")
+    line = {"metric": wl.metric, "value": fps, "unit": "frames/s", "n_gpus": world, "steps": steps, "warmup": warm,
             "ms_per_step": 1000.0 * total / steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic", "impl": "reference",
-            "config": {"workload": WORKLOAD, "grid": list(DIMS), "views": K_VIEWS},
+            "config": {"workload": wl.text, "grid": list(wl.dims), "views": wl.k},
             "stages_ms": {k: float(np.mean(v)) for k, v in stage.items()},
             "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": threads, "kind": "port", "sample": sample},
             "e2e": {"value": fps, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
-def cpu_baseline_sample():
-    """The oracle on the host (rank 0, N=1): 2 frames of C2 (~10-20 s)."""
+def cpu_baseline_sample(wl):
+    """The oracle on the host (rank 0, N=1): 2 frames of the workload (~10-30 s)."""
     from oracle import oracle as O
-    rig = O.make_circle_rig(K_VIEWS, 0, 2500, 1000, W, H, F)
+    rig = oracle_rig(O, wl)
     ts = []
-    for f in (10, 200):
-        body = O.kick_body(STREAM, f)
-        views = [O.render_frame(rig[k], body, k, f) for k in range(K_VIEWS)]
+    picks = (wl.frames // 30, wl.frames * 2 // 3)
+    for j in picks:
+        inp = oracle_inputs(O, rig, wl, j)
         t0 = time.perf_counter()
-        r = O.reconstruct_frame(rig, [v.depth for v in views], [v.mask for v in views], [v.rgb for v in views],
-                                dims=DIMS, want_volume=False)
+        r = O.reconstruct_frame(rig, *inp, dims=wl.dims, want_volume=False)
         ts.append(time.perf_counter() - t0)
         assert r.status == 0
     threads = O.lib().orc_hardware_threads()
     return {"value": len(ts) / sum(ts), "unit": "frames/s", "cores": threads, "kind": "port",
-            "sample": f"2 frames (#10, #200) of the C2 stream; CPU oracle port of proj/core, splat on {threads} "
-                      f"threads (splat.cpp:59-78), other stages single-threaded as the reference, fp64 radix-2 "
-                      f"FFT in place of FFTW; {os.cpu_count()} host CPUs"}
+            "sample": f"2 frames (kick #{wl.kick_frame(picks[0])}, #{wl.kick_frame(picks[1])}) of the "
+                      f"{wl.key.upper()} stream; CPU oracle port of proj/core, splat on {threads} threads "
+                      f"(splat.cpp:59-78), other stages single-threaded as the reference, fp64 radix-2 FFT in place "
+                      f"of FFTW; {os.cpu_count()} host CPUs"}
 
 
 # ------------------------------------------------------------------ GPU arm
@@ -209,7 +262,7 @@ def survey_bytes(nx, ny, nz, P, V, T, k):
             "ifft_x": 8 * Nh + 4 * N, "iso": P * 44, "mc": 4 * N + V * 24 + T * 12, "texture": V * (15 + 13 * k)}
 
 
-def profile_kernels(lib, h, sensors, views_list, cfg, dims, out):
+def profile_kernels(lib, h, sensors, views_list, cfg, dims, out, k=4):
     """Per-stage and per-kernel-group CUDA-event times (profiling replay on
     context h, outside the timed loop) + the roofline of the dominant kernel."""
     from paper_1712_03084_b200 import _lib as L
@@ -221,7 +274,7 @@ def profile_kernels(lib, h, sensors, views_list, cfg, dims, out):
     n = len(views_list)
     ker = np.zeros(11)
     for views in views_list:
-        L.check(lib.vc_reconstruct_frame(h, sensors, views, K_VIEWS, C.byref(cfg), C.byref(out), C.byref(tm)), h)
+        L.check(lib.vc_reconstruct_frame(h, sensors, views, k, C.byref(cfg), C.byref(out), C.byref(tm)), h)
         for nm, _ in L.StageTimings._fields_:
             acc[nm] = acc.get(nm, 0.0) + getattr(tm, nm) / n
         lib.vc_ctx_kernel_times(h, kt, 16)
@@ -233,7 +286,7 @@ def profile_kernels(lib, h, sensors, views_list, cfg, dims, out):
     pos = np.zeros((P, 3))
     L.check(lib.vc_export_points(h, C.c_void_p(pos.ctypes.data), None, None, None, None), h)
     sp = sparse_stats(pos, out.grid.origin[:], out.grid.edge_mm, *dims)
-    ab = alg_bytes(*dims, P, V, T, K_VIEWS, *sp)
+    ab = alg_bytes(*dims, P, V, T, k, *sp)
     bw = {nm: ab[nm] / (kernel_ms[nm] * 1e-3) / 1e9 for nm in names if kernel_ms[nm] > 0}
     if not all(nm in bw for nm in ["clear", "fft_x", "fft_y", "fft_z", "ifft_y", "ifft_x"]):
         raise RuntimeError(f"per-kernel event timings missing: {kernel_ms}")
@@ -247,7 +300,7 @@ def profile_kernels(lib, h, sensors, views_list, cfg, dims, out):
             traffic = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))[dom]["dram_bytes_per_launch"]
         except Exception:
             traffic = None
-    sb = survey_bytes(*dims, P, V, T, K_VIEWS)
+    sb = survey_bytes(*dims, P, V, T, k)
     alg = sb.get(dom, ab[dom])
     achieved = alg / (kernel_ms[dom] * 1e-3) / 1e9
     roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm, "unit": "GB/s",
@@ -260,6 +313,38 @@ def profile_kernels(lib, h, sensors, views_list, cfg, dims, out):
             "sparse": sp}
 
 
+def fft_comparator(lib, device, grids):
+    """cuFFT timed as a comparator (north_star): batched R2C of
+    the 3 components + one fused filter kernel + C2R (the FFTW calls of
+    integrate.cpp:31-34,44,63 on the GPU library) against our chain on the same
+    dense pseudo-random field (no sparsity shortcuts), device-resident, CUDA
+    events.  Timing only: cuFFT's C2R on the non-Hermitian filtered planes is
+    undefined, so parity stays with our kernels."""
+    from paper_1712_03084_b200 import _lib as L
+    from paper_1712_03084_b200 import volcap as vc
+    out = []
+    try:
+        cmp = C.CDLL(os.path.join(ROOT, "paper_1712_03084_b200", "libvc_cufft_cmp.so"))
+    except OSError as e:
+        return [{"error": f"libvc_cufft_cmp.so: {e}"}]
+    for n in grids:
+        iters = 20 if n <= 512 else 5
+        ms_c = (C.c_double * 4)()
+        rc = cmp.vcx_cufft_integrate_time(device, n, n, n, iters, ms_c)
+        ctx = vc.Context(device)
+        ms_o = (C.c_double * 6)()
+        st = lib.vc_time_integrate(ctx.handle, n, n, n, iters, ms_o)
+        ctx.close()
+        if rc != 0 or st != 0:
+            out.append({"grid": [n] * 3, "error": f"cufft rc={rc}, ours status={st}"})
+            continue
+        out.append({"grid": [n] * 3, "cufft_ms": ms_c[3], "ours_ms": ms_o[5], "speedup": ms_c[3] / ms_o[5],
+                     "cufft_split_ms": {"r2c_x3": ms_c[0], "filter": ms_c[1], "c2r": ms_c[2]},
+                     "ours_split_ms": dict(zip(["fft_x", "fft_y", "fft_z", "ifft_y", "ifft_x"], list(ms_o)[:5])),
+                     "field": "dense pseudo-random 3-component field (every row/plane non-empty)", "iters": iters})
+    return out
+
+
 def run_gpu(args):
     rank, world, local = dist_env()
     import torch
@@ -269,6 +354,9 @@ def run_gpu(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_1712_03084_b200 import _lib as L
     from paper_1712_03084_b200 import volcap as vc
+    from paper_1712_03084_b200.frame_parallel import max_over_ranks, rank_frames, stream_frame
+    wl = WORKLOADS[args.workload]
+    K, dims = wl.k, wl.dims
     lib = L.lib()
     S = max(1, args.streams)
     ctxs = [vc.Context(local) for _ in range(S)]  # one context (stream + buffers) per concurrent frame
@@ -277,51 +365,51 @@ def run_gpu(args):
     dev = torch.device("cuda", local)
     streams = [torch.cuda.ExternalStream(c.stream(), device=dev) for c in ctxs]
 
-    rig = vc.make_circle_rig(K_VIEWS, 0, 2500, W, H, F)
-    sensors = rig.c_array(K_VIEWS)
+    rig = vc.make_hd_rig(K) if wl.hd else vc.make_circle_rig(K, 0, 2500, W, H, F)
+    sensors = rig.c_array(K)
     n_pix = W * H
-    per_view = n_pix * 2 + n_pix + n_pix * 3
-    frame_bytes = K_VIEWS * per_view
+    per_view, frame_bytes, NF = wl.view_bytes, wl.frame_bytes, wl.frames
     # device-resident stream (rendered on the GPU) + pinned host copy for e2e
     dbuf = C.c_void_p()
-    L.check(lib.vc_device_alloc(h, C.c_size_t(STREAM * frame_bytes), C.byref(dbuf)), h)
+    L.check(lib.vc_device_alloc(h, C.c_size_t(NF * frame_bytes), C.byref(dbuf)), h)
     hbuf = C.c_void_p()
-    L.check(lib.vc_host_alloc(h, C.c_size_t(STREAM * frame_bytes), C.byref(hbuf)), h)
+    L.check(lib.vc_host_alloc(h, C.c_size_t(NF * frame_bytes), C.byref(hbuf)), h)
 
-    def view_ptrs(base, f, k):
-        o = base + f * frame_bytes + k * per_view
+    def view_ptrs(base, j, k):
+        o = base + j * frame_bytes + k * per_view
         return o, o + 2 * n_pix, o + 3 * n_pix
 
-    for f in range(STREAM):
+    for j in range(NF):
+        f = wl.kick_frame(j)
         body = vc.kick_body(STREAM, f)
-        for k in range(K_VIEWS):
-            d, m, c = view_ptrs(dbuf.value, f, k)
+        for k in range(K):
+            d, m, c = view_ptrs(dbuf.value, j, k)
             L.check(lib.vc_synth_render(h, C.byref(sensors[k]), C.byref(body), C.c_double(0.0), C.c_uint64(1),
                                         C.c_double(1.0), k, f, C.c_void_p(d), C.c_void_p(m), C.c_void_p(c),
                                         L.VC_MEM_DEVICE), h)
-    L.check(lib.vc_memcpy(h, hbuf, dbuf, C.c_size_t(STREAM * frame_bytes), L.VC_MEM_HOST, L.VC_MEM_DEVICE), h)
+    L.check(lib.vc_memcpy(h, hbuf, dbuf, C.c_size_t(NF * frame_bytes), L.VC_MEM_HOST, L.VC_MEM_DEVICE), h)
 
-    def views_for(base, f, kind):
-        arr = (L.View * K_VIEWS)()
-        for k in range(K_VIEWS):
-            d, m, c = view_ptrs(base, f, k)
+    def views_for(base, j, kind):
+        arr = (L.View * K)()
+        for k in range(K):
+            d, m, c = view_ptrs(base, j, k)
             arr[k] = L.View(d, m, c, 0, 0, 0, kind)
         return arr
 
-    dev_views = [views_for(dbuf.value, f, L.VC_MEM_DEVICE) for f in range(STREAM)]
-    host_views = [views_for(hbuf.value, f, L.VC_MEM_HOST) for f in range(STREAM)]
-    from paper_1712_03084_b200.frame_parallel import max_over_ranks, shard_frames
-    cfg = vc.ReconConfig(dims=DIMS).to_c()
+    dev_views = [views_for(dbuf.value, j, L.VC_MEM_DEVICE) for j in range(NF)]
+    host_views = [views_for(hbuf.value, j, L.VC_MEM_HOST) for j in range(NF)]
+    cfg = vc.ReconConfig(dims=dims).to_c()
     outs = [L.TexturedMesh() for _ in range(S)]
     out = outs[0]
-    my_frames = shard_frames(STREAM, rank, world) or [0]
+    # global step g = i * world + rank reconstructs resident frame stream_frame(g): every pose is sampled
+    my_frames = rank_frames(rank, world, max(args.steps, args.warmup, S), NF)
     d2h_acc = [0] * S
 
     def frame(i, views, s=0):
         o = outs[s]
-        L.check(lib.vc_reconstruct_frame(ctxs[s].handle, sensors, views[my_frames[i % len(my_frames)]], K_VIEWS,
+        L.check(lib.vc_reconstruct_frame(ctxs[s].handle, sensors, views[my_frames[i % len(my_frames)]], K,
                                          C.byref(cfg), C.byref(o), None), ctxs[s].handle)
-        d2h_acc[s] += o.vertex_count * (12 + 12 + 24 + 3 + 1 + K_VIEWS * (1 + 8 + 4)) + o.triangle_count * 12
+        d2h_acc[s] += o.vertex_count * (12 + 12 + 24 + 3 + 1 + K * (1 + 8 + 4)) + o.triangle_count * 12
 
     def run_steps(views, steps):
         """`steps` frames over S host threads, each driving its own context."""
@@ -378,9 +466,9 @@ def run_gpu(args):
     value = total_frames / (ms / 1000.0)
     kernels = lib.vc_ctx_kernels_per_frame(h)
 
-    # ---- per-stage / per-kernel timings (profiling replay, separate from the timed loop)
-    prof = profile_kernels(lib, h, sensors, [dev_views[(i * 13) % STREAM] for i in range(min(20, STREAM))], cfg,
-                           DIMS, out)
+    # ---- per-stage / per-kernel timings (profiling replay of the first 20 global steps, outside the timed loop)
+    prof = profile_kernels(lib, h, sensors, [dev_views[stream_frame(i, NF)] for i in range(min(20, NF))], cfg,
+                           dims, out, K)
     acc, kernel_ms, bw, ab, roofline = prof["stages"], prof["kernel_ms"], prof["bw"], prof["ab"], prof["roofline"]
     P, V, T = prof["P"], prof["V"], prof["T"]
     chunks, nzrows, nzplanes = prof["sparse"]
@@ -402,15 +490,23 @@ def run_gpu(args):
         split = {"h2d_only_fps": total_frames / (h2d_ms / 1000.0), "d2h_only_fps": total_frames / (d2h_ms / 1000.0)}
 
     if rank == 0:
-        cpu = cpu_baseline_sample() if (world == 1 and not args.no_cpu_baseline) else None
+        cmp = None
+        if world == 1 and not args.no_fft_comparator:
+            cmp = fft_comparator(lib, local, [dims[0], 1024] if dims[0] < 1024 else [dims[0]])
+            frame_fft = sum(kernel_ms[k] for k in ("fft_x", "fft_y", "fft_z", "ifft_y", "ifft_x"))
+            for c in cmp:
+                if c.get("grid") == list(dims):
+                    c["ours_in_frame_ms"] = frame_fft  # the frame's chain with the splat's sparsity
+        cpu = cpu_baseline_sample(wl) if (world == 1 and not args.no_cpu_baseline) else None
         line = {
-            "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
+            "metric": wl.metric, "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": WORKLOAD, "grid": list(DIMS), "views": K_VIEWS, "splat": "weighted",
+            "config": {"workload": wl.text, "grid": list(dims), "views": K, "splat": "weighted",
                        "frames_per_rank": args.steps, "parallelism": f"frame-parallel x{world}",
+                       "frame_order": f"global step g = i*{world} + rank reconstructs resident frame (97 g) mod {NF}",
                        "streams_per_gpu": S,
-                       "l2": "per-step working set (~0.55 GB volume buffers + 5.2 MB inputs) exceeds the 126 MB L2",
+                       "l2": "per-step working set (volume buffers >= 0.5 GB + inputs) exceeds the 126 MB L2",
                        "precision": "fp32 splat/FFT, fp64 binning, projections, MC vertices"},
             "e2e": {"value": e2e_value, "unit": "frames/s", "h2d_bytes_per_step": frame_bytes,
                     "d2h_bytes_per_step": int(d2h_per)},
@@ -420,13 +516,15 @@ def run_gpu(args):
             "kernel_ms": {k: round(v, 4) for k, v in kernel_ms.items()},
             "kernel_gbs": {k: round(v, 1) for k, v in bw.items()},
             "mesh": {"points": P, "vertices": V, "triangles": T},
-            "sparsity": {"touched_chunks": chunks, "chunks_total": DIMS[1] * DIMS[2] * (DIMS[0] // 32),
-                         "nonzero_rows": nzrows, "rows_total": DIMS[1] * DIMS[2],
-                         "nonzero_planes": nzplanes, "planes_total": DIMS[2]},
+            "sparsity": {"touched_chunks": chunks, "chunks_total": dims[1] * dims[2] * (dims[0] // 32),
+                         "nonzero_rows": nzrows, "rows_total": dims[1] * dims[2],
+                         "nonzero_planes": nzplanes, "planes_total": dims[2]},
             "algorithmic_bytes": ab,
             "clocks": clk.summary(),
             "wall_s": wall,
         }
+        if cmp is not None:
+            line["fft_comparator"] = cmp
         if split:
             line["e2e_split"] = split
         if cpu:
@@ -583,6 +681,43 @@ def run_c5(args):
         torch.distributed.destroy_process_group()
 
 
+def free_port():
+    import socket
+    so = socket.socket()
+    so.bind(("127.0.0.1", 0))
+    p = so.getsockname()[1]
+    so.close()
+    return p
+
+
+def launch_ranks(n):
+    """`--gpus N` (N > 1) outside torchrun: re-run this script as N ranks, one
+    process per GPU, under torch.distributed.run on 127.0.0.1 (the driver's own
+    launch line); rank 0 prints the JSON line."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={free_port()}", os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.run(cmd).returncode
+
+
+def run_plan(args):
+    """--plan: the frame-to-rank assignment this launch would run (no GPU): each
+    rank computes its frames, rank 0 gathers them (gloo) and prints one JSON line."""
+    from paper_1712_03084_b200.frame_parallel import rank_frames
+    rank, world, _ = dist_env()
+    wl = WORKLOADS[args.workload]
+    mine = [wl.kick_frame(j) for j in rank_frames(rank, world, args.steps, wl.frames)]
+    allf = [mine]
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("gloo")
+        allf = [None] * world
+        dist.all_gather_object(allf, mine)
+        dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps({"plan": True, "n_gpus": world, "steps": args.steps, "workload": wl.key,
+                          "frames_by_rank": allf}), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -590,14 +725,28 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--workload", default="c2", choices=["c2", "c5"],
-                    help="c2: the BASELINE metric (256^3 stream, frame-parallel); c5: 1024^3 frames (z-slabs on N>1)")
+    ap.add_argument("--no-fft-comparator", action="store_true")
+    ap.add_argument("--workload", default="c2", choices=["c2", "c3", "c5"],
+                    help="c2: the BASELINE metric (256^3 stream, frame-parallel); c3: 512^3, 6 views + HD colour; "
+                         "c5: 1024^3 frames (z-slabs on N>1)")
     ap.add_argument("--streams", type=int, default=4,
                     help="concurrent frames per GPU (one context + host thread each)")
+    ap.add_argument("--plan", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
     if args.warmup < 3 and args.impl != "reference":
         args.warmup = 3
-    if args.impl == "reference":
+    if args.gpus < 1:
+        raise SystemExit("--gpus must be >= 1")
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(launch_ranks(args.gpus))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} does not match WORLD_SIZE={world}")
+    if args.plan:
+        run_plan(args)
+    elif args.impl == "reference":
+        if args.workload == "c5":
+            raise SystemExit("--impl reference runs c2/c3 (the CPU path at 1024^3 takes minutes per frame)")
         run_reference(args)
     elif args.workload == "c5":
         run_c5(args)

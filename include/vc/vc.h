@@ -250,6 +250,10 @@ vc_status vc_stage_splat(vc_ctx* ctx, const double* pos, const double* nrm, cons
 /* integrate.cpp:19-74: field 3N floats (interleaved) -> A N floats. */
 vc_status vc_stage_integrate(vc_ctx* ctx, const float* field, int32_t nx, int32_t ny, int32_t nz, float* A);
 /* splat.cpp:91-101: mean trilinear A (fp32 volume) at the points. */
+/* Measurement: the integrate chain on a dense pseudo-random field of the given
+ * dims, device-resident; ms[0..4] = F-x, F-y, Z, I-y, I-x per launch, ms[5] =
+ * the chain (average of `iters` runs).  Used by bench.py's cuFFT comparator. */
+vc_status vc_time_integrate(vc_ctx* ctx, int32_t nx, int32_t ny, int32_t nz, int32_t iters, double ms[6]);
 vc_status vc_stage_iso_level(vc_ctx* ctx, const float* A, const vc_grid_spec* grid, const double* pos, int64_t n,
                              double* level);
 /* marching_cubes.cpp:131-210 on an fp32 volume at a double level.  Vertices

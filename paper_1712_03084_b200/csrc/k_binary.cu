@@ -223,12 +223,12 @@ void launch_binarize(const float* A, int nx, int ny, int nz, double level, int32
   const size_t n = (size_t)nx * ny * nz;
   const int rows = ny * nz;
   bin_reset_kernel<<<1, 1, 0, st>>>(reinterpret_cast<int*>(maxbuf), best);
-  bin_max_kernel<<<148 * 8, 256, 0, st>>>(A, n, maxbuf);
-  bin_init_kernel<<<148 * 8, 256, 0, st>>>(A, n, float_round_up(level), reinterpret_cast<const int*>(maxbuf),
+  bin_max_kernel<<<sm_count() * 8, 256, 0, st>>>(A, n, maxbuf);
+  bin_init_kernel<<<sm_count() * 8, 256, 0, st>>>(A, n, float_round_up(level), reinterpret_cast<const int*>(maxbuf),
                                            parent, size);
-  bin_union_kernel<<<148 * 8, 256, 0, st>>>(parent, nx, ny, nz);
-  bin_compress_kernel<<<148 * 8, 256, 0, st>>>(parent, size, n);
-  bin_best_kernel<<<148 * 8, 256, 0, st>>>(parent, size, n, best);
+  bin_union_kernel<<<sm_count() * 8, 256, 0, st>>>(parent, nx, ny, nz);
+  bin_compress_kernel<<<sm_count() * 8, 256, 0, st>>>(parent, size, n);
+  bin_best_kernel<<<sm_count() * 8, 256, 0, st>>>(parent, size, n, best);
   bin_rows_kernel<<<(rows * 32 + 255) / 256, 256, 0, st>>>(parent, best, nx, rows, keep, rowcnt);
   bin_scan_kernel<<<1, 1024, 0, st>>>(rowcnt, rows);
 }
@@ -241,7 +241,7 @@ void launch_binarize_emit(const int32_t* parent, const unsigned long long* best,
 
 void launch_boundary_flags(const uint8_t* keep, const int32_t* voxels, int64_t n, int nx, int ny, int nz,
                            uint8_t* flag, cudaStream_t st) {
-  if (n > 0) bin_boundary_flag_kernel<<<148 * 8, 256, 0, st>>>(keep, voxels, n, nx, ny, nz, flag);
+  if (n > 0) bin_boundary_flag_kernel<<<sm_count() * 8, 256, 0, st>>>(keep, voxels, n, nx, ny, nz, flag);
 }
 
 }  // namespace vc

@@ -191,7 +191,7 @@ __global__ void __launch_bounds__(1024) pairs_compact_kernel(const int32_t* part
 }  // namespace
 
 void launch_color_apply(const uint8_t* in, uint8_t* out, int64_t n, double gain, double offset, cudaStream_t st) {
-  color_apply_kernel<<<148 * 8, 256, 0, st>>>(in, out, n, gain, offset);
+  color_apply_kernel<<<sm_count() * 8, 256, 0, st>>>(in, out, n, gain, offset);
 }
 
 size_t grid_scratch_bytes(int n) {
@@ -222,10 +222,10 @@ GridBufs carve_grid(void* scratch, int n) {
 }
 Grid build_grid(const double* pts, int n, double cell, void* scratch, cudaStream_t st) {
   GridBufs b = carve_grid(scratch, n);
-  grid_clear_kernel<<<148 * 2, 256, 0, st>>>(b.keys, b.counts, b.cap);
-  if (n > 0) grid_insert_kernel<<<148 * 4, 256, 0, st>>>(pts, n, cell, b.keys, b.counts, b.slot_of, b.cap);
+  grid_clear_kernel<<<sm_count() * 2, 256, 0, st>>>(b.keys, b.counts, b.cap);
+  if (n > 0) grid_insert_kernel<<<sm_count() * 4, 256, 0, st>>>(pts, n, cell, b.keys, b.counts, b.slot_of, b.cap);
   grid_scan_kernel<<<1, 1024, 0, st>>>(b.counts, b.starts, b.cursor, b.cap);
-  if (n > 0) grid_scatter_kernel<<<148 * 4, 256, 0, st>>>(n, b.slot_of, b.cursor, b.items);
+  if (n > 0) grid_scatter_kernel<<<sm_count() * 4, 256, 0, st>>>(n, b.slot_of, b.cursor, b.items);
   return Grid{b.keys, b.counts, b.starts, b.items, pts, b.cap, cell};
 }
 }  // namespace
@@ -234,7 +234,7 @@ void launch_mutual_pairs(const double* a, int na, const double* b, int nb, doubl
                          void* scratch_b, int32_t* partner, int32_t* pairs, int32_t* n_pairs, cudaStream_t st) {
   const Grid ga = build_grid(a, na, max_dist, scratch_a, st);
   const Grid gb = build_grid(b, nb, max_dist, scratch_b, st);
-  if (na > 0) mutual_kernel<<<148 * 4, 128, 0, st>>>(ga, gb, a, na, max_dist, partner);
+  if (na > 0) mutual_kernel<<<sm_count() * 4, 128, 0, st>>>(ga, gb, a, na, max_dist, partner);
   pairs_compact_kernel<<<1, 1024, 0, st>>>(partner, na, pairs, n_pairs);
 }
 

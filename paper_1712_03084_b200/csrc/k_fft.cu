@@ -25,6 +25,7 @@
 #include <vector>
 
 #include "vc_shared.hpp"
+#include "vc_device.cuh"
 
 namespace vc {
 namespace {
@@ -819,7 +820,7 @@ struct RunFx {
     using C = XCfg<N>;
     const int rows = a.ny * a.nzl;
     const int need = (rows / 2 + C::TEAMS - 1) / C::TEAMS;
-    const int grid = a.rowlist && need > 148 * 2 ? 148 * 2 : need;  // persistent teams over the row list
+    const int grid = a.rowlist && need > sm_count() * 2 ? sm_count() * 2 : need;  // persistent teams over the row list
     fx_kernel<N><<<grid, C::THREADS, C::SMEM, a.st>>>(a.acc, a.S0, a.S1, a.S2, rows, a.H, a.rowbits, a.mode, a.twx,
                                                       a.rowlist);
   }
@@ -880,7 +881,7 @@ struct RunIx {
     using C = IXCfg<N>;
     const int rows = a.ny * a.nzl;
     const int need = (rows / 2 + C::TEAMS - 1) / C::TEAMS;
-    const int grid = need < 148 * 4 ? need : 148 * 4;  // persistent teams
+    const int grid = need < sm_count() * 4 ? need : sm_count() * 4;  // persistent teams
     const float scale = (float)(1.0 / ((double)a.nx * a.ny * a.nz));
     ix_kernel<N><<<grid, C::THREADS, C::SMEM, a.st>>>(a.Rout, a.A, rows, a.H, scale, a.twx, a.rowmm);
   }
@@ -919,6 +920,24 @@ void launch_fft_z(const SlabFft& a) { dispatch_n<RunZ>(a.nz, a); }
 void launch_fft_inverse_yx(const SlabFft& a) {
   dispatch_n<RunIy>(a.ny, a);
   dispatch_n<RunIx>(a.nx, a);
+}
+
+// Dense pseudo-random accumulator (U' in [-1, 1), d' = 1) for timing the
+// chain without the splat's sparsity.
+__global__ void fill_random_acc_kernel(float4* acc, size_t n, uint32_t seed) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    uint32_t h = (uint32_t)i * 2654435761u ^ seed;
+    float v[3];
+    for (int c = 0; c < 3; ++c) {
+      h ^= h >> 16, h *= 0x7feb352du, h ^= h >> 15, h *= 0x846ca68bu, h ^= h >> 16;
+      v[c] = (float)(h >> 8) * (2.0f / 16777216.0f) - 1.0f;
+    }
+    acc[i] = make_float4(v[0], v[1], v[2], 1.0f);
+  }
+}
+
+void launch_fill_random_acc(float4* acc, size_t n, uint32_t seed, cudaStream_t st) {
+  fill_random_acc_kernel<<<sm_count() * 8, 256, 0, st>>>(acc, n, seed);
 }
 
 void launch_integrate(const float4* acc, float2* spec, float* A, int nx, int ny, int nz, int mode,

@@ -597,7 +597,7 @@ __global__ void add_f64_kernel(double* dst, const double* src, size_t n) {
 }  // namespace
 
 void launch_add_f64(double* dst, const double* src, size_t n, cudaStream_t st) {
-  add_f64_kernel<<<148 * 4, 256, 0, st>>>(dst, src, n);
+  add_f64_kernel<<<sm_count() * 4, 256, 0, st>>>(dst, src, n);
 }
 
 void launch_mc_set_voff(const int32_t* counts, int rank, DevCtl* ctl, cudaStream_t st) {
@@ -638,23 +638,23 @@ void launch_marching_cubes_count(const float* A, DevCtl* ctl, MeshBufs mb, int n
   int3* ucnt = reinterpret_cast<int3*>(mb.unitcnt);
   mc_rows_kernel<<<nblk, kRowThreads, 0, st>>>(mb.rowmm, ctl, ny, nz, sl, rowmask);
   mc_units_kernel<<<1, 1024, 0, st>>>(rowmask, (units + 31) / 32, mb.units, ctl);
-  mc_count_kernel<<<148 * 8, 256, 0, st>>>(A, ctl, nx, ny, nz, sl, mb.units, ucnt, mb);
+  mc_count_kernel<<<sm_count() * 8, 256, 0, st>>>(A, ctl, nx, ny, nz, sl, mb.units, ucnt, mb);
   mc_scan_kernel<<<1, 1024, 0, st>>>(ucnt, ctl, ctl, mb.v_cap, mb.t_cap, mb.c_cap);
 }
 
 void launch_marching_cubes_emit(const float* A, DevCtl* ctl, MeshBufs mb, int nx, int ny, int nz, McSlab sl,
                                 cudaStream_t st, cudaStream_t aux, cudaEvent_t fork, cudaEvent_t join) {
   int3* ucnt = reinterpret_cast<int3*>(mb.unitcnt);
-  mc_emit_kernel<<<148 * 8, 256, 0, st>>>(A, ctl, nx, ny, nz, sl, mb.units, ucnt, mb);
+  mc_emit_kernel<<<sm_count() * 8, 256, 0, st>>>(A, ctl, nx, ny, nz, sl, mb.units, ucnt, mb);
   if (aux) {  // normals and triangles are independent: normals on the side stream
     cudaEventRecord(fork, st);
     cudaStreamWaitEvent(aux, fork, 0);
-    mc_normals_kernel<<<148 * 4, 256, 0, aux>>>(A, ctl, nx, ny, nz, mb);
+    mc_normals_kernel<<<sm_count() * 4, 256, 0, aux>>>(A, ctl, nx, ny, nz, mb);
     cudaEventRecord(join, aux);
-    mc_tris_kernel<<<148 * 4, 256, 0, st>>>(A, ctl, nx, ny, nz, mb);
+    mc_tris_kernel<<<sm_count() * 4, 256, 0, st>>>(A, ctl, nx, ny, nz, mb);
   } else {
-    mc_normals_kernel<<<148 * 4, 256, 0, st>>>(A, ctl, nx, ny, nz, mb);
-    mc_tris_kernel<<<148 * 4, 256, 0, st>>>(A, ctl, nx, ny, nz, mb);
+    mc_normals_kernel<<<sm_count() * 4, 256, 0, st>>>(A, ctl, nx, ny, nz, mb);
+    mc_tris_kernel<<<sm_count() * 4, 256, 0, st>>>(A, ctl, nx, ny, nz, mb);
   }
 }
 
@@ -667,7 +667,7 @@ void launch_marching_cubes(const float* A, DevCtl* ctl, MeshBufs mb, int nx, int
 
 void launch_iso_samples(const DevPoints& pts, const float* A, const DevCtl* ctl, int zoff, int nzl, double* samples,
                         cudaStream_t st) {
-  iso_sample_kernel<<<148 * 4, 256, 0, st>>>(pts.pos, A, ctl, zoff, nzl, samples);
+  iso_sample_kernel<<<sm_count() * 4, 256, 0, st>>>(pts.pos, A, ctl, zoff, nzl, samples);
 }
 
 void launch_iso_final_samples(const double* samples, DevCtl* ctl, double* partial, cudaStream_t st) {

@@ -223,11 +223,11 @@ __global__ void mt_terms_kernel(const double* mx_, const double* my_, const doub
 
 }  // namespace
 
-constexpr int kMtGrid = 148 * 4;
+static int mt_grid() { return sm_count() * 4; }
 
 void launch_vre(const uint8_t* a, const uint8_t* b, int n, unsigned long long* cnt, cudaStream_t st) {
   cudaMemsetAsync(cnt, 0, 16, st);
-  mt_vre_kernel<<<kMtGrid, 256, 0, st>>>(a, b, n, cnt);
+  mt_vre_kernel<<<mt_grid(), 256, 0, st>>>(a, b, n, cnt);
 }
 
 size_t dt_scratch_bytes(int w, int h) {
@@ -241,7 +241,7 @@ void launch_distance_transform(const uint8_t* mask, int w, int h, void* scratch,
   double* tmp = g + n;
   double* zb = tmp + n;
   int* vb = reinterpret_cast<int*>(zb + (size_t)(w + h) * (m + 2));
-  mt_dt_init_kernel<<<kMtGrid, 256, 0, st>>>(mask, (int)n, g);
+  mt_dt_init_kernel<<<mt_grid(), 256, 0, st>>>(mask, (int)n, g);
   mt_dt_cols_kernel<<<(w + 127) / 128, 128, 0, st>>>(g, tmp, vb, zb, w, h);
   mt_dt_rows_kernel<<<(h + 127) / 128, 128, 0, st>>>(g, tmp, vb, zb, w, h, out);
 }
@@ -249,35 +249,35 @@ void launch_distance_transform(const uint8_t* mask, int w, int h, void* scratch,
 void launch_hausdorff(const uint8_t* a, const uint8_t* b, const float* dta, const float* dtb, int n, int* maxbits,
                       cudaStream_t st) {
   cudaMemsetAsync(maxbits, 0, 4, st);
-  mt_hausdorff_kernel<<<kMtGrid, 256, 0, st>>>(a, b, dta, dtb, n, maxbits);
+  mt_hausdorff_kernel<<<mt_grid(), 256, 0, st>>>(a, b, dta, dtb, n, maxbits);
 }
 
 void launch_nearest(const double* ground, int ng, const double* recon, int nr, double* out, cudaStream_t st) {
-  mt_nearest_kernel<<<(ng + 255) / 256 < kMtGrid ? (ng + 255) / 256 : kMtGrid, 256, 0, st>>>(ground, ng, recon, nr,
+  mt_nearest_kernel<<<(ng + 255) / 256 < mt_grid() ? (ng + 255) / 256 : mt_grid(), 256, 0, st>>>(ground, ng, recon, nr,
                                                                                             out);
 }
 
 void launch_ssim_gray(const uint8_t* rgb, int n, double* g, cudaStream_t st) {
-  mt_gray_kernel<<<kMtGrid, 256, 0, st>>>(rgb, n, g);
+  mt_gray_kernel<<<mt_grid(), 256, 0, st>>>(rgb, n, g);
 }
 void launch_ssim_gauss(const double* in, double* tmp, double* out, int w, int h, const double* k, int r,
                        cudaStream_t st) {
-  mt_gauss_kernel<<<kMtGrid, 256, 0, st>>>(in, tmp, w, h, k, r, 0);
-  mt_gauss_kernel<<<kMtGrid, 256, 0, st>>>(tmp, out, w, h, k, r, 1);
+  mt_gauss_kernel<<<mt_grid(), 256, 0, st>>>(in, tmp, w, h, k, r, 0);
+  mt_gauss_kernel<<<mt_grid(), 256, 0, st>>>(tmp, out, w, h, k, r, 1);
 }
 void launch_ssim_mul(const double* a, const double* b, double* o, int n, cudaStream_t st) {
-  mt_mul_kernel<<<kMtGrid, 256, 0, st>>>(a, b, o, n);
+  mt_mul_kernel<<<mt_grid(), 256, 0, st>>>(a, b, o, n);
 }
 void launch_ssim_down(const double* in, int w, int h, double* out, int ow, int oh, cudaStream_t st) {
-  mt_down_kernel<<<kMtGrid, 256, 0, st>>>(in, w, h, out, ow, oh);
+  mt_down_kernel<<<mt_grid(), 256, 0, st>>>(in, w, h, out, ow, oh);
 }
 void launch_ssim_down_or(const uint8_t* in, int w, int h, uint8_t* out, int ow, int oh, cudaStream_t st) {
-  mt_down_or_kernel<<<kMtGrid, 256, 0, st>>>(in, w, h, out, ow, oh);
+  mt_down_or_kernel<<<mt_grid(), 256, 0, st>>>(in, w, h, out, ow, oh);
 }
 void launch_ssim_terms(const double* mx, const double* my, const double* xx, const double* yy, const double* xy,
                        const uint8_t* mask, int w, int h, int r, double c1, double c2, double c3, double* terms,
                        cudaStream_t st) {
-  mt_terms_kernel<<<kMtGrid, 256, 0, st>>>(mx, my, xx, yy, xy, mask, w, h, r, c1, c2, c3, terms);
+  mt_terms_kernel<<<mt_grid(), 256, 0, st>>>(mx, my, xx, yy, xy, mask, w, h, r, c1, c2, c3, terms);
 }
 
 }  // namespace vc

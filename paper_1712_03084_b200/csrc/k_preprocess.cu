@@ -529,13 +529,13 @@ void launch_preprocess(const SensorSet& ss, DevPoints pts, float* weight_maps, i
   pre_prefix_tri_kernel<<<(rows * 32 + 255) / 256, 256, 0, st>>>(ss, rows, s.pref, s.ppitch, ctl, disc_mm, s.tri,
                                                                   s.spr, s.counts, s.flags, weight_maps, s.act,
                                                                   s.rowcnt);
-  const int pgrid = s.nseg < 148 * 16 ? s.nseg : 148 * 16;  // resident one-warp CTAs (registers: 16 warps/SM)
+  const int pgrid = s.nseg < sm_count() * 16 ? s.nseg : sm_count() * 16;  // resident one-warp CTAs (registers: 16 warps/SM)
   pre_points_kernel<<<pgrid, kSegPx, 0, st>>>(ss, sil_r, s.tri, s.pref, s.ppitch, s.stage, s.flags, s.counts, ctl,
                                               weight_maps, s.act, s.spr, s.rowcnt);
   // exclusive scan of the per-row point counts (segment order within a row is
   // resolved by pre_gather from the segment counts)
   pre_scan_kernel<<<1, 1024, 0, st>>>(s.rowcnt, s.offsets, rows, pts.cap, ctl, rowlist_reset, nx, ny, nz, padding);
-  pre_gather_kernel<<<148 * 8, 128, 0, st>>>(ss, s.stage, s.flags, s.offsets, s.counts, pts, s.spr, s.act);
+  pre_gather_kernel<<<sm_count() * 8, 128, 0, st>>>(ss, s.stage, s.flags, s.offsets, s.counts, pts, s.spr, s.act);
 }
 
 }  // namespace vc

@@ -290,8 +290,8 @@ int64_t launch_raster_count(RzMesh m, RzCamera c, void* scratch, cudaStream_t st
   int32_t* off = cnt + npx + 1;
   int32_t* cursor = off + npx + 1;
   cudaMemsetAsync(cnt, 0, npx * 4, st);
-  if (m.V > 0) rz_vertex_kernel<<<148 * 2, 256, 0, st>>>(m, c, cam, scr, front);
-  if (m.T > 0) rz_count_kernel<<<148 * 4, 128, 0, st>>>(m, c, cam, scr, front, cnt);
+  if (m.V > 0) rz_vertex_kernel<<<sm_count() * 2, 256, 0, st>>>(m, c, cam, scr, front);
+  if (m.T > 0) rz_count_kernel<<<sm_count() * 4, 128, 0, st>>>(m, c, cam, scr, front, cnt);
   rz_scan_kernel<<<1, 1024, 0, st>>>(cnt, off, cursor, (int)npx);
   *off_out = off;
   return 0;
@@ -312,9 +312,9 @@ void launch_raster_finish(RzMesh m, RzCamera c, RzImages im, int mode, void* scr
   int32_t* cnt = reinterpret_cast<int32_t*>(p);
   int32_t* off = cnt + npx + 1;
   int32_t* cursor = off + npx + 1;
-  if (m.T > 0) rz_emit_kernel<<<148 * 4, 128, 0, st>>>(m, c, cam, scr, front, cursor, frags);
-  if (mode == 1 && m.V > 0) rz_vcolor_kernel<<<148 * 2, 128, 0, st>>>(m, im, vcol);
-  rz_resolve_kernel<<<148 * 4, 128, 0, st>>>(m, c, im, mode, off, frags, vcol, cam, depth, color, sil);
+  if (m.T > 0) rz_emit_kernel<<<sm_count() * 4, 128, 0, st>>>(m, c, cam, scr, front, cursor, frags);
+  if (mode == 1 && m.V > 0) rz_vcolor_kernel<<<sm_count() * 2, 128, 0, st>>>(m, im, vcol);
+  rz_resolve_kernel<<<sm_count() * 4, 128, 0, st>>>(m, c, im, mode, off, frags, vcol, cam, depth, color, sil);
 }
 
 }  // namespace vc

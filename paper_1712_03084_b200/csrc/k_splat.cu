@@ -204,26 +204,26 @@ __global__ void splat_finalize_kernel(const float4* acc, size_t n, int mode, int
 }  // namespace
 
 void launch_clear(float4* acc, size_t n, cudaStream_t st) {
-  clear_kernel<<<148 * 8, 256, 0, st>>>(acc, n);
+  clear_kernel<<<sm_count() * 8, 256, 0, st>>>(acc, n);
 }
 
 void launch_sparse_clear(float4* acc, uint32_t* rowbits, const int32_t* rowlist, int nx, cudaStream_t st) {
-  sparse_clear_kernel<<<148 * 4, 256, 0, st>>>(acc, rowbits, rowlist, nx);
+  sparse_clear_kernel<<<sm_count() * 4, 256, 0, st>>>(acc, rowbits, rowlist, nx);
 }
 
 void launch_splat(const DevPoints& pts, DevCtl* ctl, float4* acc, uint32_t* rowbits, int32_t* rowlist, int mode,
                   cudaStream_t st, int zoff, int nzl) {
   if (mode == 0)
-    splat_weighted_kernel<<<148 * 8, kSplatThreads, 0, st>>>(pts.pos, pts.nrm, pts.weight, ctl, acc, rowbits, zoff,
+    splat_weighted_kernel<<<sm_count() * 8, kSplatThreads, 0, st>>>(pts.pos, pts.nrm, pts.weight, ctl, acc, rowbits, zoff,
                                                              nzl);
   else
-    splat_simple_kernel<<<148 * 4, 256, 0, st>>>(pts.pos, pts.nrm, ctl, acc, rowbits, zoff, nzl);
-  rowlist_build_kernel<<<148 * 4, 256, 0, st>>>(rowbits, ctl, nzl, rowlist);
+    splat_simple_kernel<<<sm_count() * 4, 256, 0, st>>>(pts.pos, pts.nrm, ctl, acc, rowbits, zoff, nzl);
+  rowlist_build_kernel<<<sm_count() * 4, 256, 0, st>>>(rowbits, ctl, nzl, rowlist);
 }
 
 void launch_splat_finalize(const float4* acc, size_t n, int mode, int negate, double sigma2, float* field,
                            float* density, cudaStream_t st) {
-  splat_finalize_kernel<<<148 * 4, 256, 0, st>>>(acc, n, mode, negate, sigma2, field, density);
+  splat_finalize_kernel<<<sm_count() * 4, 256, 0, st>>>(acc, n, mode, negate, sigma2, field, density);
 }
 
 }  // namespace vc

@@ -155,12 +155,12 @@ void launch_texture(const SensorSet& ss, const float* weight_maps, const double*
                     cudaStream_t st, float* posf) {
   int lg = 0;
   while ((1 << lg) < ss.k) ++lg;  // K <= 16 lanes per vertex
-  texture_kernel<<<148 * 8, 128, 0, st>>>(ss, weight_maps, vpos, ctl, eps_vis, vis, uv, w, untex, rgb, posf, v_cap,
+  texture_kernel<<<sm_count() * 8, 128, 0, st>>>(ss, weight_maps, vpos, ctl, eps_vis, vis, uv, w, untex, rgb, posf, v_cap,
                                           lg);
 }
 
 void launch_mesh_to_f32(const double* pos, float* posf, const DevCtl* ctl, int v_cap, cudaStream_t st) {
-  mesh_f32_kernel<<<148 * 2, 256, 0, st>>>(pos, posf, ctl, v_cap);
+  mesh_f32_kernel<<<sm_count() * 2, 256, 0, st>>>(pos, posf, ctl, v_cap);
 }
 
 }  // namespace vc

@@ -4,9 +4,26 @@
 
 #include <cstdint>
 
+#include <cuda_runtime.h>
+
 #include "vc_shared.hpp"
 
 namespace vc {
+
+// Streaming-multiprocessor count of the calling thread's current device,
+// queried once per device (grid sizes are multiples of it: persistent and
+// grid-stride kernels size their grids as k resident CTAs per SM).
+inline int sm_count() {
+  static int cache[64];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) dev = 0;
+  int v = __atomic_load_n(&cache[dev], __ATOMIC_RELAXED);
+  if (v == 0) {
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0) v = 1;
+    __atomic_store_n(&cache[dev], v, __ATOMIC_RELAXED);
+  }
+  return v;
+}
 
 // ---------------------------------------------------------------- fp64 helpers
 // The binning paths (backprojection, to_voxel, projections) must reproduce

@@ -833,6 +833,42 @@ vc_status vc_stage_integrate(vc_ctx* ctx, const float* field, int32_t nx, int32_
   return VC_OK;
 }
 
+// Timing of the integrate chain on a DENSE field (every row and plane
+// non-empty: no sparsity shortcuts), device-resident, for the cuFFT
+// comparator in bench.py.  ms[0..4] = F-x, F-y, Z, I-y, I-x per launch,
+// ms[5] = the chain, averaged over `iters` after two warm-up runs.
+vc_status vc_time_integrate(vc_ctx* ctx, int32_t nx, int32_t ny, int32_t nz, int32_t iters, double* ms) {
+  if (!ctx || !ms || iters < 1) return fail(ctx, VC_ERR_INVALID_ARGUMENT, "null");
+  if (!pow2_ok(nx) || !pow2_ok(ny) || !pow2_ok(nz))
+    return fail(ctx, VC_ERR_INVALID_ARGUMENT, "grid dims must be powers of two in [4, 1024]");
+  cudaSetDevice(ctx->device);
+  VC_TRY(ensure_grid(ctx, nx, ny, nz));
+  const size_t N = (size_t)nx * ny * nz;
+  launch_fill_random_acc(P<float4>(ctx->acc), N, 12345u, ctx->st);
+  ctx->acc_dirty = true, ctx->layout = 0;
+  cudaEvent_t ev[6];
+  for (auto& e : ev) cudaEventCreate(&e);
+  double acc[6] = {0, 0, 0, 0, 0, 0};
+  for (int it = -2; it < iters; ++it) {
+    launch_integrate(P<float4>(ctx->acc), P<float2>(ctx->spec), P<float>(ctx->A), nx, ny, nz, 1, P<float2>(ctx->tw),
+                     ctx->st, ev, nullptr, nullptr, P<uint32_t>(ctx->planeflag));
+    VC_CUDA(cudaGetLastError());
+    VC_CUDA(cudaStreamSynchronize(ctx->st));
+    if (it < 0) continue;
+    for (int i = 0; i < 5; ++i) {
+      float t = 0;
+      cudaEventElapsedTime(&t, ev[i], ev[i + 1]);
+      acc[i] += t;
+    }
+    float t = 0;
+    cudaEventElapsedTime(&t, ev[0], ev[5]);
+    acc[5] += t;
+  }
+  for (auto& e : ev) cudaEventDestroy(e);
+  for (int i = 0; i < 6; ++i) ms[i] = acc[i] / iters;
+  return VC_OK;
+}
+
 vc_status vc_stage_iso_level(vc_ctx* ctx, const float* A, const vc_grid_spec* grid, const double* pos, int64_t n,
                              double* level) {
   if (!ctx || !A || !grid || !level) return fail(ctx, VC_ERR_INVALID_ARGUMENT, "null");

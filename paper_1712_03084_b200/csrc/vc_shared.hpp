@@ -146,6 +146,7 @@ struct SlabFft {
 void launch_fft_forward_xy(const SlabFft& a);
 void launch_fft_z(const SlabFft& a);
 void launch_fft_inverse_yx(const SlabFft& a);
+void launch_fill_random_acc(float4* acc, size_t n, uint32_t seed, cudaStream_t st);  // dense test field
 void launch_integrate(const float4* acc, float2* spec, float* A, int nx, int ny, int nz, int mode,
                       const float2* twiddles, cudaStream_t st, cudaEvent_t* ev /*nullable, 6 events*/,
                       float2* rowmm /*nullable: per-row min/max of A*/,

@@ -17,6 +17,26 @@ def shard_frames(n_frames: int, rank: int, world: int) -> list[int]:
     return list(range(rank, n_frames, world))
 
 
+STREAM_STRIDE = 97  # coprime with 300: consecutive global steps walk the whole kick stream
+
+
+def stream_frame(global_step: int, n_frames: int, stride: int = STREAM_STRIDE) -> int:
+    """Frame of the capture stream processed at `global_step` (0, 1, 2, ... over
+    all ranks): frame = stride * global_step mod n_frames.  With the stride
+    coprime to n_frames, any n_frames consecutive global steps visit every
+    frame once, so a short run samples every pose instead of the first few."""
+    return (stride * global_step) % n_frames
+
+
+def rank_frames(rank: int, world: int, steps: int, n_frames: int, stride: int = STREAM_STRIDE) -> list[int]:
+    """Frames of `rank` for `steps` steps: global steps rank, rank+world, ...
+    (the stream's frames interleaved over ranks, as shard_frames, then
+    permuted by the stride)."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("bad rank/world")
+    return [stream_frame(i * world + rank, n_frames, stride) for i in range(steps)]
+
+
 def max_over_ranks(value: float, device=None) -> float:
     """MAX all-reduce of one scalar (the benchmark's timing rule); identity when
     torch.distributed is not initialised."""

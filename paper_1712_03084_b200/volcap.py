@@ -459,6 +459,17 @@ def make_circle_rig(recon, held_out=0, radius_mm=2500.0, width=320, height=288, 
     return CameraRig([Sensor.from_c(arr[i]) for i in range(recon + held_out)], recon)
 
 
+def make_hd_rig(recon=6, radius_mm=2500.0) -> CameraRig:
+    """SURVEY §8(d) C3 rig: Kinect2-like depth 512x424 (f=365) on make_circle_rig's
+    circle + a 1920x1080 colour camera (f=1060, cx=959.5, cy=539.5) offset 52 mm
+    along x from each depth camera (Sensor::rgb_relative, types.hpp:68-76)."""
+    rig = make_circle_rig(recon, 0, radius_mm, 512, 424, 365.0)
+    for s in rig.sensors:
+        s.rgb_intr = Intrinsics(1060.0, 1060.0, 959.5, 539.5, 1920, 1080)
+        s.rgb_relative = Pose(np.eye(3), np.array([52.0, 0.0, 0.0]))
+    return rig
+
+
 def xpose_body() -> L.Body:
     b = L.Body()
     L.check(L.lib().vc_synth_xpose_body(C.byref(b)))

@@ -51,3 +51,35 @@ def test_gloo_two_ranks():
     assert out[0][0] == out[1][0] == 15.0  # max over ranks
     assert out[0][1] == out[1][1] == 300   # every frame processed exactly once
     assert out[0][2] == [0, 2, 4] and out[1][2] == [1, 3, 5]
+
+
+def test_stream_order_visits_every_pose():
+    from paper_1712_03084_b200.frame_parallel import rank_frames, stream_frame
+    assert sorted(stream_frame(g, 300) for g in range(300)) == list(range(300))
+    assert sorted(stream_frame(g, 60) for g in range(60)) == list(range(60))
+    for world in (1, 2, 4, 8):
+        steps = 300 // world if 300 % world == 0 else 300 // world + 1
+        got = [f for r in range(world) for f in rank_frames(r, world, steps, 300)]
+        assert set(got) == set(range(300))
+    # the first 20 global steps already span the stream (not the flat first poses)
+    assert max(stream_frame(g, 300) for g in range(20)) - min(stream_frame(g, 300) for g in range(20)) > 250
+
+
+def test_bench_launcher_spawns_ranks():
+    """`bench.py --gpus 2` outside torchrun re-launches itself as 2 ranks
+    (torch.distributed.run, gloo here); the ranks' frame plans are disjoint
+    and together cover the stream once."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--plan", "--gpus", "2", "--steps", "150"],
+                         capture_output=True, text=True, timeout=300, cwd=root, env=env)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and len(d["frames_by_rank"]) == 2
+    a, b = d["frames_by_rank"]
+    assert not set(a) & set(b) and sorted(a + b) == list(range(300))

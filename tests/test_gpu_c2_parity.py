@@ -1,0 +1,108 @@
+# SPDX-License-Identifier: Apache-2.0
+"""Parity at the benchmarked configuration (BASELINE.json configs[1], C2):
+256^3 grid, 4 views 512x424 (f=365) of the 300-frame kick stream — the exact
+kernels the headline number times (fx/ix at 256 points, the 256-point Z pass
+with its own launch bounds, F-y/I-y at 256) against the CPU oracle
+(restatement of reconstruct.cpp:37-78, integrate.cpp:19-74,
+marching_cubes.cpp:131-210, texture.cpp:11-72).
+
+Tolerances are BASELINE.json's: indicator A within 1e-4 relative L2, MC case
+indices / topology / vertices bit-exact on an identical field, vertices within
+0.5 voxel Hausdorff, texture channels bit-exact, colours within 1/255."""
+import numpy as np
+import pytest
+from scipy.spatial import cKDTree
+
+from paper_1712_03084_b200 import volcap as vc
+
+pytestmark = pytest.mark.gpu
+
+REL_L2_A = 1e-4
+HAUSDORFF_VOX = 0.5
+COLOR_TOL = 1
+FFT_REL = 2e-5       # fp32 FFT chain vs fp64 oracle on unit-variance noise
+STREAM = 300
+DIMS = (256, 256, 256)
+
+
+def rel_l2(a, b):
+    return float(np.linalg.norm(np.asarray(a, np.float64) - b) / max(np.linalg.norm(b), 1e-300))
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    return vc.default_context(0)
+
+
+@pytest.fixture(scope="module")
+def rigs(O):
+    return vc.make_circle_rig(4, 0, 2500, 512, 424, 365), O.make_circle_rig(4, 0, 2500, 1000, 512, 424, 365)
+
+
+# ------------------------------------------------------------ 256-point FFT kernels
+@pytest.mark.parametrize("shape", [(256, 8, 4), (4, 8, 256), (4, 256, 8), (8, 4, 256), (256, 4, 256)])
+def test_integrate_256_point_lines(O, ctx, shape):
+    """shape = (nz, ny, nx): nz=256 instantiates z_kernel<256>, nx=256 the
+    x-R2C/C2R kernels at 256, ny=256 the y passes at 256 (non-Hermitian
+    filtered spectra on the kx=0, nx/2 planes)."""
+    rng = np.random.default_rng(sum(shape) * 7 + 1)
+    field = rng.normal(size=shape + (3,)).astype(np.float32)
+    A = vc.integrate_fft(field, ctx=ctx)
+    assert rel_l2(A, O.integrate_fft(field.astype(np.float64))) < FFT_REL
+
+
+def test_integrate_random_256_cube(O, ctx):
+    """The whole C2 integrate chain (F-x, F-y, Z, I-y, I-x at 256^3) on a random
+    dense field: every plane non-empty, every row non-empty."""
+    rng = np.random.default_rng(256)
+    field = rng.normal(size=DIMS[::-1] + (3,)).astype(np.float32)
+    A = vc.integrate_fft(field, ctx=ctx)
+    ref = O.integrate_fft(field.astype(np.float64))
+    assert rel_l2(A, ref) < FFT_REL
+    assert abs(float(A.astype(np.float64).mean())) < 1e-6  # DC removed (integrate.cpp:48)
+
+
+# ------------------------------------------------------------ whole C2 frames
+def _mc_bit_exact(O, ctx, A, level, grid):
+    nz, ny, nx = A.shape
+    g = vc.GridSpec(nx, ny, nz, np.array(grid.origin), grid.edge_mm)
+    m = vc.marching_cubes(A, g, level, ctx=ctx)
+    o = O.marching_cubes(A.astype(np.float64), O.grid(nx, ny, nz, tuple(grid.origin), grid.edge_mm), level)
+    assert np.array_equal(np.sort(o.edge_ids), m.edge_ids)
+    assert np.array_equal(m.edge_ids[m.triangles], o.edge_ids[o.triangles])
+    order = np.argsort(o.edge_ids)
+    assert np.array_equal(m.vertices, o.vertices[order])
+    assert np.allclose(m.normals, o.normals[order], atol=1e-6)
+
+
+@pytest.mark.parametrize("frame", [0, 150, 299])
+def test_c2_kick_frame_vs_oracle(O, ctx, rigs, frame):
+    rig, orig = rigs
+    body = vc.kick_body(STREAM, frame)
+    frames = [vc.render_frame(rig, body, k, frame, ctx=ctx) for k in range(4)]
+    rec = vc.reconstruct_frame(frames, rig, vc.ReconConfig(dims=DIMS), ctx=ctx, want_volume=True, want_clouds=True)
+    ref = O.reconstruct_frame(orig, [f.depth for f in frames], [f.foreground for f in frames],
+                              [f.color for f in frames], dims=DIMS)
+    assert ref.status == 0
+    # binning: oriented points, weights and the fitted grid bit-exact
+    assert np.array_equal(rec.clouds.position, ref.points["position"])
+    assert np.array_equal(rec.clouds.weight, ref.points["weight"])
+    g = rec.volume.grid
+    assert g.edge_mm == ref.grid.edge and list(g.origin) == list(ref.grid.origin[:])
+    # indicator field and level
+    assert rel_l2(rec.volume.values, ref.volume) < REL_L2_A
+    assert abs(rec.volume.iso_level - ref.iso_level) < 1e-4 * abs(ref.iso_level)
+    # mesh: 0.5-voxel Hausdorff, watertight
+    d1, _ = cKDTree(ref.mesh.vertices).query(rec.mesh.vertices)
+    d2, _ = cKDTree(rec.mesh.vertices).query(ref.mesh.vertices)
+    assert max(d1.max(), d2.max()) <= HAUSDORFF_VOX * ref.grid.edge
+    assert O.analyze_topology(rec.mesh.triangles, len(rec.mesh.vertices))["edge_manifold"]
+    # MC case indices + table topology + vertices bit-exact on the identical fp32 field
+    _mc_bit_exact(O, ctx, rec.volume.values, rec.volume.iso_level, g)
+    # texture channels bit-exact on identical vertices, colours within 1/255
+    tm = vc.texture(ref.mesh.vertices, rig, frames, ref.weight_maps, ctx=ctx)
+    assert np.array_equal(tm.visible, ref.vis)
+    assert np.array_equal(tm.weight, ref.weight)
+    assert np.array_equal(tm.untextured, ref.untextured)
+    assert np.array_equal(tm.uv, ref.uv.astype(np.float32))
+    assert np.max(np.abs(tm.rgb.astype(int) - ref.rgb8.astype(int))) <= COLOR_TOL

@@ -380,11 +380,7 @@ def test_repeatability_and_graph_replay(scene, ctx):
 def hd_rig(vc, k=6):
     """C3: K=6 Kinect2 depth 512x424 (f=365) + 1920x1080 colour (f~1060,
     cx=959.5, cy=539.5) offset by 52 mm along x."""
-    rig = vc.make_circle_rig(k, 0, 2500, 512, 424, 365)
-    for s in rig.sensors:
-        s.rgb_intr = vc.Intrinsics(1060.0, 1060.0, 959.5, 539.5, 1920, 1080)
-        s.rgb_relative = vc.Pose(np.eye(3), np.array([52.0, 0.0, 0.0]))
-    return rig
+    return vc.make_hd_rig(k)
 
 
 def to_oracle_rig(O, rig):
