@@ -9,10 +9,14 @@
 //   auto out = vc::adapter::reconstruct_frame(frames, rig, config);   // drop-in for
 //   // recon::reconstruct_frame + appearance::vertex_visibility + assign_texture
 //
-// Needs Eigen (the reference's headers); it is not compiled in this repo's
-// build (Eigen is absent here) — see INTEGRATION.md.
+// Needs the reference's headers (and so Eigen).  In this repo it is compiled
+// against the reference's own headers + the Eigen-API shim of oracle/ref_shim
+// by `make -C oracle ref` (oracle/adapter_check.cpp, run by
+// tests/test_gpu_c2_parity.py on the B200) — see INTEGRATION.md.
 #pragma once
 
+#include <algorithm>
+#include <span>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -45,7 +49,7 @@ inline void check(vc_status s, vc_ctx* ctx) {
 }
 
 struct Result {
-  volcap::recon::FrameReconstruction recon;  // clouds left empty; volume + mesh filled
+  volcap::recon::FrameReconstruction recon;  // clouds (want_clouds), volume (want_volume) + mesh
   volcap::appearance::TexturedMesh textured;
   std::vector<volcap::Rgb8> vertex_colors;
 };
@@ -54,7 +58,8 @@ struct Result {
 // assign_texture (texture.hpp:32-42) in one call on the GPU.
 inline Result reconstruct_frame(std::span<const volcap::RgbdFrame> frames, const volcap::CameraRig& rig,
                                 const volcap::recon::ReconConfig& config, vc_ctx* ctx,
-                                volcap::recon::StageTimings* timings = nullptr, bool want_volume = true) {
+                                volcap::recon::StageTimings* timings = nullptr, bool want_volume = true,
+                                bool want_clouds = true) {
   if (frames.size() != static_cast<std::size_t>(rig.recon_count))
     throw std::invalid_argument("reconstruct_frame: one frame per reconstruction sensor required");
   const int k = rig.recon_count;
@@ -98,6 +103,32 @@ inline Result reconstruct_frame(std::span<const volcap::RgbdFrame> frames, const
     std::vector<float> a(out.recon.volume.values.size());
     check(vc_export_volume(ctx, a.data(), VC_MEM_HOST), ctx);
     for (std::size_t i = 0; i < a.size(); ++i) out.recon.volume.values.data()[i] = a[i];
+  }
+  if (want_clouds) {  // OrientedCloud per sensor (cloud.hpp:13-26), concatenated in sensor order on the device
+    const std::size_t P = static_cast<std::size_t>(m.point_count);
+    std::vector<double> pos(3 * P), nrm(3 * P), w(P);
+    std::vector<int32_t> pix(3 * P);
+    std::size_t wm_total = 0;
+    for (int i = 0; i < k; ++i) wm_total += static_cast<std::size_t>(frames[i].depth.width()) * frames[i].depth.height();
+    std::vector<float> wm(wm_total);
+    check(vc_export_points(ctx, pos.data(), nrm.data(), w.data(), pix.data(), wm.data()), ctx);
+    out.recon.clouds.resize(k);
+    std::size_t wo = 0;
+    for (int i = 0; i < k; ++i) {
+      auto& c = out.recon.clouds[i];
+      c.sensor = i;
+      c.weight_map = volcap::Image<float>(frames[i].depth.width(), frames[i].depth.height(), 0.f);
+      std::copy(wm.begin() + wo, wm.begin() + wo + c.weight_map.size(), c.weight_map.data().begin());
+      wo += c.weight_map.size();
+    }
+    for (std::size_t p = 0; p < P; ++p) {
+      volcap::recon::OrientedPoint op;
+      op.position = volcap::Vec3(pos[3 * p], pos[3 * p + 1], pos[3 * p + 2]);
+      op.normal = volcap::Vec3(nrm[3 * p], nrm[3 * p + 1], nrm[3 * p + 2]);
+      op.weight = w[p];
+      op.px = pix[3 * p], op.py = pix[3 * p + 1], op.sensor = pix[3 * p + 2];
+      out.recon.clouds.at(op.sensor).points.push_back(op);
+    }
   }
   auto& tm = out.textured;
   tm.mesh = mesh;

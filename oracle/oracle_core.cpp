@@ -388,7 +388,8 @@ void fft_yz(cd* S, int nh, int ny, int nz, bool inverse) {
 }  // namespace
 
 // numpy.fft.rfftn over axes (z,y,x) of real[nz][ny][nx] -> [nz][ny][nx/2+1]
-static void rfft3(const double* in, cd* S, int nx, int ny, int nz) {
+// (also the transform behind oracle/ref_shim/fftw3.h's fftw_plan_dft_r2c_3d)
+void rfft3(const double* in, cd* S, int nx, int ny, int nz) {
   const int nh = nx / 2 + 1;
   const Plan1D px = make_plan(nx);
   std::vector<cd> row(nx), scratch;
@@ -401,7 +402,8 @@ static void rfft3(const double* in, cd* S, int nx, int ny, int nz) {
 }
 
 // numpy.fft.irfftn (unnormalised, like FFTW c2r): destroys S.
-static void irfft3(cd* S, double* out, int nx, int ny, int nz) {
+// (also the transform behind oracle/ref_shim/fftw3.h's fftw_plan_dft_c2r_3d)
+void irfft3(cd* S, double* out, int nx, int ny, int nz) {
   const int nh = nx / 2 + 1;
   fft_yz(S, nh, ny, nz, true);
   const Plan1D px = make_plan(nx);

@@ -106,3 +106,60 @@ def test_c2_kick_frame_vs_oracle(O, ctx, rigs, frame):
     assert np.array_equal(tm.untextured, ref.untextured)
     assert np.array_equal(tm.uv, ref.uv.astype(np.float32))
     assert np.max(np.abs(tm.rgb.astype(int) - ref.rgb8.astype(int))) <= COLOR_TOL
+
+
+# ------------------------------------------------------------ against the reference's own code
+def _ref():
+    from oracle import ref as R
+    return R if R.available(0) else None
+
+
+@pytest.mark.skipif(_ref() is None, reason="reference not built (make -C oracle ref)")
+def test_c2_frame_vs_reference_code(O, ctx, rigs):
+    """GPU vs the reference's own sources (oracle/_ref, compiled unmodified
+    against oracle/ref_shim) on a 256^3 kick frame, no oracle in between."""
+    R = _ref()
+    rig, orig = rigs
+    frame = 299
+    body = vc.kick_body(STREAM, frame)
+    frames = [vc.render_frame(rig, body, k, frame, ctx=ctx) for k in range(4)]
+    ref = R.reconstruct_frame(orig, [f.depth for f in frames], [f.foreground for f in frames],
+                              [f.color for f in frames], dims=DIMS)
+    assert ref.status == 0
+    rec = vc.reconstruct_frame(frames, rig, vc.ReconConfig(dims=DIMS), ctx=ctx, want_volume=True, want_clouds=True)
+    for key, got in (("position", rec.clouds.position), ("normal", rec.clouds.normal), ("weight", rec.clouds.weight)):
+        assert np.array_equal(got, ref.points[key]), key
+    assert rec.volume.grid.edge_mm == ref.grid.edge and list(rec.volume.grid.origin) == list(ref.grid.origin[:])
+    assert rel_l2(rec.volume.values, ref.volume) < REL_L2_A
+    d1, _ = cKDTree(ref.mesh.vertices).query(rec.mesh.vertices)
+    d2, _ = cKDTree(rec.mesh.vertices).query(ref.mesh.vertices)
+    assert max(d1.max(), d2.max()) <= HAUSDORFF_VOX * ref.grid.edge
+    # MC on the identical fp32 field: the reference's first-touch mesh = ours re-indexed
+    A = rec.volume.values
+    g = rec.volume.grid
+    v, n, t = R.marching_cubes(A.astype(np.float64), O.grid(g.nx, g.ny, g.nz, tuple(g.origin), g.edge_mm),
+                               rec.volume.iso_level)
+    m = vc.marching_cubes(A, g, rec.volume.iso_level, ctx=ctx)
+    o = O.marching_cubes(A.astype(np.float64), O.grid(g.nx, g.ny, g.nz, tuple(g.origin), g.edge_mm),
+                         rec.volume.iso_level)
+    assert np.array_equal(v, o.vertices) and np.array_equal(t, o.triangles)  # reference == oracle (first touch)
+    order = np.argsort(o.edge_ids)                                            # first touch -> edge-id order
+    assert np.array_equal(m.vertices, v[order])
+    inv = np.empty_like(order)
+    inv[order] = np.arange(len(order))
+    assert np.array_equal(m.triangles, inv[t])  # our triangles = the reference's, vertex ids re-indexed
+
+
+@pytest.mark.skipif(_ref() is None, reason="reference not built (make -C oracle ref)")
+@pytest.mark.parametrize("r,frame", [(6, 0), (7, 150)])
+def test_adapter_drop_in_from_reference_caller(r, frame):
+    """include/vc/volcap_adapter.hpp compiled against the reference's headers,
+    called like recon::reconstruct_frame (oracle/adapter_check.cpp)."""
+    import os
+    import subprocess
+    exe = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "oracle", "_ref", "o0",
+                       "adapter_check")
+    if not os.path.exists(exe):
+        pytest.skip("adapter_check not built")
+    out = subprocess.run([exe, str(r), str(frame)], capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0 and "ADAPTER OK" in out.stdout, out.stdout + out.stderr
