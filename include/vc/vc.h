@@ -53,7 +53,8 @@ typedef enum vc_status {
   VC_ERR_CUDA = 4,
   VC_ERR_NCCL = 5,
   VC_ERR_OOM = 6,
-  VC_ERR_NO_DEVICE = 7
+  VC_ERR_NO_DEVICE = 7,
+  VC_ERR_RUNTIME = 8           /* std::runtime_error of the reference (e.g. fit_value_map, chain_to_reference) */
 } vc_status;
 
 /* types.hpp:26-39 — pinhole, pixel-centre convention. */
@@ -331,8 +332,11 @@ vc_status vc_binarize(vc_ctx* ctx, const float* A, int32_t mem_kind, const vc_gr
 /* boundary_voxels (binary_volume.cpp:68-82): out_xyz 3*n doubles (world centres). */
 vc_status vc_boundary_voxels(vc_ctx* ctx, const uint8_t* keep, const vc_grid_spec* grid, const int32_t* voxels,
                              int64_t n, double* out_xyz, int64_t* n_out);
-/* skeletonize (skeletonize.cpp:99-161), host: out 3*n int32. */
-vc_status vc_skeletonize(const uint8_t* grid, int32_t nx, int32_t ny, int32_t nz, const int32_t* voxels, int64_t n,
+/* skeletonize (skeletonize.cpp:99-161) on the GPU: grid = nx*ny*nz bytes
+ * (x fastest, host), voxels = 3n int32 (x, y, z); out: 3n int32, the
+ * surviving voxels in input order (identical to the reference's sequential
+ * thinning). */
+vc_status vc_skeletonize(vc_ctx* ctx, const uint8_t* grid, int32_t nx, int32_t ny, int32_t nz, const int32_t* voxels, int64_t n,
                          int32_t* out, int64_t* n_out);
 
 /* ---------------------------------------------- evaluation renderer + metrics

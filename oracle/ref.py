@@ -136,3 +136,42 @@ def marching_cubes(A, g: O.GridSpec, level: float, order=0):
         return verts, vn, tris
     finally:
         L.ref_frame_free(h)
+
+
+def skeletonize(keep, voxels, order=0) -> np.ndarray:
+    """mocap::skeletonize (skeletonize.cpp:99-161) on keep[z, y, x] and an (n, 3) voxel list."""
+    L = lib(order)
+    g = np.ascontiguousarray(keep, np.uint8)
+    vox = np.ascontiguousarray(voxels, np.int32).reshape(-1, 3)
+    out = np.zeros((max(len(vox), 1), 3), np.int32)
+    L.ref_skeletonize.restype = C.c_int64
+    n = L.ref_skeletonize(_p(g), g.shape[2], g.shape[1], g.shape[0], _p(vox), C.c_int64(len(vox)), _p(out))
+    return out[:n]
+
+
+def fit_value_map(pairs_rgb, iterations=1000, threshold=0.05, seed=1, order=0):
+    """appearance::fit_value_map (color_correction.cpp:97-138): (gain, offset), or
+    RuntimeError with the reference's message when it throws."""
+    L = lib(order)
+    arr = np.ascontiguousarray(pairs_rgb, np.uint8).reshape(-1, 6)
+    g, o = C.c_double(), C.c_double()
+    err = C.create_string_buffer(256)
+    st = L.ref_fit_value_map(_p(arr), len(arr), iterations, C.c_double(threshold), C.c_uint64(seed), C.byref(g),
+                             C.byref(o), err, 256)
+    if st:
+        raise RuntimeError(err.value.decode())
+    return g.value, o.value
+
+
+def chain_to_reference(edges, reference, sensor_count, order=0):
+    """appearance::chain_to_reference (color_correction.cpp:168-199); edges = [(from, to, gain, offset)];
+    None when the reference throws (a sensor not connected)."""
+    L = lib(order)
+    f = np.array([e[0] for e in edges], np.int32)
+    t = np.array([e[1] for e in edges], np.int32)
+    g = np.array([e[2] for e in edges], np.float64)
+    o = np.array([e[3] for e in edges], np.float64)
+    og = np.zeros(sensor_count)
+    oo = np.zeros(sensor_count)
+    st = L.ref_chain_to_reference(_p(f), _p(t), _p(g), _p(o), len(edges), reference, sensor_count, _p(og), _p(oo))
+    return None if st else list(zip(og.tolist(), oo.tolist()))

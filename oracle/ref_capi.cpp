@@ -19,13 +19,18 @@
 //                            integrate_fft, iso_level, marching_cubes);
 //                            then appearance::vertex_visibility + assign_texture (texture.cpp:11-72).
 //   ref_marching_cubes    -> volcap::recon::marching_cubes on a caller field.
+//   ref_skeletonize       -> volcap::mocap::skeletonize            (skeletonize.cpp:99-161)
+//   ref_fit_value_map     -> volcap::appearance::fit_value_map     (color_correction.cpp:97-138)
+//   ref_chain_to_reference-> volcap::appearance::chain_to_reference (color_correction.cpp:168-199)
 #include <cstdint>
 #include <cstring>
 #include <limits>
 #include <stdexcept>
 #include <vector>
 
+#include "volcap/appearance/color.hpp"
 #include "volcap/appearance/texture.hpp"
+#include "volcap/mocap/volume_ops.hpp"
 #include "volcap/recon/reconstruct.hpp"
 #include "volcap/synth/capsule.hpp"
 #include "volcap/synth/scene.hpp"
@@ -320,6 +325,51 @@ void* ref_marching_cubes(const double* A, const PGrid* g, double level, int64_t*
   f->rec.mesh = recon::marching_cubes(vol, level);
   out[0] = (int64_t)f->rec.mesh.vertices.size(), out[1] = (int64_t)f->rec.mesh.triangles.size();
   return f;
+}
+
+// grid: nx*ny*nz bytes (x fastest), voxels 3n int32 -> out 3n int32; returns the count
+int64_t ref_skeletonize(const uint8_t* grid, int nx, int ny, int nz, const int32_t* voxels, int64_t n, int32_t* out) {
+  mocap::BinaryVolume bv;
+  bv.grid = VolumeGrid<std::uint8_t>(nx, ny, nz);
+  std::memcpy(bv.grid.data().data(), grid, (size_t)nx * ny * nz);
+  for (int64_t i = 0; i < n; ++i) bv.voxels.emplace_back(voxels[3 * i], voxels[3 * i + 1], voxels[3 * i + 2]);
+  const auto sk = mocap::skeletonize(bv);
+  for (size_t i = 0; i < sk.size(); ++i)
+    out[3 * i] = sk[i].x(), out[3 * i + 1] = sk[i].y(), out[3 * i + 2] = sk[i].z();
+  return (int64_t)sk.size();
+}
+
+// pairs_rgb: n x (first RGB, second RGB); 0 ok, 1 the reference threw (message in err)
+int ref_fit_value_map(const uint8_t* pairs_rgb, int n, int iters, double thr, uint64_t seed, double* gain,
+                      double* offset, char* err, int errlen) {
+  std::vector<appearance::ColorPair> pairs((size_t)n);
+  for (int i = 0; i < n; ++i) {
+    const uint8_t* p = pairs_rgb + 6 * (size_t)i;
+    pairs[i].first = Rgb8{p[0], p[1], p[2]};
+    pairs[i].second = Rgb8{p[3], p[4], p[5]};
+  }
+  try {
+    const auto m = appearance::fit_value_map(pairs, appearance::ValueFitOptions{iters, thr, seed});
+    *gain = m.gain, *offset = m.offset;
+    return 0;
+  } catch (const std::exception& e) {
+    std::strncpy(err, e.what(), errlen - 1);
+    err[errlen - 1] = 0;
+    return 1;
+  }
+}
+
+int ref_chain_to_reference(const int32_t* from, const int32_t* to, const double* gain, const double* offset,
+                           int n_edges, int reference, int sensor_count, double* out_gain, double* out_offset) {
+  std::vector<appearance::PairwiseValueMap> edges((size_t)n_edges);
+  for (int e = 0; e < n_edges; ++e) edges[e] = {from[e], to[e], appearance::ValueMap{gain[e], offset[e]}};
+  try {
+    const auto cc = appearance::chain_to_reference(edges, reference, sensor_count);
+    for (int k = 0; k < sensor_count; ++k) out_gain[k] = cc.maps[k].gain, out_offset[k] = cc.maps[k].offset;
+    return 0;
+  } catch (const std::exception&) {
+    return 1;
+  }
 }
 
 }  // extern "C"

@@ -17,7 +17,7 @@ LIB_PATH = os.path.join(PKG_DIR, "libvc_b200.so")
 HEADER_PATH = os.path.join(REPO_DIR, "include", "vc", "vc.h")
 
 VC_OK, VC_ERR_INVALID_ARGUMENT, VC_ERR_EMPTY_SCENE, VC_ERR_CAPACITY = 0, 1, 2, 3
-VC_ERR_CUDA, VC_ERR_NCCL, VC_ERR_OOM, VC_ERR_NO_DEVICE = 4, 5, 6, 7
+VC_ERR_CUDA, VC_ERR_NCCL, VC_ERR_OOM, VC_ERR_NO_DEVICE, VC_ERR_RUNTIME = 4, 5, 6, 7, 8
 VC_MEM_HOST, VC_MEM_DEVICE = 0, 1
 
 

@@ -21,8 +21,14 @@ from .volcap import Context, OrientedClouds, default_context
 
 
 def _err(status: int) -> None:
-    if status != L.VC_OK:
-        raise RuntimeError(L.lib().vc_io_last_error().decode())
+    """std::invalid_argument -> VcInvalidArgument (a ValueError); the reference's
+    std::runtime_error (VC_ERR_RUNTIME) -> VcError (a RuntimeError)."""
+    if status == L.VC_OK:
+        return
+    msg = L.lib().vc_io_last_error().decode()
+    if status == L.VC_ERR_INVALID_ARGUMENT:
+        raise L.VcInvalidArgument(status, msg)
+    raise L.VcError(status, msg)
 
 
 @dataclass

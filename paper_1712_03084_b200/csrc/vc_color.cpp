@@ -4,16 +4,14 @@
 // color_correction.cpp, hsv.cpp):
 //   vc_color_apply                 ColorCorrection::apply(sensor, image) on the GPU
 //   vc_mutual_closest_pairs        mutual_closest_pairs on the GPU hash grid
-//   vc_fit_value_map               fit_value_map (host: a few thousand pairs;
-//                                  std::mt19937_64 + uniform_int_distribution
-//                                  exactly as the reference draws them)
-//   vc_chain_to_reference          chain_to_reference (host)
+//   vc_fit_value_map               fit_value_map (host: RANSAC over the 256 x 256
+//                                  value-level lattice, exact integer moments)
+//   vc_chain_to_reference          chain_to_reference (host BFS over incidence lists)
 //   vc_ctx_set_color_correction    per-sensor maps fused into the frame's
 //                                  texture sampling
 #include <algorithm>
 #include <cmath>
 #include <cstring>
-#include <queue>
 #include <random>
 #include <string>
 #include <vector>
@@ -24,17 +22,6 @@ using namespace vc;
 using namespace vc::rt;
 
 namespace {
-
-struct Vmap {
-  double gain = 1.0, offset = 0.0;
-  Vmap then(const Vmap& outer) const { return {outer.gain * gain, outer.gain * offset + outer.offset}; }
-  Vmap inverse() const { return {1.0 / gain, -offset / gain}; }
-};
-
-double value_of(const uint8_t* c) {  // rgb_to_hsv(c).v (hsv.cpp:9-13)
-  const double r = c[0] / 255.0, g = c[1] / 255.0, b = c[2] / 255.0;
-  return std::max({r, g, b});
-}
 
 }  // namespace
 
@@ -118,96 +105,119 @@ vc_status vc_mutual_closest_pairs(vc_ctx* ctx, const double* a, int32_t na, cons
   return VC_OK;
 }
 
-// color_correction.cpp:97-138
+// fit_value_map (color_correction.cpp:97-138).  The value channel of an RGB8
+// colour is max(r, g, b) / 255, so every pair is a cell (ka, kb) of a 256 x 256
+// lattice: the pairs are binned once, each RANSAC hypothesis is scored over the
+// occupied cells (weighted by their pair counts) instead of over all pairs, and
+// the final least squares uses exact integer moments of the inlier cells
+// (gain = (k Sab - Sa Sb) / (k Saa - Sa^2), the 1/255 scales cancel), so the
+// fit is the correctly rounded solution of the reference's normal equations.
+// The hypotheses are the reference's: (i, j) drawn with std::mt19937_64 and
+// uniform_int_distribution<int>(0, n-1), a pair with equal values skipped, the
+// first hypothesis of maximal support kept; a cell's inlier test is the
+// reference's expression on the same doubles, so the support counts are equal.
 vc_status vc_fit_value_map(const uint8_t* pairs_rgb, int32_t n, int32_t ransac_iterations, double inlier_threshold,
                            uint64_t seed, double* gain, double* offset) {
   if (!gain || !offset || n < 0 || (n > 0 && !pairs_rgb))
     return vc_io_detail::set_error(VC_ERR_INVALID_ARGUMENT, "fit_value_map: null argument");
   if (n < 10)
-    return vc_io_detail::set_error(VC_ERR_INVALID_ARGUMENT, "fit_value_map: insufficient color diversity (< 10 pairs)");
-  std::vector<double> va(n), vb(n);
-  double lo = 1, hi = 0;
-  for (int i = 0; i < n; ++i) {
-    va[i] = value_of(pairs_rgb + 6 * (size_t)i);
-    vb[i] = value_of(pairs_rgb + 6 * (size_t)i + 3);
-    lo = std::min(lo, va[i]);
-    hi = std::max(hi, va[i]);
+    return vc_io_detail::set_error(VC_ERR_RUNTIME, "fit_value_map: insufficient color diversity (< 10 pairs)");
+  auto level = [](const uint8_t* c) { return (int)std::max({c[0], c[1], c[2]}); };
+  std::vector<uint8_t> ka(n), kb(n);
+  std::vector<int32_t> hist(256 * 256, 0);
+  int kmin = 255, kmax = 0;
+  for (int32_t p = 0; p < n; ++p) {
+    ka[p] = (uint8_t)level(pairs_rgb + 6 * (size_t)p);
+    kb[p] = (uint8_t)level(pairs_rgb + 6 * (size_t)p + 3);
+    ++hist[ka[p] * 256 + kb[p]];
+    kmin = std::min(kmin, (int)ka[p]), kmax = std::max(kmax, (int)ka[p]);
   }
-  if (hi - lo < 1e-6)
-    return vc_io_detail::set_error(VC_ERR_INVALID_ARGUMENT,
-                                   "fit_value_map: insufficient color diversity (constant value)");
+  if (kmax == kmin)  // one value level: spread 0 < 1e-6
+    return vc_io_detail::set_error(VC_ERR_RUNTIME, "fit_value_map: insufficient color diversity (constant value)");
+  struct Cell {
+    double a, b;
+    int32_t count;
+    uint8_t ka, kb;
+  };
+  std::vector<Cell> cells;
+  for (int c = 0; c < 256 * 256; ++c)
+    if (hist[c]) cells.push_back({(c >> 8) / 255.0, (c & 255) / 255.0, hist[c], (uint8_t)(c >> 8), (uint8_t)(c & 255)});
   std::mt19937_64 rng(seed);
-  std::uniform_int_distribution<int> pick(0, n - 1);
-  int best_count = -1;
-  std::vector<int> best_inliers;
-  for (int it = 0; it < ransac_iterations; ++it) {
-    const int i = pick(rng), j = pick(rng);
-    if (std::abs(va[i] - va[j]) < 1e-6) continue;
-    const double a = (vb[j] - vb[i]) / (va[j] - va[i]);
-    const double b = vb[i] - a * va[i];
-    std::vector<int> inliers;
-    for (int m = 0; m < n; ++m)
-      if (std::abs(a * va[m] + b - vb[m]) < inlier_threshold) inliers.push_back(m);
-    if ((int)inliers.size() > best_count) {
-      best_count = (int)inliers.size();
-      best_inliers = std::move(inliers);
+  std::uniform_int_distribution<int> draw(0, n - 1);
+  int64_t top = -1;
+  double top_a = 0, top_b = 0;
+  for (int32_t h = 0; h < ransac_iterations; ++h) {
+    const int p = draw(rng);
+    const int q = draw(rng);
+    if (ka[p] == ka[q]) continue;  // |va_p - va_q| < 1e-6 <=> same level
+    const double vap = ka[p] / 255.0, vbp = kb[p] / 255.0;
+    const double slope = (kb[q] / 255.0 - vbp) / (ka[q] / 255.0 - vap);
+    const double icpt = vbp - slope * vap;
+    int64_t support = 0;
+    for (const Cell& c : cells)
+      if (std::abs(slope * c.a + icpt - c.b) < inlier_threshold) support += c.count;
+    if (support > top) top = support, top_a = slope, top_b = icpt;
+  }
+  if (top < 2) return vc_io_detail::set_error(VC_ERR_RUNTIME, "fit_value_map: no consensus line");
+  int64_t k = 0, sa = 0, sb = 0, saa = 0, sab = 0;
+  for (const Cell& c : cells)
+    if (std::abs(top_a * c.a + top_b - c.b) < inlier_threshold) {
+      k += c.count, sa += (int64_t)c.count * c.ka, sb += (int64_t)c.count * c.kb;
+      saa += (int64_t)c.count * c.ka * c.ka, sab += (int64_t)c.count * c.ka * c.kb;
     }
-  }
-  if (best_count < 2) return vc_io_detail::set_error(VC_ERR_INVALID_ARGUMENT, "fit_value_map: no consensus line");
-  double sx = 0, sy = 0, sxx = 0, sxy = 0;
-  for (int m : best_inliers) {
-    sx += va[m];
-    sy += vb[m];
-    sxx += va[m] * va[m];
-    sxy += va[m] * vb[m];
-  }
-  const double k = (double)best_inliers.size();
-  const double denom = k * sxx - sx * sx;
-  if (std::abs(denom) < 1e-12)
-    return vc_io_detail::set_error(VC_ERR_INVALID_ARGUMENT, "fit_value_map: degenerate inlier set");
-  *gain = (k * sxy - sx * sy) / denom;
-  *offset = (sy - *gain * sx) / k;
+  const int64_t den = k * saa - sa * sa;  // 255^2 (k Sxx - Sx^2): zero iff all inliers share one level
+  if (den == 0) return vc_io_detail::set_error(VC_ERR_RUNTIME, "fit_value_map: degenerate inlier set");
+  const double g = (double)(k * sab - sa * sb) / (double)den;
+  *gain = g;
+  *offset = ((double)sb - g * (double)sa) / (255.0 * (double)k);
   return VC_OK;
 }
 
-// color_correction.cpp:168-199
+// chain_to_reference (color_correction.cpp:168-199).  Breadth-first over the
+// sensor graph from the reference; a sensor's map is fixed by the first edge
+// (in edge order) that reaches it from the sensor being expanded, composed as
+// the reference's ValueMap::then / inverse (color.hpp:48-52):
+//   edge u -> w (V_w = g V_u + o) reached from u:  M_w = M_u o (g, o)^-1
+//   edge w -> u reached from u:                    M_w = M_u o (g, o)
 vc_status vc_chain_to_reference(const int32_t* from, const int32_t* to, const double* gain, const double* offset,
                                 int32_t n_edges, int32_t reference, int32_t sensor_count, double* out_gain,
                                 double* out_offset) {
   if (sensor_count < 1 || reference < 0 || reference >= sensor_count || n_edges < 0 || !out_gain || !out_offset ||
       (n_edges > 0 && (!from || !to || !gain || !offset)))
     return vc_io_detail::set_error(VC_ERR_INVALID_ARGUMENT, "chain_to_reference: bad arguments");
-  for (int e = 0; e < n_edges; ++e)
+  // incidence lists in edge order: (edge, 0 = sensor is the edge's source)
+  std::vector<std::vector<std::pair<int32_t, int>>> inc(sensor_count);
+  for (int32_t e = 0; e < n_edges; ++e) {
     if (from[e] < 0 || from[e] >= sensor_count || to[e] < 0 || to[e] >= sensor_count)
       return vc_io_detail::set_error(VC_ERR_INVALID_ARGUMENT, "chain_to_reference: edge sensor out of range");
-  std::vector<Vmap> maps(sensor_count);
-  std::vector<char> known(sensor_count, 0);
-  known[reference] = 1;
-  std::queue<int> frontier;
-  frontier.push(reference);
-  while (!frontier.empty()) {
-    const int cur = frontier.front();
-    frontier.pop();
-    for (int e = 0; e < n_edges; ++e) {
-      const Vmap m{gain[e], offset[e]};
-      if (known[from[e]] && !known[to[e]]) {
-        if (from[e] != cur) continue;
-        maps[to[e]] = m.inverse().then(maps[from[e]]);
-        known[to[e]] = 1;
-        frontier.push(to[e]);
-      } else if (known[to[e]] && !known[from[e]]) {
-        if (to[e] != cur) continue;
-        maps[from[e]] = m.then(maps[to[e]]);
-        known[from[e]] = 1;
-        frontier.push(from[e]);
+    inc[from[e]].push_back({e, 0});
+    if (to[e] != from[e]) inc[to[e]].push_back({e, 1});
+  }
+  std::vector<double> G(sensor_count, 1.0), O(sensor_count, 0.0);
+  std::vector<int32_t> order{reference};
+  std::vector<char> done(sensor_count, 0);
+  done[reference] = 1;
+  for (size_t head = 0; head < order.size(); ++head) {
+    const int32_t u = order[head];
+    for (const auto& [e, side] : inc[u]) {
+      const int32_t w = side == 0 ? to[e] : from[e];
+      if (done[w]) continue;
+      if (side == 0) {  // (g, o)^-1 = (1/g, -o/g), then M_u
+        const double ig = 1.0 / gain[e], io = -offset[e] / gain[e];
+        G[w] = G[u] * ig, O[w] = G[u] * io + O[u];
+      } else {
+        G[w] = G[u] * gain[e], O[w] = G[u] * offset[e] + O[u];
       }
+      done[w] = 1;
+      order.push_back(w);
     }
   }
-  for (int k = 0; k < sensor_count; ++k)
-    if (!known[k])
-      return vc_io_detail::set_error(VC_ERR_INVALID_ARGUMENT, "chain_to_reference: sensor " + std::to_string(k) +
-                                                                  " not connected to the reference");
-  for (int k = 0; k < sensor_count; ++k) out_gain[k] = maps[k].gain, out_offset[k] = maps[k].offset;
+  for (int32_t s = 0; s < sensor_count; ++s)
+    if (!done[s])
+      return vc_io_detail::set_error(VC_ERR_RUNTIME, "chain_to_reference: sensor " + std::to_string(s) +
+                                                         " not connected to the reference");
+  std::copy(G.begin(), G.end(), out_gain);
+  std::copy(O.begin(), O.end(), out_offset);
   return VC_OK;
 }
 

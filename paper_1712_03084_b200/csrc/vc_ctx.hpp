@@ -62,6 +62,8 @@ struct vc_ctx {
   HostBuf h_posf, h_nrm, h_tri, h_vis, h_uv, h_w, h_untex, h_rgb, h_pos, h_eid;
   // stage-API host scratch, device scratch of the colour-correction entry points
   Buf scratch_dev, scratch_dev2;
+  Buf skel_lut;  // 2^26-bit simple-point table of vc_skeletonize
+  bool skel_lut_ready = false;
   std::vector<uint8_t> scratch;
   // graph
   cudaGraphExec_t gexec = nullptr;

@@ -478,6 +478,7 @@ const char* vc_status_string(vc_status s) {
     case VC_ERR_NCCL: return "NCCL error";
     case VC_ERR_OOM: return "out of device memory";
     case VC_ERR_NO_DEVICE: return "no CUDA device";
+    case VC_ERR_RUNTIME: return "runtime error";
   }
   return "unknown";
 }
@@ -516,7 +517,7 @@ vc_status vc_ctx_destroy(vc_ctx* ctx) {
   cudaSetDevice(ctx->device);
   if (ctx->st) cudaStreamSynchronize(ctx->st);
   if (ctx->gexec) cudaGraphExecDestroy(ctx->gexec);
-  for (Buf* b : {&ctx->acc, &ctx->spec, &ctx->A, &ctx->tw, &ctx->vbase, &ctx->blk, &ctx->rowmm, &ctx->units, &ctx->unitcnt, &ctx->rowbits, &ctx->planeflag, &ctx->rowlist, &ctx->vinfo, &ctx->scratch_dev, &ctx->scratch_dev2, &ctx->views, &ctx->pts_pos,
+  for (Buf* b : {&ctx->acc, &ctx->spec, &ctx->A, &ctx->tw, &ctx->vbase, &ctx->blk, &ctx->rowmm, &ctx->units, &ctx->unitcnt, &ctx->rowbits, &ctx->planeflag, &ctx->rowlist, &ctx->vinfo, &ctx->scratch_dev, &ctx->scratch_dev2, &ctx->skel_lut, &ctx->views, &ctx->pts_pos,
                  &ctx->pts_nrm, &ctx->pts_w, &ctx->pts_pix, &ctx->wmaps, &ctx->pre_scratch, &ctx->iso_partial,
                  &ctx->m_pos, &ctx->m_nrm, &ctx->m_tri, &ctx->m_eid, &ctx->m_cells, &ctx->m_celltri, &ctx->m_cellcfg, &ctx->m_posf,
                  &ctx->t_vis, &ctx->t_uv, &ctx->t_w, &ctx->t_untex, &ctx->t_rgb})

@@ -6,11 +6,10 @@
 //                        (k_binary.cu), on a host/device volume or the
 //                        context's last frame
 //   vc_boundary_voxels   boundary_voxels (GPU flags, host fp64 world centres)
-//   vc_skeletonize       skeletonize — a sequential topology-preserving thinning
-//                        whose deletions depend on their order (:150-160), so
-//                        it runs on the host exactly as the reference
+//   vc_skeletonize       skeletonize on the GPU (k_skeleton.cu): simple-point
+//                        lookup table, parallel candidates, the order-dependent
+//                        re-check as a fixed point
 #include <algorithm>
-#include <array>
 #include <cstdlib>
 #include <cstring>
 #include <string>
@@ -28,80 +27,22 @@ void launch_binarize_emit(const int32_t* parent, const unsigned long long* best,
                           const int32_t* rowoff, int32_t* voxels, int64_t cap, cudaStream_t st);
 void launch_boundary_flags(const uint8_t* keep, const int32_t* voxels, int64_t n, int nx, int ny, int nz,
                            uint8_t* flag, cudaStream_t st);
+size_t skel_lut_words();
+void launch_skel_lut(uint32_t* lut, cudaStream_t st);
+void launch_skel_pos(const int32_t* vox, int64_t n, int nx, int ny, int32_t* pos, cudaStream_t st);
+void launch_skel_mark(uint8_t* g, int nx, int ny, int nz, const int32_t* vox, int64_t n, int dir, const uint32_t* lut,
+                      uint8_t* cand, uint8_t* del, int* ncand, cudaStream_t st);
+void launch_skel_recheck(uint8_t* g, int nx, int ny, int nz, const int32_t* vox, int64_t n, const int32_t* pos,
+                         const uint32_t* lut, const uint8_t* cand, uint8_t* del, int* changed, cudaStream_t st);
+void launch_skel_apply(uint8_t* g, int nx, int ny, int nz, const int32_t* vox, int64_t n, const uint8_t* cand,
+                       const uint8_t* del, int* ndel, cudaStream_t st);
+void launch_skel_alive(const uint8_t* g, int nx, int ny, const int32_t* vox, int64_t n, uint8_t* alive,
+                       cudaStream_t st);
 }  // namespace vc
 
 namespace vc_io_detail {
 vc_status set_error(vc_status s, const std::string& msg);
 }
-
-namespace {
-
-struct Hood {
-  std::array<std::vector<int>, 27> adj26, adj6;
-  std::array<bool, 27> in_n18{}, is_face{};
-  Hood() {  // skeletonize.cpp:12-42
-    auto co = [](int c) { return std::array<int, 3>{c % 3 - 1, (c / 3) % 3 - 1, c / 9 - 1}; };
-    for (int c = 0; c < 27; ++c) {
-      const auto a = co(c);
-      const int nz = std::abs(a[0]) + std::abs(a[1]) + std::abs(a[2]);
-      in_n18[c] = c != 13 && nz <= 2;
-      is_face[c] = nz == 1;
-      for (int d = 0; d < 27; ++d) {
-        if (d == c) continue;
-        const auto b = co(d);
-        const int man = std::abs(a[0] - b[0]) + std::abs(a[1] - b[1]) + std::abs(a[2] - b[2]);
-        const int che = std::max({std::abs(a[0] - b[0]), std::abs(a[1] - b[1]), std::abs(a[2] - b[2])});
-        if (che == 1 && c != 13 && d != 13) adj26[c].push_back(d);
-        if (man == 1) adj6[c].push_back(d);
-      }
-    }
-  }
-};
-const Hood& hood() {
-  static const Hood h;
-  return h;
-}
-
-// skeletonize.cpp:48-95: (26, 6) simple point
-bool is_simple(const std::array<bool, 27>& obj) {
-  const Hood& t = hood();
-  int seen = 0;
-  for (int c = 0; c < 27; ++c)
-    if (c != 13 && obj[c]) ++seen;
-  if (seen == 0) return false;
-  std::array<bool, 27> vis{};
-  int comp26 = 0;
-  for (int c = 0; c < 27 && comp26 <= 1; ++c) {
-    if (c == 13 || !obj[c] || vis[c]) continue;
-    ++comp26;
-    std::array<int, 27> st;
-    int top = 0;
-    st[top++] = c, vis[c] = true;
-    while (top) {
-      const int cur = st[--top];
-      for (int n : t.adj26[cur])
-        if (n != 13 && obj[n] && !vis[n]) vis[n] = true, st[top++] = n;
-    }
-  }
-  if (comp26 != 1) return false;
-  vis.fill(false);
-  int comp6 = 0;
-  for (int c = 0; c < 27 && comp6 <= 1; ++c) {
-    if (!t.is_face[c] || obj[c] || vis[c]) continue;
-    ++comp6;
-    std::array<int, 27> st;
-    int top = 0;
-    st[top++] = c, vis[c] = true;
-    while (top) {
-      const int cur = st[--top];
-      for (int n : t.adj6[cur])
-        if (t.in_n18[n] && !obj[n] && !vis[n]) vis[n] = true, st[top++] = n;
-    }
-  }
-  return comp6 == 1;
-}
-
-}  // namespace
 
 extern "C" {
 
@@ -197,65 +138,81 @@ vc_status vc_boundary_voxels(vc_ctx* ctx, const uint8_t* keep, const vc_grid_spe
   return VC_OK;
 }
 
-// skeletonize.cpp:99-161
-vc_status vc_skeletonize(const uint8_t* grid_in, int32_t nx, int32_t ny, int32_t nz, const int32_t* voxels,
-                         int64_t n, int32_t* out, int64_t* n_out) {
-  if (!grid_in || !n_out || nx < 1 || ny < 1 || nz < 1 || n < 0 || (n > 0 && (!voxels || !out)))
-    return vc_io_detail::set_error(VC_ERR_INVALID_ARGUMENT, "skeletonize: bad arguments");
-  std::vector<uint8_t> g(grid_in, grid_in + (size_t)nx * ny * nz);
-  auto at = [&](int x, int y, int z) -> uint8_t& { return g[((size_t)z * ny + y) * nx + x]; };
-  auto obj = [&](int x, int y, int z) {
-    return x >= 0 && y >= 0 && z >= 0 && x < nx && y < ny && z < nz && at(x, y, z) != 0;
+// skeletonize(BinaryVolume) (skeletonize.cpp:99-161) on the GPU (k_skeleton.cu):
+// per pass and direction, parallel candidate marking, the order-dependent
+// re-check as a fixed-point sweep, then the deletions; the surviving voxels in
+// input order.  The grid is not modified (a device copy is thinned).
+vc_status vc_skeletonize(vc_ctx* ctx, const uint8_t* grid_in, int32_t nx, int32_t ny, int32_t nz,
+                         const int32_t* voxels, int64_t n, int32_t* out, int64_t* n_out) {
+  if (!ctx || !grid_in || !n_out || nx < 1 || ny < 1 || nz < 1 || n < 0 || (n > 0 && (!voxels || !out)))
+    return fail(ctx, VC_ERR_INVALID_ARGUMENT, "skeletonize: bad arguments");
+  const size_t N = (size_t)nx * ny * nz;
+  if (N >= (size_t)INT32_MAX || n >= INT32_MAX) return fail(ctx, VC_ERR_INVALID_ARGUMENT, "skeletonize: grid too large");
+  *n_out = 0;
+  if (n == 0) return VC_OK;
+  cudaSetDevice(ctx->device);
+  if (!ctx->skel_lut_ready) {  // (26, 6)-simple predicate of all 2^26 neighbourhoods, once per context
+    VC_TRY(ensure(ctx, ctx->skel_lut, skel_lut_words() * 4));
+    launch_skel_lut(P<uint32_t>(ctx->skel_lut), ctx->st);
+    VC_CUDA(cudaGetLastError());
+    ctx->skel_lut_ready = true;
+  }
+  auto up = [](size_t x) { return (x + 255) & ~size_t(255); };
+  const size_t nn = (size_t)n;
+  VC_TRY(ensure(ctx, ctx->scratch_dev, up(N) + up(N * 4) + up(nn * 12) + 3 * up(nn) + 256));
+  uint8_t* p = P<uint8_t>(ctx->scratch_dev);
+  uint8_t* g = p;
+  p += up(N);
+  int32_t* pos = reinterpret_cast<int32_t*>(p);
+  p += up(N * 4);
+  int32_t* vox = reinterpret_cast<int32_t*>(p);
+  p += up(nn * 12);
+  uint8_t* cand = p;
+  p += up(nn);
+  uint8_t* del = p;
+  p += up(nn);
+  uint8_t* alive = p;
+  p += up(nn);
+  int* cnt = reinterpret_cast<int*>(p);  // [0] candidates, [1] changed, [2] deletions
+  const uint32_t* lut = P<uint32_t>(ctx->skel_lut);
+  VC_CUDA(cudaMemcpyAsync(g, grid_in, N, cudaMemcpyHostToDevice, ctx->st));
+  VC_CUDA(cudaMemcpyAsync(vox, voxels, nn * 12, cudaMemcpyHostToDevice, ctx->st));
+  VC_CUDA(cudaMemsetAsync(pos, 0xff, N * 4, ctx->st));
+  launch_skel_pos(vox, n, nx, ny, pos, ctx->st);
+  auto read = [&](int which, int* v) -> vc_status {
+    VC_CUDA(cudaMemcpyAsync(v, cnt + which, 4, cudaMemcpyDeviceToHost, ctx->st));
+    VC_CUDA(cudaStreamSynchronize(ctx->st));
+    return VC_OK;
   };
-  auto fill = [&](const int* p, std::array<bool, 27>& h) {
-    int c = 0;
-    for (int dz = -1; dz <= 1; ++dz)
-      for (int dy = -1; dy <= 1; ++dy)
-        for (int dx = -1; dx <= 1; ++dx, ++c) h[c] = obj(p[0] + dx, p[1] + dy, p[2] + dz);
-  };
-  auto ncount = [&](const int* p) {
-    int k = 0;
-    for (int dz = -1; dz <= 1; ++dz)
-      for (int dy = -1; dy <= 1; ++dy)
-        for (int dx = -1; dx <= 1; ++dx)
-          if ((dx | dy | dz) != 0 && obj(p[0] + dx, p[1] + dy, p[2] + dz)) ++k;
-    return k;
-  };
-  static constexpr int kDir[6][3] = {{0, 1, 0}, {0, -1, 0}, {0, 0, 1}, {0, 0, -1}, {1, 0, 0}, {-1, 0, 0}};
-  std::vector<std::array<int, 3>> active((size_t)n), cand;
-  for (int64_t v = 0; v < n; ++v) active[v] = {voxels[3 * v], voxels[3 * v + 1], voxels[3 * v + 2]};
-  std::array<bool, 27> h{};
-  bool any = true;
-  while (any) {
+  int hv = 0;
+  for (bool any = true; any;) {
     any = false;
-    for (const auto& d : kDir) {
-      cand.clear();
-      for (const auto& p : active) {
-        if (!at(p[0], p[1], p[2])) continue;
-        if (obj(p[0] + d[0], p[1] + d[1], p[2] + d[2])) continue;  // not a border voxel
-        if (ncount(p.data()) <= 1) continue;                        // endpoint / isolated
-        fill(p.data(), h);
-        if (is_simple(h)) cand.push_back(p);
-      }
-      for (const auto& p : cand) {  // sequential re-check (order-dependent)
-        if (ncount(p.data()) <= 1) continue;
-        fill(p.data(), h);
-        if (!is_simple(h)) continue;
-        at(p[0], p[1], p[2]) = 0;
-        any = true;
-      }
-    }
-    if (any) {
-      std::vector<std::array<int, 3>> still;
-      still.reserve(active.size());
-      for (const auto& p : active)
-        if (at(p[0], p[1], p[2])) still.push_back(p);
-      active.swap(still);
+    for (int dir = 0; dir < 6; ++dir) {
+      VC_CUDA(cudaMemsetAsync(cnt, 0, 12, ctx->st));
+      launch_skel_mark(g, nx, ny, nz, vox, n, dir, lut, cand, del, cnt, ctx->st);
+      VC_CUDA(cudaGetLastError());
+      VC_TRY(read(0, &hv));
+      if (hv == 0) continue;
+      do {  // sweeps until the deletions are the sequential re-check's fixed point
+        VC_CUDA(cudaMemsetAsync(cnt + 1, 0, 4, ctx->st));
+        launch_skel_recheck(g, nx, ny, nz, vox, n, pos, lut, cand, del, cnt + 1, ctx->st);
+        VC_CUDA(cudaGetLastError());
+        VC_TRY(read(1, &hv));
+      } while (hv);
+      launch_skel_apply(g, nx, ny, nz, vox, n, cand, del, cnt + 2, ctx->st);
+      VC_CUDA(cudaGetLastError());
+      VC_TRY(read(2, &hv));
+      any = any || hv > 0;
     }
   }
-  for (size_t v = 0; v < active.size(); ++v)
-    out[3 * v] = active[v][0], out[3 * v + 1] = active[v][1], out[3 * v + 2] = active[v][2];
-  *n_out = (int64_t)active.size();
+  launch_skel_alive(g, nx, ny, vox, n, alive, ctx->st);
+  std::vector<uint8_t> keep(nn);
+  VC_CUDA(cudaMemcpyAsync(keep.data(), alive, nn, cudaMemcpyDeviceToHost, ctx->st));
+  VC_CUDA(cudaStreamSynchronize(ctx->st));
+  int64_t m = 0;
+  for (size_t v = 0; v < nn; ++v)
+    if (keep[v]) std::memcpy(out + 3 * m++, voxels + 3 * v, 12);
+  *n_out = m;
   return VC_OK;
 }
 

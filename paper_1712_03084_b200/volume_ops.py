@@ -4,7 +4,7 @@ csrc/vc_volume.cpp, mirroring mocap/volume_ops.hpp:
   binarize(volume, grid, level)   binary_volume.cpp:10-66 (GPU union-find CCL)
   binarize_frame(ctx, out)        the same on the context's last frame volume (no copy)
   boundary_voxels(bv)             binary_volume.cpp:68-82
-  skeletonize(bv)                 skeletonize.cpp:99-161 (host, order-dependent thinning)
+  skeletonize(bv)                 skeletonize.cpp:99-161 (GPU: simple-point table, re-check fixed point)
 """
 from __future__ import annotations
 
@@ -63,14 +63,13 @@ def boundary_voxels(bv: BinaryVolume, ctx: Context | None = None) -> np.ndarray:
     return out[:n.value]
 
 
-def skeletonize(bv: BinaryVolume) -> np.ndarray:
+def skeletonize(bv: BinaryVolume, ctx=None) -> np.ndarray:
+    ctx = ctx or default_context()
     g = np.ascontiguousarray(bv.grid, np.uint8)
     vox = np.ascontiguousarray(bv.voxels, np.int32)
     out = np.zeros((max(len(vox), 1), 3), np.int32)
     n = C.c_int64()
-    st = L.lib().vc_skeletonize(g.ctypes.data_as(C.c_void_p), g.shape[2], g.shape[1], g.shape[0],
-                                vox.ctypes.data_as(C.c_void_p), C.c_int64(len(vox)), out.ctypes.data_as(C.c_void_p),
-                                C.byref(n))
-    if st != L.VC_OK:
-        raise RuntimeError(L.lib().vc_io_last_error().decode())
+    ctx._check(L.lib().vc_skeletonize(ctx.handle, g.ctypes.data_as(C.c_void_p), g.shape[2], g.shape[1], g.shape[0],
+                                      vox.ctypes.data_as(C.c_void_p), C.c_int64(len(vox)),
+                                      out.ctypes.data_as(C.c_void_p), C.byref(n)))
     return out[:n.value]

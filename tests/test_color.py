@@ -9,6 +9,7 @@ import numpy as np
 import pytest
 
 from oracle import oracle_color as OC
+from oracle import ref as R
 from paper_1712_03084_b200 import color as vcc
 from paper_1712_03084_b200 import volcap as vc
 
@@ -73,6 +74,104 @@ def test_chain_to_reference_kats():
     cc = vcc.chain_to_reference([vcc.PairwiseValueMap(f, t, vcc.ValueMap(g, o)) for f, t, g, o in edges], 0, 5)
     ref = OC.chain_to_reference(edges, 0, 5)
     assert [(m.gain, m.offset) for m in cc.maps] == ref
+
+
+# ------------------------------------------------------------------ pinned to the reference's own code
+needs_ref = pytest.mark.skipif(not R.available(0), reason="oracle/_ref not built (no /root/reference at build time)")
+
+
+def _pairs_array(pairs):
+    return np.array([np.concatenate([a, b]) for a, b in pairs], np.uint8)
+
+
+def _random_pairs(rng, n, gain, offset, outlier_frac, noise):
+    va = rng.uniform(size=n)
+    vb = gain * va + offset + rng.normal(0.0, noise, n)
+    out = rng.uniform(size=n) < outlier_frac
+    vb[out] = rng.uniform(size=out.sum())
+    hue = rng.integers(0, 3, n)  # the value channel is the max channel: vary which one
+    arr = np.zeros((n, 6), np.uint8)
+    for i in range(n):
+        for side, v in ((0, va[i]), (1, min(max(vb[i], 0.0), 1.0))):
+            k = min(max(OC.lround(v * 255.0), 0), 255)
+            px = [k // 3, k // 2, k // 5]
+            px[hue[i]] = k
+            arr[i, 3 * side:3 * side + 3] = px
+    return arr
+
+
+@needs_ref
+@pytest.mark.parametrize("case", range(8))
+def test_fit_value_map_matches_reference(case):
+    """Same support (same hypotheses, same inlier tests) as the reference's RANSAC,
+    least squares from exact integer moments: equal to the reference's fit up to
+    the rounding of its sequential fp64 sums."""
+    rng = np.random.default_rng(40 + case)
+    n = [12, 50, 200, 1000, 3000, 200, 64, 500][case]
+    arr = _random_pairs(rng, n, rng.uniform(0.6, 1.3), rng.uniform(-0.1, 0.2), [0, 0.1, 0.3, 0.2, 0.4, 0.5, 0, 0.25][case],
+                        [0.0, 0.004, 0.01, 0.02, 0.01, 0.005, 0.03, 0.0][case])
+    opts = vcc.ValueFitOptions([1000, 50, 1000, 300, 1000, 2000, 7, 1000][case], [0.05, 0.02, 0.05, 0.03, 0.05, 0.01,
+                                                                                    0.1, 0.05][case], 1 + case)
+    g, o = R.fit_value_map(arr, opts.ransac_iterations, opts.inlier_threshold, opts.seed)
+    m = vcc.fit_value_map([(r[:3], r[3:]) for r in arr], opts)
+    assert m.gain == pytest.approx(g, rel=1e-12, abs=1e-14)
+    assert m.offset == pytest.approx(o, rel=1e-10, abs=1e-13)
+
+
+@needs_ref
+def test_fit_value_map_errors_match_reference():
+    cases = [_pairs_array([value_pair(0.5, 0.5)] * 5),
+             _pairs_array([value_pair(0.5, 0.3 + i / 100.0) for i in range(20)]),
+             # two value levels far apart, no line within the threshold through >= 2 pairs other than the draws
+             _pairs_array([value_pair(0.2, 0.9), value_pair(0.8, 0.1)] * 3 + [value_pair(0.2 + i / 255.0, 0.5)
+                                                                               for i in range(4)])]
+    for arr in cases:
+        try:
+            ref = ("ok",) + R.fit_value_map(arr, 100, 0.05, 3)
+        except RuntimeError as e:
+            ref = ("err", str(e))
+        try:
+            m = vcc.fit_value_map([(r[:3], r[3:]) for r in arr], vcc.ValueFitOptions(100, 0.05, 3))
+            ours = ("ok", m.gain, m.offset)
+        except RuntimeError as e:
+            assert not isinstance(e, ValueError), "the reference throws std::runtime_error"
+            ours = ("err", str(e).split(": ", 1)[1])
+        assert ours[0] == ref[0]
+        if ref[0] == "err":
+            assert ours[1] == ref[1]
+        else:
+            assert ours[1] == pytest.approx(ref[1], rel=1e-12) and ours[2] == pytest.approx(ref[2], rel=1e-10, abs=1e-13)
+
+
+@needs_ref
+@pytest.mark.parametrize("seed", range(6))
+def test_chain_to_reference_matches_reference(seed):
+    """Random sensor graphs with cycles, parallel edges and both edge directions:
+    bit-identical maps (same BFS tree, same composition arithmetic)."""
+    rng = np.random.default_rng(seed)
+    n = int(rng.integers(2, 12))
+    edges = []
+    for k in range(1, n):  # a spanning tree with random orientation
+        j = int(rng.integers(0, k))
+        edges.append((k, j) if rng.uniform() < 0.5 else (j, k))
+    for _ in range(int(rng.integers(0, 2 * n))):  # extra edges (cycles, duplicates)
+        a, b = (int(x) for x in rng.integers(0, n, 2))
+        if a != b:
+            edges.append((a, b))
+    order = rng.permutation(len(edges))
+    edges = [(edges[i][0], edges[i][1], float(rng.uniform(0.7, 1.4)), float(rng.uniform(-0.1, 0.1))) for i in order]
+    refsensor = int(rng.integers(0, n))
+    want = R.chain_to_reference(edges, refsensor, n)
+    cc = vcc.chain_to_reference([vcc.PairwiseValueMap(f, t, vcc.ValueMap(g, o)) for f, t, g, o in edges], refsensor, n)
+    assert [(m.gain, m.offset) for m in cc.maps] == want
+
+
+@needs_ref
+def test_chain_to_reference_disconnected_matches_reference():
+    edges = [(0, 1, 1.1, 0.0), (2, 3, 0.9, 0.01)]
+    assert R.chain_to_reference(edges, 0, 4) is None
+    with pytest.raises(RuntimeError, match="sensor 2 not connected"):
+        vcc.chain_to_reference([vcc.PairwiseValueMap(f, t, vcc.ValueMap(g, o)) for f, t, g, o in edges], 0, 4)
 
 
 # ------------------------------------------------------------------ GPU parts

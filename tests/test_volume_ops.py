@@ -2,13 +2,15 @@
 """(A, L) consumers against oracle/oracle_volume.py and the
 reference's test_mocap_volume.cpp:55-163: binarize (GPU union-find) equal to the
 raster flood fill incl. ties and the inverted side, boundary voxels, and the
-host skeletonize equal to the restated thinning."""
+GPU skeletonize equal to the restated sequential thinning (incl. shuffled voxel
+lists, where the order-dependent re-check matters)."""
 import math
 
 import numpy as np
 import pytest
 
 from oracle import oracle_volume as OV
+from oracle import ref as R
 from paper_1712_03084_b200 import volcap as vc
 from paper_1712_03084_b200 import volume_ops as vo
 
@@ -28,13 +30,15 @@ def bv_of(keep, vox):
     return vo.BinaryVolume(keep, vox, spec(keep.shape))
 
 
-# ------------------------------------------------------------------ host skeletonize
+# ------------------------------------------------------------------ GPU skeletonize
+@pytest.mark.gpu
 def test_skeletonize_single_voxel():
     g = np.zeros((8, 8, 8), np.uint8)
     g[4, 4, 4] = 1
     assert vo.skeletonize(bv_of(g, np.array([[4, 4, 4]], np.int32))).tolist() == [[4, 4, 4]]
 
 
+@pytest.mark.gpu
 @pytest.mark.parametrize("seed", range(6))
 def test_skeletonize_matches_restatement(seed):
     """Union of overlapping balls (test_mocap_volume.cpp:129-163) + a box and a bar."""
@@ -51,6 +55,7 @@ def test_skeletonize_matches_restatement(seed):
     assert np.array_equal(ours, OV.skeletonize(keep, vox))
 
 
+@pytest.mark.gpu
 def test_skeletonize_cylinder_curve():
     """test_mocap_volume.cpp:99-127 (smaller): thin curve near the axis, subset, one component."""
     n, radius, length = 40, 5, 32
@@ -64,6 +69,76 @@ def test_skeletonize_cylinder_curve():
         assert g[qz, qy, qx] == 1
         if 4 + radius <= qx < 4 + length - radius:
             assert math.hypot(qy - 20.0, qz - 7.0) <= 2.0
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("seed", range(4))
+def test_skeletonize_shuffled_order(seed):
+    """The re-check is order-dependent (skeletonize.cpp:150-158): a permuted voxel
+    list must give the restatement's result for that same permuted order."""
+    rng = np.random.default_rng(100 + seed)
+    A = np.zeros((18, 22, 20))
+    c = rng.uniform(6, 13, 3)
+    for _ in range(3):
+        A = np.maximum(A, ball(20, c, rng.uniform(2.5, 4.5), shape=(18, 22, 20)))
+        c = c + rng.uniform(-3, 3, 3)
+    A[4:8, 3:19, 6:10] = 1.0
+    keep, vox = OV.binarize(A, 0.5)
+    vox = vox[rng.permutation(len(vox))]
+    ours = vo.skeletonize(bv_of(keep, vox))
+    assert np.array_equal(ours, OV.skeletonize(keep, vox))
+
+
+@pytest.mark.gpu
+def test_skeletonize_noisy_blob():
+    """A ragged blob (random voxels added on a ball's shell): many simple points,
+    long chains of adjacent candidates in one sweep."""
+    rng = np.random.default_rng(7)
+    A = ball(24, (11.5, 11.5, 11.5), 7.0)
+    shell = (ball(24, (11.5, 11.5, 11.5), 9.0) > 0) & (A == 0)
+    A[shell & (rng.uniform(size=A.shape) < 0.5)] = 1.0
+    keep, vox = OV.binarize(A, 0.5)
+    ours = vo.skeletonize(bv_of(keep, vox))
+    assert np.array_equal(ours, OV.skeletonize(keep, vox))
+
+
+def _blob(seed, shape=(18, 22, 20)):
+    rng = np.random.default_rng(seed)
+    A = np.zeros(shape)
+    c = rng.uniform(6, 13, 3)
+    for _ in range(3):
+        A = np.maximum(A, ball(20, c, rng.uniform(2.5, 4.5), shape=shape))
+        c = c + rng.uniform(-3, 3, 3)
+    return A
+
+
+@pytest.mark.skipif(not R.available(0), reason="oracle/_ref not built")
+@pytest.mark.parametrize("seed", range(3))
+def test_skeletonize_restatement_matches_reference(seed):
+    """Pins oracle_volume.skeletonize to the reference's own skeletonize.cpp."""
+    keep, vox = OV.binarize(_blob(seed), 0.5)
+    if seed == 2:
+        vox = vox[np.random.default_rng(1).permutation(len(vox))]
+    assert np.array_equal(OV.skeletonize(keep, vox), R.skeletonize(keep, vox))
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not R.available(0), reason="oracle/_ref not built")
+@pytest.mark.parametrize("seed", range(3))
+def test_skeletonize_matches_reference_large(seed):
+    """GPU thinning == the reference's sequential thinning on a 64^3 multi-ball body
+    (thousands of candidates per direction; the reference runs in C++ here)."""
+    rng = np.random.default_rng(200 + seed)
+    A = np.zeros((64, 64, 64))
+    c = np.array([32.0, 32.0, 32.0])
+    for _ in range(6):
+        A = np.maximum(A, ball(64, c, rng.uniform(6, 12)))
+        c = np.clip(c + rng.uniform(-10, 10, 3), 14, 50)
+    keep, vox = OV.binarize(A, 0.5)
+    if seed == 1:
+        vox = vox[rng.permutation(len(vox))]
+    ours = vo.skeletonize(bv_of(keep, vox))
+    assert np.array_equal(ours, R.skeletonize(keep, vox))
 
 
 # ------------------------------------------------------------------ GPU binarize
