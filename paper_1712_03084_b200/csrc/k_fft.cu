@@ -20,8 +20,12 @@
 // n = R1*R2 transform: a team of R2 threads each holding R1 elements; step 1
 // = R1/R2 register DFTs of length R2 per thread + twiddle W_n^(j1 k2), one
 // shared-memory exchange, step 2 = one register DFT of length R1.
+#include <cuda.h>  // CUtensorMap (encoded through the runtime's driver entry point; no libcuda link)
+#include <cudaTypedefs.h>
+
 #include <cmath>
 #include <cstdlib>
+#include <mutex>
 #include <vector>
 
 #include "vc_shared.hpp"
@@ -165,13 +169,21 @@ template <int T>
 __device__ __forceinline__ unsigned team_mask(int team_lane0) {
   return T >= 32 ? 0xffffffffu : (((1u << T) - 1u) << team_lane0);
 }
-// Exchange for column tiles (y/z passes): column index innermost.
+// Exchange for column tiles (y/z passes): column index innermost.  With
+// 8-column (64 B) rows a warp's 64-bit access covers four rows in two
+// wavefronts: the stores hit rows t*R2 + k2 (same parity for every t) and
+// would conflict 2-way, so row r lives at r ^ ((r / R2) & 1) — the stores'
+// rows then alternate parity with t, the loads' rows (j1*R2 + t) still do.
 template <int N, int CW>
 struct ExCols {
   float2* buf;  // (R1*R2) x CW
   int c;
-  __device__ void st(int j1, int k2, float2 v) { buf[(j1 * Shape<N>::R2 + k2) * CW + c] = v; }
-  __device__ float2 ld(int j1, int k2) { return buf[(j1 * Shape<N>::R2 + k2) * CW + c]; }
+  static constexpr int R2 = Shape<N>::R2;
+  __device__ __forceinline__ static int row(int j1, int k2) {
+    return CW == 8 ? (j1 * R2 + k2) ^ (j1 & 1) : j1 * R2 + k2;
+  }
+  __device__ void st(int j1, int k2, float2 v) { buf[row(j1, k2) * CW + c] = v; }
+  __device__ float2 ld(int j1, int k2) { return buf[row(j1, k2) * CW + c]; }
   __device__ void sync() { __syncthreads(); }
 };
 
@@ -213,6 +225,15 @@ __device__ __forceinline__ float4 ld_pred_cs(const float4* p, bool pred) {
   float4 r = make_float4(0.f, 0.f, 0.f, 0.f);
   asm("{\n .reg .pred q;\n setp.ne.u32 q, %5, 0;\n @q ld.global.cs.v4.f32 {%0, %1, %2, %3}, [%4];\n}"
       : "+f"(r.x), "+f"(r.y), "+f"(r.z), "+f"(r.w)
+      : "l"(p), "r"((unsigned)pred));
+  return r;
+}
+
+// Predicated 8-byte load that does not allocate in L1 (zero when !pred).
+__device__ __forceinline__ float2 ld_pred_f2(const float2* p, bool pred) {
+  float2 r = make_float2(0.f, 0.f);
+  asm("{\n .reg .pred q;\n setp.ne.u32 q, %3, 0;\n @q ld.global.L1::no_allocate.v2.f32 {%0, %1}, [%2];\n}"
+      : "+f"(r.x), "+f"(r.y)
       : "l"(p), "r"((unsigned)pred));
   return r;
 }
@@ -631,6 +652,217 @@ __global__ void __launch_bounds__(ZCfg<NZ>::THREADS, NZ >= 1024 ? 1 : (NZ == 256
     z_body<NZ, false>(S0, S1, nx, ny, kyl, ky0, H, fx_step, fy_step, tw, planeflag);
 }
 
+// ------------------------------------------------------------------ Z, TMA-fed, warp-private
+// Persistent CTAs over column tiles (16 kx columns x one ky row x all NZ
+// planes of D and Z).  Tiles arrive through the tensor-memory accelerator:
+// the live planes (F-y's plane flags) form runs, each cut into boxes of
+// 32/16/8/4/2/1 planes (one tensor map per box height, 4-D view {2H floats,
+// ny, nz, component}, 128 B rows, 128B swizzle), issued against an mbarrier
+// armed with the tile's byte count; dead planes are never read (their stage
+// rows are zeroed once per CTA).  A column belongs to T adjacent lanes of one
+// warp (lane = t + T*column), so the three transposes of the column's
+// z-transforms go through a warp-private padded buffer with __syncwarp only —
+// no CTA barrier inside the tile.  Each warp copies its columns of the stage
+// to registers (the swizzle makes that conflict-free), then counts itself out;
+// the last warp out arms the barrier and issues the next tile's boxes, which
+// land while the transforms, the filter and the stores of this tile run.  The
+// kx = nx/2 column of 16 ky rows (packed tiles, not a box) takes predicated
+// register loads.
+constexpr int kZBoxes = 6;  // box heights 1, 2, 4, 8, 16, 32 planes
+struct ZMaps {
+  CUtensorMap m[kZBoxes];
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t n) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(n) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t tx) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(tx) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n ZW_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra ZW_%=;\n}" ::"r"(
+          smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, int c3,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], "
+      "[%6];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
+      : "memory");
+}
+
+template <int NZ>
+struct Z4Cfg {
+  static constexpr int CW = 16;                   // columns per tile: 128 B stage rows
+  static constexpr int T = Shape<NZ>::R2;         // lanes per column
+  static constexpr int CPW = 32 / T;              // columns per warp
+  static constexpr int WARPS = CW / CPW;
+  static constexpr int THREADS = 32 * WARPS;
+  // float2 per column exchange: padded rows, and odd columns shifted by 64 B so
+  // the two columns a half-warp touches sit in disjoint banks
+  static constexpr int XCOL = Shape<NZ>::R1 * (T + 1) + 8;
+  static constexpr int STAGE_B = 2 * NZ * CW * 8;       // D rows then Z rows
+  static constexpr int EX_B = CW * XCOL * 8;
+  static constexpr int SMEM = 1024 + STAGE_B + EX_B + NZ * 2 + 64;  // + alignment slack, segments, barrier
+  static constexpr int MINB = THREADS >= 256 ? 2 : 4;
+};
+
+template <int NZ>
+__global__ void __launch_bounds__(Z4Cfg<NZ>::THREADS, Z4Cfg<NZ>::MINB)
+    z4_kernel(const __grid_constant__ ZMaps maps, float2* __restrict__ S0, const float2* __restrict__ S1, int nx,
+              int ny, int H, int ntx, int nnyq, float fx_step, float fy_step, const float2* __restrict__ tw,
+              const uint32_t* __restrict__ planeflag) {
+  using S = Shape<NZ>;
+  using CF = Z4Cfg<NZ>;
+  constexpr int T = S::R2, R1 = S::R1, kCW = CF::CW, TH = CF::THREADS;
+  constexpr int PW = (NZ + 31) / 32;
+  static_assert(R1 <= 32, "row mask");
+  extern __shared__ uint8_t zraw[];
+  // 1024 B aligned stage: the 128B swizzle is a function of the address bits
+  // 7-9, so row z's 16-byte chunk k sits at chunk k ^ (z & 7)
+  float2* stage = reinterpret_cast<float2*>(zraw + ((1024 - (smem_u32(zraw) & 1023)) & 1023));
+  float2* exbuf = stage + CF::STAGE_B / 8;
+  uint16_t* segs = reinterpret_cast<uint16_t*>(exbuf + CF::EX_B / 8);  // z | log2(h) << 11
+  uint64_t* bar = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(segs) + ((NZ * 2 + 15) & ~15));
+  int* outcnt = reinterpret_cast<int*>(bar + 1);
+  __shared__ uint32_t pmask[PW];
+  __shared__ int nseg_s, nlive_s;
+  for (int z = threadIdx.x; z < PW * 32; z += TH) {  // plane bitmask; warp-uniform trips
+    const bool f = z < NZ && (!planeflag || __ldg(planeflag + z) != 0u);
+    const uint32_t b = __ballot_sync(0xffffffffu, f);
+    if ((z & 31) == 0) pmask[z >> 5] = b;
+  }
+  __syncthreads();
+  auto plane_live = [&](int z) { return ((pmask[z >> 5] >> (z & 31)) & 1u) != 0u; };
+  if (threadIdx.x == 0) {  // live-plane runs -> boxes of 2^k <= 32 planes
+    int n = 0, live = 0;
+    for (int z = 0; z < NZ;) {
+      if (!plane_live(z)) {
+        ++z;
+        continue;
+      }
+      int e = z;
+      while (e < NZ && plane_live(e)) ++e;
+      live += e - z;
+      while (z < e) {
+        int lg = 5;
+        while ((1 << lg) > e - z) --lg;
+        segs[n++] = (uint16_t)(z | (lg << 11));
+        z += 1 << lg;
+      }
+    }
+    nseg_s = n, nlive_s = live;
+    *outcnt = 0;
+    mbar_init(bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  for (int i = threadIdx.x; i < CF::STAGE_B / 8; i += TH)  // dead planes are never loaded: zero rows
+    if (!plane_live((i / kCW) % NZ)) stage[i] = make_float2(0.f, 0.f);
+  __syncthreads();
+  const int nseg = nseg_s;
+  const uint32_t tx_bytes = (uint32_t)nlive_s * 2u * kCW * 8u;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  // lane within the column team / column within the warp.  T = 16: lanes 0-7
+  // and 16-23 are column 0, 8-15 and 24-31 column 1, so each half-warp reads
+  // 8 rows x 2 columns of the stage = 8 distinct swizzled chunks (no conflict)
+  const int t = T == 16 ? ((lane & 7) | ((lane >> 4) << 3)) : lane % T;
+  const int cl = T == 16 ? ((lane >> 3) & 1) : lane / T;
+  const int c = warp * CF::CPW + cl;      // column within the tile
+  uint32_t rm = 0;  // bit (q*T + j2): this thread's element z = t + T*q + R1*j2 is in a live plane
+#pragma unroll
+  for (int q = 0; q < S::Q; ++q)
+#pragma unroll
+    for (int j2 = 0; j2 < T; ++j2) rm |= (plane_live(t + T * q + R1 * j2) ? 1u : 0u) << (q * T + j2);
+  const int main_tiles = ntx * ny;
+  const size_t zstride = (size_t)ny * H;
+  auto issue = [&](int tile) {  // one thread: arm the barrier, then the boxes of both components
+    const int kyr = tile / ntx, kx0 = (tile - kyr * ntx) * kCW;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic reads of the stage before async writes
+    mbar_expect_tx(bar, tx_bytes);
+    for (int s2 = 0; s2 < 2 * nseg; ++s2) {
+      const int comp = s2 >= nseg ? 1 : 0;
+      const uint32_t e = segs[s2 - comp * nseg];
+      const int z = e & 2047, lg = e >> 11;
+      tma_load_4d(stage + (comp * NZ + z) * kCW, &maps.m[lg], 2 * kx0, kyr, z, comp, bar);
+    }
+  };
+  ExTeam<NZ> ex{exbuf + c * CF::XCOL, 0xffffffffu};
+  uint32_t phase = 0;
+  if (threadIdx.x == 0 && blockIdx.x < main_tiles && tx_bytes) issue(blockIdx.x);
+  for (int tile = blockIdx.x; tile < main_tiles + nnyq; tile += gridDim.x) {
+    int kx, kyr;
+    bool live;
+    float2 d[R1], v[R1];
+    if (tile < main_tiles) {
+      kyr = tile / ntx;
+      kx = (tile - kyr * ntx) * kCW + c;
+      live = kx <= nx / 2;
+      if (tx_bytes) mbar_wait(bar, phase);
+      phase ^= 1u;
+#pragma unroll
+      for (int q = 0; q < S::Q; ++q)
+#pragma unroll
+        for (int j2 = 0; j2 < T; ++j2) {
+          const int z = t + T * q + R1 * j2;
+          const int col = ((((c >> 1) ^ z) & 7) << 1) | (c & 1);  // swizzled position of column c in row z
+          d[q * T + j2] = stage[z * kCW + col];
+          v[q * T + j2] = stage[(NZ + z) * kCW + col];
+        }
+      __syncwarp();
+      if (lane == 0) {  // count out; the last warp re-arms the stage with the next tile
+        __threadfence_block();
+        const int nt = tile + gridDim.x;
+        if (atomicAdd(outcnt, 1) == CF::WARPS - 1) {
+          *outcnt = 0;
+          if (nt < main_tiles && tx_bytes) issue(nt);
+        }
+      }
+    } else {  // the kx = nx/2 column of 16 ky rows
+      kyr = (tile - main_tiles) * kCW + c;
+      kx = nx / 2;
+      live = kyr < ny;
+      const size_t base = live ? (size_t)kyr * H + kx : 0;
+      const uint32_t lm = live ? rm : 0u;
+#pragma unroll
+      for (int q = 0; q < S::Q; ++q)
+#pragma unroll
+        for (int j2 = 0; j2 < T; ++j2) {
+          const int i = q * T + j2;
+          const size_t o = base + (size_t)(t + T * q + R1 * j2) * zstride;
+          d[i] = ld_pred_f2(S0 + o, (lm >> i) & 1u);
+          v[i] = ld_pred_f2(S1 + o, (lm >> i) & 1u);
+        }
+    }
+    fft_line<NZ, false>(d, t, tw, ex);
+    fft_line<NZ, false>(v, t, tw, ex);
+    // integrate.cpp:37-40 frequencies, filter -j(D + wz Z)/|w|^2, DC = 0 (:46-60)
+    const float wx = (float)(kx <= nx / 2 ? kx : kx - nx) * fx_step;
+    const float wy = (float)(kyr <= ny / 2 ? kyr : kyr - ny) * fy_step;
+    const float wxy = wx * wx + wy * wy;
+#pragma unroll
+    for (int k1 = 0; k1 < R1; ++k1) {
+      const int kz = t + T * k1;
+      const float wz = signed_freq<NZ>(kz);
+      const float w2 = wxy + wz * wz;
+      const float2 s2 = make_float2(d[k1].x + wz * v[k1].x, d[k1].y + wz * v[k1].y);
+      const float inv = (kx == 0 && kyr == 0 && kz == 0) ? 0.f : __fdividef(1.0f, w2);
+      d[k1] = make_float2(s2.y * inv, -s2.x * inv);  // (-i/|w|^2) * s
+    }
+    relayout_for_inverse<NZ>(d);
+    fft_line<NZ, true>(d, t, tw, ex);
+    if (live) {
+      const size_t base = (size_t)kyr * H + kx;
+#pragma unroll
+      for (int k1 = 0; k1 < R1; ++k1) st_out(S0 + base + (size_t)(t + T * k1) * zstride, d[k1]);
+    }
+  }
+}
+
 // ------------------------------------------------------------------ I-y
 template <int NY, bool NYQ>
 __device__ __forceinline__ void iy_body(const float2* Rin, float2* Rout, int nxh, int H, int lk,
@@ -810,6 +1042,7 @@ struct Prep {
       allow_smem(iy_kernel<N>, ICfg<N>::SMEM);
     } else {
       allow_smem(z_kernel<N>, 2 * ZCfg<N>::SMEM);
+      if constexpr (N == 64 || N == 128 || N == 256) allow_smem(z4_kernel<N>, Z4Cfg<N>::SMEM);
     }
   }
 };
@@ -865,6 +1098,61 @@ struct RunZ {
                                                          a.twz, a.planeflag);
   }
 };
+// VC_ZK=4 selects the TMA-fed warp-private Z kernel (opt-in: at 256^3 it
+// measured 77.6 us against 48.5 us for the staged kernel, profiles/README.md);
+// default 1, the staged kernel.
+inline int z_mode() {
+  static const int m = [] {
+    const char* e = std::getenv("VC_ZK");
+    return e ? std::atoi(e) : 1;
+  }();
+  return m;
+}
+PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }();
+  return fn;
+}
+// 4-D view {2H floats, ny, nz, component} of the D/Z spectra (component stride
+// cs complex), one map per box height 2^k planes, 16 complex (128 B) wide.
+bool encode_zmaps(ZMaps* zm, const float2* S0, int H, int ny, int nz, size_t cs) {
+  auto enc = tmap_encoder();
+  if (!enc) return false;
+  const cuuint64_t dims[4] = {(cuuint64_t)2 * H, (cuuint64_t)ny, (cuuint64_t)nz, 2};
+  const cuuint64_t strides[3] = {(cuuint64_t)H * 8, (cuuint64_t)H * 8 * ny, (cuuint64_t)cs * 8};
+  const cuuint32_t estr[4] = {1, 1, 1, 1};
+  for (int k = 0; k < kZBoxes; ++k) {
+    const cuuint32_t box[4] = {32, 1, (cuuint32_t)(1 << k), 1};
+    if (enc(&zm->m[k], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float2*>(S0), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return false;
+  }
+  return true;
+}
+template <int N>
+struct RunZ4 {
+  static void run(const SlabFft& a, const ZMaps& zm) {
+    using C = Z4Cfg<N>;
+    int ntx, nnyq;
+    if ((a.nx / 2) % C::CW == 0) {
+      ntx = a.nx / 2 / C::CW, nnyq = (a.ny + C::CW - 1) / C::CW;
+    } else {
+      ntx = (a.nx / 2 + 1 + C::CW - 1) / C::CW, nnyq = 0;
+    }
+    const int tiles = ntx * a.ny + nnyq;
+    const int cap = sm_count() * C::MINB;
+    const float fxs = (float)(2.0 * M_PI / a.nx), fys = (float)(2.0 * M_PI / a.ny);
+    z4_kernel<N><<<tiles < cap ? tiles : cap, C::THREADS, C::SMEM, a.st>>>(
+        zm, a.S0, a.S1, a.nx, a.ny, a.H, ntx, nnyq, fxs, fys, a.twz, a.planeflag);
+  }
+};
 template <int N>
 struct RunIy {
   static void run(const SlabFft& a) {
@@ -916,7 +1204,24 @@ void launch_fft_forward_xy(const SlabFft& a) {
   dispatch_n<RunFx>(a.nx, a);
   dispatch_n<RunFy>(a.ny, a);
 }
-void launch_fft_z(const SlabFft& a) { dispatch_n<RunZ>(a.nz, a); }
+void launch_fft_z(const SlabFft& a) {
+  // the TMA-fed kernel: one GPU (D and Z one component stride apart, all ky rows), 64..256 planes,
+  // rows of 16 complex (nx >= 32: the main tiles hold at least one full box width)
+  if (z_mode() == 4 && (a.nz == 256 || a.nz == 128 || a.nz == 64) && a.nx >= 32 && a.kyl == a.ny && a.R0 == a.S0 &&
+      a.R1 == a.S1) {
+    ZMaps zm;
+    if (encode_zmaps(&zm, a.S0, a.H, a.ny, a.nz, (size_t)(a.S1 - a.S0))) {
+      if (a.nz == 256)
+        RunZ4<256>::run(a, zm);
+      else if (a.nz == 128)
+        RunZ4<128>::run(a, zm);
+      else
+        RunZ4<64>::run(a, zm);
+      return;
+    }
+  }
+  dispatch_n<RunZ>(a.nz, a);
+}
 void launch_fft_inverse_yx(const SlabFft& a) {
   dispatch_n<RunIy>(a.ny, a);
   dispatch_n<RunIx>(a.nx, a);
@@ -956,7 +1261,7 @@ void launch_integrate(const float4* acc, float2* spec, float* A, int nx, int ny,
   if (ev) record_event(ev[1], st);
   dispatch_n<RunFy>(ny, a);
   if (ev) record_event(ev[2], st);
-  dispatch_n<RunZ>(nz, a);
+  launch_fft_z(a);
   if (ev) record_event(ev[3], st);
   dispatch_n<RunIy>(ny, a);
   if (ev) record_event(ev[4], st);
