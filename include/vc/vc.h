@@ -296,6 +296,19 @@ vc_status vc_ply_write_mesh(const char* path, const float* xyz, const float* nor
  * texture.cpp:74-91) for a host-memory vc_textured_mesh. */
 vc_status vc_ply_write_textured(const char* path, const vc_textured_mesh* mesh);
 
+/* ---------------------------------------------- optional depth filter
+ * BASELINE north_star preprocessing ("erosion/bilateral filtering"); the
+ * reference has no such filter (cloud.cpp:19-117), so it is OFF by default and
+ * any non-zero setting changes results versus the reference.  Erosion: a pixel
+ * stays foreground only if its (2e+1)^2 window is foreground.  Bilateral:
+ * depth' = round(sum w d / sum w) over valid neighbours within ceil(2 sigma_px),
+ * w = exp(-|dp|^2/(2 sigma_px^2) - dz^2/(2 sigma_mm^2)); sigma_px <= 4. */
+/* Applied to every view this context stages (all zero = off, the default). */
+vc_status vc_ctx_set_depth_filter(vc_ctx* ctx, int32_t erode_px, double sigma_px, double sigma_mm);
+/* One view, in place (mask eroded first, then the depth filtered). */
+vc_status vc_depth_filter(vc_ctx* ctx, uint16_t* depth, uint8_t* mask, int32_t width, int32_t height,
+                          int32_t mem_kind, int32_t erode_px, double sigma_px, double sigma_mm);
+
 /* ---------------------------------------------- colour correction
  * SURVEY §8(f) rank 2 (appearance/color_correction.cpp, hsv.cpp).  Errors of
  * the context-free entry points: vc_io_last_error(). */

@@ -169,19 +169,19 @@ template <int T>
 __device__ __forceinline__ unsigned team_mask(int team_lane0) {
   return T >= 32 ? 0xffffffffu : (((1u << T) - 1u) << team_lane0);
 }
-// Exchange for column tiles (y/z passes): column index innermost.  With
-// 8-column (64 B) rows a warp's 64-bit access covers four rows in two
-// wavefronts: the stores hit rows t*R2 + k2 (same parity for every t) and
-// would conflict 2-way, so row r lives at r ^ ((r / R2) & 1) — the stores'
-// rows then alternate parity with t, the loads' rows (j1*R2 + t) still do.
+// Exchange for column tiles (y/z passes): column index innermost.  With rows
+// narrower than 128 B (CW = 8: 64 B, CW = 4: 32 B) a warp's 64-bit access
+// covers several rows per wavefront: the stores hit rows t*R2 + k2 (the same
+// bank window for every t) and would conflict, so row r = j1*R2 + k2 lives at
+// r ^ (j1 & SW) — the stores' rows then rotate through the 128 B window with
+// t, the loads' rows (j1*R2 + t) still do.
 template <int N, int CW>
 struct ExCols {
   float2* buf;  // (R1*R2) x CW
   int c;
   static constexpr int R2 = Shape<N>::R2;
-  __device__ __forceinline__ static int row(int j1, int k2) {
-    return CW == 8 ? (j1 * R2 + k2) ^ (j1 & 1) : j1 * R2 + k2;
-  }
+  static constexpr int SW = CW * 8 >= 128 ? 0 : 128 / (CW * 8) - 1;  // rows per 128 B, minus one
+  __device__ __forceinline__ static int row(int j1, int k2) { return (j1 * R2 + k2) ^ (j1 & SW); }
   __device__ void st(int j1, int k2, float2 v) { buf[row(j1, k2) * CW + c] = v; }
   __device__ float2 ld(int j1, int k2) { return buf[row(j1, k2) * CW + c]; }
   __device__ void sync() { __syncthreads(); }
@@ -256,10 +256,13 @@ struct FCfg {
   static constexpr int SMEM = N * CW * 8;
 };
 
-// Z: 8-column tiles from 256 points up (4 CTAs/SM at 256)
+// Z: narrow tiles from 256 points up (VC_ZCW=4: 4 columns, 8 CTAs/SM at 256)
+#ifndef VC_ZCW256
+#define VC_ZCW256 8
+#endif
 template <int N>
 struct ZCfg {
-  static constexpr int CW = N >= 256 ? 8 : 16;
+  static constexpr int CW = N == 256 ? VC_ZCW256 : (N >= 256 ? 8 : 16);
   static constexpr int THREADS = CW * Shape<N>::R2;
   static constexpr int SMEM = N * CW * 8;
 };
@@ -643,7 +646,7 @@ __device__ __forceinline__ void z_body(float2* __restrict__ S0, const float2* __
 // Input: D, Z as [z][kyl][H] (kyl = ny on one GPU; a ky-slab starting at ky0
 // after the forward all-to-all).  The result overwrites S0 in place.
 template <int NZ>
-__global__ void __launch_bounds__(ZCfg<NZ>::THREADS, NZ >= 1024 ? 1 : (NZ == 256 ? 4 : 2))
+__global__ void __launch_bounds__(ZCfg<NZ>::THREADS, NZ >= 1024 ? 1 : (NZ == 256 ? 32 / VC_ZCW256 : 2))
     z_kernel(float2* __restrict__ S0, const float2* __restrict__ S1, int nx, int ny, int kyl, int ky0, int H, int nyq,
              float fx_step, float fy_step, const float2* __restrict__ tw, const uint32_t* __restrict__ planeflag) {
   if (blockIdx.x == nyq)

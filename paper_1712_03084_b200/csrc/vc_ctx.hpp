@@ -71,7 +71,11 @@ struct vc_ctx {
   cudaEvent_t ev[kEvents] = {};
   bool table_ready = false;
   int last_k = 0;
-  std::vector<double> cc_gain, cc_offset;  // per-sensor colour correction of the texture blend (empty: off)
+  std::vector<double> cc_gain, cc_offset;
+  // optional depth filter applied to every staged view (off: all zero)
+  int df_erode = 0;
+  double df_sigma_px = 0.0, df_sigma_mm = 0.0;
+  Buf df_scratch;  // per-sensor colour correction of the texture blend (empty: off)
   int kernels_per_frame = 0;
 };
 namespace vc::rt {

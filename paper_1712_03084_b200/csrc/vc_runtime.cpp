@@ -165,6 +165,16 @@ vc_status stage_views(vc_ctx* ctx, const vc_sensor* sensors, const vc_view* view
     vp.rgb = (v.rgb && need_rgb) ? base + off[3 * i + 2] : nullptr;
     vp.dpitch = w, vp.mpitch = w, vp.rpitch = rw * 3;
   }
+  if (ctx->df_erode > 0 || (depth_filter_radius(ctx->df_sigma_px) > 0 && ctx->df_sigma_mm > 0))
+    for (int i = 0; i < k; ++i) {  // optional depth filter, in place on the staged views
+      const int w = sensors[i].depth_intr.width, h = sensors[i].depth_intr.height;
+      VC_TRY(ensure(ctx, ctx->df_scratch, (size_t)w * h * 3 + 512));
+      uint8_t* s8 = P<uint8_t>(ctx->df_scratch);
+      launch_depth_filter(reinterpret_cast<uint16_t*>(base + off[3 * i]), base + off[3 * i + 1], w, h, ctx->df_erode,
+                          ctx->df_sigma_px, ctx->df_sigma_mm, s8,
+                          reinterpret_cast<uint16_t*>(s8 + (((size_t)w * h + 255) & ~size_t(255))), ctx->st);
+      VC_CUDA(cudaGetLastError());
+    }
   return VC_OK;
 }
 
@@ -517,7 +527,7 @@ vc_status vc_ctx_destroy(vc_ctx* ctx) {
   cudaSetDevice(ctx->device);
   if (ctx->st) cudaStreamSynchronize(ctx->st);
   if (ctx->gexec) cudaGraphExecDestroy(ctx->gexec);
-  for (Buf* b : {&ctx->acc, &ctx->spec, &ctx->A, &ctx->tw, &ctx->vbase, &ctx->blk, &ctx->rowmm, &ctx->units, &ctx->unitcnt, &ctx->rowbits, &ctx->planeflag, &ctx->rowlist, &ctx->vinfo, &ctx->scratch_dev, &ctx->scratch_dev2, &ctx->skel_lut, &ctx->views, &ctx->pts_pos,
+  for (Buf* b : {&ctx->acc, &ctx->spec, &ctx->A, &ctx->tw, &ctx->vbase, &ctx->blk, &ctx->rowmm, &ctx->units, &ctx->unitcnt, &ctx->rowbits, &ctx->planeflag, &ctx->rowlist, &ctx->vinfo, &ctx->scratch_dev, &ctx->scratch_dev2, &ctx->skel_lut, &ctx->df_scratch, &ctx->views, &ctx->pts_pos,
                  &ctx->pts_nrm, &ctx->pts_w, &ctx->pts_pix, &ctx->wmaps, &ctx->pre_scratch, &ctx->iso_partial,
                  &ctx->m_pos, &ctx->m_nrm, &ctx->m_tri, &ctx->m_eid, &ctx->m_cells, &ctx->m_celltri, &ctx->m_cellcfg, &ctx->m_posf,
                  &ctx->t_vis, &ctx->t_uv, &ctx->t_w, &ctx->t_untex, &ctx->t_rgb})
@@ -1035,6 +1045,45 @@ vc_status vc_synth_render(vc_ctx* ctx, const vc_sensor* sensor, const vc_body* b
   if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->st);
   cudaFree(tmp);
   if (e != cudaSuccess) return fail(ctx, VC_ERR_CUDA, cudaGetErrorString(e));
+  return VC_OK;
+}
+
+vc_status vc_ctx_set_depth_filter(vc_ctx* ctx, int32_t erode_px, double sigma_px, double sigma_mm) {
+  if (!ctx || erode_px < 0 || erode_px > 32 || !(sigma_px >= 0) || !(sigma_mm >= 0) ||
+      depth_filter_radius(sigma_px) > depth_filter_max_radius())
+    return fail(ctx, VC_ERR_INVALID_ARGUMENT, "depth filter: erode_px in [0, 32], 0 <= sigma_px <= 4, sigma_mm >= 0");
+  ctx->df_erode = erode_px, ctx->df_sigma_px = sigma_px, ctx->df_sigma_mm = sigma_mm;
+  return VC_OK;
+}
+
+vc_status vc_depth_filter(vc_ctx* ctx, uint16_t* depth, uint8_t* mask, int32_t width, int32_t height,
+                          int32_t mem_kind, int32_t erode_px, double sigma_px, double sigma_mm) {
+  if (!ctx || !depth || !mask || width < 1 || height < 1 || erode_px < 0 || erode_px > 32 || !(sigma_px >= 0) ||
+      !(sigma_mm >= 0) || depth_filter_radius(sigma_px) > depth_filter_max_radius())
+    return fail(ctx, VC_ERR_INVALID_ARGUMENT, "depth filter: bad arguments");
+  cudaSetDevice(ctx->device);
+  const size_t n = (size_t)width * height;
+  auto up = [](size_t x) { return (x + 255) & ~size_t(255); };
+  VC_TRY(ensure(ctx, ctx->scratch_dev, (mem_kind == VC_MEM_HOST ? up(2 * n) + up(n) : 0) + up(n) + up(2 * n) + 256));
+  uint8_t* p = P<uint8_t>(ctx->scratch_dev);
+  uint16_t* dd = depth;
+  uint8_t* dm = mask;
+  if (mem_kind == VC_MEM_HOST) {
+    dd = reinterpret_cast<uint16_t*>(p);
+    p += up(2 * n);
+    dm = p;
+    p += up(n);
+    VC_CUDA(cudaMemcpyAsync(dd, depth, 2 * n, cudaMemcpyHostToDevice, ctx->st));
+    VC_CUDA(cudaMemcpyAsync(dm, mask, n, cudaMemcpyHostToDevice, ctx->st));
+  }
+  launch_depth_filter(dd, dm, width, height, erode_px, sigma_px, sigma_mm, p, reinterpret_cast<uint16_t*>(p + up(n)),
+                      ctx->st);
+  VC_CUDA(cudaGetLastError());
+  if (mem_kind == VC_MEM_HOST) {
+    VC_CUDA(cudaMemcpyAsync(depth, dd, 2 * n, cudaMemcpyDeviceToHost, ctx->st));
+    VC_CUDA(cudaMemcpyAsync(mask, dm, n, cudaMemcpyDeviceToHost, ctx->st));
+  }
+  VC_CUDA(cudaStreamSynchronize(ctx->st));
   return VC_OK;
 }
 

@@ -106,6 +106,11 @@ void launch_preprocess(const SensorSet& ss, DevPoints pts, float* weight_maps, i
                        int dims_x, int dims_y, int dims_z, int padding, double disc_mm, int sil_r, cudaStream_t st,
                        int32_t* rowlist_reset = nullptr /*frame path: zero the touched-row count*/);
 void launch_mask_from_depth(const uint16_t* depth, uint8_t* mask, int n, cudaStream_t st);  // mask := depth > 0
+// optional depth preprocessing (k_depth_filter.cu; off by default)
+int depth_filter_radius(double sigma_px);
+int depth_filter_max_radius();
+void launch_depth_filter(uint16_t* depth, uint8_t* mask, int w, int h, int erode_px, double sigma_px,
+                         double sigma_mm, uint8_t* scratch8, uint16_t* scratch16, cudaStream_t st);
 // k_splat.cu
 void launch_clear(float4* acc, size_t n, cudaStream_t st);
 // zoff/nzl: the z-slab [zoff, zoff+nzl) this rank accumulates (whole grid: 0, nz).

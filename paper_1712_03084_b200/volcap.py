@@ -242,6 +242,12 @@ class Context:
     def set_profiling(self, on: bool):
         self._check(L.lib().vc_ctx_set_profiling(self._h, 1 if on else 0))
 
+    def set_depth_filter(self, erode_px: int = 0, sigma_px: float = 0.0, sigma_mm: float = 0.0):
+        """Optional erosion/bilateral filter of every staged view (north_star
+        preprocessing; the reference has none, so it stays off by default)."""
+        self._check(L.lib().vc_ctx_set_depth_filter(self._h, int(erode_px), C.c_double(sigma_px),
+                                                    C.c_double(sigma_mm)))
+
     def kernels_per_frame(self) -> int:
         return L.lib().vc_ctx_kernels_per_frame(self._h)
 
@@ -494,3 +500,15 @@ def render_frame(rig: CameraRig, body: L.Body, camera: int, frame: int = 0, sigm
                                        C.c_uint64(seed), C.c_double(gain), camera, frame, C.c_void_p(_ptr(depth)),
                                        C.c_void_p(_ptr(mask)), C.c_void_p(_ptr(rgb)), L.VC_MEM_HOST))
     return RgbdFrame(depth, rgb, mask)
+
+
+def depth_filter(depth: np.ndarray, mask: np.ndarray, erode_px: int = 0, sigma_px: float = 0.0,
+                 sigma_mm: float = 0.0, ctx: "Context | None" = None):
+    """vc_depth_filter on host copies of one view: (filtered depth, eroded mask)."""
+    ctx = ctx or default_context()
+    d = np.ascontiguousarray(depth, np.uint16).copy()
+    m = np.ascontiguousarray(mask, np.uint8).copy()
+    h, w = d.shape
+    ctx._check(L.lib().vc_depth_filter(ctx.handle, d.ctypes.data_as(C.c_void_p), m.ctypes.data_as(C.c_void_p), w, h,
+                                       L.VC_MEM_HOST, int(erode_px), C.c_double(sigma_px), C.c_double(sigma_mm)))
+    return d, m
