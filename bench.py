@@ -145,9 +145,39 @@ def oracle_inputs(O, rig, wl, j):
     return [v.depth for v in views], [v.mask for v in views], [v.rgb for v in views]
 
 
+def cpu_frame_fn(O, wl):
+    """The CPU implementation the reference legs time: the REFERENCE's own code
+    (proj/core compiled unmodified into oracle/_ref/libref.so; kind "reference")
+    when it was built, else the oracle restatement (kind "port").  Returns
+    (kind, frame(rig, depths, masks, rgbs) -> seconds, description)."""
+    from oracle import ref as R
+    if R.available(0):
+        def frame(rig, d, m, c):
+            t0 = time.perf_counter()
+            r = R.reconstruct_frame(rig, d, m, c, dims=wl.dims, want_volume=False)
+            dt = time.perf_counter() - t0
+            assert r.status == 0
+            return dt, None
+        return "reference", frame, ("the reference's own proj/core sources (reconstruct_frame + texture.cpp) compiled "
+                                    "unmodified into oracle/_ref against the Eigen/doctest shims, its FFTW3 calls "
+                                    "served by the oracle's fp64 FFT (FFTW is absent); splat on all host threads "
+                                    "(splat.cpp:59-78), other stages single-threaded as written")
+
+    def frame(rig, d, m, c):
+        t0 = time.perf_counter()
+        r = O.reconstruct_frame(rig, d, m, c, dims=wl.dims, want_volume=False)
+        dt = time.perf_counter() - t0
+        assert r.status == 0
+        return dt, r.timings
+    return "port", frame, ("CPU oracle restated from proj/core (splat on all host threads over z-slabs as "
+                           "splat.cpp:59-78, other stages single-threaded as the reference; own fp64 radix-2 FFT "
+                           "instead of FFTW)")
+
+
 def run_reference(args):
-    """The reference's CPU path (the oracle restatement of proj/core on the host
-    cores) on the same workload, frames and metric as the GPU arm."""
+    """The reference's CPU path on the host cores (its own compiled code when
+    oracle/_ref was built, else the oracle restatement) on the same workload,
+    frames and metric as the GPU arm."""
     from paper_1712_03084_b200.frame_parallel import stream_frame
     rank, world, _ = dist_env()
     if rank != 0:
@@ -156,15 +186,13 @@ def run_reference(args):
     wl = WORKLOADS[args.workload]
     rig = oracle_rig(O, wl)
     threads = O.lib().orc_hardware_threads()
-    t0 = time.perf_counter()
-    O.reconstruct_frame(rig, *oracle_inputs(O, rig, wl, stream_frame(0, wl.frames)), dims=wl.dims, want_volume=False)
-    t_frame = time.perf_counter() - t0
+    kind, frame, what = cpu_frame_fn(O, wl)
+    t_frame, _ = frame(rig, *oracle_inputs(O, rig, wl, stream_frame(0, wl.frames)))
     # bounded sample: at most ~150 s of CPU work for the timed steps
     steps = max(1, min(args.steps, int(150.0 / max(t_frame, 1e-3))))
     warm = min(args.warmup, 1)
     for i in range(warm):
-        O.reconstruct_frame(rig, *oracle_inputs(O, rig, wl, stream_frame(1 + i, wl.frames)), dims=wl.dims,
-                            want_volume=False)
+        frame(rig, *oracle_inputs(O, rig, wl, stream_frame(1 + i, wl.frames)))
     stage = {"raw_ms": [], "weights_ms": [], "volumetric_ms": [], "other_ms": [], "blend_ms": [],
              "splat_ms": [], "integrate_ms": [], "iso_ms": [], "mc_ms": []}
     total = 0.0
@@ -172,46 +200,38 @@ def run_reference(args):
     for i in range(steps):
         j = stream_frame(i, wl.frames)  # the GPU arm's global-step order
         used.append(wl.kick_frame(j))
-        inp = oracle_inputs(O, rig, wl, j)
-        t0 = time.perf_counter()
-        r = O.reconstruct_frame(rig, *inp, dims=wl.dims, want_volume=False)
-        total += time.perf_counter() - t0
-        assert r.status == 0
-        for k in stage:
-            stage[k].append(r.timings[k])
+        dt, timings = frame(rig, *oracle_inputs(O, rig, wl, j))
+        total += dt
+        if timings:
+            for k in stage:
+                stage[k].append(timings[k])
     fps = steps / total
     sample = (f"{steps} frame(s) of the {wl.key.upper()} stream (kick frames {used[:6]}{'...' if steps > 6 else ''}, "
-              f"the GPU arm's first global steps; of {args.steps} requested steps; bounded to ~150 s), CPU oracle "
-              f"restated from proj/core (splat on {threads} threads over z-slabs as splat.cpp:59-78, other stages "
-              f"single-threaded as the reference; own fp64 radix-2 FFT instead of FFTW)")
+              f"the GPU arm's first global steps; of {args.steps} requested steps; bounded to ~150 s); {what}; "
+              f"{threads} host threads")
     line = {"metric": wl.metric, "value": fps, "unit": "frames/s", "n_gpus": world, "steps": steps, "warmup": warm,
             "ms_per_step": 1000.0 * total / steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic", "impl": "reference",
             "config": {"workload": wl.text, "grid": list(wl.dims), "views": wl.k},
-            "stages_ms": {k: float(np.mean(v)) for k, v in stage.items()},
-            "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": threads, "kind": "port", "sample": sample},
+            "stages_ms": {k: float(np.mean(v)) for k, v in stage.items() if v},
+            "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": threads, "kind": kind, "sample": sample},
             "e2e": {"value": fps, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
 def cpu_baseline_sample(wl):
-    """The oracle on the host (rank 0, N=1): 2 frames of the workload (~10-30 s)."""
+    """The reference's CPU path on the host (rank 0, N=1): 2 frames of the workload (~10-30 s)."""
     from oracle import oracle as O
     rig = oracle_rig(O, wl)
+    kind, frame, what = cpu_frame_fn(O, wl)
     ts = []
     picks = (wl.frames // 30, wl.frames * 2 // 3)
     for j in picks:
-        inp = oracle_inputs(O, rig, wl, j)
-        t0 = time.perf_counter()
-        r = O.reconstruct_frame(rig, *inp, dims=wl.dims, want_volume=False)
-        ts.append(time.perf_counter() - t0)
-        assert r.status == 0
+        ts.append(frame(rig, *oracle_inputs(O, rig, wl, j))[0])
     threads = O.lib().orc_hardware_threads()
-    return {"value": len(ts) / sum(ts), "unit": "frames/s", "cores": threads, "kind": "port",
+    return {"value": len(ts) / sum(ts), "unit": "frames/s", "cores": threads, "kind": kind,
             "sample": f"2 frames (kick #{wl.kick_frame(picks[0])}, #{wl.kick_frame(picks[1])}) of the "
-                      f"{wl.key.upper()} stream; CPU oracle port of proj/core, splat on {threads} threads "
-                      f"(splat.cpp:59-78), other stages single-threaded as the reference, fp64 radix-2 FFT in place "
-                      f"of FFTW; {os.cpu_count()} host CPUs"}
+                      f"{wl.key.upper()} stream; {what}; {os.cpu_count()} host CPUs"}
 
 
 # ------------------------------------------------------------------ GPU arm
