@@ -119,25 +119,80 @@ __global__ void __launch_bounds__(256) pre_prefix_tri_kernel(const __grid_consta
   const int w = ss.s[k].w, h = ss.s[k].h;
   const uint8_t* m = v.mask + (size_t)y * v.mpitch;
   uint16_t* o = pref + (size_t)r * pitch;
+  const uint16_t* dy = v.depth + (size_t)y * v.dpitch;
+  const bool has_next = y + 1 < h;
+  const uint8_t* m1 = v.mask + (size_t)(has_next ? y + 1 : y) * v.mpitch;
+  const uint16_t* d1 = v.depth + (size_t)(has_next ? y + 1 : y) * v.dpitch;
   int carry = 0;
   for (int x0 = 0; x0 < w; x0 += 512) {
     const int xb = x0 + lane * 16;
-    uint8_t b[16];
+    // 16-pixel validity words: bit i = pixel xb+i.  Whole 16-pixel groups on
+    // 16-byte aligned mask rows and 32-byte aligned depth rows load as
+    // vectors (5 requests instead of 64 scalar ones).
+    uint32_t fgm = 0, val0 = 0, val1 = 0;  // mask row y; mask && depth row y; row y+1
+    const bool vec = xb + 16 <= w && ((reinterpret_cast<uintptr_t>(m + xb) | reinterpret_cast<uintptr_t>(m1 + xb)) & 15) == 0 &&
+                     ((reinterpret_cast<uintptr_t>(dy + xb) | reinterpret_cast<uintptr_t>(d1 + xb)) & 15) == 0;
+    if (vec) {
+      const uint4 mq = __ldg(reinterpret_cast<const uint4*>(m + xb));
+      const uint4 da = __ldg(reinterpret_cast<const uint4*>(dy + xb)), db = __ldg(reinterpret_cast<const uint4*>(dy + xb + 8));
+      const uint32_t mw[4] = {mq.x, mq.y, mq.z, mq.w};
+      const uint32_t dw[8] = {da.x, da.y, da.z, da.w, db.x, db.y, db.z, db.w};
 #pragma unroll
-    for (int i = 0; i < 16; ++i) b[i] = xb + i < w ? m[xb + i] : 0;
-    int run = 0;
+      for (int i = 0; i < 16; ++i) {
+        const bool mi = ((mw[i >> 2] >> (8 * (i & 3))) & 0xffu) != 0u;
+        const bool di = ((dw[i >> 1] >> (16 * (i & 1))) & 0xffffu) != 0u;
+        fgm |= (mi ? 1u : 0u) << i;
+        val0 |= (mi && di ? 1u : 0u) << i;
+      }
+      if (has_next) {
+        const uint4 mq1 = __ldg(reinterpret_cast<const uint4*>(m1 + xb));
+        const uint4 ea = __ldg(reinterpret_cast<const uint4*>(d1 + xb)), eb = __ldg(reinterpret_cast<const uint4*>(d1 + xb + 8));
+        const uint32_t nw[4] = {mq1.x, mq1.y, mq1.z, mq1.w};
+        const uint32_t ew[8] = {ea.x, ea.y, ea.z, ea.w, eb.x, eb.y, eb.z, eb.w};
 #pragma unroll
-    for (int i = 0; i < 16; ++i) run += b[i] ? 1 : 0;
+        for (int i = 0; i < 16; ++i)
+          val1 |= (((nw[i >> 2] >> (8 * (i & 3))) & 0xffu) != 0u && ((ew[i >> 1] >> (16 * (i & 1))) & 0xffffu) != 0u
+                       ? 1u : 0u) << i;
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const int x = xb + i;
+        if (x < w) {
+          const bool mi = __ldg(m + x) != 0;
+          fgm |= (mi ? 1u : 0u) << i;
+          val0 |= (mi && __ldg(dy + x) != 0 ? 1u : 0u) << i;
+          if (has_next) val1 |= (__ldg(m1 + x) != 0 && __ldg(d1 + x) != 0 ? 1u : 0u) << i;
+        }
+      }
+    }
+    if (xb + 16 < w) {  // pixel xb+16 closes this group's last quad
+      val0 |= (__ldg(m + xb + 16) != 0 && __ldg(dy + xb + 16) != 0 ? 1u : 0u) << 16;
+      if (has_next) val1 |= (__ldg(m1 + xb + 16) != 0 && __ldg(d1 + xb + 16) != 0 ? 1u : 0u) << 16;
+    }
+    const int run = __popc(fgm);
     int inc = run;
     for (int d = 1; d < 32; d <<= 1) {
       const int t = __shfl_up_sync(0xffffffffu, inc, d);
       if (lane >= d) inc += t;
     }
     int acc = carry + inc - run;
+    if (xb + 16 <= w && (reinterpret_cast<uintptr_t>(o + xb) & 15) == 0) {  // 16 prefix values as two 16 B stores
+      uint32_t pw[8];
 #pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      acc += b[i] ? 1 : 0;
-      if (xb + i < w) o[xb + i] = (uint16_t)acc;
+      for (int i = 0; i < 16; i += 2) {
+        const uint32_t a = (uint32_t)(acc + __popc(fgm & ((2u << i) - 1u)));
+        const uint32_t b2 = (uint32_t)(acc + __popc(fgm & ((4u << i) - 1u)));
+        pw[i >> 1] = (a & 0xffffu) | (b2 << 16);
+      }
+      reinterpret_cast<uint4*>(o + xb)[0] = make_uint4(pw[0], pw[1], pw[2], pw[3]);
+      reinterpret_cast<uint4*>(o + xb)[1] = make_uint4(pw[4], pw[5], pw[6], pw[7]);
+    } else {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        acc += (fgm >> i) & 1u;
+        if (xb + i < w) o[xb + i] = (uint16_t)acc;
+      }
     }
     carry += __shfl_sync(0xffffffffu, inc, 31);
     {  // 32-pixel segments (lane pairs): no foreground -> no point: zero its
@@ -167,18 +222,9 @@ __global__ void __launch_bounds__(256) pre_prefix_tri_kernel(const __grid_consta
       base = __shfl_sync(0xffffffffu, base, 0);
       if (lead && fg != 0) act[1 + base + __popc(ball & ((1u << lane) - 1u))] = r * spr + sx;
     }
-    if (y + 1 >= h) continue;  // no quads below the last row
+    if (!has_next) continue;  // no quads below the last row
     // pixels xb .. xb+16 valid in rows y, y+1 -> quads xb+i (i < 16) with a valid corner
-    uint32_t any = 0;
-#pragma unroll
-    for (int i = 0; i <= 16; ++i) {
-      const int x = xb + i;
-      if (x < w) {
-        const bool a0 = (i < 16 ? b[i] : __ldg(m + x)) != 0 && __ldg(v.depth + (size_t)y * v.dpitch + x) != 0;
-        const bool a1 = valid_px(v, w, h, x, y + 1);
-        any |= (a0 || a1 ? 1u : 0u) << i;
-      }
-    }
+    const uint32_t any = val0 | val1;
     uint32_t am = (any | (any >> 1)) & 0xffffu;
     const int lim = w - 1 - xb;  // quads xb+i need xb+i+1 < w
     am &= lim >= 16 ? 0xffffu : (lim <= 0 ? 0u : (1u << lim) - 1u);
