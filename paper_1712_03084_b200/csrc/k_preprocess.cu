@@ -255,6 +255,18 @@ __device__ __forceinline__ d3 ld_tri(const double* tri, int64_t q, int t, bool u
   return {__ldg(n), __ldg(n + 1), __ldg(n + 2)};
 }
 
+// both triangle normals of quad q (the record is 48 B, 16 B aligned) as three vector loads
+__device__ __forceinline__ void ld_quad(const double* tri, int64_t q, bool use, d3& a, d3& b) {
+  if (!use) {
+    a = b = {__longlong_as_double(0x7ff8000000000000ll), 0.0, 0.0};
+    return;
+  }
+  const double2* r = reinterpret_cast<const double2*>(tri + 6 * q);
+  const double2 u = __ldg(r), v = __ldg(r + 1), w2 = __ldg(r + 2);
+  a = {u.x, u.y, v.x};
+  b = {v.y, w2.x, w2.y};
+}
+
 struct Staged {  // one point (per-pixel staging slot)
   double pos[3], nrm[3], w;
   int32_t pad;
@@ -282,11 +294,11 @@ __device__ __forceinline__ void points_segment(const SensorSet& ss, int sil_r, c
     // cloud.cpp:53-71: six incident triangles in the reference's order
     // Q(x-1,y-1).T2, Q(x,y-1).T1, Q(x,y-1).T2, Q(x-1,y).T1, Q(x-1,y).T2, Q(x,y).T1
     // all six triangle records are loaded up front (one round trip)
+    // quads (x, y-1) and (x-1, y) hold both triangles: one 48 B record each, three 16 B loads
     const d3 t0 = ld_tri(tri, pix - w - 1, 1, x >= 1 && y >= 1);
-    const d3 t1 = ld_tri(tri, pix - w, 0, x <= w - 2 && y >= 1);
-    const d3 t2 = ld_tri(tri, pix - w, 1, x <= w - 2 && y >= 1);
-    const d3 t3 = ld_tri(tri, pix - 1, 0, x >= 1 && y <= h - 2);
-    const d3 t4 = ld_tri(tri, pix - 1, 1, x >= 1 && y <= h - 2);
+    d3 t1, t2, t3, t4;
+    ld_quad(tri, pix - w, x <= w - 2 && y >= 1, t1, t2);
+    ld_quad(tri, pix - 1, x >= 1 && y <= h - 2, t3, t4);
     const d3 t5 = ld_tri(tri, pix, 0, x <= w - 2 && y <= h - 2);
     const uint16_t dc = __ldg(v.depth + (size_t)y * v.dpitch + x);
     d3 sum{0.0, 0.0, 0.0};
