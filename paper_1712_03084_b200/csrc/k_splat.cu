@@ -89,12 +89,15 @@ __device__ __forceinline__ void red_add_v4(float4* addr, float4 v) {
                : "memory");
 }
 
-// splat.cpp:58-87 weighted mode: 64 threads (two warps) per point, one per support voxel
-// floor(c)-1 .. floor(c)+2 per axis (support_around, splat.cpp:19-29).  Each
-// 64-thread group walks a contiguous run of points (neighbouring pixels, so
-// mostly the same voxel rows): a row's chunk bits are or-ed in only when they
-// add to what this lane marked for the previous point, which removes most of
-// the row-mask atomics; the reduction is issued before the marking.
+// splat.cpp:58-87 weighted mode: one warp per point, two support voxels per
+// lane (the 4x4x4 support floor(c)-1 .. floor(c)+2 per axis, support_around,
+// splat.cpp:19-29: lane = (ox, oy, oz) with oz and oz + 2), so the per-point
+// work — the next point's loads, the three fp64 to_voxel divisions (lanes 0-2,
+// bit-exact) and their shuffles — is done once per 64 voxel updates.  Each warp
+// walks a contiguous run of points (neighbouring pixels, so mostly the same
+// voxel rows): a row's chunk bits are or-ed in only when they add to what this
+// lane marked for the previous point, which removes most of the row-mask
+// atomics; the reductions are issued before the marking.
 __global__ void __launch_bounds__(kSplatThreads) splat_weighted_kernel(const double* __restrict__ pos,
                                                                        const double* __restrict__ nrm,
                                                                        const double* __restrict__ wgt,
@@ -105,17 +108,16 @@ __global__ void __launch_bounds__(kSplatThreads) splat_weighted_kernel(const dou
   const int P = ctl->P;
   if (ctl->status != 0) return;
   const DevGrid g = ctl->grid;
-  const int sub = threadIdx.x & 63;
-  const int ox = sub & 3, oy = (sub >> 2) & 3, oz = sub >> 4;
+  const int lane = threadIdx.x & 31;
+  const int ox = lane & 3, oy = (lane >> 2) & 3, oz = lane >> 4;  // second voxel: oz + 2
   // exp(-s/0.75) = exp2(s * k1), exp(-s/1.125) = exp2(s * k2)
   const float k1 = -1.4426950408889634f / 0.75f, k2 = -1.4426950408889634f / 1.125f;
-  const int groups = gridDim.x * (kSplatThreads / 64);
+  const int groups = gridDim.x * (kSplatThreads / 32);
   const int run = (P + groups - 1) / groups;
-  const int p0 = (blockIdx.x * (kSplatThreads / 64) + (threadIdx.x >> 6)) * run;
+  const int p0 = (blockIdx.x * (kSplatThreads / 32) + (threadIdx.x >> 5)) * run;
   const int p1 = min(P, p0 + run);
-  int last_row = -1;
-  uint32_t last_m = 0u;
-  const int lane = threadIdx.x & 31;
+  int last_row[2] = {-1, -1};
+  uint32_t last_m[2] = {0u, 0u};
   const double o = lane == 0 ? g.origin[0] : (lane == 1 ? g.origin[1] : g.origin[2]);
   // the next point's inputs are loaded while the current one is scattered
   auto load = [&](int q, double& pc, float4& nw) {
@@ -136,23 +138,35 @@ __global__ void __launch_bounds__(kSplatThreads) splat_weighted_kernel(const dou
     const double cx = __shfl_sync(0xffffffffu, c, 0), cy = __shfl_sync(0xffffffffu, c, 1),
                  cz = __shfl_sync(0xffffffffu, c, 2);
     const int fx = (int)floor(cx);
-    const int x = fx - 1 + ox, y = (int)floor(cy) - 1 + oy, z = (int)floor(cz) - 1 + oz;
-    // z-slab [zoff, zoff+nzl) of this rank (the reference's own slab split, splat.cpp:61-77)
-    const int zl = z - zoff;
-    if (x >= 0 && y >= 0 && zl >= 0 && x < g.nx && y < g.ny && zl < nzl && z < g.nz) {
-      const float dx = (float)(cx - (double)x), dy = (float)(cy - (double)y), dz = (float)(cz - (double)z);
-      const float s = dx * dx + dy * dy + dz * dz;
-      const float g1w = exp2f(s * k1) * nw.w, g2w = exp2f(s * k2) * nw.w;
-      red_add_v4(acc + ((size_t)zl * g.ny + y) * g.nx + x, make_float4(g1w * nw.x, g1w * nw.y, g1w * nw.z, g2w));
+    const int x = fx - 1 + ox, y = (int)floor(cy) - 1 + oy;
+    const float dx = (float)(cx - (double)x), dy = (float)(cy - (double)y);
+    const float sxy = dx * dx + dy * dy;
+    const bool inxy = x >= 0 && y >= 0 && x < g.nx && y < g.ny;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int z = (int)floor(cz) - 1 + oz + 2 * h;
+      // z-slab [zoff, zoff+nzl) of this rank (the reference's own slab split, splat.cpp:61-77)
+      const int zl = z - zoff;
+      if (inxy && zl >= 0 && zl < nzl && z < g.nz) {
+        const float dz = (float)(cz - (double)z);
+        const float s = sxy + dz * dz;
+        const float g1w = exp2f(s * k1) * nw.w, g2w = exp2f(s * k2) * nw.w;
+        red_add_v4(acc + ((size_t)zl * g.ny + y) * g.nx + x, make_float4(g1w * nw.x, g1w * nw.y, g1w * nw.z, g2w));
+      }
     }
-    if (ox == 0 && y >= 0 && zl >= 0 && y < g.ny && zl < nzl && z < g.nz && fx + 2 >= 0 && fx - 1 < g.nx) {
-      const int row = zl * g.ny + y;
-      const int xa = max(fx - 1, 0), xb = min(fx + 2, g.nx - 1);
-      const uint32_t m = (0xffffffffu >> (31 - (xb >> 5))) & (0xffffffffu << (xa >> 5));
-      if (row != last_row || (m & ~last_m) != 0u) {
-        atomicOr(rowbits + row, m);
-        last_m = row == last_row ? (last_m | m) : m;
-        last_row = row;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int z = (int)floor(cz) - 1 + oz + 2 * h;
+      const int zl = z - zoff;
+      if (ox == 0 && y >= 0 && zl >= 0 && y < g.ny && zl < nzl && z < g.nz && fx + 2 >= 0 && fx - 1 < g.nx) {
+        const int row = zl * g.ny + y;
+        const int xa = max(fx - 1, 0), xb = min(fx + 2, g.nx - 1);
+        const uint32_t m = (0xffffffffu >> (31 - (xb >> 5))) & (0xffffffffu << (xa >> 5));
+        if (row != last_row[h] || (m & ~last_m[h]) != 0u) {
+          atomicOr(rowbits + row, m);
+          last_m[h] = row == last_row[h] ? (last_m[h] | m) : m;
+          last_row[h] = row;
+        }
       }
     }
   }
