@@ -7,12 +7,14 @@
 //
 //   mc_rows     per voxel row (y,z): can it hold a cut edge or cell?  (row
 //               min/max from the last FFT pass vs the level) -> ordered list
-//   mc_count    one warp per active row, 8 voxels per lane: owned cut edges
+//   mc_count    one warp per active row: 8 voxels per lane tested for a level
+//               crossing from vector row loads, then one voxel per lane over the
+//               row's straddling 32-voxel chunks only: owned cut edges
 //               (+x,+y,+z, sign test vals >= level in fp64, :168-171) and the
 //               cell's triangle count from the generated table; caches each
-//               voxel's (mask, case)
+//               voxel's (mask, case) and the row's chunk mask
 //   mc_scan     single-CTA exclusive scan of the per-row totals
-//   mc_emit     one warp per active row; vertex ids = rank of the cut edge in
+//   mc_emit     one warp per active row, its straddling chunks; vertex ids = rank of the cut edge in
 //               global edge id order ((z*ny+y)*nx+x)*3+axis (:139-142); fp64
 //               positions (:153-155, volume.hpp:45); compact list of cells
 //   mc_normals  one thread per vertex: gradient normals (:180-207)
@@ -270,29 +272,6 @@ __device__ __forceinline__ void load_rows(const float* A, int nx, int ny, int nz
   }
 }
 
-// classify() on the lane's registers: voxel x0 + j
-__device__ __forceinline__ VoxelInfo classify_regs(const RowVals& r, int j, int x, int nx, bool hy, bool hz, float Lf) {
-  VoxelInfo o{0, -1};
-  if (x >= nx) return o;
-  const bool hx = x + 1 < nx;
-  const bool a0 = r.v[0][j] >= Lf;
-  const bool a1 = hx && r.v[0][j + 1] >= Lf;
-  const bool a2 = hy && r.v[1][j] >= Lf;
-  const bool a4 = hz && r.v[2][j] >= Lf;
-  if (hx && a1 != a0) o.mask |= 1;
-  if (hy && a2 != a0) o.mask |= 2;
-  if (hz && a4 != a0) o.mask |= 4;
-  if (hx && hy && hz) {
-    int cfg = (a0 ? 1 : 0) | (a1 ? 2 : 0) | (a2 ? 4 : 0) | (a4 ? 16 : 0);
-    cfg |= (r.v[1][j + 1] >= Lf) << 3;
-    cfg |= (r.v[2][j + 1] >= Lf) << 5;
-    cfg |= (r.v[3][j] >= Lf) << 6;
-    cfg |= (r.v[3][j + 1] >= Lf) << 7;
-    o.cfg = cfg;
-  }
-  return o;
-}
-
 __device__ __forceinline__ int3 warp_sum3(int3 v) {
   for (int o = 16; o > 0; o >>= 1)
     v.x += __shfl_xor_sync(0xffffffffu, v.x, o), v.y += __shfl_xor_sync(0xffffffffu, v.y, o),
@@ -300,8 +279,42 @@ __device__ __forceinline__ int3 warp_sum3(int3 v) {
   return v;
 }
 
+// The cell / cut-edge sets of voxel x at unit (y, z): the four rows' values at
+// x and x+1 (q = 0: (y,z), 1: (y+1,z), 2: (y,z+1), 3: (y+1,z+1)).
+__device__ __forceinline__ VoxelInfo classify_voxel(const float* A, int nx, int ny, int x, int y, int z, bool hy,
+                                                    bool hz, float Lf) {
+  VoxelInfo o{0, -1};
+  if (x >= nx) return o;
+  const bool hx = x + 1 < nx;
+  const float* r0 = A + ((size_t)z * ny + y) * nx + x;
+  const float* r1 = r0 + nx;
+  const float* r2 = r0 + (size_t)nx * ny;
+  const float* r3 = r2 + nx;
+  const bool a0 = __ldg(r0) >= Lf;
+  const bool a1 = hx && __ldg(r0 + 1) >= Lf;
+  const bool a2 = hy && __ldg(r1) >= Lf;
+  const bool a4 = hz && __ldg(r2) >= Lf;
+  if (hx && a1 != a0) o.mask |= 1;
+  if (hy && a2 != a0) o.mask |= 2;
+  if (hz && a4 != a0) o.mask |= 4;
+  if (hx && hy && hz) {
+    int cfg = (a0 ? 1 : 0) | (a1 ? 2 : 0) | (a2 ? 4 : 0) | (a4 ? 16 : 0);
+    cfg |= (__ldg(r1 + 1) >= Lf) << 3;
+    cfg |= (__ldg(r2 + 1) >= Lf) << 5;
+    cfg |= (__ldg(r3) >= Lf) << 6;
+    cfg |= (__ldg(r3 + 1) >= Lf) << 7;
+    o.cfg = cfg;
+  }
+  return o;
+}
+
 // per active unit: (owned cut edges, triangles, non-trivial cells) + the
-// per-voxel (mask, case) cache the emit pass reads
+// per-voxel (mask, case) cache the emit pass reads.  Pass 1: each lane loads
+// the values its 8 voxels' cells touch (vector loads) and tests whether they
+// straddle the level; a 32-voxel chunk with no straddling lane group holds no
+// cut edge and no cell (every one of its voxels classifies to nothing).  Pass 2:
+// one voxel per lane over the straddling chunks only (typically 1-2 of a row's
+// chunks), whose cache entries and chunk mask the emit pass reuses.
 __global__ void __launch_bounds__(256) mc_count_kernel(const float* __restrict__ A, DevCtl* ctl, int nx, int ny,
                                                        int nz, McSlab sl, const int32_t* __restrict__ units,
                                                        int3* unitcnt, MeshBufs mb) {
@@ -315,32 +328,48 @@ __global__ void __launch_bounds__(256) mc_count_kernel(const float* __restrict__
     const int y = u % ny, z = sl.z0 + u / ny;
     const bool own = z < sl.zend;
     const bool hy = y + 1 < ny, hz = z + 1 < nz;
-    int3 c = make_int3(0, 0, 0);
+    uint32_t cmask = 0;
     for (int p0 = 0; p0 < nx; p0 += 32 * kVpl) {
       const int x0 = p0 + lane * kVpl;
       RowVals r;
       load_rows(A, nx, ny, nz, y, z, x0, r);
-      uint16_t info[kVpl];
+      bool above = false, below = false;
 #pragma unroll
-      for (int j = 0; j < kVpl; ++j) {
-        const VoxelInfo vi = classify_regs(r, j, x0 + j, nx, hy, hz, Lf);
-        const int nt = vi.cfg >= 0 && own ? c_mc_count[vi.cfg] : 0;
-        c.x += __popc(vi.mask), c.y += nt, c.z += nt > 0 ? 1 : 0;
-        info[j] = (uint16_t)(vi.mask | (nt > 0 ? (vi.cfg << 3) | (1 << 11) : 0));
+      for (int j = 0; j <= kVpl; ++j) {
+        if (x0 + j >= nx) continue;
+        const bool h0 = r.v[0][j] >= Lf;
+        above |= h0, below |= !h0;
+        if (hy) {
+          const bool h = r.v[1][j] >= Lf;
+          above |= h, below |= !h;
+        }
+        if (hz) {
+          const bool h = r.v[2][j] >= Lf;
+          above |= h, below |= !h;
+        }
+        if (hy && hz) {
+          const bool h = r.v[3][j] >= Lf;
+          above |= h, below |= !h;
+        }
       }
-      uint16_t* dst = mb.vinfo + (size_t)i * nx + x0;
-      if (x0 + kVpl <= nx) {
-        uint4 w;
-        w.x = info[0] | (uint32_t)info[1] << 16, w.y = info[2] | (uint32_t)info[3] << 16;
-        w.z = info[4] | (uint32_t)info[5] << 16, w.w = info[6] | (uint32_t)info[7] << 16;
-        *reinterpret_cast<uint4*>(dst) = w;
-      } else {
-        for (int j = 0; j < kVpl && x0 + j < nx; ++j) dst[j] = info[j];
-      }
+      const uint32_t b = __ballot_sync(0xffffffffu, above && below);
+      uint32_t c8 = 0;  // chunk k of this pass = lanes 4k .. 4k+3
+#pragma unroll
+      for (int k = 0; k < 8; ++k) c8 |= ((b >> (4 * k)) & 0xfu) ? 1u << k : 0u;
+      cmask |= c8 << (p0 >> 5);
+    }
+    int3 c = make_int3(0, 0, 0);
+    for (uint32_t mm = cmask; mm; mm &= mm - 1) {
+      const int x = ((__ffs(mm) - 1) << 5) + lane;
+      const VoxelInfo vi = classify_voxel(A, nx, ny, x, y, z, hy, hz, Lf);
+      const int nt = vi.cfg >= 0 && own ? c_mc_count[vi.cfg] : 0;
+      c.x += __popc(vi.mask), c.y += nt, c.z += nt > 0 ? 1 : 0;
+      if (x < nx) mb.vinfo[(size_t)i * nx + x] = (uint16_t)(vi.mask | (nt > 0 ? (vi.cfg << 3) | (1 << 11) : 0));
     }
     const int3 t = warp_sum3(c);
     if (lane == 0) {
       unitcnt[i] = t;
+      mb.ucmask[i] = cmask;
       if (!own) atomicAdd(&ctl->v_extra, t.x);
     }
   }
@@ -432,66 +461,48 @@ __global__ void __launch_bounds__(256, 4) mc_emit_kernel(const float* __restrict
     const bool own = z < sl.zend;  // else: only number the next rank's edges
     const size_t row0 = ((size_t)z * ny + y) * nx;
     int3 carry = unitoff[i];
-    for (int p0 = 0; p0 < nx; p0 += 32 * kVpl) {
-      const int x0 = p0 + lane * kVpl;
-      uint16_t info[kVpl];
-      const uint16_t* src = mb.vinfo + (size_t)i * nx + x0;
-      if (x0 + kVpl <= nx) {
-        const uint4 w = *reinterpret_cast<const uint4*>(src);
-        info[0] = w.x & 0xffff, info[1] = w.x >> 16, info[2] = w.y & 0xffff, info[3] = w.y >> 16;
-        info[4] = w.z & 0xffff, info[5] = w.z >> 16, info[6] = w.w & 0xffff, info[7] = w.w >> 16;
-      } else {
-#pragma unroll
-        for (int j = 0; j < kVpl; ++j) info[j] = x0 + j < nx ? src[j] : 0;
-      }
-      int3 cnt = make_int3(0, 0, 0);
-#pragma unroll
-      for (int j = 0; j < kVpl; ++j) {
-        const int nt = (info[j] >> 11) & 1 ? c_mc_count[(info[j] >> 3) & 255] : 0;
-        cnt.x += __popc(info[j] & 7), cnt.y += nt, cnt.z += nt > 0 ? 1 : 0;
-      }
+    // the unit's straddling 32-voxel chunks in x order, one voxel per lane
+    for (uint32_t mm = mb.ucmask[i]; mm; mm &= mm - 1) {
+      const int x = ((__ffs(mm) - 1) << 5) + lane;
+      const uint16_t info = x < nx ? mb.vinfo[(size_t)i * nx + x] : (uint16_t)0;
+      const int mask = info & 7;
+      const bool cell = (info >> 11) & 1;
+      const int cfg = (info >> 3) & 255;
+      const int nt = cell ? c_mc_count[cfg] : 0;
+      const int3 cnt = make_int3(__popc(mask), nt, cell ? 1 : 0);
       int3 inc = cnt;  // warp inclusive scan
       for (int o = 1; o < 32; o <<= 1) {
         const int a = __shfl_up_sync(0xffffffffu, inc.x, o), b = __shfl_up_sync(0xffffffffu, inc.y, o),
                   c = __shfl_up_sync(0xffffffffu, inc.z, o);
         if (lane >= o) inc.x += a, inc.y += b, inc.z += c;
       }
-      int vb = carry.x + inc.x - cnt.x, tb = carry.y + inc.y - cnt.y, cb = carry.z + inc.z - cnt.z;
+      const int vb = carry.x + inc.x - cnt.x, tb = carry.y + inc.y - cnt.y, cb = carry.z + inc.z - cnt.z;
       carry.x += __shfl_sync(0xffffffffu, inc.x, 31), carry.y += __shfl_sync(0xffffffffu, inc.y, 31),
           carry.z += __shfl_sync(0xffffffffu, inc.z, 31);
-      for (int j = 0; j < kVpl; ++j) {
-        const int mask = info[j] & 7;
-        const bool cell = (info[j] >> 11) & 1;
-        if (!mask && !cell) continue;
-        const int x = x0 + j;
-        const size_t v = row0 + x;
-        if (mask) {
-          mb.vbase[v] = ((uint32_t)vb << 3) | (uint32_t)mask;
-          if (own) {
-            const double v0 = (double)__ldg(A + v);
-            int id = vb;
-            for (int a = 0; a < 3; ++a) {
-              if (!(mask & (1 << a))) continue;
-              const double v1 = (double)__ldg(A + v + step[a]);
-              double t = ddiv(dsub(L, v0), dsub(v1, v0));
-              t = t < 1e-6 ? 1e-6 : (t > 1.0 - 1e-6 ? 1.0 - 1e-6 : t);
-              double p[3] = {(double)x, (double)y, (double)z};
-              p[a] = dadd(p[a], t);
-              for (int c = 0; c < 3; ++c) mb.pos[3 * (size_t)id + c] = dadd(g.origin[c], dmul(g.edge, p[c]));
-              mb.edge_id[id] = (uint64_t)v * 3 + a;
-              ++id;
-            }
+      if (!mask && !cell) continue;
+      const size_t v = row0 + x;
+      if (mask) {
+        mb.vbase[v] = ((uint32_t)vb << 3) | (uint32_t)mask;
+        if (own) {
+          const double v0 = (double)__ldg(A + v);
+          int id = vb;
+          for (int a = 0; a < 3; ++a) {
+            if (!(mask & (1 << a))) continue;
+            const double v1 = (double)__ldg(A + v + step[a]);
+            double t = ddiv(dsub(L, v0), dsub(v1, v0));
+            t = t < 1e-6 ? 1e-6 : (t > 1.0 - 1e-6 ? 1.0 - 1e-6 : t);
+            double p[3] = {(double)x, (double)y, (double)z};
+            p[a] = dadd(p[a], t);
+            for (int cc = 0; cc < 3; ++cc) mb.pos[3 * (size_t)id + cc] = dadd(g.origin[cc], dmul(g.edge, p[cc]));
+            mb.edge_id[id] = (uint64_t)v * 3 + a;
+            ++id;
           }
-          vb += __popc(mask);
         }
-        if (cell) {
-          const int cfg = (info[j] >> 3) & 255;
-          mb.cells[cb] = (int32_t)v;
-          mb.cell_tri[cb] = tb;
-          mb.cell_cfg[cb] = (uint8_t)cfg;
-          tb += c_mc_count[cfg];
-          ++cb;
-        }
+      }
+      if (cell) {
+        mb.cells[cb] = (int32_t)v;
+        mb.cell_tri[cb] = tb;
+        mb.cell_cfg[cb] = (uint8_t)cfg;
       }
     }
   }

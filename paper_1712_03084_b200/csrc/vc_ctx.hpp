@@ -44,7 +44,7 @@ struct vc_ctx {
 
   // grid-dependent
   int nx = 0, ny = 0, nz = 0;
-  Buf acc, spec, A, tw, vbase, blk, rowmm, units, unitcnt, rowbits, planeflag, rowlist, vinfo;
+  Buf acc, spec, A, tw, vbase, blk, rowmm, units, unitcnt, ucmask, rowbits, planeflag, rowlist, vinfo;
   bool acc_dirty = true;  // accumulator contents unknown: next frame clears densely
   int layout = 0;         // what acc/rowbits/rowlist hold: 1 whole-grid frame, 2 z-slab frame
   // view staging + clouds

@@ -246,6 +246,7 @@ vc_status ensure_mc_scratch(vc_ctx* ctx, int nx, int ny, int nz) {
   VC_TRY(ensure(ctx, ctx->rowmm, rows * sizeof(float2)));
   VC_TRY(ensure(ctx, ctx->units, rows * sizeof(int32_t)));
   VC_TRY(ensure(ctx, ctx->unitcnt, rows * 3 * sizeof(int32_t)));
+  VC_TRY(ensure(ctx, ctx->ucmask, rows * sizeof(uint32_t)));
   VC_TRY(ensure(ctx, ctx->vinfo, rows * (size_t)nx * sizeof(uint16_t)));
   return VC_OK;
 }
@@ -296,6 +297,7 @@ MeshBufs mesh_bufs(vc_ctx* ctx) {
   mb.rowmm = P<float2>(ctx->rowmm);
   mb.units = P<int32_t>(ctx->units);
   mb.unitcnt = P<int32_t>(ctx->unitcnt);
+  mb.ucmask = P<uint32_t>(ctx->ucmask);
   return mb;
 }
 
@@ -527,7 +529,7 @@ vc_status vc_ctx_destroy(vc_ctx* ctx) {
   cudaSetDevice(ctx->device);
   if (ctx->st) cudaStreamSynchronize(ctx->st);
   if (ctx->gexec) cudaGraphExecDestroy(ctx->gexec);
-  for (Buf* b : {&ctx->acc, &ctx->spec, &ctx->A, &ctx->tw, &ctx->vbase, &ctx->blk, &ctx->rowmm, &ctx->units, &ctx->unitcnt, &ctx->rowbits, &ctx->planeflag, &ctx->rowlist, &ctx->vinfo, &ctx->scratch_dev, &ctx->scratch_dev2, &ctx->skel_lut, &ctx->df_scratch, &ctx->views, &ctx->pts_pos,
+  for (Buf* b : {&ctx->acc, &ctx->spec, &ctx->A, &ctx->tw, &ctx->vbase, &ctx->blk, &ctx->rowmm, &ctx->units, &ctx->unitcnt, &ctx->ucmask, &ctx->rowbits, &ctx->planeflag, &ctx->rowlist, &ctx->vinfo, &ctx->scratch_dev, &ctx->scratch_dev2, &ctx->skel_lut, &ctx->df_scratch, &ctx->views, &ctx->pts_pos,
                  &ctx->pts_nrm, &ctx->pts_w, &ctx->pts_pix, &ctx->wmaps, &ctx->pre_scratch, &ctx->iso_partial,
                  &ctx->m_pos, &ctx->m_nrm, &ctx->m_tri, &ctx->m_eid, &ctx->m_cells, &ctx->m_celltri, &ctx->m_cellcfg, &ctx->m_posf,
                  &ctx->t_vis, &ctx->t_uv, &ctx->t_w, &ctx->t_untex, &ctx->t_rgb})

@@ -92,6 +92,7 @@ struct MeshBufs {
   float2* rowmm;     // per voxel row (ny*nz): min, max of A
   int32_t* units;    // ordered active row units (ny*nz)
   int32_t* unitcnt;  // per active unit (nv, nt, nc), then exclusive offsets (3*ny*nz)
+  uint32_t* ucmask;  // per active unit: its 32-voxel x-chunks that can hold a cut edge or cell
 };
 
 // Stage-timing events.  Profiled frames are launched directly (never from a
