@@ -36,6 +36,9 @@ struct vc_ctx {
   int device = 0;
   cudaStream_t st = nullptr;
   cudaStream_t aux = nullptr;        // side stream: branches of the frame graph
+  cudaStream_t cst = nullptr;        // copy stream: the views' RGB, staged while the frame computes
+  cudaEvent_t rgb_ev = nullptr;      // recorded once the views' RGB is staged (the texture stage waits on it)
+  bool rgb_async = false;            // stage_views: RGB on cst (vc_reconstruct_frame only)
   cudaEvent_t fork[2] = {}, join[2] = {};
   std::string err;
   int out_kind = VC_MEM_HOST;

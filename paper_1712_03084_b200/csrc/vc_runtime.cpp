@@ -129,14 +129,26 @@ vc_status stage_views(vc_ctx* ctx, const vc_sensor* sensors, const vc_view* view
                  (!need_rgb || v.rgb == h0 + off[3 * i + 2]) && (!v.depth_pitch || v.depth_pitch == w * 2) &&
                  (!v.mask_pitch || v.mask_pitch == w) && (!v.rgb_pitch || v.rgb_pitch == rw * 3);
   }
+  // RGB is first read by the texture stage at the end of the frame: with
+  // rgb_async it is staged on the copy stream while the frame computes (the
+  // texture stage waits on rgb_ev); depth and mask go first, on the frame stream.
+  const bool split_rgb = ctx->rgb_async && need_rgb;
   if (contiguous) {
-    const size_t last = need_rgb ? off[3 * k - 1] + (size_t)sensors[k - 1].rgb_intr.width *
-                                                         sensors[k - 1].rgb_intr.height * 3
-                                 : off[3 * k - 2] + (size_t)sensors[k - 1].depth_intr.width *
-                                                        sensors[k - 1].depth_intr.height;
-    VC_CUDA(cudaMemcpyAsync(base, h0, last,
-                            views[0].mem_kind == VC_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
-                            ctx->st));
+    const cudaMemcpyKind kind0 = views[0].mem_kind == VC_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    if (split_rgb) {
+      for (int i = 0; i < k; ++i) {
+        const size_t n = (size_t)sensors[i].depth_intr.width * sensors[i].depth_intr.height;
+        VC_CUDA(cudaMemcpyAsync(base + off[3 * i], h0 + off[3 * i], off[3 * i + 1] - off[3 * i] + n, kind0, ctx->st));
+        VC_CUDA(cudaMemcpyAsync(base + off[3 * i + 2], h0 + off[3 * i + 2],
+                                (size_t)sensors[i].rgb_intr.width * sensors[i].rgb_intr.height * 3, kind0, ctx->cst));
+      }
+    } else {
+      const size_t last = need_rgb ? off[3 * k - 1] + (size_t)sensors[k - 1].rgb_intr.width *
+                                                           sensors[k - 1].rgb_intr.height * 3
+                                   : off[3 * k - 2] + (size_t)sensors[k - 1].depth_intr.width *
+                                                          sensors[k - 1].depth_intr.height;
+      VC_CUDA(cudaMemcpyAsync(base, h0, last, kind0, ctx->st));
+    }
   }
   for (int i = 0; i < k; ++i) {
     const int w = sensors[i].depth_intr.width, h = sensors[i].depth_intr.height;
@@ -158,13 +170,14 @@ vc_status stage_views(vc_ctx* ctx, const vc_sensor* sensors, const vc_view* view
     }
     if (v.rgb && need_rgb && !contiguous)
       VC_CUDA(cudaMemcpy2DAsync(base + off[3 * i + 2], (size_t)rw * 3, v.rgb, v.rgb_pitch ? v.rgb_pitch : (size_t)rw * 3,
-                                (size_t)rw * 3, rh, kind, ctx->st));
+                                (size_t)rw * 3, rh, kind, split_rgb ? ctx->cst : ctx->st));
     ViewPtrs& vp = ctx->ss.v[i];
     vp.depth = reinterpret_cast<const uint16_t*>(base + off[3 * i]);
     vp.mask = base + off[3 * i + 1];
     vp.rgb = (v.rgb && need_rgb) ? base + off[3 * i + 2] : nullptr;
     vp.dpitch = w, vp.mpitch = w, vp.rpitch = rw * 3;
   }
+  VC_CUDA(cudaEventRecord(ctx->rgb_ev, split_rgb ? ctx->cst : ctx->st));
   if (ctx->df_erode > 0 || (depth_filter_radius(ctx->df_sigma_px) > 0 && ctx->df_sigma_mm > 0))
     for (int i = 0; i < k; ++i) {  // optional depth filter, in place on the staged views
       const int w = sensors[i].depth_intr.width, h = sensors[i].depth_intr.height;
@@ -353,6 +366,11 @@ int enqueue_frame(vc_ctx* ctx, const FrameCfg& f) {
                         ctx->fork[1], ctx->join[1]);
   n += 7;
   record(ctx, 5);
+  {  // the views' RGB (staged on the copy stream while the frame ran): an external event node in the graph
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(st, &cs);
+    cudaStreamWaitEvent(st, ctx->rgb_ev, cs == cudaStreamCaptureStatusActive ? cudaEventWaitExternal : 0);
+  }
   launch_texture(ctx->ss, P<float>(ctx->wmaps), P<double>(ctx->m_pos), ctx->ctl, f.eps_vis, P<uint8_t>(ctx->t_vis),
                  P<float2>(ctx->t_uv), P<float>(ctx->t_w), P<uint8_t>(ctx->t_untex), P<uint8_t>(ctx->t_rgb),
                  ctx->v_cap, st, P<float>(ctx->m_posf));
@@ -510,6 +528,8 @@ vc_status vc_ctx_create(int device, vc_ctx** out) {
   if (cudaSetDevice(device) != cudaSuccess) return cleanup(VC_ERR_CUDA);
   if (cudaStreamCreateWithFlags(&ctx->st, cudaStreamNonBlocking) != cudaSuccess) return cleanup(VC_ERR_CUDA);
   if (cudaStreamCreateWithFlags(&ctx->aux, cudaStreamNonBlocking) != cudaSuccess) return cleanup(VC_ERR_CUDA);
+  if (cudaStreamCreateWithFlags(&ctx->cst, cudaStreamNonBlocking) != cudaSuccess) return cleanup(VC_ERR_CUDA);
+  if (cudaEventCreateWithFlags(&ctx->rgb_ev, cudaEventDisableTiming) != cudaSuccess) return cleanup(VC_ERR_CUDA);
   for (int i = 0; i < 2; ++i)
     if (cudaEventCreateWithFlags(&ctx->fork[i], cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&ctx->join[i], cudaEventDisableTiming) != cudaSuccess)
@@ -538,6 +558,8 @@ vc_status vc_ctx_destroy(vc_ctx* ctx) {
                      &ctx->h_rgb, &ctx->h_pos, &ctx->h_eid})
     if (b->p) cudaFreeHost(b->p);
   if (ctx->aux) cudaStreamSynchronize(ctx->aux), cudaStreamDestroy(ctx->aux);
+  if (ctx->cst) cudaStreamSynchronize(ctx->cst), cudaStreamDestroy(ctx->cst);
+  if (ctx->rgb_ev) cudaEventDestroy(ctx->rgb_ev);
   for (int i = 0; i < 2; ++i) {
     if (ctx->fork[i]) cudaEventDestroy(ctx->fork[i]);
     if (ctx->join[i]) cudaEventDestroy(ctx->join[i]);
@@ -635,7 +657,10 @@ vc_status vc_reconstruct_frame(vc_ctx* ctx, const vc_sensor* sensors, const vc_v
   ctx->profiling = prof;
 
   if (prof) record_event(ctx->ev[8], ctx->st);
-  VC_TRY(stage_views(ctx, sensors, views, k, true));
+  ctx->rgb_async = !prof;  // profiled frames time the whole H2D as one stage
+  const vc_status sv = stage_views(ctx, sensors, views, k, true);
+  ctx->rgb_async = false;
+  VC_TRY(sv);
   if (prof) record_event(ctx->ev[9], ctx->st);
   const FrameCfg f{nx, ny, nz, config->mode, config->padding_voxels, config->silhouette_radius_px,
                    config->discontinuity_mm, config->eps_vis_mm};
