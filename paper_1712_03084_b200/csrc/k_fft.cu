@@ -13,7 +13,7 @@
 //        (integrate.cpp:46-60), inverse C2C along z -> S0           [in place]
 //   I-y  inverse C2C along y of S0                                  [in place]
 //   I-x  C2R along x (numpy irfftn / FFTW c2r semantics: Re() of bins 0 and
-//        nx/2), scale 1/N (integrate.cpp:70-72) -> A (fp32)
+//        nx/2) -> A (fp32); the 1/N scale (integrate.cpp:70-72) rides on Z's filter
 //
 // Spectra are [comp][z][y][kx] with kx pitch H = roundup4(nx/2+1) complex
 // (sector-aligned 128 B column chunks).  Every line FFT is a "four-step"
@@ -573,8 +573,8 @@ __global__ void __launch_bounds__(FCfg<NY>::THREADS, NY >= 1024 ? 1 : (NY >= 256
 // array live, three CTAs per SM).
 template <int NZ, bool NYQ>
 __device__ __forceinline__ void z_body(float2* __restrict__ S0, const float2* __restrict__ S1, int nx, int ny, int kyl,
-                                       int ky0, int H, float fx_step, float fy_step, const float2* __restrict__ tw,
-                                       const uint32_t* __restrict__ planeflag) {
+                                       int ky0, int H, float fx_step, float fy_step, float scale,
+                                       const float2* __restrict__ tw, const uint32_t* __restrict__ planeflag) {
   using S = Shape<NZ>;
   constexpr int T = S::R2, R1 = S::R1, kCW = ZCfg<NZ>::CW, TH = ZCfg<NZ>::THREADS;
   extern __shared__ float2 sh[];  // 2 tiles of NZ x kCW
@@ -629,7 +629,7 @@ __device__ __forceinline__ void z_body(float2* __restrict__ S0, const float2* __
     const float w2 = wxy + wz * wz;
     const float2 d = b0[kz * kCW + c];
     const float2 s = make_float2(d.x + wz * v[k1].x, d.y + wz * v[k1].y);
-    const float inv = (kx == 0 && ky == 0 && kz == 0) ? 0.f : __fdividef(1.0f, w2);
+    const float inv = (kx == 0 && ky == 0 && kz == 0) ? 0.f : __fdividef(scale, w2);  // 1/N of the c2r folded in
     v[k1] = make_float2(s.y * inv, -s.x * inv);  // (-i/|w|^2) * s
   }
   __syncthreads();  // everyone has read its parked D before b0 becomes the exchange
@@ -648,11 +648,12 @@ __device__ __forceinline__ void z_body(float2* __restrict__ S0, const float2* __
 template <int NZ>
 __global__ void __launch_bounds__(ZCfg<NZ>::THREADS, NZ >= 1024 ? 1 : (NZ == 256 ? 32 / VC_ZCW256 : 2))
     z_kernel(float2* __restrict__ S0, const float2* __restrict__ S1, int nx, int ny, int kyl, int ky0, int H, int nyq,
-             float fx_step, float fy_step, const float2* __restrict__ tw, const uint32_t* __restrict__ planeflag) {
+             float fx_step, float fy_step, float scale, const float2* __restrict__ tw,
+             const uint32_t* __restrict__ planeflag) {
   if (blockIdx.x == nyq)
-    z_body<NZ, true>(S0, S1, nx, ny, kyl, ky0, H, fx_step, fy_step, tw, planeflag);
+    z_body<NZ, true>(S0, S1, nx, ny, kyl, ky0, H, fx_step, fy_step, scale, tw, planeflag);
   else
-    z_body<NZ, false>(S0, S1, nx, ny, kyl, ky0, H, fx_step, fy_step, tw, planeflag);
+    z_body<NZ, false>(S0, S1, nx, ny, kyl, ky0, H, fx_step, fy_step, scale, tw, planeflag);
 }
 
 // ------------------------------------------------------------------ Z, TMA-fed, warp-private
@@ -718,8 +719,8 @@ struct Z4Cfg {
 template <int NZ>
 __global__ void __launch_bounds__(Z4Cfg<NZ>::THREADS, Z4Cfg<NZ>::MINB)
     z4_kernel(const __grid_constant__ ZMaps maps, float2* __restrict__ S0, const float2* __restrict__ S1, int nx,
-              int ny, int H, int ntx, int nnyq, float fx_step, float fy_step, const float2* __restrict__ tw,
-              const uint32_t* __restrict__ planeflag) {
+              int ny, int H, int ntx, int nnyq, float fx_step, float fy_step, float scale,
+              const float2* __restrict__ tw, const uint32_t* __restrict__ planeflag) {
   using S = Shape<NZ>;
   using CF = Z4Cfg<NZ>;
   constexpr int T = S::R2, R1 = S::R1, kCW = CF::CW, TH = CF::THREADS;
@@ -853,7 +854,7 @@ __global__ void __launch_bounds__(Z4Cfg<NZ>::THREADS, Z4Cfg<NZ>::MINB)
       const float wz = signed_freq<NZ>(kz);
       const float w2 = wxy + wz * wz;
       const float2 s2 = make_float2(d[k1].x + wz * v[k1].x, d[k1].y + wz * v[k1].y);
-      const float inv = (kx == 0 && kyr == 0 && kz == 0) ? 0.f : __fdividef(1.0f, w2);
+      const float inv = (kx == 0 && kyr == 0 && kz == 0) ? 0.f : __fdividef(scale, w2);  // 1/N of the c2r folded in
       d[k1] = make_float2(s2.y * inv, -s2.x * inv);  // (-i/|w|^2) * s
     }
     relayout_for_inverse<NZ>(d);
@@ -933,7 +934,7 @@ struct IXCfg {
 
 template <int NX>
 __global__ void __launch_bounds__(IXCfg<NX>::THREADS, 2) ix_kernel(const float2* __restrict__ S0, float* __restrict__ A,
-                                                       int rows, int H, float scale,
+                                                       int rows, int H,
                                                        const float2* __restrict__ tw, float2* __restrict__ rowmm) {
   using S = Shape<NX>;
   using CF = IXCfg<NX>;
@@ -988,7 +989,7 @@ __global__ void __launch_bounds__(IXCfg<NX>::THREADS, 2) ix_kernel(const float2*
 #pragma unroll
     for (int k1 = 0; k1 < R1; ++k1) {
       const int k = t + T * k1;
-      const float a0 = v[k1].x * scale, a1 = v[k1].y * scale;
+      const float a0 = v[k1].x, a1 = v[k1].y;  // 1/N applied by the Z pass's filter
       lo0 = fminf(lo0, a0), hi0 = fmaxf(hi0, a0), lo1 = fminf(lo1, a1), hi1 = fmaxf(hi1, a1);
       st_out(A + (size_t)l0 * NX + k, a0);
       st_out(A + (size_t)l1 * NX + k, a1);
@@ -1097,8 +1098,9 @@ struct RunZ {
     col_grid(a.nx, C::CW, &tiles, &nyq, 1);
     dim3 grid(tiles, a.kyl);
     const float fxs = (float)(2.0 * M_PI / a.nx), fys = (float)(2.0 * M_PI / a.ny);
+    const float scale = (float)(1.0 / ((double)a.nx * a.ny * a.nz));  // the c2r's 1/N (integrate.cpp:70-72)
     z_kernel<N><<<grid, C::THREADS, 2 * C::SMEM, a.st>>>(a.R0, a.R1, a.nx, a.ny, a.kyl, a.ky0, a.H, nyq, fxs, fys,
-                                                         a.twz, a.planeflag);
+                                                         scale, a.twz, a.planeflag);
   }
 };
 // VC_ZK=4 selects the TMA-fed warp-private Z kernel (opt-in: at 256^3 it
@@ -1153,7 +1155,8 @@ struct RunZ4 {
     const int cap = sm_count() * C::MINB;
     const float fxs = (float)(2.0 * M_PI / a.nx), fys = (float)(2.0 * M_PI / a.ny);
     z4_kernel<N><<<tiles < cap ? tiles : cap, C::THREADS, C::SMEM, a.st>>>(
-        zm, a.S0, a.S1, a.nx, a.ny, a.H, ntx, nnyq, fxs, fys, a.twz, a.planeflag);
+        zm, a.S0, a.S1, a.nx, a.ny, a.H, ntx, nnyq, fxs, fys, (float)(1.0 / ((double)a.nx * a.ny * a.nz)), a.twz,
+        a.planeflag);
   }
 };
 template <int N>
@@ -1173,8 +1176,7 @@ struct RunIx {
     const int rows = a.ny * a.nzl;
     const int need = (rows / 2 + C::TEAMS - 1) / C::TEAMS;
     const int grid = need < sm_count() * 4 ? need : sm_count() * 4;  // persistent teams
-    const float scale = (float)(1.0 / ((double)a.nx * a.ny * a.nz));
-    ix_kernel<N><<<grid, C::THREADS, C::SMEM, a.st>>>(a.Rout, a.A, rows, a.H, scale, a.twx, a.rowmm);
+    ix_kernel<N><<<grid, C::THREADS, C::SMEM, a.st>>>(a.Rout, a.A, rows, a.H, a.twx, a.rowmm);
   }
 };
 
