@@ -5,15 +5,17 @@
 // classify / scan / emit, with no host round trip (counts live in DevCtl;
 // capacity overflow sets a flag the host checks once per frame).
 //
-//   mc_rows     per voxel row (y,z): can it hold a cut edge or cell?  (row
+//   mc_select   per voxel row (y,z): can it hold a cut edge or cell?  (row
 //               min/max from the last FFT pass vs the level) -> ordered list
+//               in one pass (decoupled look-back over 256-unit tiles)
 //   mc_count    one warp per active row: 8 voxels per lane tested for a level
 //               crossing from vector row loads, then one voxel per lane over the
 //               row's straddling 32-voxel chunks only: owned cut edges
 //               (+x,+y,+z, sign test vals >= level in fp64, :168-171) and the
 //               cell's triangle count from the generated table; caches each
 //               voxel's (mask, case) and the row's chunk mask
-//   mc_scan     single-CTA exclusive scan of the per-row totals
+//   mc_scan     exclusive scan of the per-row totals, one pass over 1024-unit
+//               tiles with decoupled look-back
 //   mc_emit     one warp per active row, its straddling chunks; vertex ids = rank of the cut edge in
 //               global edge id order ((z*ny+y)*nx+x)*3+axis (:139-142); fp64
 //               positions (:153-155, volume.hpp:45); compact list of cells
@@ -188,11 +190,33 @@ __global__ void row_minmax_kernel(const float* __restrict__ A, int nx, int rows,
 
 constexpr int kRowThreads = 256;
 
-__global__ void __launch_bounds__(kRowThreads) mc_rows_kernel(const float2* __restrict__ rowmm, const DevCtl* ctl,
-                                                              int ny, int nz, McSlab sl, uint32_t* rowmask) {
-  const int u = blockIdx.x * kRowThreads + threadIdx.x;
+// Ordered list of the active units in one pass (single-pass scan with
+// decoupled look-back): tiles of 256 units take ids from a counter (so every
+// tile a tile waits on has started), test their units against the level
+// (row min/max of the 2x2 rows from the C2R pass), publish their active count,
+// and take the count of all earlier tiles from the published descriptors —
+// warp 0 reads 32 predecessors per step and stops at the first one whose
+// inclusive prefix is known.  Each tile then writes its units in raster order.
+// Descriptor: bits 62-63 status (1 aggregate, 2 inclusive prefix), low 32 the count.
+__device__ __forceinline__ unsigned long long ld_volatile_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.volatile.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__global__ void __launch_bounds__(kRowThreads) mc_select_kernel(const float2* __restrict__ rowmm, DevCtl* ctl, int ny,
+                                                                int nz, McSlab sl, unsigned long long* desc,
+                                                                int* tile_counter, int32_t* units) {
+  __shared__ int tile_s, wsum[kRowThreads / 32], base_s;
+  const int U = ny * sl.nzu;
+  const int ntiles = (U + kRowThreads - 1) / kRowThreads;
+  if (threadIdx.x == 0) tile_s = atomicAdd(tile_counter, 1);
+  __syncthreads();
+  const int tile = tile_s;
+  if (tile >= ntiles) return;
+  const int u = tile * kRowThreads + threadIdx.x;
   bool active = false;
-  if (u < ny * sl.nzu && ctl->status == 0) {
+  if (u < U && ctl->status == 0) {
     const double L = ctl->level;
     const int y = u % ny, z = sl.z0 + u / ny;
     float2 m = rowmm[u];
@@ -202,45 +226,47 @@ __global__ void __launch_bounds__(kRowThreads) mc_rows_kernel(const float2* __re
     if (y + 1 < ny && z + 1 < nz) m = rowmm[u + ny + 1], lo = fminf(lo, m.x), hi = fmaxf(hi, m.y);
     active = (double)hi >= L && (double)lo < L;
   }
-  const unsigned b = __ballot_sync(0xffffffffu, active);
-  if ((threadIdx.x & 31) == 0) rowmask[u >> 5] = b;
-}
-
-// single CTA: ordered list of the active units from the bit mask
-__global__ void __launch_bounds__(1024) mc_units_kernel(const uint32_t* __restrict__ rowmask, int nwords,
-                                                        int32_t* units, DevCtl* ctl) {
-  __shared__ int wsum[32];
-  const int per = (nwords + 1023) / 1024;
-  const int w0 = min(nwords, (int)threadIdx.x * per), w1 = min(nwords, w0 + per);
-  int tot = 0;
-  for (int i = w0; i < w1; ++i) tot += __popc(rowmask[i]);
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  int inc = tot;
-  for (int o = 1; o < 32; o <<= 1) {
-    const int t = __shfl_up_sync(0xffffffffu, inc, o);
-    if (lane >= o) inc += t;
-  }
-  if (lane == 31) wsum[wid] = inc;
+  const unsigned b = __ballot_sync(0xffffffffu, active);
+  if (lane == 0) wsum[wid] = __popc(b);
   __syncthreads();
   if (wid == 0) {
-    int w = wsum[lane];
-    for (int o = 1; o < 32; o <<= 1) {
-      const int t = __shfl_up_sync(0xffffffffu, w, o);
-      if (lane >= o) w += t;
+    int w = lane < kRowThreads / 32 ? wsum[lane] : 0;
+    int agg = w;
+    for (int o = 16; o > 0; o >>= 1) agg += __shfl_xor_sync(0xffffffffu, agg, o);
+    // publish the aggregate (tile 0: its inclusive prefix), then look back
+    if (lane == 0)
+      atomicExch(desc + tile, ((tile == 0 ? 2ull : 1ull) << 62) | (unsigned long long)(unsigned)agg);
+    int excl = 0;
+    for (int look = tile - 1; look >= 0; look -= 32) {
+      const int t = look - lane;
+      unsigned long long d = 2ull << 62;  // lanes before tile 0: an inclusive zero
+      if (t >= 0) {
+        do d = ld_volatile_u64(desc + t);
+        while ((d >> 62) == 0);
+      }
+      const unsigned incl = __ballot_sync(0xffffffffu, (d >> 62) == 2);
+      const int first = incl ? __ffs(incl) - 1 : 32;  // nearest predecessor with a full prefix
+      int v = lane <= first && t >= 0 ? (int)(d & 0xffffffffu) : 0;
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      excl += v;
+      if (incl) break;
     }
-    wsum[lane] = w;
+    if (lane == 0) {
+      if (tile > 0) atomicExch(desc + tile, (2ull << 62) | (unsigned long long)(unsigned)(excl + agg));
+      base_s = excl;
+      if (tile == ntiles - 1) ctl->units = excl + agg;
+    }
+    // warp-level exclusive offsets within the tile
+    int inc = w;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int q = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += q;
+    }
+    if (lane < kRowThreads / 32) wsum[lane] = inc - w;
   }
   __syncthreads();
-  int pos = (wid ? wsum[wid - 1] : 0) + inc - tot;
-  for (int i = w0; i < w1; ++i) {
-    uint32_t m = rowmask[i];
-    while (m) {
-      const int b = __ffs(m) - 1;
-      m &= m - 1;
-      units[pos++] = i * 32 + b;
-    }
-  }
-  if (threadIdx.x == 1023) ctl->units = wsum[31], ctl->v_extra = 0;
+  if (active) units[base_s + wsum[wid] + __popc(b & ((1u << lane) - 1u))] = u;
 }
 
 // One warp per active unit (voxel row), 8 consecutive voxels per lane per
@@ -375,70 +401,134 @@ __global__ void __launch_bounds__(256) mc_count_kernel(const float* __restrict__
   }
 }
 
-// Single CTA: exclusive scan of the per-unit (V, T, C) counts in chunks of
-// 4096 units (each thread 4 consecutive int3 = three 16 B loads: coalesced).
-__global__ void __launch_bounds__(1024) mc_scan_kernel(int3* blk, const DevCtl* ctl_in, DevCtl* ctl, int v_cap,
-                                                       int t_cap, int c_cap) {
-  __shared__ int3 wsum[32];
-  const int n = ctl_in->status == 0 ? ctl_in->units : 0;
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  int3 carry = make_int3(0, 0, 0);
-  for (int base = 0; base < n; base += 4096) {
-    const int i0 = base + (int)threadIdx.x * 4;
-    int3 v[4];
-    if (i0 + 4 <= n) {  // blk is 256 B aligned and i0 a multiple of 4: 48 B = three int4
-      const int4* q = reinterpret_cast<const int4*>(blk + i0);
-      const int4 a = q[0], b = q[1], c = q[2];
-      v[0] = make_int3(a.x, a.y, a.z), v[1] = make_int3(a.w, b.x, b.y);
-      v[2] = make_int3(b.z, b.w, c.x), v[3] = make_int3(c.y, c.z, c.w);
-    } else {
-#pragma unroll
-      for (int i = 0; i < 4; ++i) v[i] = i0 + i < n ? blk[i0 + i] : make_int3(0, 0, 0);
-    }
-    int3 tot = make_int3(0, 0, 0);
-#pragma unroll
-    for (int i = 0; i < 4; ++i) tot.x += v[i].x, tot.y += v[i].y, tot.z += v[i].z;
-    int3 inc = tot;
-    for (int o = 1; o < 32; o <<= 1) {
-      const int a = __shfl_up_sync(0xffffffffu, inc.x, o), b = __shfl_up_sync(0xffffffffu, inc.y, o),
-                c = __shfl_up_sync(0xffffffffu, inc.z, o);
-      if (lane >= o) inc.x += a, inc.y += b, inc.z += c;
-    }
-    if (lane == 31) wsum[wid] = inc;
-    __syncthreads();
-    if (wid == 0) {
-      int3 w = wsum[lane];
-      for (int o = 1; o < 32; o <<= 1) {
-        const int a = __shfl_up_sync(0xffffffffu, w.x, o), b = __shfl_up_sync(0xffffffffu, w.y, o),
-                  c = __shfl_up_sync(0xffffffffu, w.z, o);
-        if (lane >= o) w.x += a, w.y += b, w.z += c;
-      }
-      wsum[lane] = w;
-    }
-    __syncthreads();
-    const int3 wp = wid ? wsum[wid - 1] : make_int3(0, 0, 0);
-    int3 run = make_int3(carry.x + wp.x + inc.x - tot.x, carry.y + wp.y + inc.y - tot.y,
-                         carry.z + wp.z + inc.z - tot.z);
-    int3 o[4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) o[i] = run, run.x += v[i].x, run.y += v[i].y, run.z += v[i].z;
-    if (i0 + 4 <= n) {
-      int4* q = reinterpret_cast<int4*>(blk + i0);
-      q[0] = make_int4(o[0].x, o[0].y, o[0].z, o[1].x);
-      q[1] = make_int4(o[1].y, o[1].z, o[2].x, o[2].y);
-      q[2] = make_int4(o[2].z, o[3].x, o[3].y, o[3].z);
-    } else {
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-        if (i0 + i < n) blk[i0 + i] = o[i];
-    }
-    const int3 ct = wsum[31];
-    carry.x += ct.x, carry.y += ct.y, carry.z += ct.z;
-    __syncthreads();  // wsum is rewritten by the next chunk
+// Exclusive scan of the per-unit (V, T, C) counts in place, one pass over
+// tiles of 1024 units (256 threads x 4) with decoupled look-back: a tile
+// publishes its aggregate, sums its predecessors' published values (warp 0,
+// 32 per step, stopping at the first inclusive prefix), publishes its
+// inclusive prefix and writes its units' offsets.  Values are stored before
+// their flag with a fence between (release), read after the flag (acquire).
+// The last active tile forms V, T, C and the capacity check.
+struct ScanState {
+  int* flag;    // per tile: 0 none, 1 aggregate, 2 inclusive prefix
+  int3* agg;    // per tile
+  int3* incl;   // per tile
+  int* counter;
+};
+__device__ __forceinline__ int ld_volatile_i32(const int* p) {
+  int v;
+  asm volatile("ld.volatile.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ int3 ld_volatile_i3(const int3* p) {
+  const volatile int* q = reinterpret_cast<const volatile int*>(p);
+  return make_int3(q[0], q[1], q[2]);
+}
+__device__ __forceinline__ void st_volatile_i3(int3* p, int3 v) {
+  volatile int* q = reinterpret_cast<volatile int*>(p);
+  q[0] = v.x, q[1] = v.y, q[2] = v.z;
+}
+
+__global__ void __launch_bounds__(256) mc_scan_kernel(int3* blk, DevCtl* ctl, ScanState ss, int v_cap, int t_cap,
+                                                      int c_cap) {
+  __shared__ int tile_s;
+  __shared__ int3 wsum[8];
+  __shared__ int3 base_s;
+  const int n = ctl->status == 0 ? ctl->units : 0;
+  const int ntiles = (n + 1023) / 1024;
+  if (threadIdx.x == 0) tile_s = atomicAdd(ss.counter, 1);
+  __syncthreads();
+  const int tile = tile_s;
+  if (n == 0) {  // no unit: the totals are zero
+    if (tile == 0 && threadIdx.x == 0) ctl->V = 0, ctl->T = 0, ctl->C = 0, ctl->overflow = 0;
+    return;
   }
-  if (threadIdx.x == 0) {
-    ctl->V = carry.x - ctl->v_extra, ctl->T = carry.y, ctl->C = carry.z;
-    ctl->overflow = (carry.x > v_cap || carry.y > t_cap || carry.z > c_cap) ? 1 : 0;
+  if (tile >= ntiles) return;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int i0 = tile * 1024 + (int)threadIdx.x * 4;
+  int3 v[4];
+  if (i0 + 4 <= n) {  // blk is 256 B aligned and i0 a multiple of 4: 48 B = three int4
+    const int4* q = reinterpret_cast<const int4*>(blk + i0);
+    const int4 a = q[0], b = q[1], c = q[2];
+    v[0] = make_int3(a.x, a.y, a.z), v[1] = make_int3(a.w, b.x, b.y);
+    v[2] = make_int3(b.z, b.w, c.x), v[3] = make_int3(c.y, c.z, c.w);
+  } else {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) v[i] = i0 + i < n ? blk[i0 + i] : make_int3(0, 0, 0);
+  }
+  int3 tot = make_int3(0, 0, 0);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) tot.x += v[i].x, tot.y += v[i].y, tot.z += v[i].z;
+  int3 inc = tot;
+  for (int o = 1; o < 32; o <<= 1) {
+    const int a = __shfl_up_sync(0xffffffffu, inc.x, o), b = __shfl_up_sync(0xffffffffu, inc.y, o),
+              c = __shfl_up_sync(0xffffffffu, inc.z, o);
+    if (lane >= o) inc.x += a, inc.y += b, inc.z += c;
+  }
+  if (lane == 31) wsum[wid] = inc;
+  __syncthreads();
+  if (wid == 0) {
+    int3 w = lane < 8 ? wsum[lane] : make_int3(0, 0, 0);
+    for (int o = 1; o < 8; o <<= 1) {
+      const int a = __shfl_up_sync(0xffffffffu, w.x, o), b = __shfl_up_sync(0xffffffffu, w.y, o),
+                c = __shfl_up_sync(0xffffffffu, w.z, o);
+      if (lane >= o) w.x += a, w.y += b, w.z += c;
+    }
+    const int3 agg = make_int3(__shfl_sync(0xffffffffu, w.x, 7), __shfl_sync(0xffffffffu, w.y, 7),
+                               __shfl_sync(0xffffffffu, w.z, 7));
+    if (lane < 8) wsum[lane] = w;  // inclusive over the tile's warps
+    if (lane == 0) {
+      st_volatile_i3(tile == 0 ? ss.incl + tile : ss.agg + tile, agg);
+      __threadfence();
+      atomicExch(ss.flag + tile, tile == 0 ? 2 : 1);
+    }
+    int3 excl = make_int3(0, 0, 0);
+    for (int look = tile - 1; look >= 0; look -= 32) {
+      const int t = look - lane;
+      int f = 2;  // lanes before tile 0: an inclusive zero
+      if (t >= 0) {
+        do f = ld_volatile_i32(ss.flag + t);
+        while (f == 0);
+      }
+      __threadfence();
+      const unsigned incl = __ballot_sync(0xffffffffu, f == 2);
+      const int first = incl ? __ffs(incl) - 1 : 32;
+      int3 x = make_int3(0, 0, 0);
+      if (t >= 0 && lane <= first) x = f == 2 ? ld_volatile_i3(ss.incl + t) : ld_volatile_i3(ss.agg + t);
+      for (int o = 16; o > 0; o >>= 1)
+        x.x += __shfl_xor_sync(0xffffffffu, x.x, o), x.y += __shfl_xor_sync(0xffffffffu, x.y, o),
+            x.z += __shfl_xor_sync(0xffffffffu, x.z, o);
+      excl.x += x.x, excl.y += x.y, excl.z += x.z;
+      if (incl) break;
+    }
+    if (lane == 0) {
+      const int3 total = make_int3(excl.x + agg.x, excl.y + agg.y, excl.z + agg.z);
+      if (tile > 0) {
+        st_volatile_i3(ss.incl + tile, total);
+        __threadfence();
+        atomicExch(ss.flag + tile, 2);
+      }
+      base_s = excl;
+      if (tile == ntiles - 1) {
+        ctl->V = total.x - ctl->v_extra, ctl->T = total.y, ctl->C = total.z;
+        ctl->overflow = (total.x > v_cap || total.y > t_cap || total.z > c_cap) ? 1 : 0;
+      }
+    }
+  }
+  __syncthreads();
+  const int3 wp = wid ? wsum[wid - 1] : make_int3(0, 0, 0);
+  int3 run = make_int3(base_s.x + wp.x + inc.x - tot.x, base_s.y + wp.y + inc.y - tot.y, base_s.z + wp.z + inc.z - tot.z);
+  int3 o[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) o[i] = run, run.x += v[i].x, run.y += v[i].y, run.z += v[i].z;
+  if (i0 + 4 <= n) {
+    int4* q = reinterpret_cast<int4*>(blk + i0);
+    q[0] = make_int4(o[0].x, o[0].y, o[0].z, o[1].x);
+    q[1] = make_int4(o[1].y, o[1].z, o[2].x, o[2].y);
+    q[2] = make_int4(o[2].z, o[3].x, o[3].y, o[3].z);
+  } else {
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      if (i0 + i < n) blk[i0 + i] = o[i];
   }
 }
 
@@ -645,12 +735,22 @@ void launch_marching_cubes_count(const float* A, DevCtl* ctl, MeshBufs mb, int n
                                  cudaStream_t st) {
   const int units = ny * sl.nzu;
   const int nblk = (units + kRowThreads - 1) / kRowThreads;
-  uint32_t* rowmask = reinterpret_cast<uint32_t*>(mb.blk);  // ceil(units/32) words
+  // look-back descriptors (one u64 per tile) and the tile counter, reset ahead of the pass
+  unsigned long long* desc = reinterpret_cast<unsigned long long*>(mb.blk);
+  int* tile_counter = reinterpret_cast<int*>(desc + nblk);
+  // the count scan's look-back state: flags, aggregates, inclusive prefixes, counter
+  const int stiles = (units + 1023) / 1024;
+  ScanState ss;
+  ss.flag = tile_counter + 4;
+  ss.agg = reinterpret_cast<int3*>(ss.flag + stiles);
+  ss.incl = ss.agg + stiles;
+  ss.counter = reinterpret_cast<int*>(ss.incl + stiles);
   int3* ucnt = reinterpret_cast<int3*>(mb.unitcnt);
-  mc_rows_kernel<<<nblk, kRowThreads, 0, st>>>(mb.rowmm, ctl, ny, nz, sl, rowmask);
-  mc_units_kernel<<<1, 1024, 0, st>>>(rowmask, (units + 31) / 32, mb.units, ctl);
+  cudaMemsetAsync(desc, 0, (size_t)nblk * 8 + 16 + (size_t)stiles * 28 + 16, st);
+  cudaMemsetAsync(&ctl->v_extra, 0, sizeof(int32_t), st);
+  mc_select_kernel<<<nblk, kRowThreads, 0, st>>>(mb.rowmm, ctl, ny, nz, sl, desc, tile_counter, mb.units);
   mc_count_kernel<<<sm_count() * 8, 256, 0, st>>>(A, ctl, nx, ny, nz, sl, mb.units, ucnt, mb);
-  mc_scan_kernel<<<1, 1024, 0, st>>>(ucnt, ctl, ctl, mb.v_cap, mb.t_cap, mb.c_cap);
+  mc_scan_kernel<<<stiles, 256, 0, st>>>(ucnt, ctl, ss, mb.v_cap, mb.t_cap, mb.c_cap);
 }
 
 void launch_marching_cubes_emit(const float* A, DevCtl* ctl, MeshBufs mb, int nx, int ny, int nz, McSlab sl,
