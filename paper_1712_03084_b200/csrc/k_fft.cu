@@ -700,6 +700,14 @@ __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, i
       : "memory");
 }
 
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+
 template <int NZ>
 struct Z4Cfg {
   static constexpr int CW = 16;                   // columns per tile: 128 B stage rows
@@ -915,6 +923,47 @@ __global__ void __launch_bounds__(ICfg<NY>::THREADS, NY >= 1024 ? 2 : 3)
     iy_body<NY, false>(Rin, Rout, nxh, H, lk, tw);
 }
 
+// I-y on one GPU (plain [z][ky][H] layout): the column tile arrives through
+// the tensor-memory accelerator — one elected thread issues the 2-D boxes
+// ({CW complex, 256 rows} on a {2H floats, nz*ny rows} view of the spectrum)
+// against an mbarrier, instead of every thread computing cp.async addresses.
+// The packed Nyquist tiles keep the gather (iy_body<NY, true>).
+template <int NY>
+__global__ void __launch_bounds__(ICfg<NY>::THREADS, NY >= 1024 ? 2 : 3)
+    iy_tma_kernel(const __grid_constant__ CUtensorMap map, const float2* Rin, float2* Rout, int nxh, int H, int lk,
+                  int nyq, const float2* __restrict__ tw) {
+  if (blockIdx.x == nyq) {
+    iy_body<NY, true>(Rin, Rout, nxh, H, lk, tw);
+    return;
+  }
+  using S = Shape<NY>;
+  constexpr int T = S::R2, R1 = S::R1, kCW = ICfg<NY>::CW;
+  constexpr int BOXR = NY < 256 ? NY : 256;  // rows per box (box dims <= 256)
+  extern __shared__ float2 sh[];             // the tile (dynamic base: 1 KB aligned), then the mbarrier
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sh + NY * kCW);
+  const int c = threadIdx.x % kCW, t = threadIdx.x / kCW;
+  const int zl = blockIdx.y, kx0 = blockIdx.x * kCW, kx = kx0 + c;
+  if (threadIdx.x == 0) {
+    mbar_init(bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    mbar_expect_tx(bar, (uint32_t)(NY * kCW * 8));
+#pragma unroll
+    for (int b = 0; b < NY / BOXR; ++b) tma_load_2d(sh + b * BOXR * kCW, &map, 2 * kx0, zl * NY + b * BOXR, bar);
+  }
+  __syncthreads();  // the barrier is initialised before anyone waits on it
+  mbar_wait(bar, 0);
+  float2 v[R1];
+  tile_to_regs<NY, kCW>(sh, c, t, v);
+  __syncthreads();
+  ExCols<NY, kCW> ex{sh, c};
+  fft_line<NY, true>(v, t, tw, ex);
+  if (kx < nxh) {
+    const size_t plane = (size_t)zl * NY * H;
+#pragma unroll
+    for (int k1 = 0; k1 < R1; ++k1) st_out(Rout + plane + (size_t)(t + T * k1) * H + kx, v[k1]);
+  }
+}
+
 // ------------------------------------------------------------------ I-x
 // Persistent teams: each team (T adjacent lanes) walks line pairs with a
 // double-buffered cp.async stage of the next pair's half spectra, so the
@@ -1044,6 +1093,7 @@ struct Prep {
     } else if (axis == 1) {
       allow_smem(fy_kernel<N>, 3 * FCfg<N>::SMEM);
       allow_smem(iy_kernel<N>, ICfg<N>::SMEM);
+      allow_smem(iy_tma_kernel<N>, ICfg<N>::SMEM + 64);
     } else {
       allow_smem(z_kernel<N>, 2 * ZCfg<N>::SMEM);
       if constexpr (N == 64 || N == 128 || N == 256) allow_smem(z4_kernel<N>, Z4Cfg<N>::SMEM);
@@ -1141,6 +1191,18 @@ bool encode_zmaps(ZMaps* zm, const float2* S0, int H, int ny, int nz, size_t cs)
   }
   return true;
 }
+// 2-D view {2H floats, rows} of a spectrum component, boxes {2*cw floats, boxr rows}
+bool encode_iy_map(CUtensorMap* m, const float2* base, int H, size_t rows, int cw, int boxr) {
+  auto enc = tmap_encoder();
+  if (!enc) return false;
+  const cuuint64_t dims[2] = {(cuuint64_t)2 * H, (cuuint64_t)rows};
+  const cuuint64_t strides[1] = {(cuuint64_t)H * 8};
+  const cuuint32_t box[2] = {(cuuint32_t)(2 * cw), (cuuint32_t)boxr};
+  const cuuint32_t estr[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float2*>(base), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
 template <int N>
 struct RunZ4 {
   static void run(const SlabFft& a, const ZMaps& zm) {
@@ -1159,6 +1221,14 @@ struct RunZ4 {
         a.planeflag);
   }
 };
+bool encode_iy_map(CUtensorMap* m, const float2* base, int H, size_t rows, int cw, int boxr);
+inline bool iy_tma_on() {  // VC_IY_TMA=0: cp.async staging (A/B switch)
+  static const bool on = [] {
+    const char* e = std::getenv("VC_IY_TMA");
+    return !e || std::atoi(e) != 0;
+  }();
+  return on;
+}
 template <int N>
 struct RunIy {
   static void run(const SlabFft& a) {
@@ -1166,6 +1236,14 @@ struct RunIy {
     int tiles, nyq;
     col_grid(a.nx, C::CW, &tiles, &nyq, 2);
     dim3 grid(tiles, a.nzl);
+    CUtensorMap map;
+    // one GPU, plain layout (rows (z, ky) at stride H): the tile as tensor-map boxes
+    if (iy_tma_on() && a.kyl == a.ny && a.Rin == a.Rout && N >= 8 &&
+        encode_iy_map(&map, a.Rin, a.H, (size_t)a.nzl * a.ny, C::CW, N < 256 ? N : 256)) {
+      iy_tma_kernel<N><<<grid, C::THREADS, C::SMEM + 64, a.st>>>(map, a.Rin, a.Rout, a.nx / 2 + 1, a.H,
+                                                                ilog2(a.kyl), nyq, a.twy);
+      return;
+    }
     iy_kernel<N><<<grid, C::THREADS, C::SMEM, a.st>>>(a.Rin, a.Rout, a.nx / 2 + 1, a.H, ilog2(a.kyl), nyq, a.twy);
   }
 };
