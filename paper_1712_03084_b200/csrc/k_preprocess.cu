@@ -109,6 +109,8 @@ __global__ void __launch_bounds__(256) pre_prefix_tri_kernel(const __grid_consta
                                                              int32_t* __restrict__ act,
                                                              int32_t* __restrict__ rowcnt) {
   __shared__ uint16_t qlist[8][512];
+  __shared__ __align__(128) uint8_t rstage[8][3072];  // per warp: mask y, y+1 (512 B each), depth y, y+1 (1 KB each)
+  __shared__ __align__(8) uint64_t rbar[8];
   if (blockIdx.x == 0 && threadIdx.x < 6) ctl->bbox_key[threadIdx.x] = threadIdx.x < 3 ? ~0ull : 0ull;
   const int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31, wid = (threadIdx.x >> 5) & 7;
   if (r >= rows) return;  // whole warps
@@ -123,6 +125,48 @@ __global__ void __launch_bounds__(256) pre_prefix_tri_kernel(const __grid_consta
   const bool has_next = y + 1 < h;
   const uint8_t* m1 = v.mask + (size_t)(has_next ? y + 1 : y) * v.mpitch;
   const uint16_t* d1 = v.depth + (size_t)(has_next ? y + 1 : y) * v.dpitch;
+  // Rows of up to 512 pixels with 16-byte aligned starts are staged into shared
+  // memory by the tensor-memory accelerator (bulk copies of the four rows the
+  // warp reads, one mbarrier per warp); the loads below then come from there.
+  const bool bulk = w <= 512 && (w & 15) == 0 &&
+                    ((reinterpret_cast<uintptr_t>(m) | reinterpret_cast<uintptr_t>(m1) |
+                      reinterpret_cast<uintptr_t>(dy) | reinterpret_cast<uintptr_t>(d1)) & 15) == 0;
+  if (bulk) {
+    uint8_t* st = rstage[wid];
+    if (lane == 0) {
+      const uint32_t b = (uint32_t)__cvta_generic_to_shared(&rbar[wid]);
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b) : "memory");
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      const uint32_t bytes = (uint32_t)(3 * w) * (has_next ? 2u : 1u);
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes) : "memory");
+      auto copy = [&](uint8_t* dst, const void* src, uint32_t n) {
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                (uint32_t)__cvta_generic_to_shared(dst)),
+            "l"(src), "r"(n), "r"(b)
+            : "memory");
+      };
+      copy(st, m, (uint32_t)w);
+      copy(st + 1024, dy, (uint32_t)(2 * w));
+      if (has_next) {
+        copy(st + 512, m1, (uint32_t)w);
+        copy(st + 2048, d1, (uint32_t)(2 * w));
+      }
+    }
+    __syncwarp();
+    asm volatile(
+        "{\n .reg .pred p;\n RW_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n @!p bra RW_%=;\n}" ::"r"(
+            (uint32_t)__cvta_generic_to_shared(&rbar[wid]))
+        : "memory");
+    m = st, dy = reinterpret_cast<const uint16_t*>(st + 1024);
+    m1 = has_next ? st + 512 : st, d1 = reinterpret_cast<const uint16_t*>(has_next ? st + 2048 : st + 1024);
+  }
+  // row element loads: shared memory when staged, else the read-only global path
+  auto ld16 = [&](const void* p) {
+    return bulk ? *reinterpret_cast<const uint4*>(p) : __ldg(reinterpret_cast<const uint4*>(p));
+  };
+  auto ldm = [&](const uint8_t* p) -> uint8_t { return bulk ? *p : __ldg(p); };
+  auto ldd = [&](const uint16_t* p) -> uint16_t { return bulk ? *p : __ldg(p); };
   int carry = 0;
   for (int x0 = 0; x0 < w; x0 += 512) {
     const int xb = x0 + lane * 16;
@@ -133,8 +177,8 @@ __global__ void __launch_bounds__(256) pre_prefix_tri_kernel(const __grid_consta
     const bool vec = xb + 16 <= w && ((reinterpret_cast<uintptr_t>(m + xb) | reinterpret_cast<uintptr_t>(m1 + xb)) & 15) == 0 &&
                      ((reinterpret_cast<uintptr_t>(dy + xb) | reinterpret_cast<uintptr_t>(d1 + xb)) & 15) == 0;
     if (vec) {
-      const uint4 mq = __ldg(reinterpret_cast<const uint4*>(m + xb));
-      const uint4 da = __ldg(reinterpret_cast<const uint4*>(dy + xb)), db = __ldg(reinterpret_cast<const uint4*>(dy + xb + 8));
+      const uint4 mq = ld16(m + xb);
+      const uint4 da = ld16(dy + xb), db = ld16(dy + xb + 8);
       const uint32_t mw[4] = {mq.x, mq.y, mq.z, mq.w};
       const uint32_t dw[8] = {da.x, da.y, da.z, da.w, db.x, db.y, db.z, db.w};
 #pragma unroll
@@ -145,8 +189,8 @@ __global__ void __launch_bounds__(256) pre_prefix_tri_kernel(const __grid_consta
         val0 |= (mi && di ? 1u : 0u) << i;
       }
       if (has_next) {
-        const uint4 mq1 = __ldg(reinterpret_cast<const uint4*>(m1 + xb));
-        const uint4 ea = __ldg(reinterpret_cast<const uint4*>(d1 + xb)), eb = __ldg(reinterpret_cast<const uint4*>(d1 + xb + 8));
+        const uint4 mq1 = ld16(m1 + xb);
+        const uint4 ea = ld16(d1 + xb), eb = ld16(d1 + xb + 8);
         const uint32_t nw[4] = {mq1.x, mq1.y, mq1.z, mq1.w};
         const uint32_t ew[8] = {ea.x, ea.y, ea.z, ea.w, eb.x, eb.y, eb.z, eb.w};
 #pragma unroll
@@ -159,16 +203,16 @@ __global__ void __launch_bounds__(256) pre_prefix_tri_kernel(const __grid_consta
       for (int i = 0; i < 16; ++i) {
         const int x = xb + i;
         if (x < w) {
-          const bool mi = __ldg(m + x) != 0;
+          const bool mi = ldm(m + x) != 0;
           fgm |= (mi ? 1u : 0u) << i;
-          val0 |= (mi && __ldg(dy + x) != 0 ? 1u : 0u) << i;
-          if (has_next) val1 |= (__ldg(m1 + x) != 0 && __ldg(d1 + x) != 0 ? 1u : 0u) << i;
+          val0 |= (mi && ldd(dy + x) != 0 ? 1u : 0u) << i;
+          if (has_next) val1 |= (ldm(m1 + x) != 0 && ldd(d1 + x) != 0 ? 1u : 0u) << i;
         }
       }
     }
     if (xb + 16 < w) {  // pixel xb+16 closes this group's last quad
-      val0 |= (__ldg(m + xb + 16) != 0 && __ldg(dy + xb + 16) != 0 ? 1u : 0u) << 16;
-      if (has_next) val1 |= (__ldg(m1 + xb + 16) != 0 && __ldg(d1 + xb + 16) != 0 ? 1u : 0u) << 16;
+      val0 |= (ldm(m + xb + 16) != 0 && ldd(dy + xb + 16) != 0 ? 1u : 0u) << 16;
+      if (has_next) val1 |= (ldm(m1 + xb + 16) != 0 && ldd(d1 + xb + 16) != 0 ? 1u : 0u) << 16;
     }
     const int run = __popc(fgm);
     int inc = run;
