@@ -206,8 +206,12 @@ __device__ __forceinline__ unsigned long long ld_volatile_u64(const unsigned lon
 
 __global__ void __launch_bounds__(kRowThreads) mc_select_kernel(const float2* __restrict__ rowmm, DevCtl* ctl, int ny,
                                                                 int nz, McSlab sl, unsigned long long* desc,
-                                                                int* tile_counter, int32_t* units) {
+                                                                int* tile_counter, int32_t* units, int* zero,
+                                                                int nzero) {
   __shared__ int tile_s, wsum[kRowThreads / 32], base_s;
+  // the next pass's look-back flags and ticket counter (it starts after this grid ends)
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < nzero; j += gridDim.x * blockDim.x) zero[j] = 0;
+  if (blockIdx.x == 0 && threadIdx.x == 0) ctl->v_extra = 0;
   const int U = ny * sl.nzu;
   const int ntiles = (U + kRowThreads - 1) / kRowThreads;
   if (threadIdx.x == 0) tile_s = atomicAdd(tile_counter, 1);
@@ -274,6 +278,8 @@ __global__ void __launch_bounds__(kRowThreads) mc_select_kernel(const float2* __
 // voxels touch (two float4 + one scalar per row) and classifies all 8 from
 // registers; no block-wide barrier anywhere.
 constexpr int kVpl = 8;
+constexpr int kFuseUnits = 8;   // units per scan/emit tile
+constexpr int kCntBlock = 256;  // units per count block sum (bsum)
 
 struct RowVals {
   float v[4][kVpl + 1];  // rows (y,z), (y+1,z), (y,z+1), (y+1,z+1); x0 .. x0+8
@@ -341,62 +347,91 @@ __device__ __forceinline__ VoxelInfo classify_voxel(const float* A, int nx, int 
 // cut edge and no cell (every one of its voxels classifies to nothing).  Pass 2:
 // one voxel per lane over the straddling chunks only (typically 1-2 of a row's
 // chunks), whose cache entries and chunk mask the emit pass reuses.
+// One unit's counts; `info` = the unit's nx cache entries (global or shared).
+__device__ __forceinline__ int3 count_unit(const float* __restrict__ A, int nx, int ny, int nz, int y, int z, bool own,
+                                           float Lf, int lane, uint16_t* info, uint32_t& cmask_out) {
+  const bool hy = y + 1 < ny, hz = z + 1 < nz;
+  uint32_t cmask = 0;
+  for (int p0 = 0; p0 < nx; p0 += 32 * kVpl) {
+    const int x0 = p0 + lane * kVpl;
+    RowVals r;
+    load_rows(A, nx, ny, nz, y, z, x0, r);
+    bool above = false, below = false;
+#pragma unroll
+    for (int j = 0; j <= kVpl; ++j) {
+      if (x0 + j >= nx) continue;
+      const bool h0 = r.v[0][j] >= Lf;
+      above |= h0, below |= !h0;
+      if (hy) {
+        const bool h = r.v[1][j] >= Lf;
+        above |= h, below |= !h;
+      }
+      if (hz) {
+        const bool h = r.v[2][j] >= Lf;
+        above |= h, below |= !h;
+      }
+      if (hy && hz) {
+        const bool h = r.v[3][j] >= Lf;
+        above |= h, below |= !h;
+      }
+    }
+    const uint32_t b = __ballot_sync(0xffffffffu, above && below);
+    uint32_t c8 = 0;  // chunk k of this pass = lanes 4k .. 4k+3
+#pragma unroll
+    for (int k = 0; k < 8; ++k) c8 |= ((b >> (4 * k)) & 0xfu) ? 1u << k : 0u;
+    cmask |= c8 << (p0 >> 5);
+  }
+  int3 c = make_int3(0, 0, 0);
+  for (uint32_t mm = cmask; mm; mm &= mm - 1) {
+    const int x = ((__ffs(mm) - 1) << 5) + lane;
+    const VoxelInfo vi = classify_voxel(A, nx, ny, x, y, z, hy, hz, Lf);
+    const int nt = vi.cfg >= 0 && own ? c_mc_count[vi.cfg] : 0;
+    c.x += __popc(vi.mask), c.y += nt, c.z += nt > 0 ? 1 : 0;
+    if (x < nx) info[x] = (uint16_t)(vi.mask | (nt > 0 ? (vi.cfg << 3) | (1 << 11) : 0));
+  }
+  cmask_out = cmask;
+  return warp_sum3(c);
+}
+
+// CTA iteration k covers the 8 consecutive units 8 (blockIdx.x + k gridDim.x)
+// + warp, all in one kCntBlock block: their sum goes to the block's bsum entry
+// with one atomic triple per CTA iteration.
 __global__ void __launch_bounds__(256) mc_count_kernel(const float* __restrict__ A, DevCtl* ctl, int nx, int ny,
                                                        int nz, McSlab sl, const int32_t* __restrict__ units,
-                                                       int3* unitcnt, MeshBufs mb) {
+                                                       int3* unitcnt, int3* bsum, MeshBufs mb) {
+  static_assert(kCntBlock % 8 == 0, "a CTA iteration's units share one block");
+  __shared__ int3 part[8];
   if (ctl->status != 0) return;
   const int U = ctl->units;
   const float Lf = __double2float_ru(ctl->level);
-  const int lane = threadIdx.x & 31;
-  const int warps = gridDim.x * (blockDim.x >> 5);
-  for (int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i < U; i += warps) {
-    const int u = units[i];
-    const int y = u % ny, z = sl.z0 + u / ny;
-    const bool own = z < sl.zend;
-    const bool hy = y + 1 < ny, hz = z + 1 < nz;
-    uint32_t cmask = 0;
-    for (int p0 = 0; p0 < nx; p0 += 32 * kVpl) {
-      const int x0 = p0 + lane * kVpl;
-      RowVals r;
-      load_rows(A, nx, ny, nz, y, z, x0, r);
-      bool above = false, below = false;
-#pragma unroll
-      for (int j = 0; j <= kVpl; ++j) {
-        if (x0 + j >= nx) continue;
-        const bool h0 = r.v[0][j] >= Lf;
-        above |= h0, below |= !h0;
-        if (hy) {
-          const bool h = r.v[1][j] >= Lf;
-          above |= h, below |= !h;
-        }
-        if (hz) {
-          const bool h = r.v[2][j] >= Lf;
-          above |= h, below |= !h;
-        }
-        if (hy && hz) {
-          const bool h = r.v[3][j] >= Lf;
-          above |= h, below |= !h;
-        }
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int i0 = blockIdx.x * 8; i0 < U; i0 += gridDim.x * 8) {
+    const int i = i0 + wid;
+    int3 t = make_int3(0, 0, 0);
+    if (i < U) {
+      const int u = units[i];
+      const int y = u % ny, z = sl.z0 + u / ny;
+      const bool own = z < sl.zend;
+      uint32_t cmask;
+      t = count_unit(A, nx, ny, nz, y, z, own, Lf, lane, mb.vinfo + (size_t)i * nx, cmask);
+      if (lane == 0) {
+        unitcnt[i] = t;
+        mb.ucmask[i] = cmask;
+        if (!own) atomicAdd(&ctl->v_extra, t.x);
       }
-      const uint32_t b = __ballot_sync(0xffffffffu, above && below);
-      uint32_t c8 = 0;  // chunk k of this pass = lanes 4k .. 4k+3
-#pragma unroll
-      for (int k = 0; k < 8; ++k) c8 |= ((b >> (4 * k)) & 0xfu) ? 1u << k : 0u;
-      cmask |= c8 << (p0 >> 5);
     }
-    int3 c = make_int3(0, 0, 0);
-    for (uint32_t mm = cmask; mm; mm &= mm - 1) {
-      const int x = ((__ffs(mm) - 1) << 5) + lane;
-      const VoxelInfo vi = classify_voxel(A, nx, ny, x, y, z, hy, hz, Lf);
-      const int nt = vi.cfg >= 0 && own ? c_mc_count[vi.cfg] : 0;
-      c.x += __popc(vi.mask), c.y += nt, c.z += nt > 0 ? 1 : 0;
-      if (x < nx) mb.vinfo[(size_t)i * nx + x] = (uint16_t)(vi.mask | (nt > 0 ? (vi.cfg << 3) | (1 << 11) : 0));
-    }
-    const int3 t = warp_sum3(c);
-    if (lane == 0) {
-      unitcnt[i] = t;
-      mb.ucmask[i] = cmask;
-      if (!own) atomicAdd(&ctl->v_extra, t.x);
+    if (bsum) {
+      if (lane == 0) part[wid] = t;
+      __syncthreads();
+      if (wid == 0) {
+        int3 q = lane < 8 ? part[lane] : make_int3(0, 0, 0);
+        q = warp_sum3(q);
+        int3* d = bsum + i0 / kCntBlock;
+        if (lane == 0 && q.x) atomicAdd(&d->x, q.x);
+        if (lane == 1 && q.y) atomicAdd(&d->y, q.y);
+        if (lane == 2 && q.z) atomicAdd(&d->z, q.z);
+      }
+      __syncthreads();
     }
   }
 }
@@ -426,6 +461,43 @@ __device__ __forceinline__ int3 ld_volatile_i3(const int3* p) {
 __device__ __forceinline__ void st_volatile_i3(int3* p, int3 v) {
   volatile int* q = reinterpret_cast<volatile int*>(p);
   q[0] = v.x, q[1] = v.y, q[2] = v.z;
+}
+
+// Warp-wide (all 32 lanes): publish tile `tile`'s aggregate, sum the
+// predecessors' published values (32 per step, stopping at the first
+// inclusive prefix), publish the tile's inclusive prefix; returns the
+// exclusive prefix.
+__device__ __forceinline__ int3 lookback_publish(const ScanState& ss, int tile, int3 agg, int lane) {
+  if (lane == 0) {
+    st_volatile_i3(tile == 0 ? ss.incl + tile : ss.agg + tile, agg);
+    __threadfence();
+    atomicExch(ss.flag + tile, tile == 0 ? 2 : 1);
+  }
+  int3 excl = make_int3(0, 0, 0);
+  for (int look = tile - 1; look >= 0; look -= 32) {
+    const int t = look - lane;
+    int f = 2;  // lanes before tile 0: an inclusive zero
+    if (t >= 0) {
+      do f = ld_volatile_i32(ss.flag + t);
+      while (f == 0);
+    }
+    __threadfence();
+    const unsigned incl = __ballot_sync(0xffffffffu, f == 2);
+    const int first = incl ? __ffs(incl) - 1 : 32;
+    int3 x = make_int3(0, 0, 0);
+    if (t >= 0 && lane <= first) x = f == 2 ? ld_volatile_i3(ss.incl + t) : ld_volatile_i3(ss.agg + t);
+    for (int o = 16; o > 0; o >>= 1)
+      x.x += __shfl_xor_sync(0xffffffffu, x.x, o), x.y += __shfl_xor_sync(0xffffffffu, x.y, o),
+          x.z += __shfl_xor_sync(0xffffffffu, x.z, o);
+    excl.x += x.x, excl.y += x.y, excl.z += x.z;
+    if (incl) break;
+  }
+  if (lane == 0 && tile > 0) {
+    st_volatile_i3(ss.incl + tile, make_int3(excl.x + agg.x, excl.y + agg.y, excl.z + agg.z));
+    __threadfence();
+    atomicExch(ss.flag + tile, 2);
+  }
+  return excl;
 }
 
 __global__ void __launch_bounds__(256) mc_scan_kernel(int3* blk, DevCtl* ctl, ScanState ss, int v_cap, int t_cap,
@@ -476,37 +548,9 @@ __global__ void __launch_bounds__(256) mc_scan_kernel(int3* blk, DevCtl* ctl, Sc
     const int3 agg = make_int3(__shfl_sync(0xffffffffu, w.x, 7), __shfl_sync(0xffffffffu, w.y, 7),
                                __shfl_sync(0xffffffffu, w.z, 7));
     if (lane < 8) wsum[lane] = w;  // inclusive over the tile's warps
-    if (lane == 0) {
-      st_volatile_i3(tile == 0 ? ss.incl + tile : ss.agg + tile, agg);
-      __threadfence();
-      atomicExch(ss.flag + tile, tile == 0 ? 2 : 1);
-    }
-    int3 excl = make_int3(0, 0, 0);
-    for (int look = tile - 1; look >= 0; look -= 32) {
-      const int t = look - lane;
-      int f = 2;  // lanes before tile 0: an inclusive zero
-      if (t >= 0) {
-        do f = ld_volatile_i32(ss.flag + t);
-        while (f == 0);
-      }
-      __threadfence();
-      const unsigned incl = __ballot_sync(0xffffffffu, f == 2);
-      const int first = incl ? __ffs(incl) - 1 : 32;
-      int3 x = make_int3(0, 0, 0);
-      if (t >= 0 && lane <= first) x = f == 2 ? ld_volatile_i3(ss.incl + t) : ld_volatile_i3(ss.agg + t);
-      for (int o = 16; o > 0; o >>= 1)
-        x.x += __shfl_xor_sync(0xffffffffu, x.x, o), x.y += __shfl_xor_sync(0xffffffffu, x.y, o),
-            x.z += __shfl_xor_sync(0xffffffffu, x.z, o);
-      excl.x += x.x, excl.y += x.y, excl.z += x.z;
-      if (incl) break;
-    }
+    const int3 excl = lookback_publish(ss, tile, agg, lane);
     if (lane == 0) {
       const int3 total = make_int3(excl.x + agg.x, excl.y + agg.y, excl.z + agg.z);
-      if (tile > 0) {
-        st_volatile_i3(ss.incl + tile, total);
-        __threadfence();
-        atomicExch(ss.flag + tile, 2);
-      }
       base_s = excl;
       if (tile == ntiles - 1) {
         ctl->V = total.x - ctl->v_extra, ctl->T = total.y, ctl->C = total.z;
@@ -535,66 +579,141 @@ __global__ void __launch_bounds__(256) mc_scan_kernel(int3* blk, DevCtl* ctl, Sc
 // per active unit (one warp, 8 voxels per lane per pass), in order: vertex
 // ids = rank of the cut edge in global edge id order (x ascending, then
 // axis); fp64 positions (marching_cubes.cpp:153-155, volume.hpp:45)
+// One unit's vertices, cut-edge bases and cells from its cache entries
+// `info` and straddling-chunk mask; `carry` = the unit's first (vertex,
+// triangle, cell) ids.
+__device__ __forceinline__ void emit_unit(const float* __restrict__ A, int nx, int ny, int y, int z, bool own,
+                                          double L, const DevGrid& g, int lane, const uint16_t* info, uint32_t cmask,
+                                          int3 carry, const MeshBufs& mb) {
+  const size_t step[3] = {1, (size_t)nx, (size_t)nx * ny};
+  const size_t row0 = ((size_t)z * ny + y) * nx;
+  // the unit's straddling 32-voxel chunks in x order, one voxel per lane
+  for (uint32_t mm = cmask; mm; mm &= mm - 1) {
+    const int x = ((__ffs(mm) - 1) << 5) + lane;
+    const uint16_t inf = x < nx ? info[x] : (uint16_t)0;
+    const int mask = inf & 7;
+    const bool cell = (inf >> 11) & 1;
+    const int cfg = (inf >> 3) & 255;
+    const int nt = cell ? c_mc_count[cfg] : 0;
+    const int3 cnt = make_int3(__popc(mask), nt, cell ? 1 : 0);
+    int3 inc = cnt;  // warp inclusive scan
+    for (int o = 1; o < 32; o <<= 1) {
+      const int a = __shfl_up_sync(0xffffffffu, inc.x, o), b = __shfl_up_sync(0xffffffffu, inc.y, o),
+                c = __shfl_up_sync(0xffffffffu, inc.z, o);
+      if (lane >= o) inc.x += a, inc.y += b, inc.z += c;
+    }
+    const int vb = carry.x + inc.x - cnt.x, tb = carry.y + inc.y - cnt.y, cb = carry.z + inc.z - cnt.z;
+    carry.x += __shfl_sync(0xffffffffu, inc.x, 31), carry.y += __shfl_sync(0xffffffffu, inc.y, 31),
+        carry.z += __shfl_sync(0xffffffffu, inc.z, 31);
+    if (!mask && !cell) continue;
+    const size_t v = row0 + x;
+    if (mask) {
+      mb.vbase[v] = ((uint32_t)vb << 3) | (uint32_t)mask;
+      if (own) {
+        const double v0 = (double)__ldg(A + v);
+        int id = vb;
+        for (int a = 0; a < 3; ++a) {
+          if (!(mask & (1 << a))) continue;
+          const double v1 = (double)__ldg(A + v + step[a]);
+          double t = ddiv(dsub(L, v0), dsub(v1, v0));
+          t = t < 1e-6 ? 1e-6 : (t > 1.0 - 1e-6 ? 1.0 - 1e-6 : t);
+          double p[3] = {(double)x, (double)y, (double)z};
+          p[a] = dadd(p[a], t);
+          for (int cc = 0; cc < 3; ++cc) mb.pos[3 * (size_t)id + cc] = dadd(g.origin[cc], dmul(g.edge, p[cc]));
+          mb.edge_id[id] = (uint64_t)v * 3 + a;
+          ++id;
+        }
+      }
+    }
+    if (cell) {
+      mb.cells[cb] = (int32_t)v;
+      mb.cell_tri[cb] = tb;
+      mb.cell_cfg[cb] = (uint8_t)cfg;
+    }
+  }
+}
+
 __global__ void __launch_bounds__(256, 4) mc_emit_kernel(const float* __restrict__ A, const DevCtl* ctl, int nx, int ny,
-                                                      int nz, McSlab sl, const int32_t* __restrict__ units,
-                                                      const int3* __restrict__ unitoff, MeshBufs mb) {
+                                                         int nz, McSlab sl, const int32_t* __restrict__ units,
+                                                         const int3* __restrict__ unitoff, MeshBufs mb) {
   if (ctl->status != 0 || ctl->overflow) return;
   const int U = ctl->units;
   const double L = ctl->level;
   const DevGrid g = ctl->grid;
-  const size_t step[3] = {1, (size_t)nx, (size_t)nx * ny};
   const int lane = threadIdx.x & 31;
   const int warps = gridDim.x * (blockDim.x >> 5);
   for (int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i < U; i += warps) {
     const int u = units[i];
     const int y = u % ny, z = sl.z0 + u / ny;
-    const bool own = z < sl.zend;  // else: only number the next rank's edges
-    const size_t row0 = ((size_t)z * ny + y) * nx;
-    int3 carry = unitoff[i];
-    // the unit's straddling 32-voxel chunks in x order, one voxel per lane
-    for (uint32_t mm = mb.ucmask[i]; mm; mm &= mm - 1) {
-      const int x = ((__ffs(mm) - 1) << 5) + lane;
-      const uint16_t info = x < nx ? mb.vinfo[(size_t)i * nx + x] : (uint16_t)0;
-      const int mask = info & 7;
-      const bool cell = (info >> 11) & 1;
-      const int cfg = (info >> 3) & 255;
-      const int nt = cell ? c_mc_count[cfg] : 0;
-      const int3 cnt = make_int3(__popc(mask), nt, cell ? 1 : 0);
-      int3 inc = cnt;  // warp inclusive scan
-      for (int o = 1; o < 32; o <<= 1) {
-        const int a = __shfl_up_sync(0xffffffffu, inc.x, o), b = __shfl_up_sync(0xffffffffu, inc.y, o),
-                  c = __shfl_up_sync(0xffffffffu, inc.z, o);
-        if (lane >= o) inc.x += a, inc.y += b, inc.z += c;
+    emit_unit(A, nx, ny, y, z, z < sl.zend, L, g, lane, mb.vinfo + (size_t)i * nx, mb.ucmask[i], unitoff[i], mb);
+  }
+}
+
+
+// Scan + emit in one pass over tiles of kFuseUnits counted units (one warp
+// per unit; CTAs stride over the tiles).  A tile's first (vertex, triangle, cell) ids are the counts of
+// every unit before it: the count pass also summed the units into blocks of
+// kCntBlock (bsum), so warp 0 adds the blocks before the tile's block and the
+// units of its block before the tile — no tile waits on another (a look-back
+// over ~10^3 simultaneously started tiles costs one L2 round trip per 32
+// tiles).  Reads per tile: ceil(i0 / kCntBlock) + i0 % kCntBlock entries.
+// The tile holding the last unit forms V, T, C and the overflow flag; a tile
+// whose id range passes a capacity writes nothing (the host regrows and
+// re-runs).
+__global__ void __launch_bounds__(kFuseUnits * 32, 4) mc_scan_emit_kernel(const float* __restrict__ A, DevCtl* ctl,
+                                                                          int nx, int ny,
+                                                                          const int32_t* __restrict__ units,
+                                                                          const int3* __restrict__ unitcnt,
+                                                                          const int3* __restrict__ bsum, MeshBufs mb) {
+  __shared__ int skip_s;
+  __shared__ int3 off_s[kFuseUnits];
+  const int n = ctl->status == 0 ? ctl->units : 0;
+  if (n == 0) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) ctl->V = 0, ctl->T = 0, ctl->C = 0, ctl->overflow = 0;
+    return;
+  }
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const double L = ctl->level;
+  const DevGrid g = ctl->grid;
+  for (int i0 = blockIdx.x * kFuseUnits; i0 < n; i0 += gridDim.x * kFuseUnits) {
+    const int i = i0 + wid;
+    if (wid == 0) {
+      int3 e = make_int3(0, 0, 0);
+      const int b = i0 / kCntBlock;
+      for (int j = lane; j < b; j += 32) {
+        const int3 q = bsum[j];
+        e.x += q.x, e.y += q.y, e.z += q.z;
       }
-      const int vb = carry.x + inc.x - cnt.x, tb = carry.y + inc.y - cnt.y, cb = carry.z + inc.z - cnt.z;
-      carry.x += __shfl_sync(0xffffffffu, inc.x, 31), carry.y += __shfl_sync(0xffffffffu, inc.y, 31),
-          carry.z += __shfl_sync(0xffffffffu, inc.z, 31);
-      if (!mask && !cell) continue;
-      const size_t v = row0 + x;
-      if (mask) {
-        mb.vbase[v] = ((uint32_t)vb << 3) | (uint32_t)mask;
-        if (own) {
-          const double v0 = (double)__ldg(A + v);
-          int id = vb;
-          for (int a = 0; a < 3; ++a) {
-            if (!(mask & (1 << a))) continue;
-            const double v1 = (double)__ldg(A + v + step[a]);
-            double t = ddiv(dsub(L, v0), dsub(v1, v0));
-            t = t < 1e-6 ? 1e-6 : (t > 1.0 - 1e-6 ? 1.0 - 1e-6 : t);
-            double p[3] = {(double)x, (double)y, (double)z};
-            p[a] = dadd(p[a], t);
-            for (int cc = 0; cc < 3; ++cc) mb.pos[3 * (size_t)id + cc] = dadd(g.origin[cc], dmul(g.edge, p[cc]));
-            mb.edge_id[id] = (uint64_t)v * 3 + a;
-            ++id;
-          }
-        }
+      for (int j = b * kCntBlock + lane; j < i0; j += 32) {
+        const int3 q = unitcnt[j];
+        e.x += q.x, e.y += q.y, e.z += q.z;
       }
-      if (cell) {
-        mb.cells[cb] = (int32_t)v;
-        mb.cell_tri[cb] = tb;
-        mb.cell_cfg[cb] = (uint8_t)cfg;
+      const int3 excl = warp_sum3(e);
+      const int j = i0 + lane;
+      int3 w = lane < kFuseUnits && j < n ? unitcnt[j] : make_int3(0, 0, 0);
+      const int3 own = w;
+      for (int o = 1; o < kFuseUnits; o <<= 1) {
+        const int x = __shfl_up_sync(0xffffffffu, w.x, o), y = __shfl_up_sync(0xffffffffu, w.y, o),
+                  z = __shfl_up_sync(0xffffffffu, w.z, o);
+        if (lane >= o) w.x += x, w.y += y, w.z += z;
+      }
+      const int3 end = make_int3(excl.x + __shfl_sync(0xffffffffu, w.x, kFuseUnits - 1),
+                                 excl.y + __shfl_sync(0xffffffffu, w.y, kFuseUnits - 1),
+                                 excl.z + __shfl_sync(0xffffffffu, w.z, kFuseUnits - 1));
+      const bool over = end.x > mb.v_cap || end.y > mb.t_cap || end.z > mb.c_cap;
+      if (lane < kFuseUnits)
+        off_s[lane] = make_int3(excl.x + w.x - own.x, excl.y + w.y - own.y, excl.z + w.z - own.z);
+      if (lane == 0) {
+        skip_s = over;
+        if (i0 + kFuseUnits >= n) ctl->V = end.x, ctl->T = end.y, ctl->C = end.z, ctl->overflow = over ? 1 : 0;
       }
     }
+    __syncthreads();
+    if (i < n && !skip_s) {
+      const int u = units[i];
+      emit_unit(A, nx, ny, u % ny, u / ny, true, L, g, lane, mb.vinfo + (size_t)i * nx, mb.ucmask[i], off_s[wid], mb);
+    }
+    __syncthreads();  // off_s / skip_s are rewritten by the next tile
   }
 }
 
@@ -633,52 +752,55 @@ __device__ void vertex_normal(const float* A, int nx, int ny, int nz, double px,
   }
 }
 
-// one thread per vertex: marching_cubes.cpp:178-207 normals (fp64)
-__global__ void __launch_bounds__(256) mc_normals_kernel(const float* __restrict__ A, const DevCtl* ctl, int nx,
-                                                         int ny, int nz, MeshBufs mb) {
-  if (ctl->status != 0 || ctl->overflow) return;
-  const int V = ctl->V;
-  const double L = ctl->level;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < V; i += gridDim.x * blockDim.x) {
-    const uint64_t e = mb.edge_id[i];
-    const size_t v = (size_t)(e / 3);
-    const int a = (int)(e % 3);
-    const int x = (int)(v % nx), y = (int)((v / nx) % ny), z = (int)(v / ((size_t)nx * ny));
-    const size_t step = a == 0 ? 1 : (a == 1 ? (size_t)nx : (size_t)nx * ny);
-    const double v0 = (double)__ldg(A + v), v1 = (double)__ldg(A + v + step);
-    double t = ddiv(dsub(L, v0), dsub(v1, v0));
-    t = t < 1e-6 ? 1e-6 : (t > 1.0 - 1e-6 ? 1.0 - 1e-6 : t);
-    double p[3] = {(double)x, (double)y, (double)z};
-    p[a] = dadd(p[a], t);
-    vertex_normal(A, nx, ny, nz, p[0], p[1], p[2], mb.nrm + 3 * (size_t)i);
+// marching_cubes.cpp:178-207 normal of vertex i (fp64)
+__device__ __forceinline__ void normal_of(const float* __restrict__ A, int nx, int ny, int nz, double L,
+                                          const MeshBufs& mb, int i) {
+  const uint64_t e = mb.edge_id[i];
+  const size_t v = (size_t)(e / 3);
+  const int a = (int)(e % 3);
+  const int x = (int)(v % nx), y = (int)((v / nx) % ny), z = (int)(v / ((size_t)nx * ny));
+  const size_t step = a == 0 ? 1 : (a == 1 ? (size_t)nx : (size_t)nx * ny);
+  const double v0 = (double)__ldg(A + v), v1 = (double)__ldg(A + v + step);
+  double t = ddiv(dsub(L, v0), dsub(v1, v0));
+  t = t < 1e-6 ? 1e-6 : (t > 1.0 - 1e-6 ? 1.0 - 1e-6 : t);
+  double p[3] = {(double)x, (double)y, (double)z};
+  p[a] = dadd(p[a], t);
+  vertex_normal(A, nx, ny, nz, p[0], p[1], p[2], mb.nrm + 3 * (size_t)i);
+}
+
+// the triangles of non-trivial cell i: vertex ids from the cut-edge bases
+// (marching_cubes.cpp:163-175)
+__device__ __forceinline__ void tris_of(int nx, int ny, int voff, const MeshBufs& mb, int i) {
+  const size_t plane = (size_t)nx * ny;
+  const size_t v = (size_t)mb.cells[i];
+  const int tb = mb.cell_tri[i];
+  const int cfg = mb.cell_cfg[i];
+  const int n = c_mc_count[cfg];
+  for (int tri = 0; tri < n; ++tri) {
+    int ids[3];
+    for (int m = 0; m < 3; ++m) {
+      const int e = c_mc_tris[cfg][tri][m];
+      const int c0 = c_edge_c0[e], axis = c_edge_axis[e];
+      const size_t owner = v + (c0 & 1) + ((c0 >> 1) & 1) * (size_t)nx + ((c0 >> 2) & 1) * plane;
+      const uint32_t pk = mb.vbase[owner];
+      ids[m] = voff + (int)(pk >> 3) + __popc(pk & 7u & ((1u << axis) - 1u));
+    }
+    int32_t* o = mb.tri + 3 * (size_t)(tb + tri);
+    o[0] = ids[0], o[1] = ids[1], o[2] = ids[2];
   }
 }
 
-__global__ void __launch_bounds__(256) mc_tris_kernel(const float* __restrict__ A, const DevCtl* ctl, int nx, int ny,
-                                                      int nz, MeshBufs mb) {
+// normals and triangles in one launch: items [0, V) are vertices, [V, V + C) cells
+__global__ void __launch_bounds__(256) mc_finish_kernel(const float* __restrict__ A, const DevCtl* ctl, int nx, int ny,
+                                                        int nz, MeshBufs mb) {
   if (ctl->status != 0 || ctl->overflow) return;
-  const int C = ctl->C;
-  const int voff = ctl->voff;
-  const float Lf = __double2float_ru(ctl->level);
-  const size_t plane = (size_t)nx * ny;
-  for (int i = blockIdx.x * 256 + threadIdx.x; i < C; i += gridDim.x * 256) {
-    const size_t v = (size_t)mb.cells[i];
-    const int tb = mb.cell_tri[i];
-    VoxelInfo vi;
-    vi.cfg = mb.cell_cfg[i];
-    const int n = c_mc_count[vi.cfg];
-    for (int tri = 0; tri < n; ++tri) {
-      int ids[3];
-      for (int m = 0; m < 3; ++m) {
-        const int e = c_mc_tris[vi.cfg][tri][m];
-        const int c0 = c_edge_c0[e], axis = c_edge_axis[e];
-        const size_t owner = v + (c0 & 1) + ((c0 >> 1) & 1) * (size_t)nx + ((c0 >> 2) & 1) * plane;
-        const uint32_t pk = mb.vbase[owner];
-        ids[m] = voff + (int)(pk >> 3) + __popc(pk & 7u & ((1u << axis) - 1u));
-      }
-      int32_t* o = mb.tri + 3 * (size_t)(tb + tri);
-      o[0] = ids[0], o[1] = ids[1], o[2] = ids[2];
-    }
+  const int V = ctl->V, C = ctl->C, voff = ctl->voff;
+  const double L = ctl->level;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < V + C; i += gridDim.x * blockDim.x) {
+    if (i < V)
+      normal_of(A, nx, ny, nz, L, mb, i);
+    else
+      tris_of(nx, ny, voff, mb, i - V);
   }
 }
 
@@ -731,49 +853,79 @@ void launch_row_minmax(const float* A, int nx, int ny, int nz, float2* rowmm, cu
   row_minmax_kernel<<<(rows * 32 + 255) / 256, 256, 0, st>>>(A, nx, rows, rowmm);
 }
 
+namespace {
+// mb.blk layout: the active-unit pass's look-back descriptors (one u64 per
+// 256-unit tile) and ticket counter, the count pass's block sums (one int3
+// per kCntBlock units), then the split scan's ScanState over 1024-unit tiles
+// (ticket counter, 3 pad ints, flags, aggregates, inclusive prefixes).  The
+// block sums and the scan's counter and flags start each frame at zero.
+struct McScratch {
+  unsigned long long* desc;
+  int* tile_counter;
+  int3* bsum;
+  ScanState ss;
+  int nzero;  // ints from bsum that start each frame at zero
+};
+McScratch mc_scratch(const MeshBufs& mb, int units) {
+  const int nblk = (units + kRowThreads - 1) / kRowThreads;
+  const int nbs = (units + kCntBlock - 1) / kCntBlock;
+  const int stiles = (units + 1023) / 1024;
+  McScratch m;
+  m.desc = reinterpret_cast<unsigned long long*>(mb.blk);
+  m.tile_counter = reinterpret_cast<int*>(m.desc + nblk);
+  m.bsum = reinterpret_cast<int3*>(m.tile_counter + 4);
+  m.ss.counter = reinterpret_cast<int*>(m.bsum + nbs);
+  m.ss.flag = m.ss.counter + 4;
+  m.ss.agg = reinterpret_cast<int3*>(m.ss.flag + stiles);
+  m.ss.incl = m.ss.agg + stiles;
+  m.nzero = 3 * nbs + 4 + stiles;
+  return m;
+}
+
+void launch_select(const MeshBufs& mb, const McScratch& m, DevCtl* ctl, int ny, int nz, McSlab sl, cudaStream_t st) {
+  const int units = ny * sl.nzu;
+  const int nblk = (units + kRowThreads - 1) / kRowThreads;
+  cudaMemsetAsync(m.desc, 0, (size_t)nblk * 8 + 16, st);
+  mc_select_kernel<<<nblk, kRowThreads, 0, st>>>(mb.rowmm, ctl, ny, nz, sl, m.desc, m.tile_counter, mb.units,
+                                                 reinterpret_cast<int*>(m.bsum), m.nzero);
+}
+}  // namespace
+
 void launch_marching_cubes_count(const float* A, DevCtl* ctl, MeshBufs mb, int nx, int ny, int nz, McSlab sl,
                                  cudaStream_t st) {
   const int units = ny * sl.nzu;
-  const int nblk = (units + kRowThreads - 1) / kRowThreads;
-  // look-back descriptors (one u64 per tile) and the tile counter, reset ahead of the pass
-  unsigned long long* desc = reinterpret_cast<unsigned long long*>(mb.blk);
-  int* tile_counter = reinterpret_cast<int*>(desc + nblk);
-  // the count scan's look-back state: flags, aggregates, inclusive prefixes, counter
-  const int stiles = (units + 1023) / 1024;
-  ScanState ss;
-  ss.flag = tile_counter + 4;
-  ss.agg = reinterpret_cast<int3*>(ss.flag + stiles);
-  ss.incl = ss.agg + stiles;
-  ss.counter = reinterpret_cast<int*>(ss.incl + stiles);
+  const McScratch m = mc_scratch(mb, units);
   int3* ucnt = reinterpret_cast<int3*>(mb.unitcnt);
-  cudaMemsetAsync(desc, 0, (size_t)nblk * 8 + 16 + (size_t)stiles * 28 + 16, st);
-  cudaMemsetAsync(&ctl->v_extra, 0, sizeof(int32_t), st);
-  mc_select_kernel<<<nblk, kRowThreads, 0, st>>>(mb.rowmm, ctl, ny, nz, sl, desc, tile_counter, mb.units);
-  mc_count_kernel<<<sm_count() * 8, 256, 0, st>>>(A, ctl, nx, ny, nz, sl, mb.units, ucnt, mb);
-  mc_scan_kernel<<<stiles, 256, 0, st>>>(ucnt, ctl, ss, mb.v_cap, mb.t_cap, mb.c_cap);
+  launch_select(mb, m, ctl, ny, nz, sl, st);
+  mc_count_kernel<<<sm_count() * 8, 256, 0, st>>>(A, ctl, nx, ny, nz, sl, mb.units, ucnt, nullptr, mb);
+  mc_scan_kernel<<<(units + 1023) / 1024, 256, 0, st>>>(ucnt, ctl, m.ss, mb.v_cap, mb.t_cap, mb.c_cap);
 }
 
 void launch_marching_cubes_emit(const float* A, DevCtl* ctl, MeshBufs mb, int nx, int ny, int nz, McSlab sl,
-                                cudaStream_t st, cudaStream_t aux, cudaEvent_t fork, cudaEvent_t join) {
+                                cudaStream_t st) {
   int3* ucnt = reinterpret_cast<int3*>(mb.unitcnt);
   mc_emit_kernel<<<sm_count() * 8, 256, 0, st>>>(A, ctl, nx, ny, nz, sl, mb.units, ucnt, mb);
-  if (aux) {  // normals and triangles are independent: normals on the side stream
-    cudaEventRecord(fork, st);
-    cudaStreamWaitEvent(aux, fork, 0);
-    mc_normals_kernel<<<sm_count() * 4, 256, 0, aux>>>(A, ctl, nx, ny, nz, mb);
-    cudaEventRecord(join, aux);
-    mc_tris_kernel<<<sm_count() * 4, 256, 0, st>>>(A, ctl, nx, ny, nz, mb);
-  } else {
-    mc_normals_kernel<<<sm_count() * 4, 256, 0, st>>>(A, ctl, nx, ny, nz, mb);
-    mc_tris_kernel<<<sm_count() * 4, 256, 0, st>>>(A, ctl, nx, ny, nz, mb);
-  }
+  mc_finish_kernel<<<sm_count() * 4, 256, 0, st>>>(A, ctl, nx, ny, nz, mb);
 }
 
+// whole volume: active units, the fused count/scan/emit pass, normals + triangles
 void launch_marching_cubes(const float* A, DevCtl* ctl, MeshBufs mb, int nx, int ny, int nz, cudaStream_t st,
                            cudaStream_t aux, cudaEvent_t fork, cudaEvent_t join) {
   const McSlab whole{0, nz, nz};
-  launch_marching_cubes_count(A, ctl, mb, nx, ny, nz, whole, st);
-  launch_marching_cubes_emit(A, ctl, mb, nx, ny, nz, whole, st, aux, fork, join);
+  const int units = ny * nz;
+  const McScratch m = mc_scratch(mb, units);
+  int3* ucnt = reinterpret_cast<int3*>(mb.unitcnt);
+  launch_select(mb, m, ctl, ny, nz, whole, st);
+  mc_count_kernel<<<sm_count() * 8, 256, 0, st>>>(A, ctl, nx, ny, nz, whole, mb.units, ucnt, m.bsum, mb);
+  mc_scan_emit_kernel<<<sm_count() * 8, kFuseUnits * 32, 0, st>>>(A, ctl, nx, ny, mb.units, ucnt, m.bsum, mb);
+  if (aux) {
+    cudaEventRecord(fork, st);
+    cudaStreamWaitEvent(aux, fork, 0);
+    mc_finish_kernel<<<sm_count() * 4, 256, 0, aux>>>(A, ctl, nx, ny, nz, mb);
+    cudaEventRecord(join, aux);
+  } else {
+    mc_finish_kernel<<<sm_count() * 4, 256, 0, st>>>(A, ctl, nx, ny, nz, mb);
+  }
 }
 
 void launch_iso_samples(const DevPoints& pts, const float* A, const DevCtl* ctl, int zoff, int nzl, double* samples,

@@ -364,7 +364,7 @@ int enqueue_frame(vc_ctx* ctx, const FrameCfg& f) {
   record(ctx, 4);
   launch_marching_cubes(P<float>(ctx->A), ctx->ctl, mesh_bufs(ctx), f.nx, f.ny, f.nz, st, branch ? ctx->aux : nullptr,
                         ctx->fork[1], ctx->join[1]);
-  n += 6;  // select, count, scan, emit, normals, triangles
+  n += 4;  // active units, count, scan + emit, normals + triangles
   record(ctx, 5);
   {  // the views' RGB (staged on the copy stream while the frame ran): an external event node in the graph
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;

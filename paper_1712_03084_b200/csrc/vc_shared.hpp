@@ -167,8 +167,10 @@ int iso_blocks();
 void launch_iso_level(const DevPoints& pts, const float* A, DevCtl* ctl, double* partial, int nblk_max,
                       cudaStream_t st);
 int mc_blocks(int nx, int ny, int nz);
-// aux/fork/join (nullable): run the normals on `aux` beside the triangles; the
-// caller waits on `join` before the frame ends
+// Whole volume (rowmm written): active units and one fused count/scan/emit
+// pass on `st`, then normals + triangles in one kernel — on `aux` when given
+// (fork/join events; the caller waits on `join` before the frame ends: the
+// vertex positions, all the texture pass reads, are complete on `st`).
 void launch_marching_cubes(const float* A, DevCtl* ctl, MeshBufs mb, int nx, int ny, int nz, cudaStream_t st,
                            cudaStream_t aux = nullptr, cudaEvent_t fork = nullptr, cudaEvent_t join = nullptr);
 // Slab variant: units (voxel rows) of planes [z0, z0+nzu); planes >= zend
@@ -183,8 +185,7 @@ struct McSlab {
 void launch_marching_cubes_count(const float* A, DevCtl* ctl, MeshBufs mb, int nx, int ny, int nz, McSlab sl,
                                  cudaStream_t st);
 void launch_marching_cubes_emit(const float* A, DevCtl* ctl, MeshBufs mb, int nx, int ny, int nz, McSlab sl,
-                                cudaStream_t st, cudaStream_t aux = nullptr, cudaEvent_t fork = nullptr,
-                                cudaEvent_t join = nullptr);
+                                cudaStream_t st);
 // Slab iso level: samples[p] = trilinear(A, point p) if this rank owns the
 // point's lower z plane, else 0 (summed over ranks, then launch_iso_final_samples)
 void launch_iso_samples(const DevPoints& pts, const float* A, const DevCtl* ctl, int zoff, int nzl, double* samples,

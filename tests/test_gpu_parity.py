@@ -373,7 +373,7 @@ def test_repeatability_and_graph_replay(scene, ctx):
     a = vc.reconstruct_frame(frames, rig, cfg, ctx=ctx, want_volume=True)
     b = vc.reconstruct_frame(frames, rig, cfg, ctx=ctx, want_volume=True)
     assert rel_l2(a.volume.values, b.volume.values) < 1e-6
-    assert ctx.kernels_per_frame() >= 19
+    assert ctx.kernels_per_frame() >= 16
 
 
 # ------------------------------------------------------------------ larger configurations (BASELINE C3 / C5)

@@ -7,5 +7,5 @@ python bench.py --workload c3 --steps 40 --warmup 3 --no-cpu-baseline > gpurun_o
 python bench.py --workload c5 --steps 20 --warmup 3 --no-cpu-baseline > gpurun_out/ev/c5.json 2> gpurun_out/ev/c5.err; echo c5 $?
 CMD="python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-fft-comparator --streams 1"
 $CMD > gpurun_out/ev/plain.log 2>&1; echo plain $?
-ncu --metrics gpu__time_duration.sum --clock-control none -s 63 -c 84 --csv --log-file gpurun_out/ev/launches.csv $CMD > gpurun_out/ev/ncu_launch.log 2>&1; echo launches $?
+ncu --metrics gpu__time_duration.sum --clock-control none -s 2400 -c 160 --csv --log-file gpurun_out/ev/launches.csv $CMD > gpurun_out/ev/ncu_launch.log 2>&1; echo launches $?
 ncu --set full --clock-control none --import-source on -k regex:"fx_kernel|fy_kernel|z_kernel|iy_kernel|ix_kernel|splat_weighted|mc_count|mc_emit|texture_kernel|pre_points|pre_prefix" -s 22 -c 11 -o gpurun_out/ev/prof_full $CMD > gpurun_out/ev/ncu_full.log 2>&1; echo ncu $?
