@@ -656,6 +656,100 @@ __global__ void __launch_bounds__(ZCfg<NZ>::THREADS, NZ >= 1024 ? 1 : (NZ == 256
     z_body<NZ, false>(S0, S1, nx, ny, kyl, ky0, H, fx_step, fy_step, scale, tw, planeflag);
 }
 
+// ------------------------------------------------------------------ Z, pipelined (1024 planes)
+// One persistent CTA per SM over the main column tiles, three NZ x CW stage
+// buffers: while tile i's transforms run, tile i+1's D lands in the free
+// buffer (issued at the top of the iteration) and its Z in tile i's Z buffer
+// (issued as soon as FFT_z(Z) has released it).  At these sizes the two
+// staged tiles of z_kernel hold the SM alone (one CTA), so its loads and its
+// transforms never overlap; here they do.  Same per-tile arithmetic as
+// z_body; the packed Nyquist tiles stay with z_kernel.  (At 512 planes
+// z_kernel keeps 2-3 CTAs per SM and beats this kernel's one: 0.465 against
+// 0.684 ms per C3 frame, profiles/r02_experiments.json.)
+template <int NZ>
+struct ZPCfg {
+  static constexpr int CW = 8;
+  static constexpr int THREADS = CW * Shape<NZ>::R2;
+  static constexpr int TILE = NZ * CW;  // float2
+  static constexpr int SMEM = 3 * TILE * 8;
+};
+
+template <int NZ>
+__global__ void __launch_bounds__(ZPCfg<NZ>::THREADS, 1)
+    zp_kernel(float2* __restrict__ S0, const float2* __restrict__ S1, int nx, int ny, int kyl, int ky0, int H, int ntx,
+              float fx_step, float fy_step, float scale, const float2* __restrict__ tw,
+              const uint32_t* __restrict__ planeflag) {
+  using S = Shape<NZ>;
+  using CF = ZPCfg<NZ>;
+  constexpr int T = S::R2, R1 = S::R1, kCW = CF::CW, TH = CF::THREADS;
+  extern __shared__ float2 sh[];
+  const int c = threadIdx.x % kCW, t = threadIdx.x / kCW;
+  const size_t zstride = (size_t)kyl * H;
+  const int ntiles = ntx * kyl;
+  int tile = blockIdx.x;
+  if (tile >= ntiles) return;
+  const uint32_t pm = row_flags<NZ, kCW, TH>(planeflag);  // planes F-y skipped are zero
+  auto stage = [&](float2* dst, const float2* comp, int tl) {
+    if (tl < ntiles) {
+      const int kyr = tl / ntx;
+      stage_tile<NZ, kCW, TH>(dst, comp + (size_t)kyr * H, zstride, (tl - kyr * ntx) * kCW, H, pm);
+    }
+    cp_async_commit();  // (empty groups keep the wait counts uniform)
+  };
+  int bD = 0, bZ = 1, bF = 2;  // buffers: this tile's D, its Z, free
+  stage(sh + bD * CF::TILE, S0, tile);
+  stage(sh + bZ * CF::TILE, S1, tile);
+  for (; tile < ntiles; tile += gridDim.x) {
+    const int next = tile + gridDim.x;
+    float2* b0 = sh + bD * CF::TILE;
+    float2* b1 = sh + bZ * CF::TILE;
+    stage(sh + bF * CF::TILE, S0, next);  // in flight: D(tile), Z(tile), D(next)
+    const int kyr = tile / ntx;
+    const int kx = (tile - kyr * ntx) * kCW + c;
+    float2 v[R1];
+    cp_async_wait<2>();
+    __syncthreads();
+    tile_to_regs<NZ, kCW>(b0, c, t, v);
+    __syncthreads();
+    ExCols<NZ, kCW> e0{b0, c};
+    fft_line<NZ, false>(v, t, tw, e0);
+#pragma unroll
+    for (int k1 = 0; k1 < R1; ++k1) b0[(t + T * k1) * kCW + c] = v[k1];  // park FFT_z(D)
+    cp_async_wait<1>();
+    __syncthreads();
+    tile_to_regs<NZ, kCW>(b1, c, t, v);
+    __syncthreads();
+    ExCols<NZ, kCW> e1{b1, c};
+    fft_line<NZ, false>(v, t, tw, e1);  // ends on a barrier after its last read of b1
+    stage(b1, S1, next);                // Z(next) lands behind the filter and the inverse
+    const int ky = ky0 + kyr;
+    const float wx = (float)(kx <= nx / 2 ? kx : kx - nx) * fx_step;
+    const float wy = (float)(ky <= ny / 2 ? ky : ky - ny) * fy_step;
+    const float wxy = wx * wx + wy * wy;
+#pragma unroll
+    for (int k1 = 0; k1 < R1; ++k1) {
+      const int kz = t + T * k1;
+      const float wz = signed_freq<NZ>(kz);
+      const float w2 = wxy + wz * wz;
+      const float2 d = b0[kz * kCW + c];
+      const float2 s = make_float2(d.x + wz * v[k1].x, d.y + wz * v[k1].y);
+      const float inv = (kx == 0 && ky == 0 && kz == 0) ? 0.f : __fdividef(scale, w2);
+      v[k1] = make_float2(s.y * inv, -s.x * inv);
+    }
+    __syncthreads();  // parked D read by all before b0 becomes the exchange
+    relayout_for_inverse<NZ>(v);
+    fft_line<NZ, true>(v, t, tw, e0);
+    if (kx <= nx / 2) {
+      const size_t base = (size_t)kyr * H + kx;
+#pragma unroll
+      for (int k1 = 0; k1 < R1; ++k1) st_out(S0 + base + (size_t)(t + T * k1) * zstride, v[k1]);
+    }
+    const int f = bF;
+    bF = bD, bD = f;  // D(next) is in the old free buffer; b0 is free after the inverse's last barrier
+  }
+  cp_async_wait<0>();
+}
+
 // ------------------------------------------------------------------ Z, TMA-fed, warp-private
 // Persistent CTAs over column tiles (16 kx columns x one ky row x all NZ
 // planes of D and Z).  Tiles arrive through the tensor-memory accelerator:
@@ -1097,6 +1191,7 @@ struct Prep {
     } else {
       allow_smem(z_kernel<N>, 2 * ZCfg<N>::SMEM);
       if constexpr (N == 64 || N == 128 || N == 256) allow_smem(z4_kernel<N>, Z4Cfg<N>::SMEM);
+      if constexpr (N == 1024) allow_smem(zp_kernel<N>, ZPCfg<N>::SMEM);
     }
   }
 };
@@ -1140,12 +1235,34 @@ struct RunFy {
                                                           ilog2(a.kyl), a.twy, a.rowbits, a.planeflag + a.zoff);
   }
 };
+// VC_ZP=0 (A/B switch): the staged z_kernel at 1024 planes instead of zp_kernel
+inline bool zp_on() {
+  static const bool on = [] {
+    const char* e = std::getenv("VC_ZP");
+    return !e || std::atoi(e) != 0;
+  }();
+  return on;
+}
 template <int N>
 struct RunZ {
   static void run(const SlabFft& a) {
     using C = ZCfg<N>;
     int tiles, nyq;
     col_grid(a.nx, C::CW, &tiles, &nyq, 1);
+    if constexpr (N == 1024) {
+      static_assert(ZPCfg<N>::CW == C::CW, "one tiling");
+      if (zp_on()) {
+        const float fxs = (float)(2.0 * M_PI / a.nx), fys = (float)(2.0 * M_PI / a.ny);
+        const float scale = (float)(1.0 / ((double)a.nx * a.ny * a.nz));
+        const int ntx = nyq >= 0 ? nyq : tiles;
+        zp_kernel<N><<<sm_count(), ZPCfg<N>::THREADS, ZPCfg<N>::SMEM, a.st>>>(
+            a.R0, a.R1, a.nx, a.ny, a.kyl, a.ky0, a.H, ntx, fxs, fys, scale, a.twz, a.planeflag);
+        if (nyq >= 0)  // the packed kx = nx/2 tiles: z_kernel's Nyquist body (grid column 0 = nyq)
+          z_kernel<N><<<dim3(1, (a.kyl + C::CW - 1) / C::CW), C::THREADS, 2 * C::SMEM, a.st>>>(
+              a.R0, a.R1, a.nx, a.ny, a.kyl, a.ky0, a.H, 0, fxs, fys, scale, a.twz, a.planeflag);
+        return;
+      }
+    }
     dim3 grid(tiles, a.kyl);
     const float fxs = (float)(2.0 * M_PI / a.nx), fys = (float)(2.0 * M_PI / a.ny);
     const float scale = (float)(1.0 / ((double)a.nx * a.ny * a.nz));  // the c2r's 1/N (integrate.cpp:70-72)
