@@ -315,11 +315,11 @@ def profile_kernels(lib, h, sensors, views_list, cfg, dims, out, k=4):
     fft_names = ["fft_x", "fft_y", "fft_z", "ifft_y", "ifft_x"]
     dom = max(fft_names + ["clear"], key=lambda nm: kernel_ms[nm])
     traffic = None
-    if tuple(dims) == DIMS:
-        try:  # dram bytes per launch of the same kernel from the committed ncu --set full capture
-            traffic = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))[dom]["dram_bytes_per_launch"]
-        except Exception:
-            traffic = None
+    tkey = dom if tuple(dims) == DIMS else f"{dom}@{dims[0]}"
+    try:  # dram bytes per launch of the same kernel at this grid from the committed ncu --set full capture
+        traffic = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))[tkey]["dram_bytes_per_launch"]
+    except Exception:
+        traffic = None
     sb = survey_bytes(*dims, P, V, T, k)
     alg = sb.get(dom, ab[dom])
     achieved = alg / (kernel_ms[dom] * 1e-3) / 1e9

@@ -26,9 +26,10 @@ METRICS = [
     "smsp__inst_executed.sum", "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum",
     "launch__grid_size", "launch__block_size",
 ]
-BENCH_NAME = {"fx_kernel": "fft_x", "fy_kernel": "fft_y", "z_kernel": "fft_z", "iy_kernel": "ifft_y",
-              "ix_kernel": "ifft_x", "splat_weighted_kernel": "splat", "texture_kernel": "texture",
-              "sparse_clear_kernel": "clear"}
+BENCH_NAME = {"fx_kernel": "fft_x", "fy_kernel": "fft_y", "z_kernel": "fft_z", "zp_kernel": "fft_z",
+              "iy_kernel": "ifft_y", "iy_tma_kernel": "ifft_y", "ix_kernel": "ifft_x",
+              "splat_weighted_kernel": "splat", "texture_kernel": "texture", "sparse_clear_kernel": "clear"}
+C2_N = 256  # traffic keys: bench name at the C2 grid, "name@N" at an N^3 grid
 
 
 def short(name: str) -> str:
@@ -65,14 +66,20 @@ def main(rep, out):
     traffic = json.load(open(tpath)) if os.path.exists(tpath) else {}
     for rec in recs:
         base = rec["kernel"].split("<")[0]
+        targ = rec["kernel"].split("<")[1].split(">")[0].split(",")[0] if "<" in rec["kernel"] else ""
+        n = int(targ) if targ.isdigit() else C2_N
         if base in BENCH_NAME:
+            key = BENCH_NAME[base] if n == C2_N else f"{BENCH_NAME[base]}@{n}"
             rb, wb = rec.get("dram__bytes_read.sum", 0.0), rec.get("dram__bytes_write.sum", 0.0)
             # ncu reports (M)bytes per the unit row; raw page units are bytes for these counters
-            traffic[BENCH_NAME[base]] = {
+            traffic[key] = {
                 "dram_bytes_per_launch": int(rb + wb),
                 "ncu_duration_us": rec.get("gpu__time_duration.sum"),
                 "source": f"{os.path.basename(rep)}: ncu --set full --clock-control none, "
                           "bench.py --streams 1 (cold cache, serialised)"}
+            if n != C2_N:
+                traffic[key]["source"] = f"{os.path.basename(rep)}: ncu --set full --clock-control none, bench.py " \
+                                         f"--workload {'c3' if n == 512 else 'c5'} (one launch, serialised)"
     json.dump(traffic, open(tpath, "w"), indent=1)
     print(f"{len(recs)} launches -> {out}; traffic table {tpath}")
 
