@@ -254,6 +254,10 @@ struct FCfg {
   static constexpr int CW = N >= 256 ? 8 : 16;
   static constexpr int THREADS = CW * Shape<N>::R2;
   static constexpr int SMEM = N * CW * 8;
+  // staged tiles: all three components in flight, except at 512 points where
+  // the third reuses the first's buffer (64 KB instead of 96: 3 CTAs per SM)
+  static constexpr int NBUF = 3;
+  static constexpr int MINB = N >= 1024 ? 1 : (N == 512 ? 2 : (N >= 256 ? 4 : 2));
 };
 
 // Z: narrow tiles from 256 points up (VC_ZCW=4: 4 columns, 8 CTAs/SM at 256)
@@ -504,7 +508,7 @@ __device__ __forceinline__ void tile_to_regs(const float2* tile, int c, int t, f
 // for the slab transform that is the send layout of the forward all-to-all
 // (block s = the ky-slab of rank s); with kyl = ny it is the plain layout.
 template <int NY>
-__global__ void __launch_bounds__(FCfg<NY>::THREADS, NY >= 1024 ? 1 : (NY >= 256 ? 4 : 2)) fy_kernel(const float2* S0, const float2* S1,
+__global__ void __launch_bounds__(FCfg<NY>::THREADS, FCfg<NY>::MINB) fy_kernel(const float2* S0, const float2* S1,
                                                                  const float2* __restrict__ S2, float2* O0, float2* O1,
                                                                  int nxh, int H, int lk,
                                                                  const float2* __restrict__ tw,
@@ -512,10 +516,11 @@ __global__ void __launch_bounds__(FCfg<NY>::THREADS, NY >= 1024 ? 1 : (NY >= 256
                                                                  uint32_t* __restrict__ planeflag) {
   using S = Shape<NY>;
   constexpr int T = S::R2, R1 = S::R1, kCW = FCfg<NY>::CW, TH = FCfg<NY>::THREADS;
-  extern __shared__ float2 sh[];  // 3 tiles of NY x kCW
+  constexpr int NB = FCfg<NY>::NBUF;
+  extern __shared__ float2 sh[];  // NB tiles of NY x kCW
   float2* b0 = sh;
   float2* b1 = sh + NY * kCW;
-  float2* b2 = sh + 2 * NY * kCW;
+  float2* b2 = NB == 3 ? sh + 2 * NY * kCW : b0;
   const int c = threadIdx.x % kCW, t = threadIdx.x / kCW;
   const int kx0 = blockIdx.x * kCW, kx = kx0 + c;
   const bool live = kx < nxh;
@@ -530,15 +535,21 @@ __global__ void __launch_bounds__(FCfg<NY>::THREADS, NY >= 1024 ? 1 : (NY >= 256
   cp_async_commit();
   stage_tile<NY, kCW, TH>(b1, S1 + plane, H, kx0, H, rm);
   cp_async_commit();
-  stage_tile<NY, kCW, TH>(b2, S2 + plane, H, kx0, H, rm);
-  cp_async_commit();
+  if constexpr (NB == 3) {
+    stage_tile<NY, kCW, TH>(b2, S2 + plane, H, kx0, H, rm);
+    cp_async_commit();
+  }
   float2 d[R1], v[R1];
-  cp_async_wait<2>();
+  cp_async_wait<NB - 1>();
   __syncthreads();
   tile_to_regs<NY, kCW>(b0, c, t, d);
   __syncthreads();
   ExCols<NY, kCW> e0{b0, c};
   fft_line<NY, false>(d, t, tw, e0);
+  if constexpr (NB == 2) {  // b0 is free (fft_line ends on a barrier after its last read)
+    stage_tile<NY, kCW, TH>(b2, S2 + plane, H, kx0, H, rm);
+    cp_async_commit();
+  }
   cp_async_wait<1>();
   __syncthreads();
   tile_to_regs<NY, kCW>(b1, c, t, v);
@@ -646,7 +657,7 @@ __device__ __forceinline__ void z_body(float2* __restrict__ S0, const float2* __
 // Input: D, Z as [z][kyl][H] (kyl = ny on one GPU; a ky-slab starting at ky0
 // after the forward all-to-all).  The result overwrites S0 in place.
 template <int NZ>
-__global__ void __launch_bounds__(ZCfg<NZ>::THREADS, NZ >= 1024 ? 1 : (NZ == 256 ? 32 / VC_ZCW256 : 2))
+__global__ void __launch_bounds__(ZCfg<NZ>::THREADS, NZ >= 1024 ? 1 : (NZ == 256 ? 32 / VC_ZCW256 : (NZ == 512 ? 3 : 2)))
     z_kernel(float2* __restrict__ S0, const float2* __restrict__ S1, int nx, int ny, int kyl, int ky0, int H, int nyq,
              float fx_step, float fy_step, float scale, const float2* __restrict__ tw,
              const uint32_t* __restrict__ planeflag) {
@@ -1185,7 +1196,7 @@ struct Prep {
       allow_smem(fx_kernel<N>, XCfg<N>::SMEM);
       allow_smem(ix_kernel<N>, IXCfg<N>::SMEM);
     } else if (axis == 1) {
-      allow_smem(fy_kernel<N>, 3 * FCfg<N>::SMEM);
+      allow_smem(fy_kernel<N>, FCfg<N>::NBUF * FCfg<N>::SMEM);
       allow_smem(iy_kernel<N>, ICfg<N>::SMEM);
       allow_smem(iy_tma_kernel<N>, ICfg<N>::SMEM + 64);
     } else {
@@ -1231,7 +1242,7 @@ struct RunFy {
     // (no Nyquist packing here: F-y's per-row empty flags make the packed
     // gather slower than the one wasted tile, measured)
     dim3 grid((a.nx / 2 + 1 + C::CW - 1) / C::CW, a.nzl);
-    fy_kernel<N><<<grid, C::THREADS, 3 * C::SMEM, a.st>>>(a.S0, a.S1, a.S2, a.O0, a.O1, a.nx / 2 + 1, a.H,
+    fy_kernel<N><<<grid, C::THREADS, C::NBUF * C::SMEM, a.st>>>(a.S0, a.S1, a.S2, a.O0, a.O1, a.nx / 2 + 1, a.H,
                                                           ilog2(a.kyl), a.twy, a.rowbits, a.planeflag + a.zoff);
   }
 };
