@@ -22,6 +22,7 @@
 //   mc_normals  one thread per vertex: gradient normals (:180-207)
 //   mc_tris     one thread per active cell: triangles in the reference's cell
 //               scan order (z, y, x), table order within the cell
+#include <cstdlib>
 #include <cfloat>
 
 #include "vc_device.cuh"
@@ -916,8 +917,18 @@ void launch_marching_cubes(const float* A, DevCtl* ctl, MeshBufs mb, int nx, int
   const McScratch m = mc_scratch(mb, units);
   int3* ucnt = reinterpret_cast<int3*>(mb.unitcnt);
   launch_select(mb, m, ctl, ny, nz, whole, st);
-  mc_count_kernel<<<sm_count() * 8, 256, 0, st>>>(A, ctl, nx, ny, nz, whole, mb.units, ucnt, m.bsum, mb);
-  mc_scan_emit_kernel<<<sm_count() * 8, kFuseUnits * 32, 0, st>>>(A, ctl, nx, ny, mb.units, ucnt, m.bsum, mb);
+  static const bool split = [] {  // VC_MC_SPLIT=1 (A/B): count, 1024-unit look-back scan, emit
+    const char* e = getenv("VC_MC_SPLIT");
+    return e && atoi(e) != 0;
+  }();
+  if (split) {
+    mc_count_kernel<<<sm_count() * 8, 256, 0, st>>>(A, ctl, nx, ny, nz, whole, mb.units, ucnt, nullptr, mb);
+    mc_scan_kernel<<<(units + 1023) / 1024, 256, 0, st>>>(ucnt, ctl, m.ss, mb.v_cap, mb.t_cap, mb.c_cap);
+    mc_emit_kernel<<<sm_count() * 8, 256, 0, st>>>(A, ctl, nx, ny, nz, whole, mb.units, ucnt, mb);
+  } else {
+    mc_count_kernel<<<sm_count() * 8, 256, 0, st>>>(A, ctl, nx, ny, nz, whole, mb.units, ucnt, m.bsum, mb);
+    mc_scan_emit_kernel<<<sm_count() * 8, kFuseUnits * 32, 0, st>>>(A, ctl, nx, ny, mb.units, ucnt, m.bsum, mb);
+  }
   if (aux) {
     cudaEventRecord(fork, st);
     cudaStreamWaitEvent(aux, fork, 0);
