@@ -42,12 +42,14 @@ class Workload:
     stream_frame(g, frames) (stride 97, coprime with 300 and 60: any `frames`
     consecutive global steps visit every resident frame once)."""
 
-    def __init__(self, key, metric, dims, k, hd, frames, text):
+    def __init__(self, key, metric, dims, k, hd, frames, text, stream=STREAM, host_ring=None):
         self.key, self.metric, self.dims, self.k, self.hd, self.frames, self.text = key, metric, dims, k, hd, frames, text
         self.rgb_w, self.rgb_h = (1920, 1080) if hd else (W, H)
+        self.stream = stream        # length of the kick sequence the frames sample (make_kick_sequence(n))
+        self.host_ring = host_ring  # e2e leg: pinned host copies of the first `host_ring` frames only
 
     def kick_frame(self, j):
-        return j * STREAM // self.frames
+        return j * self.stream // self.frames
 
     @property
     def view_bytes(self):
@@ -66,6 +68,13 @@ WORKLOADS = {
                    (512, 512, 512), 6, True, 60,
                    "C3: 60 frames of the kick stream (every 5th of 300), 6 views 512x424 depth (f=365) + 1920x1080 "
                    "colour (f=1060, 52 mm offset), 512^3 grid"),
+    # a 4096-frame kick stream, 256^3, K=4, sharded frame-parallel over the ranks; the
+    # views are rendered on the device and stay resident (21 GB); one timed step per frame of the shard
+    "c4": Workload("c4", "reconstructed frames/sec over a 4096-frame kick stream at 256^3 grid, 4x512x424 RGB-D views",
+                   (256, 256, 256), 4, False, 4096,
+                   "C4: 4096-frame kick stream (make_kick_sequence(4096)), 4 views 512x424 depth+RGB, 256^3 grid, "
+                   "frame-parallel shards over the ranks; each rank reconstructs its whole shard once",
+                   stream=4096, host_ring=512),
 }
 WORKLOAD = WORKLOADS["c2"].text
 DIMS = WORKLOADS["c2"].dims
@@ -140,7 +149,7 @@ def oracle_rig(O, wl):
 def oracle_inputs(O, rig, wl, j):
     """Views of resident frame j (kick frame wl.kick_frame(j)), rendered by the oracle."""
     f = wl.kick_frame(j)
-    body = O.kick_body(STREAM, f)
+    body = O.kick_body(wl.stream, f)
     views = [O.render_frame(rig[k], body, k, f) for k in range(wl.k)]
     return [v.depth for v in views], [v.mask for v in views], [v.rgb for v in views]
 
@@ -389,11 +398,12 @@ def run_gpu(args):
     sensors = rig.c_array(K)
     n_pix = W * H
     per_view, frame_bytes, NF = wl.view_bytes, wl.frame_bytes, wl.frames
+    HF = min(NF, wl.host_ring or NF)  # frames with a pinned host copy (the e2e leg's inputs)
     # device-resident stream (rendered on the GPU) + pinned host copy for e2e
     dbuf = C.c_void_p()
     L.check(lib.vc_device_alloc(h, C.c_size_t(NF * frame_bytes), C.byref(dbuf)), h)
     hbuf = C.c_void_p()
-    L.check(lib.vc_host_alloc(h, C.c_size_t(NF * frame_bytes), C.byref(hbuf)), h)
+    L.check(lib.vc_host_alloc(h, C.c_size_t(HF * frame_bytes), C.byref(hbuf)), h)
 
     def view_ptrs(base, j, k):
         o = base + j * frame_bytes + k * per_view
@@ -401,13 +411,13 @@ def run_gpu(args):
 
     for j in range(NF):
         f = wl.kick_frame(j)
-        body = vc.kick_body(STREAM, f)
+        body = vc.kick_body(wl.stream, f)
         for k in range(K):
             d, m, c = view_ptrs(dbuf.value, j, k)
             L.check(lib.vc_synth_render(h, C.byref(sensors[k]), C.byref(body), C.c_double(0.0), C.c_uint64(1),
                                         C.c_double(1.0), k, f, C.c_void_p(d), C.c_void_p(m), C.c_void_p(c),
                                         L.VC_MEM_DEVICE), h)
-    L.check(lib.vc_memcpy(h, hbuf, dbuf, C.c_size_t(NF * frame_bytes), L.VC_MEM_HOST, L.VC_MEM_DEVICE), h)
+    L.check(lib.vc_memcpy(h, hbuf, dbuf, C.c_size_t(HF * frame_bytes), L.VC_MEM_HOST, L.VC_MEM_DEVICE), h)
 
     def views_for(base, j, kind):
         arr = (L.View * K)()
@@ -417,11 +427,13 @@ def run_gpu(args):
         return arr
 
     dev_views = [views_for(dbuf.value, j, L.VC_MEM_DEVICE) for j in range(NF)]
-    host_views = [views_for(hbuf.value, j, L.VC_MEM_HOST) for j in range(NF)]
+    host_views = [views_for(hbuf.value, j % HF, L.VC_MEM_HOST) for j in range(NF)]
     cfg = vc.ReconConfig(dims=dims).to_c()
     outs = [L.TexturedMesh() for _ in range(S)]
     out = outs[0]
     # global step g = i * world + rank reconstructs resident frame stream_frame(g): every pose is sampled
+    if wl.key == "c4":  # one timed step per frame of this rank's shard of the stream
+        args.steps = len(range(rank, NF, world))
     my_frames = rank_frames(rank, world, max(args.steps, args.warmup, S), NF)
     d2h_acc = [0] * S
 
@@ -526,6 +538,9 @@ def run_gpu(args):
                        "frames_per_rank": args.steps, "parallelism": f"frame-parallel x{world}",
                        "frame_order": f"global step g = i*{world} + rank reconstructs resident frame (97 g) mod {NF}",
                        "streams_per_gpu": S,
+                       "stream_frames": NF,
+                       "e2e_inputs": ("pinned host copies of every resident frame" if HF == NF else
+                                      f"pinned host copies of the first {HF} frames (frame j reads copy j mod {HF})"),
                        "l2": "per-step working set (volume buffers >= 0.5 GB + inputs) exceeds the 126 MB L2",
                        "precision": "fp32 splat/FFT, fp64 binning, projections, MC vertices"},
             "e2e": {"value": e2e_value, "unit": "frames/s", "h2d_bytes_per_step": frame_bytes,
@@ -725,6 +740,8 @@ def run_plan(args):
     from paper_1712_03084_b200.frame_parallel import rank_frames
     rank, world, _ = dist_env()
     wl = WORKLOADS[args.workload]
+    if wl.key == "c4":  # as run_gpu: the rank's whole shard
+        args.steps = len(range(rank, wl.frames, world))
     mine = [wl.kick_frame(j) for j in rank_frames(rank, world, args.steps, wl.frames)]
     allf = [mine]
     if world > 1:
@@ -746,8 +763,9 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-fft-comparator", action="store_true")
-    ap.add_argument("--workload", default="c2", choices=["c2", "c3", "c5"],
+    ap.add_argument("--workload", default="c2", choices=["c2", "c3", "c4", "c5"],
                     help="c2: the BASELINE metric (256^3 stream, frame-parallel); c3: 512^3, 6 views + HD colour; "
+                         "c4: the 4096-frame stream, each rank's shard once (--steps ignored); "
                          "c5: 1024^3 frames (z-slabs on N>1)")
     ap.add_argument("--streams", type=int, default=4,
                     help="concurrent frames per GPU (one context + host thread each)")

@@ -83,3 +83,21 @@ def test_bench_launcher_spawns_ranks():
     assert d["n_gpus"] == 2 and len(d["frames_by_rank"]) == 2
     a, b = d["frames_by_rank"]
     assert not set(a) & set(b) and sorted(a + b) == list(range(300))
+
+
+def test_bench_launcher_c4_shards_the_4096_stream():
+    """C4: `bench.py --workload c4 --gpus 2` gives each rank its
+    whole shard of the 4096-frame kick stream (steps = shard size, --steps
+    ignored); the shards are disjoint and cover make_kick_sequence(4096)."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--plan", "--workload", "c4", "--gpus", "2",
+                          "--steps", "10"], capture_output=True, text=True, timeout=300, cwd=root, env=env)
+    assert out.returncode == 0, out.stderr[-2000:]
+    d = json.loads([ln for ln in out.stdout.splitlines() if ln.startswith("{")][0])
+    a, b = d["frames_by_rank"]
+    assert len(a) == len(b) == 2048
+    assert not set(a) & set(b) and sorted(a + b) == list(range(4096))
