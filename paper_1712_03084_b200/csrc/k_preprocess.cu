@@ -17,11 +17,13 @@
 //   pre_points  one thread per pixel: the six incident triangles in the
 //               reference's accumulation order (cloud.cpp:53-71), world
 //               position/normal (:73-74), W = W1*W2 (:108-114) -> per-pixel
-//               staging slot + flag, weight map, per-segment count; the
-//               bbox is folded in with atomic min/max on order-preserving keys
-//   pre_scan    exclusive scan of the segment counts (single CTA) -> P,
-//               empty-scene status, fit_grid from the bbox
-//   pre_gather  one thread per pixel: staged points -> final SoA in order
+//               staging slot + flag, weight map, per-segment / per-row /
+//               per-64-row-block counts; the bbox is folded in with atomic
+//               min/max on order-preserving keys
+//   pre_gather  one warp per active segment: its first point id from the
+//               block, row and segment counts before it (no scan pass);
+//               staged points -> final SoA in order; its first warp sets P,
+//               the empty-scene status and fit_grid from the bbox
 // fp64 with the reference's operation order and no FMA (vc_device.cuh), so
 // positions — hence every downstream binning decision — are bit-exact.
 #include <cfloat>
@@ -31,6 +33,7 @@
 namespace vc {
 namespace {
 
+constexpr int kRowBlock = 64;  // depth rows per point-count block sum (pre_points adds, pre_gather reads)
 constexpr int kSegPx = 32;  // pixels per segment: one warp, one CTA of pre_points (a CTA
                             // retires with its slowest warp, so one-warp CTAs let the
                             // empty segments' slots recycle while point warps compute)
@@ -107,14 +110,16 @@ __global__ void __launch_bounds__(256) pre_prefix_tri_kernel(const __grid_consta
                                                              uint8_t* __restrict__ flags,
                                                              float* __restrict__ weight_maps,
                                                              int32_t* __restrict__ act,
-                                                             int32_t* __restrict__ rowcnt) {
+                                                             int32_t* __restrict__ rowcnt,
+                                                             int32_t* __restrict__ bsum) {
   __shared__ uint16_t qlist[8][512];
   __shared__ __align__(128) uint8_t rstage[8][3072];  // per warp: mask y, y+1 (512 B each), depth y, y+1 (1 KB each)
   __shared__ __align__(8) uint64_t rbar[8];
   if (blockIdx.x == 0 && threadIdx.x < 6) ctl->bbox_key[threadIdx.x] = threadIdx.x < 3 ? ~0ull : 0ull;
   const int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31, wid = (threadIdx.x >> 5) & 7;
   if (r >= rows) return;  // whole warps
-  if (lane == 0) rowcnt[r] = 0;  // the row's point count (pre_points adds, pre_scan scans)
+  if (lane == 0) rowcnt[r] = 0;  // the row's point count (pre_points adds, pre_gather sums)
+  if (lane == 0 && (r & (kRowBlock - 1)) == 0) bsum[r / kRowBlock] = 0;
   int k, y;
   row_of(ss, r, &k, &y);
   const ViewPtrs& v = ss.v[k];
@@ -321,7 +326,7 @@ __device__ __forceinline__ void points_segment(const SensorSet& ss, int sil_r, c
                                                Staged* __restrict__ stage, uint8_t* __restrict__ flags,
                                                int32_t* __restrict__ seg_counts, DevCtl* ctl,
                                                float* __restrict__ weight_maps, int seg, int spr,
-                                               int32_t* __restrict__ rowcnt) {
+                                               int32_t* __restrict__ rowcnt, int32_t* __restrict__ bsum) {
   const int row = seg / spr, sx = seg - row * spr;
   int k, y;
   row_of(ss, row, &k, &y);
@@ -405,7 +410,10 @@ __device__ __forceinline__ void points_segment(const SensorSet& ss, int sil_r, c
   const unsigned ball = __ballot_sync(0xffffffffu, is_pt);
   if (lane == 0) seg_counts[seg] = __popc(ball);
   if (ball == 0u) return;  // warp-uniform: most segments of a frame hold no point
-  if (lane == 0) atomicAdd(rowcnt + row, __popc(ball));
+  if (lane == 0) {
+    atomicAdd(rowcnt + row, __popc(ball));
+    atomicAdd(bsum + row / kRowBlock, __popc(ball));
+  }
   double lo[3] = {p.x, p.y, p.z}, hi[3] = {is_pt ? p.x : -inf, is_pt ? p.y : -inf, is_pt ? p.z : -inf};
 #pragma unroll
   for (int a = 0; a < 3; ++a)
@@ -427,88 +435,44 @@ __global__ void __launch_bounds__(kSegPx) pre_points_kernel(const __grid_constan
                                                             int32_t* __restrict__ seg_counts, DevCtl* ctl,
                                                             float* __restrict__ weight_maps,
                                                             const int32_t* __restrict__ act, int spr,
-                                                            int32_t* __restrict__ rowcnt) {
+                                                            int32_t* __restrict__ rowcnt,
+                                                            int32_t* __restrict__ bsum) {
   const int n = act[0];
   for (int i = blockIdx.x; i < n; i += gridDim.x)
     points_segment(ss, sil_r, tri, pref, ppitch, stage, flags, seg_counts, ctl, weight_maps, act[1 + i], spr,
-                   rowcnt);
+                   rowcnt, bsum);
 }
 
-// single CTA: exclusive scan of the segment counts, in chunks of 8192 (each
-// thread 8 consecutive counts as two 16 B loads: coalesced)
 __device__ void fit_grid_dev(DevCtl* ctl, int nx, int ny, int nz, int pad);
 
-__global__ void __launch_bounds__(1024) pre_scan_kernel(const int32_t* counts, int32_t* offsets, int n, int cap,
-                                                        DevCtl* ctl, int32_t* rowlist_reset, int nx, int ny, int nz,
-                                                        int pad) {
-  __shared__ int wsum[32];
-  __shared__ int carry_s;
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  int carry = 0;
-  for (int base = 0; base < n; base += 8192) {
-    const int i0 = base + (int)threadIdx.x * 8;
-    int v[8];
-    if (i0 + 8 <= n) {  // counts/offsets are 256 B aligned, i0 a multiple of 8
-      const int4 a = reinterpret_cast<const int4*>(counts + i0)[0], b = reinterpret_cast<const int4*>(counts + i0)[1];
-      v[0] = a.x, v[1] = a.y, v[2] = a.z, v[3] = a.w, v[4] = b.x, v[5] = b.y, v[6] = b.z, v[7] = b.w;
-    } else {
-#pragma unroll
-      for (int i = 0; i < 8; ++i) v[i] = i0 + i < n ? counts[i0 + i] : 0;
-    }
-    int tot = 0;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) tot += v[i];
-    int inc = tot;
-    for (int o = 1; o < 32; o <<= 1) {
-      const int t = __shfl_up_sync(0xffffffffu, inc, o);
-      if (lane >= o) inc += t;
-    }
-    if (lane == 31) wsum[wid] = inc;
-    __syncthreads();
-    if (wid == 0) {
-      int s = wsum[lane];
-      for (int o = 1; o < 32; o <<= 1) {
-        const int t = __shfl_up_sync(0xffffffffu, s, o);
-        if (lane >= o) s += t;
-      }
-      wsum[lane] = s;
-      if (lane == 31) carry_s = carry + s;
-    }
-    __syncthreads();
-    int run = carry + (wid ? wsum[wid - 1] : 0) + inc - tot;
-    int o8[8];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) o8[i] = run, run += v[i];
-    if (i0 + 8 <= n) {
-      reinterpret_cast<int4*>(offsets + i0)[0] = make_int4(o8[0], o8[1], o8[2], o8[3]);
-      reinterpret_cast<int4*>(offsets + i0)[1] = make_int4(o8[4], o8[5], o8[6], o8[7]);
-    } else {
-#pragma unroll
-      for (int i = 0; i < 8; ++i)
-        if (i0 + i < n) offsets[i0 + i] = o8[i];
-    }
-    carry = carry_s;
-    __syncthreads();  // wsum / carry_s are rewritten by the next chunk
-  }
-  if (threadIdx.x == 0) {
-    const int P = carry;
-    ctl->P = P;
-    ctl->status = P == 0 ? 2 : (P > cap ? 3 : 0);
-    ctl->voff = 0;
-    if (rowlist_reset) *rowlist_reset = 0;  // the frame's clear (launched before) has read the previous list
-    fit_grid_dev(ctl, nx, ny, nz, pad);
-  }
-}
-
 // one warp per active segment (the others hold no point): staged point -> its
-// rank in segment order
+// rank = the points of the row blocks before its row's block (bsum) + of the
+// block's rows before its row (rowcnt) + of the row's segments before it
+// (seg_counts), summed by the warp — no separate scan pass.  Warp 0 of CTA 0
+// first closes the preprocess: the point count P (sum of the block sums), the
+// status, and the grid fit from the bbox pre_points left (the splat follows).
 __global__ void __launch_bounds__(128) pre_gather_kernel(const __grid_constant__ SensorSet ss,
                                                          const Staged* __restrict__ stage,
                                                          const uint8_t* __restrict__ flags,
-                                                         const int32_t* __restrict__ row_offsets,
+                                                         const int32_t* __restrict__ rowcnt,
+                                                         const int32_t* __restrict__ bsum,
                                                          const int32_t* __restrict__ seg_counts, DevPoints pts,
-                                                         int spr, const int32_t* __restrict__ act) {
+                                                         int spr, const int32_t* __restrict__ act, int rows,
+                                                         DevCtl* ctl, int32_t* rowlist_reset, int nx, int ny, int nz,
+                                                         int pad) {
   const int lane = threadIdx.x & 31;
+  if (blockIdx.x == 0 && threadIdx.x < 32) {
+    int P = 0;
+    for (int j = lane; j < (rows + kRowBlock - 1) / kRowBlock; j += 32) P += bsum[j];
+    for (int o = 16; o > 0; o >>= 1) P += __shfl_xor_sync(0xffffffffu, P, o);
+    if (lane == 0) {
+      ctl->P = P;
+      ctl->status = P == 0 ? 2 : (P > pts.cap ? 3 : 0);
+      ctl->voff = 0;
+      if (rowlist_reset) *rowlist_reset = 0;  // the frame's clear (launched before) has read the previous list
+      fit_grid_dev(ctl, nx, ny, nz, pad);
+    }
+  }
   const int n = act[0];
   for (int i = blockIdx.x * 4 + (threadIdx.x >> 5); i < n; i += gridDim.x * 4) {
     const int seg = act[1 + i];
@@ -520,12 +484,15 @@ __global__ void __launch_bounds__(128) pre_gather_kernel(const __grid_constant__
     const int64_t pix = ss.pix_offset[k] + (int64_t)y * w + x;
     const bool is_pt = x < w && flags[pix];
     const unsigned ball = __ballot_sync(0xffffffffu, is_pt);
-    // the segment's rank: its row's offset + the points of the row's earlier segments
+    const int rb = row / kRowBlock;
     int before = 0;
+    for (int j = lane; j < rb; j += 32) before += bsum[j];
+    for (int j = rb * kRowBlock + lane; j < row; j += 32) before += rowcnt[j];
     for (int b = 0; b < sx; b += 32) before += b + lane < sx ? seg_counts[row * spr + b + lane] : 0;
     for (int o = 16; o > 0; o >>= 1) before += __shfl_xor_sync(0xffffffffu, before, o);
     if (!is_pt) continue;
-    const int idx = row_offsets[row] + before + __popc(ball & ((1u << lane) - 1u));
+    const int idx = before + __popc(ball & ((1u << lane) - 1u));
+    if (idx >= pts.cap) continue;  // status 3 (cannot happen: the capacity is one point per pixel)
     const Staged s = stage[pix];
     pts.pos[3 * idx + 0] = s.pos[0], pts.pos[3 * idx + 1] = s.pos[1], pts.pos[3 * idx + 2] = s.pos[2];
     pts.nrm[3 * idx + 0] = s.nrm[0], pts.nrm[3 * idx + 1] = s.nrm[1], pts.nrm[3 * idx + 2] = s.nrm[2];
@@ -568,7 +535,7 @@ struct Scratch {
   uint8_t* flags;     // per pixel
   uint16_t* pref;     // rows x ppitch
   int32_t* counts;    // per segment
-  int32_t* offsets;   // per segment
+  int32_t* bsum;      // per kRowBlock depth rows: points
   int32_t* act;       // [count, active segment ids...]
   int32_t* rowcnt;    // per depth row: points
   int ppitch, spr, nseg;
@@ -595,7 +562,7 @@ Scratch carve(const SensorSet& ss, void* base) {
   p = up(p + (size_t)rows * s.ppitch * sizeof(uint16_t));
   s.counts = reinterpret_cast<int32_t*>(p);
   p = up(p + (size_t)s.nseg * sizeof(int32_t));
-  s.offsets = reinterpret_cast<int32_t*>(p);
+  s.bsum = reinterpret_cast<int32_t*>(p);
   p = up(p + (size_t)s.nseg * sizeof(int32_t));
   s.act = reinterpret_cast<int32_t*>(p);
   p = up(p + (size_t)(s.nseg + 1) * sizeof(int32_t));
@@ -630,14 +597,12 @@ void launch_preprocess(const SensorSet& ss, DevPoints pts, float* weight_maps, i
   cudaMemsetAsync(s.act, 0, sizeof(int32_t), st);
   pre_prefix_tri_kernel<<<(rows * 32 + 255) / 256, 256, 0, st>>>(ss, rows, s.pref, s.ppitch, ctl, disc_mm, s.tri,
                                                                   s.spr, s.counts, s.flags, weight_maps, s.act,
-                                                                  s.rowcnt);
+                                                                  s.rowcnt, s.bsum);
   const int pgrid = s.nseg < sm_count() * 16 ? s.nseg : sm_count() * 16;  // resident one-warp CTAs (registers: 16 warps/SM)
   pre_points_kernel<<<pgrid, kSegPx, 0, st>>>(ss, sil_r, s.tri, s.pref, s.ppitch, s.stage, s.flags, s.counts, ctl,
-                                              weight_maps, s.act, s.spr, s.rowcnt);
-  // exclusive scan of the per-row point counts (segment order within a row is
-  // resolved by pre_gather from the segment counts)
-  pre_scan_kernel<<<1, 1024, 0, st>>>(s.rowcnt, s.offsets, rows, pts.cap, ctl, rowlist_reset, nx, ny, nz, padding);
-  pre_gather_kernel<<<sm_count() * 8, 128, 0, st>>>(ss, s.stage, s.flags, s.offsets, s.counts, pts, s.spr, s.act);
+                                              weight_maps, s.act, s.spr, s.rowcnt, s.bsum);
+  pre_gather_kernel<<<sm_count() * 8, 128, 0, st>>>(ss, s.stage, s.flags, s.rowcnt, s.bsum, s.counts, pts, s.spr, s.act,
+                                                    rows, ctl, rowlist_reset, nx, ny, nz, padding);
 }
 
 }  // namespace vc

@@ -344,7 +344,7 @@ int enqueue_frame(vc_ctx* ctx, const FrameCfg& f) {
   // the clear has joined, just before this frame's splat appends to it)
   launch_preprocess(ctx->ss, points(ctx), P<float>(ctx->wmaps), P<int32_t>(ctx->pre_scratch), ctx->ctl, f.nx, f.ny,
                     f.nz, f.pad, f.disc, f.sil_r, st, branch ? nullptr : P<int32_t>(ctx->rowlist));
-  n += 4;
+  n += 3;  // prefix + triangles, points, gather
   record(ctx, 1);
   if (branch) {
     cudaStreamWaitEvent(st, ctx->join[0], 0);
