@@ -579,6 +579,100 @@ __global__ void __launch_bounds__(FCfg<NY>::THREADS, FCfg<NY>::MINB) fy_kernel(c
   }
 }
 
+// ------------------------------------------------------------------ F-y, pipelined (1024 points)
+// At 1024 points the three staged 64 KB tiles hold the SM alone (one CTA), so
+// fy_kernel's loads and transforms never overlap.  Here persistent CTAs walk
+// the tiles of the live planes only (fy_planes_kernel lists them, and writes
+// every plane's flag for Z): as soon as a component's transform has released
+// its buffer, the next tile's same component is staged into it, under the
+// remaining transforms and the stores.  Same per-tile arithmetic as fy_kernel.
+__global__ void __launch_bounds__(256) fy_planes_kernel(const uint32_t* __restrict__ rowbits, int ny, int nzl,
+                                                        uint32_t* __restrict__ planeflag, int32_t* __restrict__ plist) {
+  const int z = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (z >= nzl) return;
+  bool any = rowbits == nullptr;
+  for (int y = lane; y < ny && !any; y += 32) any = __ldg(rowbits + (size_t)z * ny + y) != 0u;
+  const bool live = __any_sync(0xffffffffu, any);
+  if (lane == 0) {
+    planeflag[z] = live ? 1u : 0u;
+    if (live) plist[1 + atomicAdd(plist, 1)] = z;
+  }
+}
+
+template <int NY>
+__global__ void __launch_bounds__(FCfg<NY>::THREADS, 1)
+    fyp_kernel(const float2* S0, const float2* S1, const float2* __restrict__ S2, float2* O0, float2* O1, int nxh,
+               int H, int lk, const float2* __restrict__ tw, const uint32_t* __restrict__ rowbits,
+               const int32_t* __restrict__ plist, int ntx, int nzl) {
+  using S = Shape<NY>;
+  constexpr int T = S::R2, R1 = S::R1, kCW = FCfg<NY>::CW, TH = FCfg<NY>::THREADS;
+  extern __shared__ float2 sh[];  // 3 tiles of NY x kCW
+  float2* b0 = sh;
+  float2* b1 = sh + NY * kCW;
+  float2* b2 = sh + 2 * NY * kCW;
+  const int c = threadIdx.x % kCW, t = threadIdx.x / kCW;
+  const int ntiles = plist[0] * ntx;
+  int tile = blockIdx.x;
+  if (tile >= ntiles) return;
+  auto plane_of = [&](int tl) { return plist[1 + tl / ntx]; };
+  auto rmask = [&](int tl) {
+    return tl < ntiles ? row_flags<NY, kCW, TH>(rowbits ? rowbits + (size_t)plane_of(tl) * NY : nullptr) : 0u;
+  };
+  auto stage = [&](float2* dst, const float2* comp, int tl, uint32_t rm) {
+    if (tl < ntiles) stage_tile<NY, kCW, TH>(dst, comp + (size_t)plane_of(tl) * NY * H, H, (tl % ntx) * kCW, H, rm);
+    cp_async_commit();  // (empty groups keep the wait counts uniform)
+  };
+  {
+    const uint32_t rm = rmask(tile);
+    stage(b0, S0, tile, rm);
+    stage(b1, S1, tile, rm);
+    stage(b2, S2, tile, rm);
+  }
+  for (; tile < ntiles; tile += gridDim.x) {
+    const int next = tile + gridDim.x;
+    const uint32_t rmn = rmask(next);
+    const int z = plane_of(tile), kx = (tile % ntx) * kCW + c;
+    float2 d[R1], v[R1];
+    cp_async_wait<2>();  // this tile's S0 (S1, S2 and the next tiles' may be in flight)
+    __syncthreads();
+    tile_to_regs<NY, kCW>(b0, c, t, d);
+    __syncthreads();
+    ExCols<NY, kCW> e0{b0, c};
+    fft_line<NY, false>(d, t, tw, e0);
+    stage(b0, S0, next, rmn);
+    cp_async_wait<2>();
+    __syncthreads();
+    tile_to_regs<NY, kCW>(b1, c, t, v);
+    __syncthreads();
+    ExCols<NY, kCW> e1{b1, c};
+    fft_line<NY, false>(v, t, tw, e1);
+    stage(b1, S1, next, rmn);
+#pragma unroll
+    for (int k1 = 0; k1 < R1; ++k1) {
+      const float wy = signed_freq<NY>(t + T * k1);
+      d[k1] = make_float2(d[k1].x + wy * v[k1].x, d[k1].y + wy * v[k1].y);
+    }
+    cp_async_wait<2>();
+    __syncthreads();
+    tile_to_regs<NY, kCW>(b2, c, t, v);
+    __syncthreads();
+    ExCols<NY, kCW> e2{b2, c};
+    fft_line<NY, false>(v, t, tw, e2);
+    stage(b2, S2, next, rmn);
+    if (kx < nxh) {
+      const int kyl = 1 << lk;
+#pragma unroll
+      for (int k1 = 0; k1 < R1; ++k1) {
+        const int ky = t + T * k1;
+        const size_t o = ((size_t)((ky >> lk) * nzl + z) * kyl + (ky & (kyl - 1))) * H + kx;
+        st_out(O0 + o, d[k1]);
+        st_out(O1 + o, v[k1]);
+      }
+    }
+  }
+  cp_async_wait<0>();
+}
+
 // ------------------------------------------------------------------ Z (fused)
 // FFT_z(D) is parked in its staged tile while FFT_z(Z) runs (one register
 // array live, three CTAs per SM).
@@ -1197,6 +1291,7 @@ struct Prep {
       allow_smem(ix_kernel<N>, IXCfg<N>::SMEM);
     } else if (axis == 1) {
       allow_smem(fy_kernel<N>, FCfg<N>::NBUF * FCfg<N>::SMEM);
+      if constexpr (N == 1024) allow_smem(fyp_kernel<N>, 3 * FCfg<N>::SMEM);
       allow_smem(iy_kernel<N>, ICfg<N>::SMEM);
       allow_smem(iy_tma_kernel<N>, ICfg<N>::SMEM + 64);
     } else {
@@ -1235,13 +1330,32 @@ inline void col_grid(int nx, int cw, int* tiles, int* nyq, int bit) {
     *tiles = (nx / 2 + 1 + cw - 1) / cw, *nyq = -1;
   }
 }
+// VC_FYP=0 (A/B switch): the staged fy_kernel at 1024 points instead of fyp_kernel
+inline bool fyp_on() {
+  static const bool on = [] {
+    const char* e = std::getenv("VC_FYP");
+    return !e || std::atoi(e) != 0;
+  }();
+  return on;
+}
 template <int N>
 struct RunFy {
   static void run(const SlabFft& a) {
     using C = FCfg<N>;
     // (no Nyquist packing here: F-y's per-row empty flags make the packed
     // gather slower than the one wasted tile, measured)
-    dim3 grid((a.nx / 2 + 1 + C::CW - 1) / C::CW, a.nzl);
+    const int ntx = (a.nx / 2 + 1 + C::CW - 1) / C::CW;
+    if constexpr (N == 1024) {
+      if (fyp_on() && a.zoff == 0 && a.nzl == a.nz) {  // one GPU: the live-plane list sits after the nz flags
+        int32_t* plist = reinterpret_cast<int32_t*>(a.planeflag + a.nz);
+        cudaMemsetAsync(plist, 0, sizeof(int32_t), a.st);
+        fy_planes_kernel<<<(a.nzl * 32 + 255) / 256, 256, 0, a.st>>>(a.rowbits, a.ny, a.nzl, a.planeflag, plist);
+        fyp_kernel<N><<<sm_count(), C::THREADS, 3 * C::SMEM, a.st>>>(a.S0, a.S1, a.S2, a.O0, a.O1, a.nx / 2 + 1, a.H,
+                                                                     ilog2(a.kyl), a.twy, a.rowbits, plist, ntx, a.nzl);
+        return;
+      }
+    }
+    dim3 grid(ntx, a.nzl);
     fy_kernel<N><<<grid, C::THREADS, C::NBUF * C::SMEM, a.st>>>(a.S0, a.S1, a.S2, a.O0, a.O1, a.nx / 2 + 1, a.H,
                                                           ilog2(a.kyl), a.twy, a.rowbits, a.planeflag + a.zoff);
   }

@@ -286,7 +286,7 @@ vc_status ensure_rank(DistRank& rk, const Geo& g, const vc_sensor* sensors, cons
   VC_TRY(ensure(ctx, ctx->acc, Nl * sizeof(float4)));
   VC_TRY(ensure(ctx, ctx->rowbits, (size_t)g.ny * g.nzl * sizeof(uint32_t)));
   VC_TRY(ensure(ctx, ctx->rowlist, ((size_t)g.ny * g.nzl + 1) * sizeof(int32_t)));
-  VC_TRY(ensure(ctx, ctx->planeflag, (size_t)g.nz * sizeof(uint32_t) + 256));
+  VC_TRY(ensure(ctx, ctx->planeflag, (size_t)(2 * g.nz + 2) * sizeof(uint32_t) + 256));  // flags + F-y live-plane list
   VC_TRY(ensure(ctx, ctx->spec, 3 * g.E * sizeof(float2)));
   VC_TRY(ensure(ctx, rk.sd, 2 * g.E * sizeof(float2)));
   VC_TRY(ensure(ctx, ctx->A, g.plane * (g.nzl + 3) * sizeof(float)));

@@ -270,7 +270,7 @@ vc_status ensure_grid(vc_ctx* ctx, int nx, int ny, int nz) {
   VC_TRY(ensure(ctx, ctx->acc, N * sizeof(float4)));
   VC_TRY(ensure(ctx, ctx->rowbits, (size_t)ny * nz * sizeof(uint32_t)));
   VC_TRY(ensure(ctx, ctx->rowlist, ((size_t)ny * nz + 1) * sizeof(int32_t)));
-  VC_TRY(ensure(ctx, ctx->planeflag, (size_t)nz * sizeof(uint32_t) + 256));
+  VC_TRY(ensure(ctx, ctx->planeflag, (size_t)(2 * nz + 2) * sizeof(uint32_t) + 256));  // flags + F-y's live-plane list
   if (ctx->acc.p != acc_before || ctx->nx != nx || ctx->ny != ny || ctx->nz != nz || ctx->layout != 1)
     ctx->acc_dirty = true;
   ctx->layout = 1;

@@ -146,7 +146,7 @@ struct SlabFft {
   cudaStream_t st;
   float2* rowmm;
   const uint32_t* rowbits;
-  uint32_t* planeflag;     // nz entries (global); F-y writes [zoff, zoff+nzl)
+  uint32_t* planeflag;     // nz entries (global); F-y writes [zoff, zoff+nzl); one GPU: + nz+1 (live-plane list)
   const int32_t* rowlist;  // touched-row list [count, rows...] (F-x works through it), or null: all rows
 };
 void launch_fft_forward_xy(const SlabFft& a);

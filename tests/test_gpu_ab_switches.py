@@ -7,9 +7,10 @@ variant runs in a child process):
   kernels instead of the fused scan + emit (k_mc.cu): same mesh, bit for bit,
   on the same fields (a smooth one, and a noise field past the initial
   capacity, which regrows and reruns).
-* VC_ZP=0 — the staged z_kernel<1024> instead of the pipelined zp_kernel<1024>
-  (k_fft.cu): the same per-tile arithmetic in the same order (two kernels,
-  so the compiler's FMA contraction may differ: rel-L2 < 1e-6)."""
+* VC_ZP=0 / VC_FYP=0 — the staged z_kernel<1024> / fy_kernel<1024> instead of
+  the pipelined zp_kernel / fyp_kernel (k_fft.cu): the same per-tile
+  arithmetic in the same order (two kernels, so the compiler's FMA
+  contraction may differ: rel-L2 < 1e-6)."""
 import os
 import subprocess
 import sys
@@ -37,7 +38,9 @@ m1 = vc.marching_cubes(smooth, g1, 0.0, ctx=ctx)
 m2 = vc.marching_cubes(noise, g2, 0.0, ctx=ctx)
 f = rng.normal(size=(1024, 4, 8, 3)).astype(np.float32)   # (z, y, x, component): a 1024-plane Z pass
 a = vc.integrate_fft(f, ctx=ctx)
-np.savez(sys.argv[1], v1=m1.vertices, t1=m1.triangles, n1=m1.normals, v2=m2.vertices, t2=m2.triangles, a=a)
+f2 = rng.normal(size=(4, 1024, 8, 3)).astype(np.float32)  # a 1024-point F-y pass
+a2 = vc.integrate_fft(f2, ctx=ctx)
+np.savez(sys.argv[1], v1=m1.vertices, t1=m1.triangles, n1=m1.normals, v2=m2.vertices, t2=m2.triangles, a=a, a2=a2)
 print("ok")
 '''
 
@@ -55,9 +58,10 @@ def _run(tmp_path, name, env_extra):
 def test_ab_switches_match_default(tmp_path):
     base = _run(tmp_path, "default", {})
     split = _run(tmp_path, "mc_split", {"VC_MC_SPLIT": "1"})
-    staged = _run(tmp_path, "z_staged", {"VC_ZP": "0"})
+    staged = _run(tmp_path, "staged", {"VC_ZP": "0", "VC_FYP": "0"})
     assert base["v1"].shape[0] > 10000 and base["v2"].shape[0] > 40 ** 3 // 16
     for k in ("v1", "t1", "n1", "v2", "t2"):
         assert np.array_equal(base[k], split[k]), k
-    a, b = base["a"].astype(np.float64), staged["a"].astype(np.float64)
-    assert np.linalg.norm(a - b) / np.linalg.norm(a) < 1e-6
+    for k in ("a", "a2"):
+        a, b = base[k].astype(np.float64), staged[k].astype(np.float64)
+        assert np.linalg.norm(a - b) / np.linalg.norm(a) < 1e-6, k
