@@ -75,6 +75,9 @@ WORKLOADS = {
                    "C4: 4096-frame kick stream (make_kick_sequence(4096)), 4 views 512x424 depth+RGB, 256^3 grid, "
                    "frame-parallel shards over the ranks; each rank reconstructs its whole shard once",
                    stream=4096, host_ring=512),
+    # one GPU: whole 1024^3 frames (two in flight: ~40 GB of buffers each); N>1: run_c5's z-slab decomposition
+    "c5": Workload("c5", "reconstructed frames/sec at 1024^3 grid, 4x512x424 RGB-D views", (1024, 1024, 1024), 4, False,
+                   4, "C5: 4 views 512x424 of the kick stream (4 resident frames), 1024^3 grid, weighted splat"),
 }
 WORKLOAD = WORKLOADS["c2"].text
 DIMS = WORKLOADS["c2"].dims
@@ -387,7 +390,7 @@ def run_gpu(args):
     wl = WORKLOADS[args.workload]
     K, dims = wl.k, wl.dims
     lib = L.lib()
-    S = max(1, args.streams)
+    S = max(1, args.streams if args.streams else (2 if wl.key == "c5" else 4))
     ctxs = [vc.Context(local) for _ in range(S)]  # one context (stream + buffers) per concurrent frame
     ctx = ctxs[0]
     h = ctx.handle
@@ -523,13 +526,14 @@ def run_gpu(args):
 
     if rank == 0:
         cmp = None
-        if world == 1 and not args.no_fft_comparator:
+        if world == 1 and not args.no_fft_comparator and wl.key != "c5":  # (the C2 line times 1024^3 too)
             cmp = fft_comparator(lib, local, [dims[0], 1024] if dims[0] < 1024 else [dims[0]])
             frame_fft = sum(kernel_ms[k] for k in ("fft_x", "fft_y", "fft_z", "ifft_y", "ifft_x"))
             for c in cmp:
                 if c.get("grid") == list(dims):
                     c["ours_in_frame_ms"] = frame_fft  # the frame's chain with the splat's sparsity
-        cpu = cpu_baseline_sample(wl) if (world == 1 and not args.no_cpu_baseline) else None
+        # (none at 1024^3: the reference's CPU path takes minutes per frame there)
+        cpu = cpu_baseline_sample(wl) if (world == 1 and not args.no_cpu_baseline and wl.key != "c5") else None
         line = {
             "metric": wl.metric, "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
@@ -579,9 +583,9 @@ C5_METRIC = "reconstructed frames/sec at 1024^3 grid, 4x512x424 RGB-D views"
 
 
 def run_c5(args):
-    """Config C5: one 1024^3 frame per step.  N=1: the single-GPU frame path
-    (fits: ~40 GB); N>1 (torchrun): the z-slab decomposition over NCCL
-    (vc_reconstruct_frame_dist), strong scaling, time = max over ranks."""
+    """Config C5 on N>1 GPUs (torchrun): one 1024^3 frame per step through the
+    z-slab decomposition over NCCL (vc_reconstruct_frame_dist), strong
+    scaling, time = max over ranks.  (N=1 runs whole frames in run_gpu.)"""
     rank, world, local = dist_env()
     import torch
     from paper_1712_03084_b200 import _lib as L
@@ -590,17 +594,15 @@ def run_c5(args):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     lib = L.lib()
-    sr = None
-    if world > 1:
-        import torch.distributed as dist
-        from paper_1712_03084_b200.slab import SlabReconstructor, nccl_unique_id
-        dist.init_process_group("nccl", device_id=dev)
-        obj = [nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0)
-        sr = SlabReconstructor.nccl(world, rank, local, obj[0])
-        ctx = sr.contexts[0]
-    else:
-        ctx = vc.Context(local)
+    if world < 2:
+        raise SystemExit("run_c5 is the N>1 z-slab path")
+    import torch.distributed as dist
+    from paper_1712_03084_b200.slab import SlabReconstructor, nccl_unique_id
+    dist.init_process_group("nccl", device_id=dev)
+    obj = [nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    sr = SlabReconstructor.nccl(world, rank, local, obj[0])
+    ctx = sr.contexts[0]
     h = ctx.handle
     stream = torch.cuda.ExternalStream(ctx.stream(), device=dev)
     rig = vc.make_circle_rig(K_VIEWS, 0, 2500, W, H, F)
@@ -640,12 +642,8 @@ def run_c5(args):
     d2h = [0]
 
     def frame(i, views):
-        if sr is None:
-            L.check(lib.vc_reconstruct_frame(h, sensors, views[i % C5_FRAMES], K_VIEWS, C.byref(cfg), C.byref(out),
-                                             None), h)
-        else:
-            L.check(lib.vc_reconstruct_frame_dist(sr._h, sensors, views[i % C5_FRAMES], K_VIEWS, C.byref(cfg),
-                                                  C.byref(out), C.byref(info), None), h)
+        L.check(lib.vc_reconstruct_frame_dist(sr._h, sensors, views[i % C5_FRAMES], K_VIEWS, C.byref(cfg),
+                                              C.byref(out), C.byref(info), None), h)
         d2h[0] += out.vertex_count * (12 + 12 + 24 + 3 + 1 + K_VIEWS * 13) + out.triangle_count * 12
 
     def timed(views, steps):
@@ -668,29 +666,23 @@ def run_c5(args):
         ms, _ = timed(dev_views, args.steps)
     value = args.steps / (ms / 1000.0)
     tm = L.StageTimings()
-    if sr is None:
-        prof = profile_kernels(lib, h, sensors, dev_views[:2], cfg, C5_DIMS, out)
-        roofline, stages, kernel_ms = prof["roofline"], prof["stages"], prof["kernel_ms"]
-        launches = lib.vc_ctx_kernels_per_frame(h) * args.steps
-        mesh = {"points": prof["P"], "vertices": prof["V"], "triangles": prof["T"]}
-    else:
-        L.check(lib.vc_reconstruct_frame_dist(sr._h, sensors, dev_views[0], K_VIEWS, C.byref(cfg), C.byref(out),
-                                              C.byref(info), C.byref(tm)), h)
-        stages = {nm: getattr(tm, nm) for nm, _ in L.StageTimings._fields_}
-        kernel_ms = None
-        # slab integrate: this rank's share of the whole-grid FFT chain bytes over fft_ms (incl. the exchanges)
-        nx, ny, nz = C5_DIMS
-        Nh = nz * ny * (nx // 2 + 1)
-        fft_bytes = (16 * nx * ny * nz + 3 * 8 * Nh + 2 * 3 * 8 * Nh + 4 * 8 * Nh + 2 * 8 * Nh + 8 * Nh
-                     + 4 * nx * ny * nz) / world
-        pk = peaks()
-        hbm = float(pk.get("hbm_gbs", 6650.0))
-        ach = fft_bytes / (tm.fft_ms * 1e-3) / 1e9
-        roofline = {"bound": "hbm", "kernel": "slab integrate (x/y, all-to-all, z, all-to-all, y/x)",
-                    "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm, "traffic": None,
-                    "algorithmic_bytes": fft_bytes, "avg_launch_ms": tm.fft_ms}
-        launches = None
-        mesh = {"vertices_total": info.vertex_total, "triangles_total": info.triangle_total}
+    L.check(lib.vc_reconstruct_frame_dist(sr._h, sensors, dev_views[0], K_VIEWS, C.byref(cfg), C.byref(out),
+                                          C.byref(info), C.byref(tm)), h)
+    stages = {nm: getattr(tm, nm) for nm, _ in L.StageTimings._fields_}
+    kernel_ms = None
+    # slab integrate: this rank's share of the whole-grid FFT chain bytes over fft_ms (incl. the exchanges)
+    nx, ny, nz = C5_DIMS
+    Nh = nz * ny * (nx // 2 + 1)
+    fft_bytes = (16 * nx * ny * nz + 3 * 8 * Nh + 2 * 3 * 8 * Nh + 4 * 8 * Nh + 2 * 8 * Nh + 8 * Nh
+                 + 4 * nx * ny * nz) / world
+    pk = peaks()
+    hbm = float(pk.get("hbm_gbs", 6650.0))
+    ach = fft_bytes / (tm.fft_ms * 1e-3) / 1e9
+    roofline = {"bound": "hbm", "kernel": "slab integrate (x/y, all-to-all, z, all-to-all, y/x)",
+                "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm, "traffic": None,
+                "algorithmic_bytes": fft_bytes, "avg_launch_ms": tm.fft_ms}
+    launches = None
+    mesh = {"vertices_total": info.vertex_total, "triangles_total": info.triangle_total}
     lib.vc_ctx_set_output(h, L.VC_MEM_HOST)
     for i in range(min(args.warmup, 2)):
         frame(i, host_views)
@@ -700,7 +692,7 @@ def run_c5(args):
                 "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
                 "config": {"workload": "C5: 4 views 512x424 of the kick stream, 1024^3 grid, weighted splat",
-                           "grid": list(C5_DIMS), "parallelism": "single GPU" if world == 1 else f"z-slab x{world}",
+                           "grid": list(C5_DIMS), "parallelism": f"z-slab x{world}",
                            "l2": "working set ~40 GB >> 126 MB L2"},
                 "e2e": {"value": args.steps / (e2e_ms / 1000.0), "unit": "frames/s",
                         "h2d_bytes_per_step": frame_bytes, "d2h_bytes_per_step": int(d2h_per)},
@@ -711,9 +703,8 @@ def run_c5(args):
         print(json.dumps(line), flush=True)
     lib.vc_device_free(h, dbuf)
     lib.vc_host_free(h, hbuf)
-    if sr is not None:
-        sr.close()
-        torch.distributed.destroy_process_group()
+    sr.close()
+    torch.distributed.destroy_process_group()
 
 
 def free_port():
@@ -767,8 +758,8 @@ def main():
                     help="c2: the BASELINE metric (256^3 stream, frame-parallel); c3: 512^3, 6 views + HD colour; "
                          "c4: the 4096-frame stream, each rank's shard once (--steps ignored); "
                          "c5: 1024^3 frames (z-slabs on N>1)")
-    ap.add_argument("--streams", type=int, default=4,
-                    help="concurrent frames per GPU (one context + host thread each)")
+    ap.add_argument("--streams", type=int, default=None,
+                    help="concurrent frames per GPU (one context + host thread each; default 4, c5: 2)")
     ap.add_argument("--plan", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
     if args.warmup < 3 and args.impl != "reference":
@@ -786,7 +777,7 @@ def main():
         if args.workload == "c5":
             raise SystemExit("--impl reference runs c2/c3 (the CPU path at 1024^3 takes minutes per frame)")
         run_reference(args)
-    elif args.workload == "c5":
+    elif args.workload == "c5" and world > 1:
         run_c5(args)
     else:
         run_gpu(args)
