@@ -57,10 +57,27 @@ __global__ void __launch_bounds__(128, 8) texture_kernel(const __grid_constant__
                                                       double eps_vis, uint8_t* vis, float2* uv, float* wout,
                                                       uint8_t* untex, uint8_t* rgb, float* posf, int v_cap,
                                                       int lg) {
+  // the K sensors' parameters in shared memory: a warp's lanes index them by
+  // view, and divergent indices into the kernel-parameter bank serialise
+  __shared__ DevSensor sh_s[kMaxViews];
+  __shared__ ViewPtrs sh_v[kMaxViews];
+  __shared__ int64_t sh_off[kMaxViews];
   if (ctl->status != 0 || ctl->overflow) return;
   const int V = ctl->V;
   if (V > v_cap) return;
   const int G = 1 << lg, K = ss.k;
+  {
+    static_assert(sizeof(DevSensor) % 8 == 0 && sizeof(ViewPtrs) % 8 == 0, "8-byte words");
+    constexpr int WS = sizeof(DevSensor) / 8, WV = sizeof(ViewPtrs) / 8;
+    const uint64_t* gs = reinterpret_cast<const uint64_t*>(ss.s);
+    const uint64_t* gv = reinterpret_cast<const uint64_t*>(ss.v);
+    uint64_t* ds = reinterpret_cast<uint64_t*>(sh_s);
+    uint64_t* dv = reinterpret_cast<uint64_t*>(sh_v);
+    for (int j = threadIdx.x; j < K * WS; j += blockDim.x) ds[j] = gs[j];
+    for (int j = threadIdx.x; j < K * WV; j += blockDim.x) dv[j] = gv[j];
+    for (int j = threadIdx.x; j < K; j += blockDim.x) sh_off[j] = ss.pix_offset[j];
+    __syncthreads();
+  }
   const int lane = threadIdx.x & 31, k = lane & (G - 1), lead = lane - k;
   const int per_warp = 32 >> lg;
   const int warps = gridDim.x * (blockDim.x >> 5);
@@ -75,8 +92,8 @@ __global__ void __launch_bounds__(128, 8) texture_kernel(const __grid_constant__
     double tr = 0.0, tg = 0.0, tb = 0.0, twd = 0.0;
     if (live) {
       const d3 X = mk3(vpos[3 * i], vpos[3 * i + 1], vpos[3 * i + 2]);
-      const DevSensor& s = ss.s[k];
-      const ViewPtrs& v = ss.v[k];
+      const DevSensor& s = sh_s[k];
+      const ViewPtrs& v = sh_v[k];
       // texture.cpp:19-31 — world_to_cam = pose.inverse(); lround pixel
       const d3 local = add3(mat3(s.Ri, X), ld3(s.ti));
       double u, w;
@@ -100,7 +117,7 @@ __global__ void __launch_bounds__(128, 8) texture_kernel(const __grid_constant__
           if (project_local(s.fx, s.fy, s.cx, s.cy, mat3t(s.R, sub3(X, ld3(s.t))), &ud, &vd)) {
             const long long px = lround_d(ud), py = lround_d(vd);
             if (px >= 0 && px < s.w && py >= 0 && py < s.h)
-              wk = __ldg(weight_maps + ss.pix_offset[k] + py * s.w + px);
+              wk = __ldg(weight_maps + sh_off[k] + py * s.w + px);
           }
           // rasterize.cpp:136-150 at the vertex: skip w <= 1e-9, terms w*s
           const double wd = (double)wk;
