@@ -30,10 +30,17 @@
 namespace vc {
 namespace {
 
-__constant__ int8_t c_mc_count[256];
-__constant__ int8_t c_mc_tris[256][5][3];
-__constant__ int8_t c_edge_c0[12];  // low corner of each cube edge
-__constant__ int8_t c_edge_axis[12];
+// The case tables in global memory, read through L1: the kernels index them by
+// each lane's cell case, and divergent indices into the constant bank
+// serialise (they were a fifth of the triangle pass's stalls).
+__device__ int8_t g_mc_count[256];
+__device__ int8_t g_mc_tris[256][5][3];
+__device__ __forceinline__ int mc_count(int cfg) { return __ldg(&g_mc_count[cfg]); }
+__device__ __forceinline__ int mc_tri_edge(int cfg, int tri, int m) { return __ldg(&g_mc_tris[cfg][tri][m]); }
+// cube edge e (marching_cubes.cpp:15-19): axis e / 4; low corner 2e (x edges),
+// {0, 1, 4, 5} (y edges), e - 8 (z edges) — corner bits (x, y, z)
+__device__ __forceinline__ int edge_axis(int e) { return e >> 2; }
+__device__ __forceinline__ int edge_c0(int e) { return e < 4 ? 2 * e : (e < 8 ? (e & 1) | ((e & 2) << 1) : e - 8); }
 
 
 __device__ __forceinline__ float vol_at(const float* A, int nx, int ny, int x, int y, int z) {
@@ -386,7 +393,7 @@ __device__ __forceinline__ int3 count_unit(const float* __restrict__ A, int nx, 
   for (uint32_t mm = cmask; mm; mm &= mm - 1) {
     const int x = ((__ffs(mm) - 1) << 5) + lane;
     const VoxelInfo vi = classify_voxel(A, nx, ny, x, y, z, hy, hz, Lf);
-    const int nt = vi.cfg >= 0 && own ? c_mc_count[vi.cfg] : 0;
+    const int nt = vi.cfg >= 0 && own ? mc_count(vi.cfg) : 0;
     c.x += __popc(vi.mask), c.y += nt, c.z += nt > 0 ? 1 : 0;
     if (x < nx) info[x] = (uint16_t)(vi.mask | (nt > 0 ? (vi.cfg << 3) | (1 << 11) : 0));
   }
@@ -595,7 +602,7 @@ __device__ __forceinline__ void emit_unit(const float* __restrict__ A, int nx, i
     const int mask = inf & 7;
     const bool cell = (inf >> 11) & 1;
     const int cfg = (inf >> 3) & 255;
-    const int nt = cell ? c_mc_count[cfg] : 0;
+    const int nt = cell ? mc_count(cfg) : 0;
     const int3 cnt = make_int3(__popc(mask), nt, cell ? 1 : 0);
     int3 inc = cnt;  // warp inclusive scan
     for (int o = 1; o < 32; o <<= 1) {
@@ -776,12 +783,12 @@ __device__ __forceinline__ void tris_of(int nx, int ny, int voff, const MeshBufs
   const size_t v = (size_t)mb.cells[i];
   const int tb = mb.cell_tri[i];
   const int cfg = mb.cell_cfg[i];
-  const int n = c_mc_count[cfg];
+  const int n = mc_count(cfg);
   for (int tri = 0; tri < n; ++tri) {
     int ids[3];
     for (int m = 0; m < 3; ++m) {
-      const int e = c_mc_tris[cfg][tri][m];
-      const int c0 = c_edge_c0[e], axis = c_edge_axis[e];
+      const int e = mc_tri_edge(cfg, tri, m);
+      const int c0 = edge_c0(e), axis = edge_axis(e);
       const size_t owner = v + (c0 & 1) + ((c0 >> 1) & 1) * (size_t)nx + ((c0 >> 2) & 1) * plane;
       const uint32_t pk = mb.vbase[owner];
       ids[m] = voff + (int)(pk >> 3) + __popc(pk & 7u & ((1u << axis) - 1u));
@@ -829,12 +836,8 @@ void launch_mc_set_voff(const int32_t* counts, int rank, DevCtl* ctl, cudaStream
 }
 
 void upload_case_table_data(const int8_t* counts, const int8_t* tris, cudaStream_t st) {
-  cudaMemcpyToSymbolAsync(c_mc_count, counts, 256, 0, cudaMemcpyHostToDevice, st);
-  cudaMemcpyToSymbolAsync(c_mc_tris, tris, 256 * 15, 0, cudaMemcpyHostToDevice, st);
-  const int8_t c0[12] = {0, 2, 4, 6, 0, 1, 4, 5, 0, 1, 2, 3};  // marching_cubes.cpp:15-19
-  const int8_t ax[12] = {0, 0, 0, 0, 1, 1, 1, 1, 2, 2, 2, 2};
-  cudaMemcpyToSymbolAsync(c_edge_c0, c0, 12, 0, cudaMemcpyHostToDevice, st);
-  cudaMemcpyToSymbolAsync(c_edge_axis, ax, 12, 0, cudaMemcpyHostToDevice, st);
+  cudaMemcpyToSymbolAsync(g_mc_count, counts, 256, 0, cudaMemcpyHostToDevice, st);
+  cudaMemcpyToSymbolAsync(g_mc_tris, tris, 256 * 15, 0, cudaMemcpyHostToDevice, st);
   cudaStreamSynchronize(st);
 }
 
