@@ -70,6 +70,17 @@ __device__ double trilinear(const float* A, const DevGrid& g, double vx, double 
   return dadd(dmul(c0, uz), dmul(c1, tz));
 }
 
+// Fixed-order sum over 256 threads (deterministic): butterfly within each
+// warp, then the 8 warp sums in order by thread 0 (the result is thread 0's).
+__device__ __forceinline__ double block_sum_256(double v, double* sh) {
+  for (int o = 16; o > 0; o >>= 1) v = dadd(v, __shfl_xor_sync(0xffffffffu, v, o));
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = v;
+  __syncthreads();
+  double s = 0.0;
+  if (threadIdx.x == 0)
+    for (int w = 0; w < 8; ++w) s = dadd(s, sh[w]);
+  return s;
+}
 constexpr int kIsoBlocks = 296;
 
 __device__ void iso_final_tree(const double* partial, int n, DevCtl* ctl, double* sh);
@@ -90,15 +101,10 @@ __global__ void __launch_bounds__(256) iso_partial_kernel(const double* __restri
       sum = dadd(sum, trilinear(A, g, vx, vy, vz));
     }
   }
-  sh[threadIdx.x] = sum;
-  __syncthreads();
-  for (int o = 128; o > 0; o >>= 1) {
-    if (threadIdx.x < o) sh[threadIdx.x] = dadd(sh[threadIdx.x], sh[threadIdx.x + o]);
-    __syncthreads();
-  }
+  sum = block_sum_256(sum, sh);
   __shared__ bool last;
   if (threadIdx.x == 0) {
-    partial[blockIdx.x] = sh[0];
+    partial[blockIdx.x] = sum;
     __threadfence();
     last = atomicAdd(&ctl->iso_ticket, 1) == (int)gridDim.x - 1;
   }
@@ -108,18 +114,13 @@ __global__ void __launch_bounds__(256) iso_partial_kernel(const double* __restri
   iso_final_tree(partial, gridDim.x, ctl, sh);
   if (threadIdx.x == 0) ctl->iso_ticket = 0;
 }
-// 512-slot tree over the partials (slot i >= n holds 0) with 256 threads: the
-// first level adds slots t and t+256, then halves, as iso_final_kernel does
+// the partials (slot i >= n holds 0): thread t adds slots t and t + 256, then
+// the block sum, as iso_final_kernel does
 __device__ void iso_final_tree(const double* partial, int n, DevCtl* ctl, double* sh) {
   const int t = threadIdx.x;
   const volatile double* vp = partial;
-  sh[t] = dadd(t < n ? vp[t] : 0.0, t + 256 < n ? vp[t + 256] : 0.0);
-  __syncthreads();
-  for (int o = 128; o > 0; o >>= 1) {
-    if (t < o) sh[t] = dadd(sh[t], sh[t + o]);
-    __syncthreads();
-  }
-  if (t == 0 && ctl->status == 0) ctl->level = ddiv(sh[0], (double)ctl->P);
+  const double s = block_sum_256(dadd(t < n ? vp[t] : 0.0, t + 256 < n ? vp[t + 256] : 0.0), sh);
+  if (t == 0 && ctl->status == 0) ctl->level = ddiv(s, (double)ctl->P);
 }
 
 // trilinear()'s lower z plane of the point, owned by exactly one slab
@@ -148,24 +149,13 @@ __global__ void __launch_bounds__(256) iso_partial_samples_kernel(const double* 
     const int P = ctl->P;
     for (int p = blockIdx.x * 256 + threadIdx.x; p < P; p += gridDim.x * 256) sum = dadd(sum, samples[p]);
   }
-  sh[threadIdx.x] = sum;
-  __syncthreads();
-  for (int o = 128; o > 0; o >>= 1) {
-    if (threadIdx.x < o) sh[threadIdx.x] = dadd(sh[threadIdx.x], sh[threadIdx.x + o]);
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) partial[blockIdx.x] = sh[0];
+  sum = block_sum_256(sum, sh);
+  if (threadIdx.x == 0) partial[blockIdx.x] = sum;
 }
 
-__global__ void iso_final_kernel(const double* partial, int n, DevCtl* ctl) {
-  __shared__ double sh[512];
-  sh[threadIdx.x] = threadIdx.x < n ? partial[threadIdx.x] : 0.0;
-  __syncthreads();
-  for (int o = 256; o > 0; o >>= 1) {
-    if (threadIdx.x < o) sh[threadIdx.x] = dadd(sh[threadIdx.x], sh[threadIdx.x + o]);
-    __syncthreads();
-  }
-  if (threadIdx.x == 0 && ctl->status == 0) ctl->level = ddiv(sh[0], (double)ctl->P);
+__global__ void __launch_bounds__(256) iso_final_kernel(const double* partial, int n, DevCtl* ctl) {
+  __shared__ double sh[8];
+  iso_final_tree(partial, n, ctl, sh);  // the same order as the single-GPU path's last CTA
 }
 
 struct VoxelInfo {
@@ -949,7 +939,7 @@ void launch_iso_samples(const DevPoints& pts, const float* A, const DevCtl* ctl,
 
 void launch_iso_final_samples(const double* samples, DevCtl* ctl, double* partial, cudaStream_t st) {
   iso_partial_samples_kernel<<<kIsoBlocks, 256, 0, st>>>(samples, ctl, partial);
-  iso_final_kernel<<<1, 512, 0, st>>>(partial, kIsoBlocks, ctl);
+  iso_final_kernel<<<1, 256, 0, st>>>(partial, kIsoBlocks, ctl);
 }
 
 }  // namespace vc
