@@ -13,15 +13,19 @@
 //               row's straddling 32-voxel chunks only: owned cut edges
 //               (+x,+y,+z, sign test vals >= level in fp64, :168-171) and the
 //               cell's triangle count from the generated table; caches each
-//               voxel's (mask, case) and the row's chunk mask
-//   mc_scan     exclusive scan of the per-row totals, one pass over 1024-unit
-//               tiles with decoupled look-back
-//   mc_emit     one warp per active row, its straddling chunks; vertex ids = rank of the cut edge in
-//               global edge id order ((z*ny+y)*nx+x)*3+axis (:139-142); fp64
-//               positions (:153-155, volume.hpp:45); compact list of cells
-//   mc_normals  one thread per vertex: gradient normals (:180-207)
-//   mc_tris     one thread per active cell: triangles in the reference's cell
-//               scan order (z, y, x), table order within the cell
+//               voxel's (mask, case) and the row's chunk mask; per-256-row
+//               block sums of the (vertex, triangle, cell) counts
+//   mc_scan_emit  per 8-row tile: its first ids from the block sums and row
+//               counts before it, then one warp per row over its straddling
+//               chunks; vertex ids = rank of the cut edge in global edge id
+//               order ((z*ny+y)*nx+x)*3+axis (:139-142); fp64 positions
+//               (:153-155, volume.hpp:45); compact list of cells
+//               (the z-slab path splits this into mc_scan, a 1024-row-tile
+//               look-back, and mc_emit: its vertex ids need the other ranks'
+//               counts between the two)
+//   mc_finish   one thread per vertex (gradient normals, :180-207) or per
+//               active cell (triangles in the reference's cell scan order
+//               (z, y, x), table order within the cell)
 #include <cstdlib>
 #include <cfloat>
 
