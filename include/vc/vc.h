@@ -161,9 +161,10 @@ vc_status vc_ctx_set_graphs(vc_ctx* ctx, int32_t enable);
 void* vc_ctx_stream(vc_ctx* ctx);
 /* Number of kernels one vc_reconstruct_frame launches (excluding retries). */
 int32_t vc_ctx_kernels_per_frame(const vc_ctx* ctx);
-/* Per-kernel CUDA-event times (ms) of the last frame run with profiling on,
- * in launch order: preprocess (3 kernels), clear, splat, fft_x, fft_y, fft_z,
- * ifft_y, ifft_x, iso(2), mc(4), texture(2).  Returns the count written. */
+/* Per-stage CUDA-event times (ms) of the last frame run with profiling on, 11
+ * entries: preprocess (3 kernels), clear, splat (+ touched-row list), fft_x,
+ * fft_y, fft_z, ifft_y, ifft_x, iso, mc (4 kernels), texture.  Returns the
+ * count written. */
 int32_t vc_ctx_kernel_times(const vc_ctx* ctx, double* ms, int32_t max_n);
 /* Pinned host memory helpers (for zero-staging H2D of views). */
 vc_status vc_host_alloc(vc_ctx* ctx, size_t bytes, void** out);

@@ -325,10 +325,10 @@ int enqueue_frame(vc_ctx* ctx, const FrameCfg& f) {
   cudaStream_t st = ctx->st;
   int n = 0;
   // the clear walks the previous frame's touched-row list: before the
-  // preprocess, whose scan resets the list for this frame's splat
+  // preprocess, whose gather pass resets the list for this frame's splat
   // Graph branches (not in profiled frames, which time each kernel on one
-  // stream): the clear runs beside the preprocess, the MC normals beside the
-  // triangles and texturing.
+  // stream): the clear runs beside the preprocess, the MC normals and
+  // triangles beside the texturing.
   const bool branch = !ctx->profiling && ctx->aux;
   record(ctx, 12);
   if (branch) {
