@@ -197,13 +197,25 @@ def test_integrate_blob_and_zero(ctx):
 
 
 def test_integrate_large_sizes(O, ctx):
-    for shape in [(512, 4, 8), (4, 512, 8), (8, 4, 1024), (1024, 8, 4)]:
+    for shape in [(512, 4, 8), (4, 512, 8), (8, 4, 1024), (1024, 8, 4), (4, 1024, 8)]:
         rng = np.random.default_rng(1)
         field = rng.normal(size=shape + (3,)).astype(np.float32)
         assert rel_l2(vc.integrate_fft(field, ctx=ctx), O.integrate_fft(field.astype(np.float64))) < 2e-5
 
 
 # ------------------------------------------------------------------ whole frame A
+@pytest.mark.parametrize("dims", [(64, 1024, 64), (64, 64, 1024), (1024, 64, 64)])
+def test_indicator_field_1024_point_axes(O, scene, ctx, dims):
+    """The 1024-point passes on sparse frame fields against the oracle: the
+    pipelined F-y (live-plane list) and Z kernels and the 1024-point x passes
+    (mostly empty planes and rows: the body spans a fraction of the long axis)."""
+    rig, _, frames, orig = scene
+    rec = vc.reconstruct_frame(frames, rig, vc.ReconConfig(dims=dims), ctx=ctx, want_volume=True)
+    ref = oracle_frame(O, orig, frames, dims=dims)
+    assert rel_l2(rec.volume.values, ref.volume) < REL_L2_A
+    assert abs(rec.volume.iso_level - ref.iso_level) < 1e-4 * abs(ref.iso_level)
+
+
 @pytest.mark.parametrize("dims", [(128, 128, 128), (128, 256, 128)])
 def test_indicator_field_rel_l2(O, scene, ctx, dims):
     rig, _, frames, orig = scene
