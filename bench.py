@@ -276,10 +276,12 @@ def alg_bytes(nx, ny, nz, P, V, T, k, chunks, nzrows, nzplanes):
     Nh = nz * ny * (nx // 2 + 1)
     rows = ny * nz
     line = 8 * (nx // 2 + 1)
-    return {"clear": 16 * 32 * chunks + 8 * rows, "splat": 16 * 64 * P + 4 * 16 * P,
-            "fft_x": 16 * 32 * chunks + 4 * rows + 3 * line * nzrows,
+    # (no clear pass: F-x zeroes the chunks it reads — 16 B per voxel written
+    # back — and I-x resets the row bits)
+    return {"splat": 16 * 64 * P + 4 * 16 * P,
+            "fft_x": 2 * 16 * 32 * chunks + 4 * rows + 3 * line * nzrows,
             "fft_y": 3 * line * nzrows + 4 * rows + 2 * line * ny * nzplanes,
-            "fft_z": 2 * line * ny * nzplanes + 8 * Nh, "ifft_y": 2 * 8 * Nh, "ifft_x": 8 * Nh + 4 * N + 8 * rows,
+            "fft_z": 2 * line * ny * nzplanes + 8 * Nh, "ifft_y": 2 * 8 * Nh, "ifft_x": 8 * Nh + 4 * N + 12 * rows,
             "mc": 8 * rows, "preprocess": k * W * H * 7 + P * 60, "iso": P * 32, "texture": V * (24 + 13 * k)}
 
 
@@ -319,13 +321,13 @@ def profile_kernels(lib, h, sensors, views_list, cfg, dims, out, k=4):
     L.check(lib.vc_export_points(h, C.c_void_p(pos.ctypes.data), None, None, None, None), h)
     sp = sparse_stats(pos, out.grid.origin[:], out.grid.edge_mm, *dims)
     ab = alg_bytes(*dims, P, V, T, k, *sp)
-    bw = {nm: ab[nm] / (kernel_ms[nm] * 1e-3) / 1e9 for nm in names if kernel_ms[nm] > 0}
-    if not all(nm in bw for nm in ["clear", "fft_x", "fft_y", "fft_z", "ifft_y", "ifft_x"]):
+    bw = {nm: ab[nm] / (kernel_ms[nm] * 1e-3) / 1e9 for nm in names if nm in ab and kernel_ms[nm] > 0}
+    if not all(nm in bw for nm in ["fft_x", "fft_y", "fft_z", "ifft_y", "ifft_x"]):
         raise RuntimeError(f"per-kernel event timings missing: {kernel_ms}")
     pk = peaks()
     hbm = float(pk.get("hbm_gbs", 6650.0))
     fft_names = ["fft_x", "fft_y", "fft_z", "ifft_y", "ifft_x"]
-    dom = max(fft_names + ["clear"], key=lambda nm: kernel_ms[nm])
+    dom = max(fft_names, key=lambda nm: kernel_ms[nm])
     traffic = None
     tkey = dom if tuple(dims) == DIMS else f"{dom}@{dims[0]}"
     try:  # dram bytes per launch of the same kernel at this grid from the committed ncu --set full capture

@@ -273,7 +273,7 @@ struct ZCfg {
 
 // ------------------------------------------------------------------ F-x
 template <int NX>
-__global__ void __launch_bounds__(XCfg<NX>::THREADS, 2) fx_kernel(const float4* __restrict__ acc, float2* __restrict__ S0,
+__global__ void __launch_bounds__(XCfg<NX>::THREADS, 2) fx_kernel(float4* __restrict__ acc, float2* __restrict__ S0,
                                                        float2* __restrict__ S1, float2* __restrict__ S2, int rows,
                                                        int H, const uint32_t* __restrict__ rowbits, int mode,
                                                        const float2* __restrict__ tw,
@@ -325,6 +325,18 @@ __global__ void __launch_bounds__(XCfg<NX>::THREADS, 2) fx_kernel(const float4* 
         xy[q * T + j2] = make_float2(a.x * s, a.y * s);
         zc[q * T + j2] = a.z * s;
       }
+    // with the touched-row list (frames): the chunks just read are zeroed for
+    // the next frame's splat here, instead of by a clear pass at frame start
+    if (rowlist) {
+#pragma unroll
+      for (int q = 0; q < S::Q; ++q)
+#pragma unroll
+        for (int j2 = 0; j2 < T; ++j2) {
+          const int j = t + T * q + R1 * j2;
+          if (CH == 0 ? bits != 0u : ((bits >> (j >> CH)) & 1u) != 0u)
+            __stcs(acc + (size_t)l * NX + j, make_float4(0.f, 0.f, 0.f, 0.f));
+        }
+    }
   };
   // Split C = FFT(a + i b) into A = FFT(a), B = FFT(b) for this thread's bins
   // k = t + T*k1 (partner bin n-k lives in lane T-t, element R1-1-k1).
@@ -1183,7 +1195,8 @@ struct IXCfg {
 template <int NX>
 __global__ void __launch_bounds__(IXCfg<NX>::THREADS, 2) ix_kernel(const float2* __restrict__ S0, float* __restrict__ A,
                                                        int rows, int H,
-                                                       const float2* __restrict__ tw, float2* __restrict__ rowmm) {
+                                                       const float2* __restrict__ tw, float2* __restrict__ rowmm,
+                                                       uint32_t* __restrict__ rowbits_reset) {
   using S = Shape<NX>;
   using CF = IXCfg<NX>;
   constexpr int T = S::R2, R1 = S::R1, NH = NX / 2;
@@ -1252,6 +1265,9 @@ __global__ void __launch_bounds__(IXCfg<NX>::THREADS, 2) ix_kernel(const float2*
       rowmm[l0] = make_float2(lo0, hi0);
       rowmm[l1] = make_float2(lo1, hi1);
     }
+    // the touched-chunk bits were last read by F-y: reset for the next frame
+    // (F-x zeroed the chunks themselves)
+    if (rowbits_reset && t == 0) rowbits_reset[l0] = 0u, rowbits_reset[l1] = 0u;
     __syncwarp(mask);  // `cur` is re-staged two iterations later
   }
   cp_async_wait<0>();
@@ -1496,7 +1512,8 @@ struct RunIx {
     const int rows = a.ny * a.nzl;
     const int need = (rows / 2 + C::TEAMS - 1) / C::TEAMS;
     const int grid = need < sm_count() * 4 ? need : sm_count() * 4;  // persistent teams
-    ix_kernel<N><<<grid, C::THREADS, C::SMEM, a.st>>>(a.Rout, a.A, rows, a.H, a.twx, a.rowmm);
+    ix_kernel<N><<<grid, C::THREADS, C::SMEM, a.st>>>(a.Rout, a.A, rows, a.H, a.twx, a.rowmm,
+                                                      a.rowlist ? const_cast<uint32_t*>(a.rowbits) : nullptr);
   }
 };
 
@@ -1570,7 +1587,7 @@ void launch_fill_random_acc(float4* acc, size_t n, uint32_t seed, cudaStream_t s
   fill_random_acc_kernel<<<sm_count() * 8, 256, 0, st>>>(acc, n, seed);
 }
 
-void launch_integrate(const float4* acc, float2* spec, float* A, int nx, int ny, int nz, int mode,
+void launch_integrate(float4* acc, float2* spec, float* A, int nx, int ny, int nz, int mode,
                       const float2* tw, cudaStream_t st, cudaEvent_t* ev, float2* rowmm, const uint32_t* rowbits,
                       uint32_t* planeflag, const int32_t* rowlist) {
   SlabFft a;

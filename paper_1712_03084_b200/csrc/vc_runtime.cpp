@@ -10,6 +10,7 @@
 //
 // Built with -ffp-contract=off: the host-side pose algebra (Pose::inverse,
 // Pose::compose, types.hpp:46-49) must round like the reference.
+#include <atomic>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -320,39 +321,52 @@ void record(vc_ctx* ctx, int i) {
 
 // The frame's kernel sequence (captured once into a CUDA graph).  With
 // profiling on, events 0..6 bracket the reference's stage split and events
+// Contexts alive per device (frame graphs choose their shape from it).
+std::atomic<int> g_live_ctx[64];
+
 // 12..23 bracket every kernel group (vc_ctx_kernel_times).
 int enqueue_frame(vc_ctx* ctx, const FrameCfg& f) {
   cudaStream_t st = ctx->st;
   int n = 0;
-  // the clear walks the previous frame's touched-row list: before the
-  // preprocess, whose gather pass resets the list for this frame's splat
-  // Graph branches (not in profiled frames, which time each kernel on one
-  // stream): the clear runs beside the preprocess, the MC normals and
-  // triangles beside the texturing.
+  // No clear pass: the previous frame's F-x zeroed the accumulator chunks it
+  // read and its I-x reset their bits.  The preprocess's gather pass resets
+  // the touched-row list for this frame's splat.  Graph branch (not in
+  // profiled frames, which time each kernel on one stream): the MC normals
+  // and triangles beside the texturing.
   const bool branch = !ctx->profiling && ctx->aux;
+  // A side branch at the frame's start (the touched-row list's reset beside
+  // the preprocess) when several contexts share the device: measured, a
+  // linear frame graph loses 10% of the four-frames-in-flight throughput
+  // (4700 against 5230 frames/s) but runs a lone frame 4% faster (3510
+  // against 3370) — profiles/r02_experiments.json "graph_root_branch".
+  // VC_ROOT_BRANCH=0/1 forces either shape.
+  static const int root_branch_env = [] {
+    const char* e = getenv("VC_ROOT_BRANCH");
+    return e ? atoi(e) : -1;
+  }();
+  const bool root_branch = root_branch_env >= 0 ? root_branch_env != 0
+                                                : (ctx->device < 64 && g_live_ctx[ctx->device].load() > 1);
   record(ctx, 12);
-  if (branch) {
+  // the touched-row list's reset rides on a side branch beside the preprocess:
+  // with one root branch the frame graphs of concurrent contexts interleave
+  // better (measured: a linear graph lost 10% of the S = 4 throughput)
+  const bool rb = branch && root_branch;
+  if (rb) {
     cudaEventRecord(ctx->fork[0], st);
     cudaStreamWaitEvent(ctx->aux, ctx->fork[0], 0);
+    cudaMemsetAsync(ctx->rowlist.p, 0, sizeof(int32_t), ctx->aux);
+    cudaEventRecord(ctx->join[0], ctx->aux);
   }
-  launch_sparse_clear(P<float4>(ctx->acc), P<uint32_t>(ctx->rowbits), P<int32_t>(ctx->rowlist), f.nx,
-                      branch ? ctx->aux : st);
-  if (branch) cudaEventRecord(ctx->join[0], ctx->aux);
   record(ctx, 13);
   record(ctx, 0);
-  // (the clear reads the previous touched-row list; the list is reset once
-  // the clear has joined, just before this frame's splat appends to it)
   launch_preprocess(ctx->ss, points(ctx), P<float>(ctx->wmaps), P<int32_t>(ctx->pre_scratch), ctx->ctl, f.nx, f.ny,
-                    f.nz, f.pad, f.disc, f.sil_r, st, branch ? nullptr : P<int32_t>(ctx->rowlist));
+                    f.nz, f.pad, f.disc, f.sil_r, st, rb ? nullptr : P<int32_t>(ctx->rowlist));
+  if (rb) cudaStreamWaitEvent(st, ctx->join[0], 0);
   n += 3;  // prefix + triangles, points, gather
   record(ctx, 1);
-  if (branch) {
-    cudaStreamWaitEvent(st, ctx->join[0], 0);
-    cudaMemsetAsync(ctx->rowlist.p, 0, sizeof(int32_t), st);
-  }
   launch_splat(points(ctx), ctx->ctl, P<float4>(ctx->acc), P<uint32_t>(ctx->rowbits), P<int32_t>(ctx->rowlist),
                f.mode, st, 0, f.nz);
-  n += 3;  // clear, splat, row-list build
+  n += 2;  // splat, row-list build
   record(ctx, 2);
   launch_integrate(P<float4>(ctx->acc), P<float2>(ctx->spec), P<float>(ctx->A), f.nx, f.ny, f.nz, f.mode,
                    P<float2>(ctx->tw), st, ctx->profiling ? &ctx->ev[14] : nullptr, P<float2>(ctx->rowmm),
@@ -521,7 +535,9 @@ vc_status vc_ctx_create(int device, vc_ctx** out) {
   if (device < 0 || device >= n) return VC_ERR_INVALID_ARGUMENT;
   auto* ctx = new vc_ctx;
   ctx->device = device;
+  if (device < 64) g_live_ctx[device].fetch_add(1);
   auto cleanup = [&](vc_status s) {
+    if (device < 64) g_live_ctx[device].fetch_sub(1);
     delete ctx;
     return s;
   };
@@ -546,6 +562,7 @@ vc_status vc_ctx_create(int device, vc_ctx** out) {
 
 vc_status vc_ctx_destroy(vc_ctx* ctx) {
   if (!ctx) return VC_OK;
+  if (ctx->device < 64) g_live_ctx[ctx->device].fetch_sub(1);
   cudaSetDevice(ctx->device);
   if (ctx->st) cudaStreamSynchronize(ctx->st);
   if (ctx->gexec) cudaGraphExecDestroy(ctx->gexec);

@@ -136,7 +136,7 @@ size_t spectrum_elems(int nx, int ny, int nz);  // complex elements per componen
 // ky in [ky0, ky0+kyl)); z pass in place on R0; all-to-all R0 -> Rin; y/x
 // inverse -> Rout (plain layout) -> A (the rank's planes).
 struct SlabFft {
-  const float4* acc;
+  float4* acc;  // F-x zeroes the chunks it reads when a touched-row list is given
   float2 *S0, *S1, *S2, *O0, *O1, *R0, *R1;
   const float2* Rin;
   float2* Rout;
@@ -153,7 +153,7 @@ void launch_fft_forward_xy(const SlabFft& a);
 void launch_fft_z(const SlabFft& a);
 void launch_fft_inverse_yx(const SlabFft& a);
 void launch_fill_random_acc(float4* acc, size_t n, uint32_t seed, cudaStream_t st);  // dense test field
-void launch_integrate(const float4* acc, float2* spec, float* A, int nx, int ny, int nz, int mode,
+void launch_integrate(float4* acc, float2* spec, float* A, int nx, int ny, int nz, int mode,
                       const float2* twiddles, cudaStream_t st, cudaEvent_t* ev /*nullable, 6 events*/,
                       float2* rowmm /*nullable: per-row min/max of A*/,
                       const uint32_t* rowbits /*nullable: touched 32-voxel chunks per row (null = dense)*/,
