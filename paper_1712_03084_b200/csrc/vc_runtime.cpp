@@ -536,6 +536,7 @@ vc_status vc_ctx_create(int device, vc_ctx** out) {
   auto* ctx = new vc_ctx;
   ctx->device = device;
   if (device < 64) g_live_ctx[device].fetch_add(1);
+  if (const char* e = getenv("VC_GRAPHS")) ctx->graphs = atoi(e) != 0;  // A/B: direct launches
   auto cleanup = [&](vc_status s) {
     if (device < 64) g_live_ctx[device].fetch_sub(1);
     delete ctx;
