@@ -243,7 +243,12 @@ __global__ void splat_finalize_kernel(const float4* acc, size_t n, int mode, int
   }
 }
 
+// the touched-row list's count, reset at the start of a frame
+__global__ void reset_count_kernel(int32_t* count) { *count = 0; }
+
 }  // namespace
+
+void launch_reset_rowlist(int32_t* rowlist, cudaStream_t st) { reset_count_kernel<<<1, 1, 0, st>>>(rowlist); }
 
 void launch_clear(float4* acc, size_t n, cudaStream_t st) {
   clear_kernel<<<sm_count() * 8, 256, 0, st>>>(acc, n);

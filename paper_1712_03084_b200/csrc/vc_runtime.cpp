@@ -354,7 +354,7 @@ int enqueue_frame(vc_ctx* ctx, const FrameCfg& f) {
   if (rb) {
     cudaEventRecord(ctx->fork[0], st);
     cudaStreamWaitEvent(ctx->aux, ctx->fork[0], 0);
-    cudaMemsetAsync(ctx->rowlist.p, 0, sizeof(int32_t), ctx->aux);
+    launch_reset_rowlist(P<int32_t>(ctx->rowlist), ctx->aux);  // a kernel node (a memset node here tripped ncu)
     cudaEventRecord(ctx->join[0], ctx->aux);
   }
   record(ctx, 13);

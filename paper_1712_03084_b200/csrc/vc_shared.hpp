@@ -124,6 +124,7 @@ void launch_splat(const DevPoints& pts, DevCtl* ctl, float4* acc, uint32_t* rowb
                   cudaStream_t st, int zoff, int nzl);
 // Zero the chunks of the rows the previous frame listed, reset their masks.
 // Runs before the frame's preprocess (which resets the list count).
+void launch_reset_rowlist(int32_t* rowlist, cudaStream_t st);  // count := 0 (one-thread kernel)
 void launch_sparse_clear(float4* acc, uint32_t* rowbits, const int32_t* rowlist, int nx, cudaStream_t st);
 void launch_splat_finalize(const float4* acc, size_t n, int mode, int negate, double sigma2, float* field,
                            float* density, cudaStream_t st);
