@@ -355,6 +355,7 @@ int enqueue_frame(vc_ctx* ctx, const FrameCfg& f) {
     cudaEventRecord(ctx->fork[0], st);
     cudaStreamWaitEvent(ctx->aux, ctx->fork[0], 0);
     launch_reset_rowlist(P<int32_t>(ctx->rowlist), ctx->aux);  // a kernel node (a memset node here tripped ncu)
+    n += 1;
     cudaEventRecord(ctx->join[0], ctx->aux);
   }
   record(ctx, 13);
