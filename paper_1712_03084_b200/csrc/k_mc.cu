@@ -398,7 +398,7 @@ __device__ __forceinline__ int3 count_unit(const float* __restrict__ A, int nx, 
 // CTA iteration k covers the 8 consecutive units 8 (blockIdx.x + k gridDim.x)
 // + warp, all in one kCntBlock block: their sum goes to the block's bsum entry
 // with one atomic triple per CTA iteration.
-__global__ void __launch_bounds__(256) mc_count_kernel(const float* __restrict__ A, DevCtl* ctl, int nx, int ny,
+__global__ void __launch_bounds__(256, 4) mc_count_kernel(const float* __restrict__ A, DevCtl* ctl, int nx, int ny,
                                                        int nz, McSlab sl, const int32_t* __restrict__ units,
                                                        int3* unitcnt, int3* bsum, MeshBufs mb) {
   static_assert(kCntBlock % 8 == 0, "a CTA iteration's units share one block");
@@ -793,7 +793,7 @@ __device__ __forceinline__ void tris_of(int nx, int ny, int voff, const MeshBufs
 }
 
 // normals and triangles in one launch: items [0, V) are vertices, [V, V + C) cells
-__global__ void __launch_bounds__(256) mc_finish_kernel(const float* __restrict__ A, const DevCtl* ctl, int nx, int ny,
+__global__ void __launch_bounds__(256, 4) mc_finish_kernel(const float* __restrict__ A, const DevCtl* ctl, int nx, int ny,
                                                         int nz, MeshBufs mb) {
   if (ctl->status != 0 || ctl->overflow) return;
   const int V = ctl->V, C = ctl->C, voff = ctl->voff;
